@@ -1,0 +1,723 @@
+"""CPU oracle (TEST INFRASTRUCTURE ONLY) for the surrogate/full IGA assembly hot path.
+
+This module is a plain-numpy restatement of the reference algorithm of
+arXiv 1904.06971's ``surriga`` package (``/root/reference/pkg/src/surriga``),
+written independently of the reference's code structure (points are
+vectorised, elements are processed in one batch, CSR positions are analytic).
+It exists so that the CUDA path can be checked on machines where the
+reference is not installed (the GPU box).  It is pinned against golden
+vectors produced by the real reference (``tests/golden/make_golden.py``) in
+``tests/test_oracle_golden.py``.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline
+leg may import this module; the product package never does.
+
+Citations (reference file:line) are given per function.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from fractions import Fraction
+
+import numpy as np
+
+FORMS = ("poisson", "mass", "biharmonic", "stokes_velocity")
+_DERIV = {"poisson": 1, "mass": 0, "biharmonic": 2, "stokes_velocity": 1}
+
+
+# ---------------------------------------------------------------------------
+# problem description (duck-typed from either the reference or the product)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class Problem:
+    form: str
+    p: int
+    ms: tuple              # basis functions per direction (solution space)
+    g: int                 # Gauss points per direction
+    sol_w: np.ndarray      # solution-space weights (colex)
+    geo_p: int
+    geo_ms: tuple
+    geo_w: np.ndarray
+    geo_ctrl: np.ndarray   # (Ng, n), colex
+    coefficient: float = 1.0
+
+    @property
+    def n(self):
+        return len(self.ms)
+
+    @property
+    def N(self):
+        return int(np.prod(self.ms))
+
+    @property
+    def spans(self):
+        return tuple(m - self.p for m in self.ms)
+
+    @property
+    def rational(self):
+        # assembly.py:418 -- `weights.is_unit` (all weights equal) selects the polynomial path
+        w = self.sol_w
+        return not bool(np.all(w == w[0]))
+
+
+def problem_from_disc(form, disc, coefficient=1.0) -> Problem:
+    fname = form.value if hasattr(form, "value") else str(form)
+    space = disc.space
+    gsp = disc.geom.space
+    return Problem(
+        form=fname,
+        p=int(space.kvs[0].p),
+        ms=tuple(int(kv.m) for kv in space.kvs),
+        g=int(disc.gauss),
+        sol_w=np.asarray(disc.weights.weights, dtype=float),
+        geo_p=int(gsp.kvs[0].p),
+        geo_ms=tuple(int(kv.m) for kv in gsp.kvs),
+        geo_w=np.asarray(disc.geom.weights.weights, dtype=float),
+        geo_ctrl=np.asarray(disc.geom.control, dtype=float),
+        coefficient=float(coefficient),
+    )
+
+
+# ---------------------------------------------------------------------------
+# splines (bspline.py:45-124, 186-238)
+# ---------------------------------------------------------------------------
+
+def open_uniform_knots(p: int, m: int) -> np.ndarray:
+    """bspline.py:225-238: p+1 zeros, k/(m-p) interior, p+1 ones (correctly rounded)."""
+    s = m - p
+    return np.array([0.0] * (p + 1) + [float(Fraction(k, s)) for k in range(1, s)] + [1.0] * (p + 1))
+
+
+def span_breaks(p: int, m: int) -> np.ndarray:
+    """bspline.py:213-215."""
+    s = m - p
+    return np.array([float(Fraction(k, s)) for k in range(s + 1)])
+
+
+def basis_ders(knots: np.ndarray, p: int, x: np.ndarray, nu: int):
+    """Cox-de Boor values + derivatives (NURBS book A2.2/A2.3), vectorised over points.
+
+    Follows bspline.py:45-109 (span search with right-clamping, inverted
+    knot-difference triangle, derivative recursion).  Returns
+    ``(span[npts], ders[npts, nu+1, p+1])``.
+    """
+    x = np.asarray(x, dtype=float).ravel()
+    npts = x.size
+    nb = knots.size - p - 1
+    span = np.searchsorted(knots, x, side="right") - 1
+    span = np.clip(span, p, nb - 1)
+    left = np.zeros((npts, p + 1))
+    right = np.zeros((npts, p + 1))
+    ndu = np.zeros((npts, p + 1, p + 1))
+    ndu[:, 0, 0] = 1.0
+    for j in range(1, p + 1):
+        left[:, j] = x - knots[span + 1 - j]
+        right[:, j] = knots[span + j] - x
+        saved = np.zeros(npts)
+        for r in range(j):
+            ndu[:, j, r] = right[:, r + 1] + left[:, j - r]
+            tmp = ndu[:, r, j - 1] / ndu[:, j, r]
+            ndu[:, r, j] = saved + right[:, r + 1] * tmp
+            saved = left[:, j - r] * tmp
+        ndu[:, j, j] = saved
+    ders = np.zeros((npts, nu + 1, p + 1))
+    ders[:, 0, :] = ndu[:, :, p]
+    nd = min(nu, p)
+    for r in range(p + 1):
+        a_prev = np.zeros((npts, p + 1))
+        a_prev[:, 0] = 1.0
+        for k in range(1, nd + 1):
+            a_cur = np.zeros((npts, p + 1))
+            d = np.zeros(npts)
+            rk, pk = r - k, p - k
+            if r >= k:
+                a_cur[:, 0] = a_prev[:, 0] / ndu[:, pk + 1, rk]
+                d = a_cur[:, 0] * ndu[:, rk, pk]
+            j1 = 1 if rk >= -1 else -rk
+            j2 = k - 1 if r - 1 <= pk else p - r
+            for j in range(j1, j2 + 1):
+                a_cur[:, j] = (a_prev[:, j] - a_prev[:, j - 1]) / ndu[:, pk + 1, rk + j]
+                d = d + a_cur[:, j] * ndu[:, rk + j, pk]
+            if r <= pk:
+                a_cur[:, k] = -a_prev[:, k - 1] / ndu[:, pk + 1, r]
+                d = d + a_cur[:, k] * ndu[:, r, pk]
+            ders[:, k, r] = d
+            a_prev = a_cur
+    fac = float(p)
+    for k in range(1, nd + 1):
+        ders[:, k, :] *= fac
+        fac *= p - k
+    return span, ders
+
+
+def collocation_matrix(knots, p, sites):
+    """Dense B_j(site_i) (bspline.py:127-135)."""
+    nb = knots.size - p - 1
+    span, t = basis_ders(knots, p, sites, 0)
+    E = np.zeros((sites.size, nb))
+    for i in range(sites.size):
+        E[i, span[i] - p: span[i] + 1] = t[i, 0]
+    return E
+
+
+# ---------------------------------------------------------------------------
+# quadrature (assembly.py:100-125)
+# ---------------------------------------------------------------------------
+
+def gauss_axes(p, m, g):
+    x, w = np.polynomial.legendre.leggauss(g)
+    h = 1.0 / (m - p)
+    offs = (x + 1.0) * (0.5 * h)
+    br = span_breaks(p, m)[:-1]
+    return (br[:, None] + offs[None, :]).ravel(), w * (0.5 * h)
+
+
+# ---------------------------------------------------------------------------
+# tensor fields on point grids (geometry.py:185-229, assembly.py:418-437)
+# ---------------------------------------------------------------------------
+
+def _multi(n, order):
+    """All per-direction derivative multi-indices with total order == ``order``."""
+    out = []
+    for a in np.ndindex(*([order + 1] * n)):
+        if sum(a) == order:
+            out.append(tuple(a))
+    return out
+
+
+def field_on_grid(p, ms, coef, axes, nu):
+    """Evaluate a tensor spline field with coefficients ``coef`` (N, C) on a grid.
+
+    Returns dict: multi-index alpha -> array (G_0, ..., G_{n-1}, C).
+    Contractions run direction by direction over the p+1 nonzero taps.
+    """
+    n = len(ms)
+    coef = np.asarray(coef, dtype=float).reshape(tuple(ms) + (-1,), order="F")
+    tabs = []
+    for d in range(n):
+        kn = open_uniform_knots(p, ms[d])
+        tabs.append(basis_ders(kn, p, axes[d], nu))
+    out = {}
+    for order in range(nu + 1):
+        for alpha in _multi(n, order):
+            t = coef
+            for d in range(n):
+                span, ders = tabs[d]
+                E = ders[:, alpha[d], :]             # (Gd, p+1)
+                idx = span[:, None] - p + np.arange(p + 1)[None, :]
+                t = np.moveaxis(t, d, 0)             # (m_d, ...)
+                g = t[idx]                           # (Gd, p+1, ...)
+                t = np.einsum("xr,xr...->x...", E, g)
+                t = np.moveaxis(t, 0, d)
+            out[alpha] = t
+    return out
+
+
+def _unit(n, a):
+    return tuple(1 if d == a else 0 for d in range(n))
+
+
+def _pair(n, a, b):
+    return tuple((1 if d == a else 0) + (1 if d == b else 0) for d in range(n))
+
+
+def geometry_on_grid(prob: Problem, axes, nu):
+    """Rational map, Jacobian ``jac[...,c,a]``, det, Hessian ``hess[...,c,a,b]`` (geometry.py:185-229)."""
+    n = prob.n
+    w = prob.geo_w
+    hom = np.concatenate([prob.geo_ctrl * w[:, None], w[:, None]], axis=1)
+    f = field_on_grid(prob.geo_p, prob.geo_ms, hom, axes, nu)
+    num = f[(0,) * n]
+    W = num[..., n]
+    phi = num[..., :n] / W[..., None]
+    res = {"phi": phi, "W": W}
+    if nu == 0:
+        return res
+    jac = np.empty(W.shape + (n, n))
+    dW = np.empty(W.shape + (n,))
+    for a in range(n):
+        dn = f[_unit(n, a)]
+        dW[..., a] = dn[..., n]
+        jac[..., :, a] = (dn[..., :n] - phi * dn[..., n, None]) / W[..., None]
+    res["jac"] = jac
+    res["det"] = det(jac)
+    if nu == 1:
+        return res
+    hess = np.empty(W.shape + (n, n, n))
+    for a in range(n):
+        for b in range(a, n):
+            d2 = f[_pair(n, a, b)]
+            v = (d2[..., :n] - jac[..., :, a] * dW[..., b, None] - jac[..., :, b] * dW[..., a, None]
+                 - phi * d2[..., n, None]) / W[..., None]
+            hess[..., :, a, b] = v
+            hess[..., :, b, a] = v
+    res["hess"] = hess
+    return res
+
+
+def det(J):
+    """geometry.py:98-111 (cofactor expansion along the first row)."""
+    n = J.shape[-1]
+    if n == 1:
+        return J[..., 0, 0].copy()
+    if n == 2:
+        return J[..., 0, 0] * J[..., 1, 1] - J[..., 0, 1] * J[..., 1, 0]
+    return (J[..., 0, 0] * (J[..., 1, 1] * J[..., 2, 2] - J[..., 1, 2] * J[..., 2, 1])
+            - J[..., 0, 1] * (J[..., 1, 0] * J[..., 2, 2] - J[..., 1, 2] * J[..., 2, 0])
+            + J[..., 0, 2] * (J[..., 1, 0] * J[..., 2, 1] - J[..., 1, 1] * J[..., 2, 0]))
+
+
+def adj(J):
+    """geometry.py:114-131: inv = adj / det."""
+    n = J.shape[-1]
+    A = np.empty_like(J)
+    if n == 1:
+        A[..., 0, 0] = 1.0
+        return A
+    if n == 2:
+        A[..., 0, 0] = J[..., 1, 1]
+        A[..., 0, 1] = -J[..., 0, 1]
+        A[..., 1, 0] = -J[..., 1, 0]
+        A[..., 1, 1] = J[..., 0, 0]
+        return A
+    for a in range(3):
+        for b in range(3):
+            r = [i for i in range(3) if i != b]
+            c = [j for j in range(3) if j != a]
+            A[..., a, b] = (-1.0) ** (a + b) * (J[..., r[0], c[0]] * J[..., r[1], c[1]]
+                                                 - J[..., r[0], c[1]] * J[..., r[1], c[0]])
+    return A
+
+
+# ---------------------------------------------------------------------------
+# CSR pattern (analytic; equals csr_from_triplets' pattern, assembly.py:245-270)
+# ---------------------------------------------------------------------------
+
+def row_col_range(ms, p, multi):
+    lo = np.maximum(multi - p, 0)
+    hi = np.minimum(multi + p, np.asarray(ms) - 1)
+    return lo, hi
+
+
+def pattern(ms, p, rows=None):
+    """indptr/indices of the basis-overlap pattern, restricted to ``rows`` if given.
+
+    Columns of row i are i + shift(o) for the colex offsets o in [-p,p]^n that
+    stay inside the index box; colex offset order is ascending column order
+    (surrogate.py:312-322), so no sort is needed.
+    """
+    ms = tuple(ms)
+    n = len(ms)
+    N = int(np.prod(ms))
+    offs = offsets(p, n)
+    strides = np.cumprod((1,) + ms[:-1])
+    rsel = np.arange(N) if rows is None else np.asarray(rows, dtype=np.int64)
+    multi = np.stack(np.unravel_index(rsel, ms, order="F"), axis=-1)
+    jm = multi[:, None, :] + offs[None, :, :]
+    ok = np.all((jm >= 0) & (jm < np.asarray(ms)), axis=-1)
+    cnt = np.zeros(N, dtype=np.int64)
+    cnt[rsel] = ok.sum(1)
+    indptr = np.zeros(N + 1, dtype=np.int64)
+    np.cumsum(cnt, out=indptr[1:])
+    cols = (jm * strides).sum(-1)
+    indices = cols[ok].astype(np.int32)
+    return indptr, indices
+
+
+# ---------------------------------------------------------------------------
+# element quadrature (assembly.py:402-651)
+# ---------------------------------------------------------------------------
+
+def _dir_tables(prob: Problem, nu):
+    tabs, axes, pws = [], [], []
+    for d in range(prob.n):
+        ax, pw = gauss_axes(prob.p, prob.ms[d], prob.g)
+        span, ders = basis_ders(open_uniform_knots(prob.p, prob.ms[d]), prob.p, ax, nu)
+        S = prob.spans[d]
+        assert np.array_equal(span.reshape(S, prob.g), (np.arange(S) + prob.p)[:, None].repeat(prob.g, 1))
+        tabs.append(ders.reshape(S, prob.g, nu + 1, prob.p + 1))
+        axes.append(ax)
+        pws.append(pw)
+    return tabs, axes, pws
+
+
+def _to_elements(arr, spans, g):
+    """grid (G_0..G_{n-1}, extra...) -> (E, Q, extra...) with colex element and point order."""
+    n = len(spans)
+    extra = arr.shape[n:]
+    shp = []
+    for s in spans:
+        shp += [s, g]
+    B = arr.reshape(tuple(shp) + extra, order="C")
+    # axes (e0, q0, e1, q1, ...) -> element colex (e_{n-1} slowest ... e_0 fastest) etc.
+    eax = [2 * d for d in range(n)][::-1]
+    qax = [2 * d + 1 for d in range(n)][::-1]
+    B = np.transpose(B, eax + qax + list(range(2 * n, 2 * n + len(extra))))
+    return B.reshape((int(np.prod(spans)), g ** n) + extra)
+
+
+def _local_tensor(tabs, et, alpha, p, g):
+    """Tensor-product basis derivative ``alpha`` on elements ``et``: (E, Q, L)."""
+    n = len(tabs)
+    out = None
+    for d in range(n):
+        v = tabs[d][et[:, d], :, alpha[d], :]          # (E, g, p+1)
+        if out is None:
+            out = v
+        else:
+            E = v.shape[0]
+            # point index q_d slower, function index l_d slower (colex)
+            out = (v[:, :, None, :, None] * out[:, None, :, None, :]).reshape(E, -1, out.shape[-1] * (p + 1))
+    return out
+
+
+def element_matrices(prob: Problem, eids):
+    """Local element matrices (E, L, L) for the listed elements (assembly.py:531-551)."""
+    n, p, g = prob.n, prob.p, prob.g
+    form = prob.form
+    nu = _DERIV[form]
+    gnu = 2 if form == "biharmonic" else 1
+    tabs, axes, pws = _dir_tables(prob, nu)
+    wq = pws[0]
+    for d in range(1, n):
+        wq = (pws[d][:, None] * wq[None, :]).ravel()
+    spans = prob.spans
+    geo = geometry_on_grid(prob, axes, gnu)
+    et = np.stack(np.unravel_index(eids, spans, order="F"), axis=-1)
+    detE = _to_elements(geo["det"], spans, g)[eids]
+    jacE = _to_elements(geo["jac"], spans, g)[eids]
+    A = adj(jacE)
+
+    B = _local_tensor(tabs, et, (0,) * n, p, g)
+    dB = d2B = None
+    if nu >= 1:
+        dB = np.stack([_local_tensor(tabs, et, _unit(n, a), p, g) for a in range(n)], axis=-1)
+    if nu >= 2:
+        d2B = np.empty(B.shape + (n, n))
+        for a in range(n):
+            for b in range(n):
+                d2B[..., a, b] = _local_tensor(tabs, et, _pair(n, a, b), p, g)
+
+    if prob.rational:
+        Wf = field_on_grid(p, prob.ms, prob.sol_w[:, None], axes, nu)
+        W = _to_elements(Wf[(0,) * n][..., 0], spans, g)[eids][..., None]
+        # local weights per element function (colex)
+        L = (p + 1) ** n
+        Il = np.stack(np.unravel_index(np.arange(L), (p + 1,) * n, order="F"), axis=-1)
+        strides = np.cumprod((1,) + tuple(prob.ms[:-1]))
+        cols = ((et[:, None, :] + Il[None, :, :]) * strides).sum(-1)
+        wl = prob.sol_w[cols][:, None, :]
+        N = wl * B / W
+        if nu >= 1:
+            dW = np.stack([_to_elements(Wf[_unit(n, a)][..., 0], spans, g)[eids] for a in range(n)], axis=-1)
+            dN = np.empty_like(dB)
+            for a in range(n):
+                dN[..., a] = (wl * dB[..., a] - N * dW[..., a][..., None]) / W
+        if nu >= 2:
+            d2N = np.empty_like(d2B)
+            for a in range(n):
+                for b in range(n):
+                    d2W = _to_elements(Wf[_pair(n, a, b)][..., 0], spans, g)[eids][..., None]
+                    d2N[..., a, b] = (wl * d2B[..., a, b] - dN[..., a] * dW[..., b][..., None]
+                                      - dN[..., b] * dW[..., a][..., None] - N * d2W) / W
+        B = N
+        if nu >= 1:
+            dB = dN
+        if nu >= 2:
+            d2B = d2N
+
+    if form in ("poisson", "stokes_velocity"):
+        K = np.einsum("eqab,eqcb->eqac", A, A) / detE[..., None, None]
+        K = K * prob.coefficient
+        Kw = K * wq[None, :, None, None]
+        loc = np.einsum("eqla,eqab,eqkb->elk", dB, Kw, dB)
+    elif form == "mass":
+        s = detE * wq[None, :]
+        loc = np.einsum("eql,eq,eqk->elk", B, s, B)
+    elif form == "biharmonic":
+        hessE = _to_elements(geo["hess"], spans, g)[eids]
+        C = np.einsum("eqac,eqbc->eqab", A, A) / (detE ** 2)[..., None, None]
+        pg = np.einsum("eqla,eqac->eqlc", dB, A) / detE[..., None, None]
+        T = d2B - np.einsum("eqlc,eqcab->eqlab", pg, hessE)
+        lap = np.einsum("eqlab,eqab->eql", T, C)
+        s = detE * wq[None, :]
+        loc = np.einsum("eql,eq,eqk->elk", lap, s, lap)
+    else:
+        raise ValueError(f"unsupported square form {form}")
+    # upper triangle mirrored (assembly.py:524-528)
+    Lr = loc.shape[1]
+    up = np.arange(Lr)[:, None] <= np.arange(Lr)[None, :]
+    return np.where(up[None], loc, np.swapaxes(loc, 1, 2)), et
+
+
+def elements_for_rows(ms, p, rows):
+    """Ascending colex ids of elements supporting any of ``rows`` (assembly.py:347-360).
+
+    Computed as a separable box dilation of the row mask instead of a loop.
+    """
+    ms = tuple(ms)
+    n = len(ms)
+    spans = tuple(m - p for m in ms)
+    rmask = np.zeros(int(np.prod(ms)), dtype=bool)
+    rmask[np.asarray(rows, dtype=np.int64)] = True
+    R = rmask.reshape(ms, order="F")
+    # element e touches rows e..e+p per direction
+    for d in range(n):
+        R = np.moveaxis(R, d, 0)
+        acc = np.zeros((spans[d],) + R.shape[1:], dtype=bool)
+        for r in range(p + 1):
+            acc |= R[r:r + spans[d]]
+        R = np.moveaxis(acc, 0, d)
+    return np.flatnonzero(R.ravel(order="F"))
+
+
+def assemble(prob: Problem, rows=None, chunk=4096):
+    """Full or row-restricted Galerkin matrix (assembly.py:579-651).
+
+    Returns ``(indptr, indices, data, symmetric, populated_rows)``.
+    """
+    if prob.form == "biharmonic" and prob.p < 2:
+        raise ValueError("the fourth-order form needs degree >= 2 for C^1 continuity")
+    if prob.coefficient != 1.0 and prob.form not in ("poisson", "stokes_velocity"):
+        raise ValueError("coefficient is only supported for the second-order forms")
+    n, p = prob.n, prob.p
+    ms = prob.ms
+    N = prob.N
+    if rows is None:
+        eids = np.arange(int(np.prod(prob.spans)))
+        rowsel = None
+    else:
+        rowsel = np.unique(np.asarray(rows, dtype=np.int64))
+        if rowsel.size and (rowsel[0] < 0 or rowsel[-1] >= N):
+            raise ValueError("row index out of range")
+        eids = elements_for_rows(ms, p, rowsel) if rowsel.size else np.zeros(0, np.int64)
+    indptr, indices = pattern(ms, p, rowsel)
+    data = np.zeros(indices.size)
+    if rowsel is not None:
+        keep = np.zeros(N, dtype=bool)
+        keep[rowsel] = True
+    L = (p + 1) ** n
+    Il = np.stack(np.unravel_index(np.arange(L), (p + 1,) * n, order="F"), axis=-1)
+    strides = np.cumprod((1,) + tuple(ms[:-1]))
+    for s in range(0, eids.size, chunk):
+        ce = eids[s:s + chunk]
+        loc, et = element_matrices(prob, ce)
+        gm = et[:, None, :] + Il[None, :, :]                 # (E, L, n) global multi
+        cols = (gm * strides).sum(-1)                         # (E, L)
+        # position of (row=gm_l, col=gm_k) inside the CSR row of gm_l
+        lo = np.maximum(gm - p, 0)
+        hi = np.minimum(gm + p, np.asarray(ms) - 1)
+        cnt = hi - lo + 1
+        rel = gm[:, None, :, :] - lo[:, :, None, :]          # (E, Lrow, Lcol, n)
+        cstr = np.concatenate([np.ones(cnt.shape[:2] + (1,), np.int64), np.cumprod(cnt[..., :-1], -1)], -1)
+        colpos = (rel * cstr[:, :, None, :]).sum(-1)
+        rr = np.broadcast_to(cols[:, :, None], colpos.shape)
+        if rowsel is not None:
+            sel = keep[rr]
+        else:
+            sel = np.ones(rr.shape, dtype=bool)
+        pos = indptr[rr[sel]] + colpos[sel]
+        data += np.bincount(pos, weights=loc[sel], minlength=data.size)
+    sym = prob.form in FORMS
+    return indptr, indices, data, (sym and rows is None), (None if rows is None else rowsel)
+
+
+# ---------------------------------------------------------------------------
+# surrogate (surrogate.py:36-691)
+# ---------------------------------------------------------------------------
+
+DEFAULT_MODE = {"poisson": "symmetric_kernel_preserving", "biharmonic": "symmetric_kernel_preserving",
+                "mass": "symmetric", "stokes_velocity": "symmetric"}
+
+
+def offsets(p, n):
+    """[-p, p]^n colex (surrogate.py:103-122)."""
+    rng = np.arange(-p, p + 1)
+    k = rng.size
+    grid = np.unravel_index(np.arange(k ** n), (k,) * n, order="F")
+    return np.stack([rng[g] for g in grid], axis=-1)
+
+
+def box_range(p, m):
+    """In-box 0-based indices [2p, m-2p-1] (surrogate.py:150-152)."""
+    return 2 * p, m - 2 * p - 1
+
+
+def lattice_indices(p, m, M):
+    """surrogate.py:236-253."""
+    lo, hi = box_range(p, m)
+    idx = np.arange(lo, hi + 1, M)
+    if idx[-1] != hi:
+        idx = np.append(idx, hi)
+    return idx
+
+
+def midpoints(p, m, idx):
+    """surrogate.py:231-233: ((2i+1-p)/2) h exactly, then rounded."""
+    h = Fraction(1, m - p)
+    return np.array([float(Fraction(2 * int(i) + 1 - p, 2) * h) for i in idx])
+
+
+def averaging_knots(sites, q):
+    """surrogate.py:386-390."""
+    k = sites.size
+    interior = [np.mean(sites[j + 1:j + q + 1]) for j in range(k - q - 1)]
+    return np.concatenate([np.full(q + 1, sites[0]), interior, np.full(q + 1, sites[-1])])
+
+
+def surrogate(prob: Problem, M: int, q: int = 3, mode=None):
+    """Surrogate matrix + report dict (surrogate.py:538-691)."""
+    from scipy.linalg import solve
+
+    n, p, ms = prob.n, prob.p, prob.ms
+    N = prob.N
+    mode = DEFAULT_MODE[prob.form] if mode is None else mode
+    if mode == "symmetric_kernel_preserving" and prob.form not in ("poisson", "biharmonic"):
+        raise ValueError(f"kernel-preserving mode is not defined for {prob.form}")
+    h0 = 1.0 / (ms[0] - p)
+    empty = any(m <= 4 * p for m in ms)
+    if empty:
+        ip, ix, dt, _, _ = assemble(prob)
+        rep = dict(N=N, p=p, q=q, M=M, H=M * h0, quad_entries=ix.size, interp_entries=0,
+                   quad_fraction=1.0, active_elements=int(np.prod(prob.spans)), flags=["surrogate=disabled"])
+        return (ip, ix, dt), True, rep
+
+    lat = [lattice_indices(p, m, M) for m in ms]
+    inb = []
+    smp = []
+    for d, m in enumerate(ms):
+        lo, hi = box_range(p, m)
+        a = np.zeros(m, bool)
+        a[lo:hi + 1] = True
+        s = np.zeros(m, bool)
+        s[lat[d]] = True
+        inb.append(a)
+        smp.append(s)
+
+    def flat(masks):
+        acc = np.ones(1, bool)
+        for mk in masks[::-1]:
+            acc = (acc[:, None] & mk[None, :]).ravel()
+        return acc
+
+    in_flat = flat(inb)
+    samp_flat = flat(smp)
+    quad_rows = np.flatnonzero(~in_flat | samp_flat)
+    interp_rows = np.flatnonzero(in_flat & ~samp_flat)
+    ipq, ixq, dq, _, _ = assemble(prob, rows=quad_rows)
+    active = elements_for_rows(ms, p, quad_rows).size
+    H = M * h0
+    nI = interp_rows.size
+    if nI == 0:
+        rep = dict(N=N, p=p, q=q, M=M, H=H, quad_entries=ixq.size, interp_entries=0,
+                   quad_fraction=1.0, active_elements=active, flags=[])
+        return (ipq, ixq, dq), prob.form in FORMS, rep
+
+    offs = offsets(p, n)
+    P = offs.shape[0]
+    center = (P - 1) // 2
+    strides = np.cumprod((1,) + tuple(ms[:-1]))
+    # samples: row positions o in each lattice row (surrogate.py:336-379)
+    lat_grid = np.stack([g.ravel(order="F") for g in np.meshgrid(*lat, indexing="ij")], -1)
+    lat_rows = lat_grid @ strides
+    assert np.all(np.diff(ipq)[lat_rows] == P)
+    S = dq[ipq[lat_rows][:, None] + np.arange(P)[None, :]]           # (nlat, P)
+    lat_shape = tuple(x.size for x in lat)
+    coef = S.T.reshape((P,) + lat_shape, order="F")                 # (P, l0, l1, ...)
+
+    flags = []
+    qd, kn = [], []
+    for d in range(n):
+        sites = midpoints(p, ms[d], lat[d])
+        qq = min(q, sites.size - 1)
+        if qq < q and "interpolation-order-lowered" not in flags:
+            flags.append("interpolation-order-lowered")
+        qd.append(qq)
+        kn.append(averaging_knots(sites, qq) if qq >= 1 else None)
+        if qq >= 1:
+            C = collocation_matrix(kn[d], qq, sites)
+            moved = np.moveaxis(coef, 1 + d, 0)
+            sol = solve(C, moved.reshape(sites.size, -1))
+            coef = np.moveaxis(sol.reshape(moved.shape), 0, 1 + d)
+    # evaluate on all in-box midpoints
+    V = coef
+    box_n = []
+    for d in range(n):
+        lo, hi = box_range(p, ms[d])
+        pts = midpoints(p, ms[d], np.arange(lo, hi + 1))
+        box_n.append(pts.size)
+        E = np.ones((pts.size, 1)) if kn[d] is None else collocation_matrix(kn[d], qd[d], pts)
+        V = np.moveaxis(np.tensordot(E, np.moveaxis(V, 1 + d, 0), axes=(1, 0)), 0, 1 + d)
+    VF = V.reshape(P, -1, order="F")
+    box_str = np.cumprod((1,) + tuple(box_n[:-1]))
+    Im = np.stack(np.unravel_index(interp_rows, ms, order="F"), -1)
+    Ib = (Im - 2 * p) @ box_str
+
+    # final matrix = quad rows from Aq, interp rows filled per offset
+    indptr, indices = pattern(ms, p)
+    data = np.zeros(indices.size)
+    rowid = np.repeat(np.arange(N), np.diff(indptr))
+    isq = np.zeros(N, dtype=bool)
+    isq[quad_rows] = True
+    data[isq[rowid]] = dq
+    canonical_from = center
+    offd = np.zeros(nI, np.int64)
+    n_interp = 0
+    for o in range(P):
+        sh = offs[o]
+        jm = Im + sh[None, :]
+        jflat = jm @ strides
+        jin = np.ones(nI, bool)
+        jsm = np.ones(nI, bool)
+        for d in range(n):
+            jin &= inb[d][jm[:, d]]
+            jsm &= smp[d][jm[:, d]]
+        jint = jin & ~jsm
+        vals = np.empty(nI)
+        t = ~jint
+        vals[t] = dq[ipq[jflat[t]] + (P - 1 - o)]
+        if mode == "general" or o >= canonical_from:
+            vals[jint] = VF[o, Ib[jint]]
+        else:
+            jb = (jm[jint] - 2 * p) @ box_str
+            vals[jint] = VF[P - 1 - o, jb]
+        if o != center:
+            offd[jint] += 1
+        n_interp += int(jint.sum())
+        data[indptr[interp_rows] + o] = vals
+    # merge drops exact zeros (scipy csr add, surrogate.py:670)
+    nz = data != 0.0
+    if not np.all(nz):
+        keep_cnt = np.add.reduceat(nz.astype(np.int64), indptr[:-1]) * (np.diff(indptr) > 0)
+        new_ip = np.zeros_like(indptr)
+        np.cumsum(keep_cnt, out=new_ip[1:])
+        indices, data, indptr = indices[nz], data[nz], new_ip
+    if mode == "symmetric_kernel_preserving":
+        reset = interp_rows[offd > 0]
+        if reset.size:
+            take = indptr[reset][:, None] + np.arange(P)[None, :]
+            rv = data[take]
+            data[indptr[reset] + center] = rv[:, center] - rv.sum(axis=1)
+    quad_entries = int(ixq.size + nI * P - n_interp)
+    rep = dict(N=N, p=p, q=q, M=M, H=H, quad_entries=quad_entries, interp_entries=n_interp,
+               quad_fraction=quad_entries / (quad_entries + n_interp), active_elements=int(active), flags=flags)
+    return (indptr, indices, data), mode in ("symmetric", "symmetric_kernel_preserving"), rep
+
+
+# ---------------------------------------------------------------------------
+# comparisons
+# ---------------------------------------------------------------------------
+
+def row_scaled_error(ipA, ixA, dA, ipB, ixB, dB):
+    """max_ij |A_ij - B_ij| / max_k |A_ik| (patterns must already agree)."""
+    if not (np.array_equal(ipA, ipB) and np.array_equal(ixA, ixB)):
+        return np.inf
+    if dA.size == 0:
+        return 0.0
+    cnt = np.diff(ipA)
+    rows = np.repeat(np.arange(cnt.size), cnt)
+    scale = np.zeros(cnt.size)
+    np.maximum.at(scale, rows, np.abs(dA))
+    err = np.abs(dA - dB) / np.where(scale[rows] > 0, scale[rows], 1.0)
+    return float(err.max())
