@@ -1,0 +1,120 @@
+/*
+ * surriga_b200 -- C ABI of the B200 (sm_100a) surrogate / full-quadrature IGA assembly path.
+ *
+ * The reference (arXiv 1904.06971 "surriga", pure Python) exposes the hot path as two
+ * Python functions; this library sits behind exactly those two calls:
+ *
+ *   assemble(form, disc, rows=None, coefficient=1.0) -> SparseMatrix
+ *        reference: pkg/src/surriga/assembly.py:579-651      -> sg_assemble()
+ *   build_surrogate_matrix(form, disc, strategy=None, q=3, mode=None, coefficient=1.0)
+ *        -> (SparseMatrix, AssemblyReport)
+ *        reference: pkg/src/surriga/surrogate.py:538-691     -> sg_surrogate()
+ *
+ * The Python host (paper_1904_06971_b200/) validates arguments with the reference's error
+ * messages, performs the exact-rational setup (knots, Gauss points, lattice), and calls these
+ * entry points through ctypes.  All O(nnz) and O(elements * Q * L^2) work runs on the GPU.
+ *
+ * Conventions: plain pointers and sizes only; every input pointer is a HOST pointer that is
+ * borrowed for the duration of the call (copied to the device inside the call).  Results live
+ * on the device behind an opaque handle until sg_result_free().  Every function returns 0 on
+ * success and a negative status on failure; sg_last_error() gives a thread-local message.
+ * Multi-index / flat-index order is colex (first direction fastest), as in bspline.py:306-339.
+ */
+#ifndef SURRIGA_B200_H
+#define SURRIGA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* assembly.py:51-58 FormKind.  STOKES_VELOCITY is Poisson times a coefficient (assembly.py:533). */
+enum sg_form { SG_POISSON = 0, SG_MASS = 1, SG_BIHARMONIC = 2 };
+
+/* surrogate.py:36-41 SurrogateMode */
+enum sg_mode { SG_GENERAL = 0, SG_SYMMETRIC = 1, SG_SYMMETRIC_KERNEL_PRESERVING = 2 };
+
+/* Everything the hot path reads from a Discretization (assembly.py:133-176). */
+typedef struct sg_problem {
+    int32_t n;              /* parametric dimension 1..3                                 */
+    int32_t p;              /* solution degree (all directions), 1..SG_MAX_P             */
+    int32_t form;           /* enum sg_form                                              */
+    int32_t m[3];           /* basis functions per direction (m = spans + p)             */
+    int32_t g;              /* Gauss points per direction (assembly.py:173)               */
+    const double* knots[3]; /* solution knots per direction, m+p+1 each (float of exact)  */
+    const double* qpts[3];  /* Gauss points per direction, (m-p)*g each (assembly.py:108)  */
+    const double* qwts[3];  /* per-direction point weights, g each (w * h/2)              */
+    const double* sol_w;    /* N solution weights (colex) or NULL when `weights.is_unit`  */
+    int32_t geo_p;          /* geometry degree                                            */
+    int32_t geo_m[3];       /* geometry basis functions per direction                     */
+    const double* geo_knots[3];
+    const double* geo_hom;  /* Ng x (n+1): control*w | w, colex (geometry.py:193-195)      */
+    double coefficient;     /* Poisson / Stokes-velocity multiplier (assembly.py:606-610)  */
+} sg_problem;
+
+/* Row-slab / device options for one call. */
+typedef struct sg_exec {
+    int32_t device;         /* CUDA device ordinal                                        */
+    void* stream;           /* cudaStream_t to run on, or NULL for a per-call stream      */
+    int64_t slab_lo;        /* rows [slab_lo, slab_hi) assembled on this device (row slab) */
+    int64_t slab_hi;        /* slab_hi <= 0 means "all rows"                               */
+} sg_exec;
+
+/* Surrogate parameters (host-resolved: M from the sampling strategy, lattice from tilde box). */
+typedef struct sg_surrogate_params {
+    int32_t M;              /* sampling stride (surrogate.py:236-253)                     */
+    int32_t q;              /* requested interpolation order                              */
+    int32_t mode;           /* enum sg_mode                                               */
+    int32_t nlat[3];        /* lattice sites per direction                                */
+    const int64_t* lat_idx[3];   /* 0-based lattice basis indices per direction           */
+    int32_t qd[3];          /* per-direction interpolation degree (lowered, 0 = constant)  */
+    const double* interp_knots[3]; /* averaged knots per direction (nlat+qd+1) or NULL    */
+    const double* colloc_inv[3];   /* nlat x nlat inverse collocation matrix (row-major)  */
+    const double* box_pts[3];      /* in-box midpoints per direction (box count each)     */
+} sg_surrogate_params;
+
+/* Integer/float facts the host needs to build AssemblyReport (surrogate.py:478-502). */
+typedef struct sg_surrogate_stats {
+    int64_t n_interp_rows;
+    int64_t n_quad_rows;
+    int64_t n_interp_entries;   /* (interp row, offset) pairs filled from an interpolant  */
+    int64_t n_zero_dropped;     /* exact zeros removed by the CSR merge (surrogate.py:670) */
+    int64_t n_reset_rows;       /* kernel-preserving diagonal resets (surrogate.py:673)    */
+} sg_surrogate_stats;
+
+typedef struct sg_result sg_result;
+
+/* Full or row-restricted assembly.  rows == NULL: all rows (the reference's rows=None).
+ * rows != NULL: nrows sorted unique 0-based rows; only their entries are emitted
+ * (assembly.py:613-622,638-640), bitwise equal to the full rows. */
+int sg_assemble(const sg_problem* prob, const int64_t* rows, int64_t nrows, const sg_exec* ex, sg_result** out);
+
+/* Surrogate assembly (quadrature rows + interpolated interior rows + merge + SKP diagonal). */
+int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* sp, const sg_exec* ex, sg_result** out,
+                 sg_surrogate_stats* stats);
+
+/* Result inspection / transfer. */
+int sg_result_sizes(const sg_result* r, int64_t* nrows, int64_t* nnz);
+/* Copy CSR to host: indptr int32[nrows+1] (or int64 if *_i64 variant), indices int32[nnz], data f64[nnz]. */
+int sg_result_copy(const sg_result* r, int32_t* indptr, int32_t* indices, double* data);
+int sg_result_copy_i64(const sg_result* r, int64_t* indptr, int32_t* indices, double* data);
+/* Device pointers (for device-resident consumers and timing). */
+int sg_result_device_ptrs(const sg_result* r, void** indptr_i64, void** indices_i32, void** data_f64);
+/* Deterministic fp64 checksums {nnz, sum a, sum a^2, sum |a|, sum of row sums} of the rows in the result. */
+int sg_result_checksum(const sg_result* r, double out[5]);
+int sg_result_free(sg_result* r);
+
+/* Device-time of the kernels of the last call on this thread (ms), and their launch count. */
+int sg_last_timing(double* ms_total, int32_t* launches);
+/* Per-kernel breakdown of the last call: name list (comma separated) and ms values. */
+int sg_last_kernel_times(char* names, int32_t names_cap, double* ms, int32_t cap, int32_t* count);
+
+const char* sg_last_error(void);
+const char* sg_version(void);
+int sg_max_degree(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SURRIGA_B200_H */

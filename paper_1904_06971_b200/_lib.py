@@ -1,0 +1,158 @@
+"""ctypes binding of ``libsurriga_b200.so`` (C ABI in ``include/surriga_b200.h``).
+
+There is no CPU fallback: if the library or a CUDA device is missing, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsurriga_b200.so")
+
+_d = C.POINTER(C.c_double)
+_i64 = C.POINTER(C.c_int64)
+_i32 = C.POINTER(C.c_int32)
+
+
+class SgProblem(C.Structure):
+    _fields_ = [
+        ("n", C.c_int32), ("p", C.c_int32), ("form", C.c_int32), ("m", C.c_int32 * 3), ("g", C.c_int32),
+        ("knots", _d * 3), ("qpts", _d * 3), ("qwts", _d * 3), ("sol_w", _d),
+        ("geo_p", C.c_int32), ("geo_m", C.c_int32 * 3), ("geo_knots", _d * 3), ("geo_hom", _d),
+        ("coefficient", C.c_double),
+    ]
+
+
+class SgExec(C.Structure):
+    _fields_ = [("device", C.c_int32), ("stream", C.c_void_p), ("slab_lo", C.c_int64), ("slab_hi", C.c_int64)]
+
+
+class SgSurrogateParams(C.Structure):
+    _fields_ = [
+        ("M", C.c_int32), ("q", C.c_int32), ("mode", C.c_int32), ("nlat", C.c_int32 * 3), ("lat_idx", _i64 * 3),
+        ("qd", C.c_int32 * 3), ("interp_knots", _d * 3), ("colloc_inv", _d * 3), ("box_pts", _d * 3),
+    ]
+
+
+class SgSurrogateStats(C.Structure):
+    _fields_ = [("n_interp_rows", C.c_int64), ("n_quad_rows", C.c_int64), ("n_interp_entries", C.c_int64),
+                ("n_zero_dropped", C.c_int64), ("n_reset_rows", C.c_int64)]
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def lib():
+    """Load the sm_100a library (once).  Raises if it is missing -- no fallback path exists."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise NativeError(f"{LIB_PATH} not built; run __graft_entry__.build() (nvcc, sm_100a)")
+        L = C.CDLL(LIB_PATH)
+        L.sg_last_error.restype = C.c_char_p
+        L.sg_version.restype = C.c_char_p
+        L.sg_assemble.argtypes = [C.POINTER(SgProblem), _i64, C.c_int64, C.POINTER(SgExec), C.POINTER(C.c_void_p)]
+        L.sg_surrogate.argtypes = [C.POINTER(SgProblem), C.POINTER(SgSurrogateParams), C.POINTER(SgExec),
+                                   C.POINTER(C.c_void_p), C.POINTER(SgSurrogateStats)]
+        L.sg_result_sizes.argtypes = [C.c_void_p, _i64, _i64]
+        L.sg_result_copy.argtypes = [C.c_void_p, _i32, _i32, _d]
+        L.sg_result_copy_i64.argtypes = [C.c_void_p, _i64, _i32, _d]
+        L.sg_result_device_ptrs.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]
+        L.sg_result_checksum.argtypes = [C.c_void_p, _d]
+        L.sg_result_free.argtypes = [C.c_void_p]
+        L.sg_last_timing.argtypes = [_d, _i32]
+        L.sg_last_kernel_times.argtypes = [C.c_char_p, C.c_int32, _d, C.c_int32, _i32]
+        _lib = L
+    return _lib
+
+
+SYMBOLS = ("sg_assemble", "sg_surrogate", "sg_result_sizes", "sg_result_copy", "sg_result_copy_i64",
+           "sg_result_device_ptrs", "sg_result_checksum", "sg_result_free", "sg_last_timing",
+           "sg_last_kernel_times", "sg_last_error", "sg_version", "sg_max_degree")
+
+
+def check(rc):
+    if rc != 0:
+        msg = lib().sg_last_error().decode(errors="replace")
+        if rc == -1:
+            raise ValueError(msg)
+        raise NativeError(f"surriga_b200 error {rc}: {msg}")
+
+
+def dptr(a):
+    return a.ctypes.data_as(_d) if a is not None else None
+
+
+class Result:
+    """Owning handle of a device-resident CSR produced by the library."""
+
+    def __init__(self, handle):
+        self.h = C.c_void_p(handle)
+
+    def sizes(self):
+        nr, nz = C.c_int64(), C.c_int64()
+        check(lib().sg_result_sizes(self.h, C.byref(nr), C.byref(nz)))
+        return nr.value, nz.value
+
+    def to_host(self):
+        """D2H copy -> (indptr, indices, data) with scipy's index dtype (int32 when it fits)."""
+        nrows, nnz = self.sizes()
+        indices = np.empty(nnz, dtype=np.int32)
+        data = np.empty(nnz, dtype=np.float64)
+        if nnz < 2**31 - 1:
+            indptr = np.empty(nrows + 1, dtype=np.int32)
+            check(lib().sg_result_copy(self.h, indptr.ctypes.data_as(_i32), indices.ctypes.data_as(_i32), dptr(data)))
+        else:
+            indptr = np.empty(nrows + 1, dtype=np.int64)
+            check(lib().sg_result_copy_i64(self.h, indptr.ctypes.data_as(_i64), indices.ctypes.data_as(_i32), dptr(data)))
+        return indptr, indices, data
+
+    def device_ptrs(self):
+        a, b, c = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        check(lib().sg_result_device_ptrs(self.h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    def checksum(self):
+        out = np.zeros(5)
+        check(lib().sg_result_checksum(self.h, dptr(out)))
+        return out
+
+    def free(self):
+        if self.h is not None and self.h.value:
+            lib().sg_result_free(self.h)
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def last_timing():
+    ms = C.c_double()
+    n = C.c_int32()
+    lib().sg_last_timing(C.byref(ms), C.byref(n))
+    return ms.value, n.value
+
+
+def last_kernel_times():
+    names = C.create_string_buffer(4096)
+    ms = (C.c_double * 64)()
+    cnt = C.c_int32()
+    lib().sg_last_kernel_times(names, 4096, ms, 64, C.byref(cnt))
+    nm = names.value.decode().split(",") if cnt.value else []
+    return list(zip(nm, [ms[i] for i in range(min(cnt.value, 64))]))

@@ -1,0 +1,299 @@
+"""Drop-in ``assemble`` (reference: surriga/assembly.py:579-651) on the B200.
+
+The host does what the reference does before its element loop -- argument validation with
+the reference's messages, exact-rational knots and Gauss points (assembly.py:100-125) -- and
+hands plain arrays to ``sg_assemble`` (include/surriga_b200.h).  Basis tables, geometry,
+element quadrature and CSR emission all run on the GPU.  Both the reference's own
+``FormKind``/``Discretization`` objects and this package's mirrors are accepted.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from enum import Enum
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _lib
+from .geometry import GeometryMap, weights_for_space
+from .spaces import NurbsWeights, TensorSpace, make_open_uniform_knots, make_tensor_space
+
+__all__ = [
+    "FormKind", "Discretization", "SparseMatrix", "gauss_rule", "make_discretization", "assemble", "assemble_device",
+    "elements_for_rows", "is_bitwise_symmetric", "matrices_bitwise_equal", "form_is_symmetric", "set_device",
+    "problem_arrays",
+]
+
+
+class FormKind(Enum):
+    """assembly.py:51-58."""
+
+    POISSON = "poisson"
+    MASS = "mass"
+    BIHARMONIC = "biharmonic"
+    STOKES_VELOCITY = "stokes_velocity"
+    STOKES_DIVERGENCE = "stokes_divergence"
+
+
+_SYMMETRIC = {"poisson": True, "mass": True, "biharmonic": True, "stokes_velocity": True, "stokes_divergence": False}
+_NATIVE_FORM = {"poisson": 0, "stokes_velocity": 0, "mass": 1, "biharmonic": 2}
+
+
+def _fname(form) -> str:
+    v = getattr(form, "value", form)
+    if v not in _SYMMETRIC:
+        raise ValueError(f"unsupported form {form!r}")
+    return v
+
+
+def form_is_symmetric(form) -> bool:
+    return _SYMMETRIC[_fname(form)]
+
+
+@dataclass(frozen=True)
+class QuadratureRule:
+    g: int
+    nodes: np.ndarray
+    weights: np.ndarray
+
+
+def gauss_rule(g: int) -> QuadratureRule:
+    """assembly.py:100-105 (numpy leggauss, same message)."""
+    if g < 1:
+        raise ValueError(f"need at least one quadrature point, got g={g}")
+    x, w = np.polynomial.legendre.leggauss(g)
+    return QuadratureRule(g=g, nodes=x, weights=w)
+
+
+def _quad_axes(kvs, g: int):
+    """assembly.py:108-117: points break_k + (x+1) h/2, weights w h/2."""
+    rule = gauss_rule(g)
+    axes, pw = [], []
+    for kv in kvs:
+        h = 1.0 / (kv.m - kv.p)
+        offs = (rule.nodes + 1.0) * (0.5 * h)
+        br = make_open_uniform_knots(kv.p, kv.m).span_breaks()[:-1]
+        axes.append(np.ascontiguousarray((br[:, None] + offs[None, :]).ravel()))
+        pw.append(np.ascontiguousarray(rule.weights * (0.5 * h)))
+    return axes, pw
+
+
+@dataclass
+class Discretization:
+    """assembly.py:132-155."""
+
+    geom: GeometryMap
+    space: TensorSpace
+    weights: NurbsWeights
+    gauss: int
+
+    @property
+    def n(self) -> int:
+        return self.space.n
+
+    @property
+    def p(self) -> int:
+        return self.space.p
+
+    @property
+    def spans(self) -> tuple:
+        return tuple(kv.spans for kv in self.space.kvs)
+
+    @property
+    def ndof(self) -> int:
+        return self.space.N
+
+
+def make_discretization(geom: GeometryMap, p: int, spans, gauss: int | None = None) -> Discretization:
+    """assembly.py:158-176."""
+    n = geom.n
+    if np.isscalar(spans):
+        spans = (int(spans),) * n
+    spans = tuple(int(s) for s in spans)
+    if len(spans) != n:
+        raise ValueError(f"need {n} span counts, got {len(spans)}")
+    space = make_tensor_space(p, [s + p for s in spans])
+    w = weights_for_space(geom, space)
+    g = int(gauss) if gauss is not None else p + 1
+    if g < 1:
+        raise ValueError("quadrature order must be positive")
+    return Discretization(geom=geom, space=space, weights=w, gauss=g)
+
+
+@dataclass
+class SparseMatrix:
+    """assembly.py:214-242: CSR (int32 indices, float64 data, sorted) + metadata."""
+
+    mat: sp.csr_matrix
+    symmetric: bool = False
+    populated_rows: np.ndarray | None = None
+
+    @property
+    def shape(self) -> tuple:
+        return self.mat.shape
+
+    @property
+    def nnz(self) -> int:
+        return self.mat.nnz
+
+    def toarray(self) -> np.ndarray:
+        return self.mat.toarray()
+
+    def row_sums(self) -> np.ndarray:
+        return np.asarray(self.mat.sum(axis=1)).ravel()
+
+    def max_abs(self) -> float:
+        return float(np.max(np.abs(self.mat.data))) if self.mat.nnz else 0.0
+
+
+def is_bitwise_symmetric(A) -> bool:
+    M = A.mat.copy()
+    M.sort_indices()
+    T = A.mat.transpose().tocsr()
+    T.sort_indices()
+    return (np.array_equal(M.indptr, T.indptr) and np.array_equal(M.indices, T.indices)
+            and np.array_equal(M.data.view(np.int64), T.data.view(np.int64)))
+
+
+def matrices_bitwise_equal(A, B, rows=None) -> bool:
+    MA, MB = A.mat, B.mat
+    if rows is not None:
+        rows = np.asarray(rows)
+        MA, MB = MA[rows], MB[rows]
+    MA = MA.tocsr().copy()
+    MB = MB.tocsr().copy()
+    MA.sort_indices()
+    MB.sort_indices()
+    return (np.array_equal(MA.indptr, MB.indptr) and np.array_equal(MA.indices, MB.indices)
+            and np.array_equal(MA.data.view(np.int64), MB.data.view(np.int64)))
+
+
+def elements_for_rows(disc, rows) -> np.ndarray:
+    """Ascending colex ids of elements supporting ``rows`` (assembly.py:347-370); separable dilation."""
+    return _elements_for_rows(tuple(kv.m for kv in disc.space.kvs), disc.space.kvs[0].p, rows)
+
+
+def _elements_for_rows(ms, p, rows) -> np.ndarray:
+    ms = tuple(ms)
+    spans = tuple(m - p for m in ms)
+    R = np.zeros(int(np.prod(ms)), dtype=bool)
+    R[np.asarray(rows, dtype=np.int64).reshape(-1)] = True
+    R = R.reshape(ms, order="F")
+    for d in range(len(ms)):
+        R = np.moveaxis(R, d, 0)
+        acc = np.zeros((spans[d],) + R.shape[1:], dtype=bool)
+        for r in range(p + 1):
+            acc |= R[r:r + spans[d]]
+        R = np.moveaxis(acc, 0, d)
+    return np.flatnonzero(R.ravel(order="F"))
+
+
+# ---------------------------------------------------------------------------------------
+# device selection
+# ---------------------------------------------------------------------------------------
+
+_DEVICE = int(os.environ.get("SURRIGA_B200_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+
+
+def set_device(dev: int) -> None:
+    global _DEVICE
+    _DEVICE = int(dev)
+
+
+# ---------------------------------------------------------------------------------------
+# problem marshalling
+# ---------------------------------------------------------------------------------------
+
+class _Keep:
+    """Keeps the numpy arrays referenced by a ctypes struct alive."""
+
+    def __init__(self):
+        self.arrays = []
+
+    def ptr(self, a):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        self.arrays.append(a)
+        return _lib.dptr(a)
+
+
+def problem_arrays(form, disc, coefficient: float = 1.0):
+    """Validate like assembly.py:596-607 and build the C ``sg_problem`` (+ keep-alive)."""
+    fname = _fname(form)
+    if fname == "stokes_divergence":
+        raise ValueError("use assemble_divergence for the mixed pairing")
+    space = disc.space
+    p = int(space.kvs[0].p)
+    if fname == "biharmonic" and p < 2:
+        raise ValueError("the fourth-order form needs degree >= 2 for C^1 continuity")
+    g = int(disc.gauss)
+    axes, pw = _quad_axes(space.kvs, g)
+    if coefficient != 1.0 and fname not in ("poisson", "stokes_velocity"):
+        raise ValueError("coefficient is only supported for the second-order forms")
+    n = len(space.kvs)
+    keep = _Keep()
+    pr = _lib.SgProblem()
+    pr.n = n
+    pr.p = p
+    pr.form = _NATIVE_FORM[fname]
+    pr.g = g
+    for d, kv in enumerate(space.kvs):
+        pr.m[d] = int(kv.m)
+        pr.knots[d] = keep.ptr(make_open_uniform_knots(p, int(kv.m)).knots)
+        pr.qpts[d] = keep.ptr(axes[d])
+        pr.qwts[d] = keep.ptr(pw[d])
+    w = np.asarray(disc.weights.weights, dtype=float)
+    pr.sol_w = None if bool(np.all(w == w[0])) else keep.ptr(w)     # weights.is_unit (assembly.py:418)
+    gs = disc.geom.space
+    pg = int(gs.kvs[0].p)
+    pr.geo_p = pg
+    for d, kv in enumerate(gs.kvs):
+        pr.geo_m[d] = int(kv.m)
+        pr.geo_knots[d] = keep.ptr(make_open_uniform_knots(pg, int(kv.m)).knots)
+    gw = np.asarray(disc.geom.weights.weights, dtype=float)
+    hom = np.concatenate([np.asarray(disc.geom.control, float) * gw[:, None], gw[:, None]], axis=1)
+    pr.geo_hom = keep.ptr(hom)
+    pr.coefficient = float(coefficient)
+    N = int(np.prod([kv.m for kv in space.kvs]))
+    return pr, keep, fname, N
+
+
+def _exec(device=None, stream=None, slab=None):
+    ex = _lib.SgExec()
+    ex.device = _DEVICE if device is None else int(device)
+    ex.stream = stream
+    if slab is not None:
+        ex.slab_lo, ex.slab_hi = int(slab[0]), int(slab[1])
+    else:
+        ex.slab_lo, ex.slab_hi = 0, 0
+    return ex
+
+
+def assemble_device(form, disc, rows=None, coefficient: float = 1.0, *, device=None, stream=None, slab=None):
+    """Assemble on the GPU and keep the CSR in HBM; returns ``(_lib.Result, symmetric, rows)``."""
+    pr, keep, fname, N = problem_arrays(form, disc, coefficient)
+    L = _lib.lib()
+    rsel = None
+    rptr, nr = None, 0
+    if rows is not None:
+        rsel = np.unique(np.asarray(rows, dtype=np.int64))
+        if rsel.size and (rsel[0] < 0 or rsel[-1] >= N):
+            raise ValueError("row index out of range")
+        rptr, nr = rsel.ctypes.data_as(_lib._i64), rsel.size
+    ex = _exec(device, stream, slab)
+    h = C.c_void_p()
+    _lib.check(L.sg_assemble(C.byref(pr), rptr, nr, C.byref(ex), C.byref(h)))
+    del keep
+    return _lib.Result(h.value), _SYMMETRIC[fname] and rows is None, rsel
+
+
+def assemble(form, disc, rows=None, coefficient: float = 1.0) -> SparseMatrix:
+    """Assemble a square Galerkin matrix, fully or for selected rows (assembly.py:579-651)."""
+    res, sym, rsel = assemble_device(form, disc, rows=rows, coefficient=coefficient)
+    indptr, indices, data = res.to_host()
+    res.free()
+    N = int(np.prod([kv.m for kv in disc.space.kvs]))
+    mat = sp.csr_matrix((data, indices, indptr), shape=(N, N))
+    mat.has_sorted_indices = True
+    return SparseMatrix(mat=mat, symmetric=sym, populated_rows=None if rows is None else rsel)

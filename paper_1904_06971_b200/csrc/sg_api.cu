@@ -1,0 +1,705 @@
+// C-ABI entry points (include/surriga_b200.h): workspace management, basis tabulation (K2),
+// analytic CSR row pointers (K1), tile planning and launch of the assembly kernel (K4),
+// result handles, transfers and checksums.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/surriga_b200.h"
+#include "sg_common.cuh"
+#include "sg_internal.h"
+
+namespace sg {
+
+// ------------------------------------------------------------------------------------------
+// errors / timing (thread local: the library is re-entrant, ctypes releases the GIL)
+// ------------------------------------------------------------------------------------------
+static thread_local std::string g_err;
+static thread_local double g_last_ms = 0.0;
+static thread_local int g_last_launches = 0;
+static thread_local std::vector<std::pair<std::string, double>> g_ktimes;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+Call::Call(const sg_exec* ex) {
+    dev = ex ? ex->device : 0;
+    cudaSetDevice(dev);
+    if (ex && ex->stream) {
+        stream = (cudaStream_t)ex->stream;
+        own_stream = false;
+    } else {
+        cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking);
+        own_stream = true;
+    }
+    static thread_local bool pool_set[64] = {false};
+    if (dev >= 0 && dev < 64 && !pool_set[dev]) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        pool_set[dev] = true;
+    }
+    cudaEventCreate(&ev0);
+    cudaEventCreate(&ev1);
+    cudaEventRecord(ev0, stream);
+    launches = 0;
+}
+
+Call::~Call() {
+    for (void* p : temps) cudaFreeAsync(p, stream);
+    for (auto& k : kev) {
+        cudaEventDestroy(k.a);
+        cudaEventDestroy(k.b);
+    }
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (own_stream) {
+        cudaStreamSynchronize(stream);
+        cudaStreamDestroy(stream);
+    }
+}
+
+void* Call::alloc(size_t bytes, bool temp) {
+    void* p = nullptr;
+    if (bytes == 0) bytes = 8;
+    if (cudaMallocAsync(&p, bytes, stream) != cudaSuccess) return nullptr;
+    if (temp) temps.push_back(p);
+    return p;
+}
+
+void* Call::upload(const void* host, size_t bytes) {
+    void* d = alloc(bytes, true);
+    if (d && host && bytes) cudaMemcpyAsync(d, host, bytes, cudaMemcpyHostToDevice, stream);
+    return d;
+}
+
+void Call::kbegin(const char* name) {
+    KEv k;
+    k.name = name;
+    cudaEventCreate(&k.a);
+    cudaEventCreate(&k.b);
+    cudaEventRecord(k.a, stream);
+    kev.push_back(k);
+    launches++;
+}
+void Call::kend() { cudaEventRecord(kev.back().b, stream); }
+
+int Call::finish() {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(-3, "CUDA launch error: %s", cudaGetErrorString(e));
+    cudaEventRecord(ev1, stream);
+    return 0;
+}
+
+void Call::record_timing() {
+    // called after the caller synchronised; collects device times
+    float ms = 0.f;
+    if (cudaEventSynchronize(ev1) == cudaSuccess && cudaEventElapsedTime(&ms, ev0, ev1) == cudaSuccess) g_last_ms = ms;
+    g_last_launches = launches;
+    g_ktimes.clear();
+    for (auto& k : kev) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, k.a, k.b);
+        g_ktimes.push_back({k.name, (double)t});
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K2: Cox-de Boor tables at many points (bspline.py:112-124), one thread per point
+// ------------------------------------------------------------------------------------------
+__global__ void tabulate_kernel(const double* __restrict__ knots, int nk, int p, const double* __restrict__ pts, int npts,
+                                int nu, int* __restrict__ span_out, double* __restrict__ tab_out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= npts) return;
+    double ders[(SG_MAX_PG + 1) * 3];
+    const int span = basis_ders(knots, nk, p, pts[i], nu, ders);
+    if (span_out) span_out[i] = span;
+    const int w = (nu + 1) * (p + 1);
+    for (int k = 0; k < w; ++k) tab_out[(long long)i * w + k] = ders[k];
+}
+
+int tabulate(Call& c, const double* d_knots, int nk, int p, const double* d_pts, int npts, int nu, int* d_span,
+             double* d_tab) {
+    if (npts <= 0) return 0;
+    c.kbegin("tabulate");
+    tabulate_kernel<<<(npts + 127) / 128, 128, 0, c.stream>>>(d_knots, nk, p, d_pts, npts, nu, d_span, d_tab);
+    c.kend();
+    return 0;
+}
+
+// ------------------------------------------------------------------------------------------
+// K1: analytic row pointers of the basis-overlap pattern.  Row i has prod_d cnt_d(i_d) columns,
+// cnt(k) = min(m-1,k+p) - max(0,k-p) + 1; the colex prefix factorises per direction.
+// ------------------------------------------------------------------------------------------
+__host__ __device__ inline int64_t cnt1d(int64_t k, int64_t m, int p) {
+    return min(m - 1, k + p) - max((int64_t)0, k - p) + 1;
+}
+__host__ __device__ inline int64_t pre1d(int64_t k, int64_t m, int p) {
+    const int64_t c = min(k, m - p);
+    int64_t s = c * (c - 1) / 2 + c * (p + 1) + (k - c) * m;
+    const int64_t t = k - 1 - p;
+    if (t >= 1) s -= t * (t + 1) / 2;
+    return s;
+}
+
+struct Dims {
+    int64_t m[3];
+    int p;
+};
+
+__global__ void indptr_full_kernel(Dims D, int64_t N, int64_t base, int64_t* __restrict__ rowstart) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > N) return;
+    if (i == N) {
+        int64_t tot = 1;
+        for (int d = 0; d < 3; ++d) tot *= pre1d(D.m[d], D.m[d], D.p);
+        rowstart[N] = tot - base;
+        return;
+    }
+    const int64_t i0 = i % D.m[0], i1 = (i / D.m[0]) % D.m[1], i2 = i / (D.m[0] * D.m[1]);
+    const int p = D.p;
+    const int64_t t0 = pre1d(D.m[0], D.m[0], p), t1 = pre1d(D.m[1], D.m[1], p);
+    rowstart[i] = pre1d(i2, D.m[2], p) * t1 * t0 +
+                  cnt1d(i2, D.m[2], p) * (pre1d(i1, D.m[1], p) * t0 + cnt1d(i1, D.m[1], p) * pre1d(i0, D.m[0], p)) - base;
+}
+
+__global__ void row_counts_kernel(Dims D, int64_t N, const uint8_t* __restrict__ mask, int64_t* __restrict__ counts) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > N) return;
+    if (i == N) { counts[N] = 0; return; }
+    const int64_t i0 = i % D.m[0], i1 = (i / D.m[0]) % D.m[1], i2 = i / (D.m[0] * D.m[1]);
+    const int p = D.p;
+    counts[i] = mask[i] ? cnt1d(i0, D.m[0], p) * cnt1d(i1, D.m[1], p) * cnt1d(i2, D.m[2], p) : 0;
+}
+
+__global__ void rebase_kernel(int64_t* a, int64_t n, int64_t sub) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) a[i] -= sub;
+}
+
+__global__ void scatter_mask_kernel(const int64_t* __restrict__ rows, int64_t n, uint8_t* __restrict__ mask) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) mask[rows[i]] = 1;
+}
+
+
+// ------------------------------------------------------------------------------------------
+// problem upload + tables
+// ------------------------------------------------------------------------------------------
+int prepare_problem(Call& c, const sg_problem* pr, DevProblem& dp) {
+    if (!pr) return fail(-1, "null problem");
+    if (pr->n < 1 || pr->n > 3) return fail(-1, "supported dimensions: 1, 2, 3");
+    if (pr->p < 1 || pr->p > SG_MAX_P) return fail(-1, "degree p=%d outside the compiled range 1..%d", pr->p, SG_MAX_P);
+    if (pr->g < 1 || pr->g > 8) return fail(-1, "gauss=%d outside the supported range 1..8", pr->g);
+    if (pr->geo_p < 1 || pr->geo_p > SG_MAX_PG) return fail(-1, "geometry degree %d unsupported", pr->geo_p);
+    if (pr->form < 0 || pr->form > 2) return fail(-1, "unknown form %d", pr->form);
+    if (pr->form == BIHARMONIC && pr->p < 2) return fail(-1, "the fourth-order form needs degree >= 2 for C^1 continuity");
+    dp.pr = *pr;
+    dp.n = pr->n;
+    dp.p = pr->p;
+    dp.g = pr->g;
+    dp.nu = form_deriv(pr->form);
+    dp.nug = geo_deriv(pr->form);
+    dp.N = 1;
+    dp.Ng = 1;
+    for (int d = 0; d < 3; ++d) {
+        if (d < pr->n) {
+            dp.m[d] = pr->m[d];
+            dp.S[d] = pr->m[d] - pr->p;
+            dp.mg[d] = pr->geo_m[d];
+            if (dp.S[d] < 1 || pr->m[d] < 2 * pr->p + 1) return fail(-1, "basis count m=%d below 2p+1=%d", pr->m[d], 2 * pr->p + 1);
+        } else {
+            dp.m[d] = 1;
+            dp.S[d] = 1;
+            dp.mg[d] = 1;
+        }
+        dp.N *= dp.m[d];
+        dp.Ng *= dp.mg[d];
+    }
+    dp.rational = pr->sol_w != nullptr;
+    // uploads
+    for (int d = 0; d < pr->n; ++d) {
+        const int npts = dp.S[d] * dp.g;
+        double* kn = (double*)c.upload(pr->knots[d], sizeof(double) * (dp.m[d] + dp.p + 1));
+        double* qp = (double*)c.upload(pr->qpts[d], sizeof(double) * npts);
+        dp.qw[d] = (double*)c.upload(pr->qwts[d], sizeof(double) * dp.g);
+        dp.B[d] = (double*)c.alloc(sizeof(double) * npts * (dp.nu + 1) * (dp.p + 1), true);
+        dp.bspan[d] = (int*)c.alloc(sizeof(int) * npts, true);
+        tabulate(c, kn, dp.m[d] + dp.p + 1, dp.p, qp, npts, dp.nu, dp.bspan[d], dp.B[d]);
+        double* gk = (double*)c.upload(pr->geo_knots[d], sizeof(double) * (dp.mg[d] + pr->geo_p + 1));
+        dp.G[d] = (double*)c.alloc(sizeof(double) * npts * (dp.nug + 1) * (pr->geo_p + 1), true);
+        dp.gspan[d] = (int*)c.alloc(sizeof(int) * npts, true);
+        tabulate(c, gk, dp.mg[d] + pr->geo_p + 1, pr->geo_p, qp, npts, dp.nug, dp.gspan[d], dp.G[d]);
+        // host copies of geometry spans for the smem bound
+        std::vector<double> hk(pr->geo_knots[d], pr->geo_knots[d] + dp.mg[d] + pr->geo_p + 1);
+        dp.hgspan[d].resize(npts);
+        for (int i = 0; i < npts; ++i)
+            dp.hgspan[d][i] = find_span(hk.data(), (int)hk.size(), pr->geo_p, pr->qpts[d][i]);
+    }
+    for (int d = pr->n; d < 3; ++d) {
+        dp.qw[d] = nullptr;
+        dp.B[d] = nullptr;
+        dp.G[d] = nullptr;
+        dp.gspan[d] = nullptr;
+        dp.hgspan[d].assign(1, 0);
+    }
+    dp.hom = (double*)c.upload(pr->geo_hom, sizeof(double) * dp.Ng * (pr->n + 1));
+    dp.sol_w = dp.rational ? (double*)c.upload(pr->sol_w, sizeof(double) * dp.N) : nullptr;
+    return 0;
+}
+
+// ------------------------------------------------------------------------------------------
+// tile planning + kernel launch
+// ------------------------------------------------------------------------------------------
+#define SG_DECL(nd, f) extern void* assemble_kernel_##nd##_##f(int p, bool rat, int* kmax);
+SG_DECL(1, 0) SG_DECL(1, 1) SG_DECL(1, 2) SG_DECL(2, 0) SG_DECL(2, 1) SG_DECL(2, 2) SG_DECL(3, 0) SG_DECL(3, 1) SG_DECL(3, 2)
+#undef SG_DECL
+
+static void* get_kernel(int n, int form, int p, bool rat, int* kmax) {
+    typedef void* (*Fn)(int, bool, int*);
+    static const Fn tab[3][3] = {{assemble_kernel_1_0, assemble_kernel_1_1, assemble_kernel_1_2},
+                                 {assemble_kernel_2_0, assemble_kernel_2_1, assemble_kernel_2_2},
+                                 {assemble_kernel_3_0, assemble_kernel_3_1, assemble_kernel_3_2}};
+    if (n < 1 || n > 3 || form < 0 || form > 2) return nullptr;
+    return tab[n - 1][form](p, rat, kmax);
+}
+
+struct Layout {
+    int T[3];
+    int ypad, GN[2];
+    size_t off[14];
+    size_t total;  // doubles
+};
+
+static Layout make_layout(const DevProblem& dp, int T0, int T1, int T2) {
+    const int n = dp.n, P = dp.p, g = dp.g;
+    const Tables TT = make_tables(n, dp.pr.form, dp.rational);
+    const int MS = TT.MS, U = MS * (MS + 1) / 2;
+    const int NU = dp.nu, NUG = dp.nug, pg = dp.pr.geo_p;
+    const int NB = (NU + 1) * (P + 1), NBG = (NUG + 1) * (pg + 1);
+    const int W2P = 2 * P + 1;
+    Layout L;
+    L.T[0] = T0;
+    L.T[1] = n >= 2 ? T1 : 1;
+    L.T[2] = n >= 3 ? T2 : 1;
+    const int X0 = (std::min(T0 + P, dp.S[0])) * g;
+    const int X1 = n >= 2 ? (std::min(L.T[1] + P, dp.S[1])) * g : 1;
+    L.ypad = n >= 2 ? (X1 | 1) : 1;
+    // geometry functions per window: max over windows of span range + pg + 1
+    for (int d = 0; d < 2; ++d) {
+        L.GN[d] = 1;
+        if (d >= n) continue;
+        const int Td = L.T[d];
+        const int tg = (dp.m[d] + Td - 1) / Td;
+        for (int t = 0; t < tg; ++t) {
+            const int b = t * Td;
+            const int lo = std::max(0, b - P), hi = std::min(dp.S[d] - 1, b + Td - 1);
+            const int s0 = dp.hgspan[d][lo * g], s1 = dp.hgspan[d][hi * g + g - 1];
+            L.GN[d] = std::max(L.GN[d], s1 - s0 + pg + 1);
+        }
+    }
+    const int C = n + 1;
+    const int NCg = n == 3 ? (NUG + 1) * (NUG + 2) / 2 : NUG + 1;
+    const int NCw = n == 3 ? (NU + 1) * (NU + 2) / 2 : NU + 1;
+    const int WN0 = L.T[0] + 2 * P, WN1 = L.T[1] + 2 * P;
+    size_t sz[14];
+    sz[0] = (size_t)X0 * NB;                                        // B0
+    sz[1] = n >= 2 ? (size_t)X1 * NB : 0;                            // B1
+    sz[2] = (size_t)X0 * NBG;                                       // G0
+    sz[3] = n >= 2 ? (size_t)X1 * NBG : 0;                           // G1
+    sz[4] = (X0 + 1) / 2 + 1;                                       // gs0 (ints)
+    sz[5] = (X1 + 1) / 2 + 1;                                       // gs1
+    sz[6] = n == 3 ? (size_t)L.GN[0] * L.GN[1] * C * (NUG + 1) : 0;  // Hz
+    sz[7] = n >= 2 ? (size_t)X1 * L.GN[0] * C * NCg : 0;             // Hy
+    sz[8] = (n == 3 && dp.rational) ? (size_t)WN0 * WN1 * (NU + 1) : 0;  // Wz
+    sz[9] = (n >= 2 && dp.rational) ? (size_t)X1 * WN0 * NCw : 0;   // Wy
+    sz[10] = (size_t)U * X0 * L.ypad;                               // D
+    sz[11] = n >= 2 ? (size_t)TT.NG1 * T0 * W2P * L.ypad : 0;       // T1
+    sz[12] = n == 3 ? (size_t)TT.NG2 * T0 * W2P * L.T[1] * W2P : 0; // T2
+    sz[13] = 24 + NB + NBG + (X0 + X1) / 2 + 4;                     // misc
+    size_t o = 0;
+    for (int k = 0; k < 14; ++k) {
+        L.off[k] = o;
+        o += sz[k];
+        o = (o + 1) & ~size_t(1);  // 16-byte alignment
+    }
+    L.total = o;
+    return L;
+}
+
+static const size_t kSmemCap = 227 * 1024;
+
+static int choose_layout(const DevProblem& dp, int kmax, int nthreads, Layout& out) {
+    const int n = dp.n, P = dp.p;
+    const int W2P = 2 * P + 1;
+    int best = -1;
+    for (int T = (n == 1 ? 256 : 16); T >= 1; --T) {
+        if (n == 1 && T > 256) continue;
+        const int T2 = n == 3 ? 16 : 1;
+        Layout L = make_layout(dp, T, T, T2);
+        if (L.total * sizeof(double) > kSmemCap) continue;
+        if (n == 3 && (size_t)T * W2P * T * W2P * (P + 1) > (size_t)kmax * nthreads) continue;
+        best = T;
+        out = L;
+        break;
+    }
+    if (best < 0) return fail(-2, "no tile configuration fits shared memory for this problem (p=%d, n=%d)", P, n);
+    return 0;
+}
+
+int launch_assembly(Call& c, DevProblem& dp, const uint8_t* d_rowmask, const int64_t* d_rowstart, const int64_t* h_rows,
+                    int64_t nrows, int64_t slab_lo, int64_t slab_hi, int* d_indices, double* d_data) {
+    int kmax = 1;
+    void* kfn = nullptr;
+    const bool rat = dp.rational;
+    kfn = get_kernel(dp.n, dp.pr.form, dp.p, rat, &kmax);
+    if (!kfn) return fail(-2, "no kernel instantiated for n=%d p=%d form=%d", dp.n, dp.p, dp.pr.form);
+    const int nthreads = 512;
+    Layout L;
+    int rc = choose_layout(dp, kmax, nthreads, L);
+    if (rc) return rc;
+    AsmParams prm;
+    memset(&prm, 0, sizeof(prm));
+    prm.n = dp.n;
+    prm.p = dp.p;
+    prm.g = dp.g;
+    for (int d = 0; d < 3; ++d) {
+        prm.m[d] = dp.m[d];
+        prm.S[d] = dp.S[d];
+        prm.B[d] = dp.B[d];
+        prm.qw[d] = dp.qw[d];
+        prm.mg[d] = dp.mg[d];
+        prm.gspan[d] = dp.gspan[d];
+        prm.G[d] = dp.G[d];
+        prm.T[d] = L.T[d];
+        prm.tgrid[d] = (dp.m[d] + L.T[d] - 1) / L.T[d];
+    }
+    prm.sol_w = dp.sol_w;
+    prm.pg = dp.pr.geo_p;
+    prm.hom = dp.hom;
+    prm.coef = dp.pr.coefficient;
+    prm.GN[0] = L.GN[0];
+    prm.GN[1] = L.GN[1];
+    prm.ypad = L.ypad;
+    int* offs[14] = {&prm.off_B0, &prm.off_B1, &prm.off_G0, &prm.off_G1, &prm.off_gs0, &prm.off_gs1, &prm.off_Hz,
+                     &prm.off_Hy, &prm.off_Wz, &prm.off_Wy, &prm.off_D, &prm.off_T1, &prm.off_T2, &prm.off_misc};
+    for (int k = 0; k < 14; ++k) *offs[k] = (int)L.off[k];
+    prm.rowmask = d_rowmask;
+    prm.rowstart = d_rowstart;
+    prm.slab_lo = slab_lo;
+    prm.slab_hi = slab_hi;
+    prm.indices = d_indices;
+    prm.data = d_data;
+
+    // tile list
+    const int64_t ntiles_all = (int64_t)prm.tgrid[0] * prm.tgrid[1] * prm.tgrid[2];
+    std::vector<int> tiles;
+    const bool full_slab = (slab_lo <= 0 && slab_hi >= dp.N);
+    if (h_rows || !full_slab) {
+        std::vector<uint8_t> mark(ntiles_all, 0);
+        auto mark_row = [&](int64_t r) {
+            const int64_t i0 = r % dp.m[0], i1 = (r / dp.m[0]) % dp.m[1], i2 = r / ((int64_t)dp.m[0] * dp.m[1]);
+            mark[(i0 / L.T[0]) + prm.tgrid[0] * ((i1 / L.T[1]) + (int64_t)prm.tgrid[1] * (i2 / L.T[2]))] = 1;
+        };
+        if (h_rows) {
+            for (int64_t k = 0; k < nrows; ++k)
+                if (h_rows[k] >= slab_lo && h_rows[k] < slab_hi) mark_row(h_rows[k]);
+        } else {
+            // slab: tiles whose row box intersects [slab_lo, slab_hi)
+            for (int64_t t = 0; t < ntiles_all; ++t) {
+                const int64_t t0 = t % prm.tgrid[0], t1 = (t / prm.tgrid[0]) % prm.tgrid[1], t2 = t / ((int64_t)prm.tgrid[0] * prm.tgrid[1]);
+                const int64_t lo = t0 * L.T[0] + dp.m[0] * (t1 * L.T[1] + (int64_t)dp.m[1] * t2 * L.T[2]);
+                const int64_t hi = std::min<int64_t>(t0 * L.T[0] + L.T[0], dp.m[0]) - 1 +
+                                   dp.m[0] * (std::min<int64_t>(t1 * L.T[1] + L.T[1], dp.m[1]) - 1 +
+                                              (int64_t)dp.m[1] * (std::min<int64_t>(t2 * L.T[2] + L.T[2], dp.m[2]) - 1));
+                if (hi >= slab_lo && lo < slab_hi) mark[t] = 1;
+            }
+        }
+        for (int64_t t = 0; t < ntiles_all; ++t)
+            if (mark[t]) tiles.push_back((int)t);
+        if (tiles.empty()) return 0;
+        prm.tiles = (const int*)c.upload(tiles.data(), sizeof(int) * tiles.size());
+    }
+    const int64_t nblocks = prm.tiles ? (int64_t)tiles.size() : ntiles_all;
+    const size_t smem = L.total * sizeof(double);
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    void* args[] = {&prm};
+    c.kbegin("assemble_tiles");
+    cudaError_t e = cudaLaunchKernel(kfn, dim3((unsigned)nblocks), dim3(nthreads), args, smem, c.stream);
+    c.kend();
+    if (e != cudaSuccess) return fail(-3, "assembly launch failed: %s (smem %zu B, %lld tiles)", cudaGetErrorString(e), smem, (long long)nblocks);
+    dp.last_tiles = nblocks;
+    dp.last_T[0] = L.T[0];
+    dp.last_T[1] = L.T[1];
+    dp.last_T[2] = L.T[2];
+    dp.last_smem = smem;
+    return 0;
+}
+
+// ------------------------------------------------------------------------------------------
+// checksum (fixed-order reduction: deterministic)
+// ------------------------------------------------------------------------------------------
+__global__ void checksum_partial(const int64_t* __restrict__ indptr, const double* __restrict__ data, int64_t nrows,
+                                 double* __restrict__ part) {
+    // part[block*5 + k]
+    __shared__ double sh[5][256];
+    double s[5] = {0, 0, 0, 0, 0};
+    const int64_t per = (nrows + gridDim.x - 1) / gridDim.x;
+    const int64_t r0 = blockIdx.x * per, r1 = min(nrows, r0 + per);
+    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+        double rs = 0.0;
+        for (int64_t k = indptr[r]; k < indptr[r + 1]; ++k) {
+            const double a = data[k];
+            s[1] += a;
+            s[2] += a * a;
+            s[3] += fabs(a);
+            rs += a;
+        }
+        s[0] += (double)(indptr[r + 1] - indptr[r]);
+        s[4] += fabs(rs);
+    }
+    for (int k = 0; k < 5; ++k) sh[k][threadIdx.x] = s[k];
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w)
+            for (int k = 0; k < 5; ++k) sh[k][threadIdx.x] += sh[k][threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        for (int k = 0; k < 5; ++k) part[blockIdx.x * 5 + k] = sh[k][0];
+}
+
+}  // namespace sg
+
+using namespace sg;
+
+// ==========================================================================================
+// C ABI
+// ==========================================================================================
+extern "C" {
+
+const char* sg_last_error(void) { return g_err.c_str(); }
+const char* sg_version(void) { return "surriga_b200 0.1.0 (sm_100a)"; }
+int sg_max_degree(void) { return SG_MAX_P; }
+
+int sg_last_timing(double* ms_total, int32_t* launches) {
+    if (ms_total) *ms_total = g_last_ms;
+    if (launches) *launches = g_last_launches;
+    return 0;
+}
+
+int sg_last_kernel_times(char* names, int32_t names_cap, double* ms, int32_t cap, int32_t* count) {
+    std::string s;
+    int k = 0;
+    for (auto& kt : g_ktimes) {
+        if (k < cap && ms) ms[k] = kt.second;
+        if (!s.empty()) s += ",";
+        s += kt.first;
+        k++;
+    }
+    if (names && names_cap > 0) {
+        strncpy(names, s.c_str(), names_cap - 1);
+        names[names_cap - 1] = 0;
+    }
+    if (count) *count = k;
+    return 0;
+}
+
+int sg_assemble(const sg_problem* prob, const int64_t* rows, int64_t nrows, const sg_exec* ex, sg_result** out) {
+    if (!out) return fail(-1, "null output handle");
+    *out = nullptr;
+    Call c(ex);
+    DevProblem dp;
+    int rc = prepare_problem(c, prob, dp);
+    if (rc) return rc;
+    int64_t slab_lo = 0, slab_hi = dp.N;
+    if (ex && ex->slab_hi > 0) {
+        slab_lo = std::max<int64_t>(0, ex->slab_lo);
+        slab_hi = std::min<int64_t>(dp.N, ex->slab_hi);
+        if (slab_lo >= slab_hi) return fail(-1, "empty row slab");
+    }
+    for (int64_t k = 0; rows && k < nrows; ++k) {
+        if (rows[k] < 0 || rows[k] >= dp.N) return fail(-1, "row index out of range");
+        if (k && rows[k] <= rows[k - 1]) return fail(-1, "rows must be sorted and unique");
+    }
+    Dims D;
+    for (int d = 0; d < 3; ++d) D.m[d] = dp.m[d];
+    D.p = dp.p;
+    sg_result* r = new sg_result();
+    r->dev = c.dev;
+    r->nrows_global = dp.N;
+    r->row_lo = slab_lo;
+    r->nrows = slab_hi - slab_lo;
+    const int64_t N = dp.N;
+    int64_t* rowstart = (int64_t*)c.alloc(sizeof(int64_t) * (N + 1), true);
+    uint8_t* mask = nullptr;
+    if (!rows) {
+        // full pattern; slab rows rebased so the slab's first entry sits at 0
+        int64_t base = 0;
+        if (slab_lo > 0) {
+            const int64_t i0 = slab_lo % dp.m[0], i1 = (slab_lo / dp.m[0]) % dp.m[1], i2 = slab_lo / ((int64_t)dp.m[0] * dp.m[1]);
+            const int64_t t0 = pre1d(dp.m[0], dp.m[0], dp.p), t1 = pre1d(dp.m[1], dp.m[1], dp.p);
+            base = pre1d(i2, dp.m[2], dp.p) * t1 * t0 +
+                   cnt1d(i2, dp.m[2], dp.p) * (pre1d(i1, dp.m[1], dp.p) * t0 + cnt1d(i1, dp.m[1], dp.p) * pre1d(i0, dp.m[0], dp.p));
+        }
+        c.kbegin("indptr_full");
+        indptr_full_kernel<<<(unsigned)((N + 1 + 255) / 256), 256, 0, c.stream>>>(D, N, base, rowstart);
+        c.kend();
+    } else {
+        mask = (uint8_t*)c.alloc(N + 1, true);
+        cudaMemsetAsync(mask, 0, N + 1, c.stream);
+        std::vector<int64_t> sel;
+        for (int64_t k = 0; k < nrows; ++k)
+            if (rows[k] >= slab_lo && rows[k] < slab_hi) sel.push_back(rows[k]);
+        if (!sel.empty()) {
+            int64_t* drows = (int64_t*)c.upload(sel.data(), sizeof(int64_t) * sel.size());
+            c.kbegin("rows_mask");
+            scatter_mask_kernel<<<(unsigned)((sel.size() + 255) / 256), 256, 0, c.stream>>>(drows, (int64_t)sel.size(), mask);
+            c.kend();
+        }
+        int64_t* counts = (int64_t*)c.alloc(sizeof(int64_t) * (N + 1), true);
+        c.kbegin("row_counts");
+        row_counts_kernel<<<(unsigned)((N + 1 + 255) / 256), 256, 0, c.stream>>>(D, N, mask, counts);
+        c.kend();
+        size_t tmp_bytes = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, rowstart, N + 1, c.stream);
+        void* tmp = c.alloc(tmp_bytes, true);
+        c.kbegin("row_scan");
+        cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, rowstart, N + 1, c.stream);
+        c.kend();
+    }
+    // nnz of this result
+    int64_t nnz_lo = 0, nnz_hi = 0;
+    cudaMemcpyAsync(&nnz_lo, rowstart + slab_lo, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream);
+    cudaMemcpyAsync(&nnz_hi, rowstart + slab_hi, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream);
+    cudaStreamSynchronize(c.stream);
+    r->nnz = nnz_hi - nnz_lo;
+    // result arrays (owned by the handle)
+    r->indptr = (int64_t*)c.alloc(sizeof(int64_t) * (r->nrows + 1), false);
+    r->indices = (int*)c.alloc(sizeof(int) * std::max<int64_t>(r->nnz, 1), false);
+    r->data = (double*)c.alloc(sizeof(double) * std::max<int64_t>(r->nnz, 1), false);
+    if (!r->indptr || !r->indices || !r->data) {
+        delete r;
+        return fail(-4, "device allocation failed (nnz=%lld)", (long long)(nnz_hi - nnz_lo));
+    }
+    // rowstart relative to the slab start -> write positions directly into the result arrays
+    if (nnz_lo != 0) {
+        // shift: rowstart -= nnz_lo (only for rows of this slab; others are skipped by the kernel)
+        c.kbegin("rebase");
+        rebase_kernel<<<(unsigned)((N + 1 + 255) / 256), 256, 0, c.stream>>>(rowstart, N + 1, nnz_lo);
+        c.kend();
+    }
+    cudaMemcpyAsync(r->indptr, rowstart + slab_lo, sizeof(int64_t) * (r->nrows + 1), cudaMemcpyDeviceToDevice, c.stream);
+    if (r->nnz > 0) {
+        rc = launch_assembly(c, dp, mask, rowstart, rows, nrows, slab_lo, slab_hi, r->indices, r->data);
+        if (rc) {
+            sg_result_free(r);
+            return rc;
+        }
+    }
+    r->stream_hint = nullptr;
+    rc = c.finish();
+    if (rc) {
+        sg_result_free(r);
+        return rc;
+    }
+    cudaStreamSynchronize(c.stream);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        sg_result_free(r);
+        return fail(-3, "CUDA error after assembly: %s", cudaGetErrorString(e));
+    }
+    c.record_timing();
+    r->tiles = dp.last_tiles;
+    *out = r;
+    return 0;
+}
+
+int sg_result_sizes(const sg_result* r, int64_t* nrows, int64_t* nnz) {
+    if (!r) return fail(-1, "null result");
+    if (nrows) *nrows = r->nrows;
+    if (nnz) *nnz = r->nnz;
+    return 0;
+}
+
+int sg_result_copy_i64(const sg_result* r, int64_t* indptr, int32_t* indices, double* data) {
+    if (!r) return fail(-1, "null result");
+    cudaSetDevice(r->dev);
+    if (indptr && cudaMemcpy(indptr, r->indptr, sizeof(int64_t) * (r->nrows + 1), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return fail(-3, "indptr copy failed");
+    if (r->nnz > 0) {
+        if (indices && cudaMemcpy(indices, r->indices, sizeof(int32_t) * r->nnz, cudaMemcpyDeviceToHost) != cudaSuccess)
+            return fail(-3, "indices copy failed");
+        if (data && cudaMemcpy(data, r->data, sizeof(double) * r->nnz, cudaMemcpyDeviceToHost) != cudaSuccess)
+            return fail(-3, "data copy failed");
+    }
+    return 0;
+}
+
+int sg_result_copy(const sg_result* r, int32_t* indptr, int32_t* indices, double* data) {
+    if (!r) return fail(-1, "null result");
+    if (r->nnz >= INT32_MAX) return fail(-1, "nnz exceeds int32; use sg_result_copy_i64");
+    std::vector<int64_t> ip(r->nrows + 1);
+    int rc = sg_result_copy_i64(r, ip.data(), indices, data);
+    if (rc) return rc;
+    if (indptr)
+        for (int64_t k = 0; k <= r->nrows; ++k) indptr[k] = (int32_t)ip[k];
+    return 0;
+}
+
+int sg_result_device_ptrs(const sg_result* r, void** indptr_i64, void** indices_i32, void** data_f64) {
+    if (!r) return fail(-1, "null result");
+    if (indptr_i64) *indptr_i64 = r->indptr;
+    if (indices_i32) *indices_i32 = r->indices;
+    if (data_f64) *data_f64 = r->data;
+    return 0;
+}
+
+int sg_result_checksum(const sg_result* r, double out[5]) {
+    if (!r) return fail(-1, "null result");
+    cudaSetDevice(r->dev);
+    const int nb = 256;
+    double* part = nullptr;
+    cudaMalloc(&part, sizeof(double) * nb * 5);
+    if (r->nrows > 0) checksum_partial<<<nb, 256>>>(r->indptr, r->data, r->nrows, part);
+    else cudaMemset(part, 0, sizeof(double) * nb * 5);
+    std::vector<double> h(nb * 5);
+    cudaMemcpy(h.data(), part, sizeof(double) * nb * 5, cudaMemcpyDeviceToHost);
+    cudaFree(part);
+    for (int k = 0; k < 5; ++k) {
+        double s = 0.0;
+        for (int b = 0; b < nb; ++b) s += h[b * 5 + k];
+        out[k] = s;
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(-3, "checksum failed: %s", cudaGetErrorString(e));
+    return 0;
+}
+
+int sg_result_free(sg_result* r) {
+    if (!r) return 0;
+    cudaSetDevice(r->dev);
+    cudaDeviceSynchronize();
+    if (r->indptr) cudaFreeAsync(r->indptr, 0);
+    if (r->indices) cudaFreeAsync(r->indices, 0);
+    if (r->data) cudaFreeAsync(r->data, 0);
+    cudaStreamSynchronize(0);
+    delete r;
+    return 0;
+}
+
+}  // extern "C"

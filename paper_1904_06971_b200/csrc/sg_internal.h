@@ -1,0 +1,78 @@
+// Internal host-side structures shared by the C-ABI translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/surriga_b200.h"
+
+struct sg_result {
+    int dev = 0;
+    int64_t nrows = 0;         // rows held (slab)
+    int64_t nrows_global = 0;  // N of the matrix
+    int64_t row_lo = 0;        // first global row held
+    int64_t nnz = 0;
+    int64_t* indptr = nullptr;  // device, nrows+1 (relative to this result)
+    int* indices = nullptr;     // device
+    double* data = nullptr;     // device
+    int64_t tiles = 0;
+    void* stream_hint = nullptr;
+};
+
+namespace sg {
+
+int fail(int code, const char* fmt, ...);
+
+// One API call: stream, stream-ordered temporaries, per-kernel event timing.
+struct Call {
+    int dev = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::vector<void*> temps;
+    struct KEv {
+        std::string name;
+        cudaEvent_t a, b;
+    };
+    std::vector<KEv> kev;
+    int launches = 0;
+    explicit Call(const sg_exec* ex);
+    ~Call();
+    void* alloc(size_t bytes, bool temp);
+    void* upload(const void* host, size_t bytes);
+    void kbegin(const char* name);
+    void kend();
+    int finish();
+    void record_timing();
+};
+
+struct DevProblem {
+    sg_problem pr;
+    int n = 0, p = 0, g = 0, nu = 0, nug = 0;
+    int m[3], S[3], mg[3];
+    int64_t N = 0, Ng = 0;
+    bool rational = false;
+    double* B[3];
+    int* bspan[3];
+    double* qw[3];
+    double* G[3];
+    int* gspan[3];
+    std::vector<int> hgspan[3];
+    double* hom = nullptr;
+    double* sol_w = nullptr;
+    int64_t last_tiles = 0;
+    int last_T[3];
+    size_t last_smem = 0;
+};
+
+int prepare_problem(Call& c, const sg_problem* pr, DevProblem& dp);
+int launch_assembly(Call& c, DevProblem& dp, const uint8_t* d_rowmask, const int64_t* d_rowstart, const int64_t* h_rows,
+                    int64_t nrows, int64_t slab_lo, int64_t slab_hi, int* d_indices, double* d_data);
+int tabulate(Call& c, const double* d_knots, int nk, int p, const double* d_pts, int npts, int nu, int* d_span,
+             double* d_tab);
+
+__global__ void rebase_kernel(int64_t* a, int64_t n, int64_t sub);
+
+}  // namespace sg
