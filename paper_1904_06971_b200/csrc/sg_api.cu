@@ -145,17 +145,6 @@ int tabulate(Call& c, const double* d_knots, int nk, int p, const double* d_pts,
 // K1: analytic row pointers of the basis-overlap pattern.  Row i has prod_d cnt_d(i_d) columns,
 // cnt(k) = min(m-1,k+p) - max(0,k-p) + 1; the colex prefix factorises per direction.
 // ------------------------------------------------------------------------------------------
-__host__ __device__ inline int64_t cnt1d(int64_t k, int64_t m, int p) {
-    return min(m - 1, k + p) - max((int64_t)0, k - p) + 1;
-}
-__host__ __device__ inline int64_t pre1d(int64_t k, int64_t m, int p) {
-    const int64_t c = min(k, m - p);
-    int64_t s = c * (c - 1) / 2 + c * (p + 1) + (k - c) * m;
-    const int64_t t = k - 1 - p;
-    if (t >= 1) s -= t * (t + 1) / 2;
-    return s;
-}
-
 struct Dims {
     int64_t m[3];
     int p;
@@ -196,6 +185,15 @@ __global__ void scatter_mask_kernel(const int64_t* __restrict__ rows, int64_t n,
     if (i < n) mask[rows[i]] = 1;
 }
 
+
+void launch_indptr_full(Call& c, const DevProblem& dp, int64_t base, int64_t* rowstart) {
+    Dims D;
+    for (int d = 0; d < 3; ++d) D.m[d] = dp.m[d];
+    D.p = dp.p;
+    c.kbegin("indptr_full");
+    indptr_full_kernel<<<(unsigned)((dp.N + 1 + 255) / 256), 256, 0, c.stream>>>(D, dp.N, base, rowstart);
+    c.kend();
+}
 
 // ------------------------------------------------------------------------------------------
 // problem upload + tables
@@ -361,17 +359,42 @@ static int choose_layout(const DevProblem& dp, int kmax, int nthreads, Layout& o
     return 0;
 }
 
-int launch_assembly(Call& c, DevProblem& dp, const uint8_t* d_rowmask, const int64_t* d_rowstart, const int64_t* h_rows,
-                    int64_t nrows, int64_t slab_lo, int64_t slab_hi, int* d_indices, double* d_data) {
-    int kmax = 1;
-    void* kfn = nullptr;
-    const bool rat = dp.rational;
-    kfn = get_kernel(dp.n, dp.pr.form, dp.p, rat, &kmax);
-    if (!kfn) return fail(-2, "no kernel instantiated for n=%d p=%d form=%d", dp.n, dp.p, dp.pr.form);
-    const int nthreads = 512;
+int plan_assembly(DevProblem& dp, Plan& pl) {
+    pl.kfn = get_kernel(dp.n, dp.pr.form, dp.p, dp.rational, &pl.kmax);
+    if (!pl.kfn) return fail(-2, "no kernel instantiated for n=%d p=%d form=%d", dp.n, dp.p, dp.pr.form);
+    pl.nthreads = 512;
     Layout L;
-    int rc = choose_layout(dp, kmax, nthreads, L);
+    int rc = choose_layout(dp, pl.kmax, pl.nthreads, L);
     if (rc) return rc;
+    for (int d = 0; d < 3; ++d) {
+        pl.T[d] = L.T[d];
+        pl.tgrid[d] = (dp.m[d] + L.T[d] - 1) / L.T[d];
+    }
+    pl.ypad = L.ypad;
+    pl.GN[0] = L.GN[0];
+    pl.GN[1] = L.GN[1];
+    for (int k = 0; k < 14; ++k) pl.off[k] = (int)L.off[k];
+    pl.smem = L.total * sizeof(double);
+    pl.ntiles = (int64_t)pl.tgrid[0] * pl.tgrid[1] * pl.tgrid[2];
+    return 0;
+}
+
+void tile_box(const Plan& pl, const DevProblem& dp, int64_t t, int64_t lo[3], int64_t hi[3]) {
+    int64_t tc[3] = {t % pl.tgrid[0], (t / pl.tgrid[0]) % pl.tgrid[1], t / ((int64_t)pl.tgrid[0] * pl.tgrid[1])};
+    for (int d = 0; d < 3; ++d) {
+        lo[d] = tc[d] * pl.T[d];
+        hi[d] = std::min<int64_t>(lo[d] + pl.T[d], dp.m[d]) - 1;
+    }
+}
+
+int64_t tile_of_row(const Plan& pl, const DevProblem& dp, int64_t r) {
+    const int64_t i0 = r % dp.m[0], i1 = (r / dp.m[0]) % dp.m[1], i2 = r / ((int64_t)dp.m[0] * dp.m[1]);
+    return (i0 / pl.T[0]) + pl.tgrid[0] * ((i1 / pl.T[1]) + (int64_t)pl.tgrid[1] * (i2 / pl.T[2]));
+}
+
+int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* tiles, const uint8_t* d_rowmask,
+                 const int64_t* d_rowstart, int64_t slab_lo, int64_t slab_hi, int* d_indices, double* d_data,
+                 unsigned long long* d_zeros) {
     AsmParams prm;
     memset(&prm, 0, sizeof(prm));
     prm.n = dp.n;
@@ -385,69 +408,67 @@ int launch_assembly(Call& c, DevProblem& dp, const uint8_t* d_rowmask, const int
         prm.mg[d] = dp.mg[d];
         prm.gspan[d] = dp.gspan[d];
         prm.G[d] = dp.G[d];
-        prm.T[d] = L.T[d];
-        prm.tgrid[d] = (dp.m[d] + L.T[d] - 1) / L.T[d];
+        prm.T[d] = pl.T[d];
+        prm.tgrid[d] = pl.tgrid[d];
     }
     prm.sol_w = dp.sol_w;
     prm.pg = dp.pr.geo_p;
     prm.hom = dp.hom;
     prm.coef = dp.pr.coefficient;
-    prm.GN[0] = L.GN[0];
-    prm.GN[1] = L.GN[1];
-    prm.ypad = L.ypad;
+    prm.GN[0] = pl.GN[0];
+    prm.GN[1] = pl.GN[1];
+    prm.ypad = pl.ypad;
     int* offs[14] = {&prm.off_B0, &prm.off_B1, &prm.off_G0, &prm.off_G1, &prm.off_gs0, &prm.off_gs1, &prm.off_Hz,
                      &prm.off_Hy, &prm.off_Wz, &prm.off_Wy, &prm.off_D, &prm.off_T1, &prm.off_T2, &prm.off_misc};
-    for (int k = 0; k < 14; ++k) *offs[k] = (int)L.off[k];
+    for (int k = 0; k < 14; ++k) *offs[k] = pl.off[k];
     prm.rowmask = d_rowmask;
     prm.rowstart = d_rowstart;
     prm.slab_lo = slab_lo;
     prm.slab_hi = slab_hi;
     prm.indices = d_indices;
     prm.data = d_data;
-
-    // tile list
-    const int64_t ntiles_all = (int64_t)prm.tgrid[0] * prm.tgrid[1] * prm.tgrid[2];
-    std::vector<int> tiles;
-    const bool full_slab = (slab_lo <= 0 && slab_hi >= dp.N);
-    if (h_rows || !full_slab) {
-        std::vector<uint8_t> mark(ntiles_all, 0);
-        auto mark_row = [&](int64_t r) {
-            const int64_t i0 = r % dp.m[0], i1 = (r / dp.m[0]) % dp.m[1], i2 = r / ((int64_t)dp.m[0] * dp.m[1]);
-            mark[(i0 / L.T[0]) + prm.tgrid[0] * ((i1 / L.T[1]) + (int64_t)prm.tgrid[1] * (i2 / L.T[2]))] = 1;
-        };
-        if (h_rows) {
-            for (int64_t k = 0; k < nrows; ++k)
-                if (h_rows[k] >= slab_lo && h_rows[k] < slab_hi) mark_row(h_rows[k]);
-        } else {
-            // slab: tiles whose row box intersects [slab_lo, slab_hi)
-            for (int64_t t = 0; t < ntiles_all; ++t) {
-                const int64_t t0 = t % prm.tgrid[0], t1 = (t / prm.tgrid[0]) % prm.tgrid[1], t2 = t / ((int64_t)prm.tgrid[0] * prm.tgrid[1]);
-                const int64_t lo = t0 * L.T[0] + dp.m[0] * (t1 * L.T[1] + (int64_t)dp.m[1] * t2 * L.T[2]);
-                const int64_t hi = std::min<int64_t>(t0 * L.T[0] + L.T[0], dp.m[0]) - 1 +
-                                   dp.m[0] * (std::min<int64_t>(t1 * L.T[1] + L.T[1], dp.m[1]) - 1 +
-                                              (int64_t)dp.m[1] * (std::min<int64_t>(t2 * L.T[2] + L.T[2], dp.m[2]) - 1));
-                if (hi >= slab_lo && lo < slab_hi) mark[t] = 1;
-            }
-        }
-        for (int64_t t = 0; t < ntiles_all; ++t)
-            if (mark[t]) tiles.push_back((int)t);
-        if (tiles.empty()) return 0;
-        prm.tiles = (const int*)c.upload(tiles.data(), sizeof(int) * tiles.size());
+    prm.zeros = d_zeros;
+    int64_t nblocks = pl.ntiles;
+    if (tiles) {
+        if (tiles->empty()) return 0;
+        prm.tiles = (const int*)c.upload(tiles->data(), sizeof(int) * tiles->size());
+        nblocks = (int64_t)tiles->size();
     }
-    const int64_t nblocks = prm.tiles ? (int64_t)tiles.size() : ntiles_all;
-    const size_t smem = L.total * sizeof(double);
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(pl.kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
     void* args[] = {&prm};
     c.kbegin("assemble_tiles");
-    cudaError_t e = cudaLaunchKernel(kfn, dim3((unsigned)nblocks), dim3(nthreads), args, smem, c.stream);
+    cudaError_t e = cudaLaunchKernel(pl.kfn, dim3((unsigned)nblocks), dim3(pl.nthreads), args, pl.smem, c.stream);
     c.kend();
-    if (e != cudaSuccess) return fail(-3, "assembly launch failed: %s (smem %zu B, %lld tiles)", cudaGetErrorString(e), smem, (long long)nblocks);
+    if (e != cudaSuccess)
+        return fail(-3, "assembly launch failed: %s (smem %zu B, %lld tiles)", cudaGetErrorString(e), pl.smem, (long long)nblocks);
     dp.last_tiles = nblocks;
-    dp.last_T[0] = L.T[0];
-    dp.last_T[1] = L.T[1];
-    dp.last_T[2] = L.T[2];
-    dp.last_smem = smem;
     return 0;
+}
+
+int launch_assembly(Call& c, DevProblem& dp, const uint8_t* d_rowmask, const int64_t* d_rowstart, const int64_t* h_rows,
+                    int64_t nrows, int64_t slab_lo, int64_t slab_hi, int* d_indices, double* d_data) {
+    Plan pl;
+    int rc = plan_assembly(dp, pl);
+    if (rc) return rc;
+    const bool full_slab = (slab_lo <= 0 && slab_hi >= dp.N);
+    if (!h_rows && full_slab) return run_assembly(c, dp, pl, nullptr, d_rowmask, d_rowstart, slab_lo, slab_hi, d_indices, d_data, nullptr);
+    std::vector<uint8_t> mark(pl.ntiles, 0);
+    if (h_rows) {
+        for (int64_t k = 0; k < nrows; ++k)
+            if (h_rows[k] >= slab_lo && h_rows[k] < slab_hi) mark[tile_of_row(pl, dp, h_rows[k])] = 1;
+    } else {
+        for (int64_t t = 0; t < pl.ntiles; ++t) {
+            int64_t lo[3], hi[3];
+            tile_box(pl, dp, t, lo, hi);
+            const int64_t flo = lo[0] + dp.m[0] * (lo[1] + (int64_t)dp.m[1] * lo[2]);
+            const int64_t fhi = hi[0] + dp.m[0] * (hi[1] + (int64_t)dp.m[1] * hi[2]);
+            if (fhi >= slab_lo && flo < slab_hi) mark[t] = 1;
+        }
+    }
+    std::vector<int> tiles;
+    for (int64_t t = 0; t < pl.ntiles; ++t)
+        if (mark[t]) tiles.push_back((int)t);
+    return run_assembly(c, dp, pl, &tiles, d_rowmask, d_rowstart, slab_lo, slab_hi, d_indices, d_data, nullptr);
 }
 
 // ------------------------------------------------------------------------------------------

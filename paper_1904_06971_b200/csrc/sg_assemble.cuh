@@ -536,6 +536,7 @@ __global__ void __launch_bounds__(512, 1) assemble_tiles(const AsmParams prm) {
                                 if constexpr (RAT) v = v * (si * prm.sol_w[j0]);
                                 prm.data[base + (j0 - lo)] = v;
                                 prm.indices[base + (j0 - lo)] = j0;
+                                if (prm.zeros && v == 0.0) atomicAdd(prm.zeros, 1ull);
                             }
                         }
                     } else {
@@ -633,6 +634,7 @@ __global__ void __launch_bounds__(512, 1) assemble_tiles(const AsmParams prm) {
                                     const int64_t pos = base + (j0 - lo0) + (int64_t)cnt0 * (j1 - lo1);
                                     prm.data[pos] = v;
                                     prm.indices[pos] = (int)col;
+                                    if (prm.zeros && v == 0.0) atomicAdd(prm.zeros, 1ull);
                                 }
                             }
                         }
@@ -715,6 +717,7 @@ __global__ void __launch_bounds__(512, 1) assemble_tiles(const AsmParams prm) {
                     const int64_t col = (int64_t)j0 + (int64_t)prm.m[0] * ((int64_t)j1 + (int64_t)prm.m[1] * j2);
                     if (e2 == last) {
                         if constexpr (RAT) v = v * (si * prm.sol_w[col]);
+                        if (prm.zeros && v == 0.0) atomicAdd(prm.zeros, 1ull);
                     }
                     if (e2 == first) prm.indices[pos] = (int)col;
                     prm.data[pos] = v;

@@ -98,6 +98,23 @@ __host__ __device__ inline int basis_ders(const double* knots, int nknots, int p
     return span;
 }
 
+// CSR pattern counts: row k of a 1D factor couples columns [max(0,k-p), min(m-1,k+p)];
+// pre1d(k) = sum_{k'<k} cnt1d(k') in closed form.  (The colex prefix factorises per direction.)
+__host__ __device__ inline int64_t cnt1d(int64_t k, int64_t m, int p) {
+    const int64_t hi = (m - 1 < k + p) ? m - 1 : k + p;
+    const int64_t lo = (k - p > 0) ? k - p : 0;
+    return hi - lo + 1;
+}
+__host__ __device__ inline int64_t pre1d(int64_t k, int64_t m, int p) {
+    // sum_{k'<k} [min(m-1, k'+p) - max(0, k'-p) + 1], valid for any m >= 1 (also degenerate m=1 axes)
+    int64_t c = m - 1 - p;
+    c = c < 0 ? 0 : (c > k ? k : c);
+    int64_t s = c * (c - 1) / 2 + c * p + (k - c) * (m - 1) + k;
+    const int64_t t = k - 1 - p;
+    if (t >= 1) s -= t * (t + 1) / 2;
+    return s;
+}
+
 // ---------------------------------------------------------------------------------------------
 // Form algebra.  Every square form is written as
 //     A_ij = s_i s_j  sum_q  sum_{mu,nu in Mset} D_{mu nu}(q) d^mu B_i(q) d^nu B_j(q)
@@ -297,6 +314,7 @@ struct AsmParams {
     int64_t slab_lo, slab_hi;    // owned row range (colex flat); rows outside are skipped
     int* indices;
     double* data;
+    unsigned long long* zeros;   // optional: count of exact zeros written (surrogate merge check)
 };
 
 }  // namespace sg

@@ -67,7 +67,22 @@ struct DevProblem {
     size_t last_smem = 0;
 };
 
+struct Plan {
+    void* kfn = nullptr;
+    int kmax = 1, nthreads = 512;
+    int T[3], tgrid[3], ypad, GN[2], off[14];
+    size_t smem = 0;
+    int64_t ntiles = 0;
+};
+
 int prepare_problem(Call& c, const sg_problem* pr, DevProblem& dp);
+int plan_assembly(DevProblem& dp, Plan& pl);
+void tile_box(const Plan& pl, const DevProblem& dp, int64_t t, int64_t lo[3], int64_t hi[3]);
+int64_t tile_of_row(const Plan& pl, const DevProblem& dp, int64_t r);
+int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* tiles, const uint8_t* d_rowmask,
+                 const int64_t* d_rowstart, int64_t slab_lo, int64_t slab_hi, int* d_indices, double* d_data,
+                 unsigned long long* d_zeros);
+void launch_indptr_full(Call& c, const DevProblem& dp, int64_t base, int64_t* rowstart);
 int launch_assembly(Call& c, DevProblem& dp, const uint8_t* d_rowmask, const int64_t* d_rowstart, const int64_t* h_rows,
                     int64_t nrows, int64_t slab_lo, int64_t slab_hi, int* d_indices, double* d_data);
 int tabulate(Call& c, const double* d_knots, int nk, int p, const double* d_pts, int npts, int nu, int* d_span,

@@ -1,0 +1,65 @@
+"""GPU parity of the surrogate assembly against the reference's golden vectors and the oracle."""
+import numpy as np
+import pytest
+
+from golden_io import cases, load, oracle_problem
+from gpu_util import disc_from_golden, form_of
+from oracle import surriga_oracle as O
+
+TOL = 1e-12
+SURR = [c for c in cases() if load(c)[0]["kind"] == "surrogate"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", SURR)
+def test_gpu_surrogate_matches_reference_golden(case):
+    import paper_1904_06971_b200 as pkg
+
+    meta, arr = load(case)
+    disc = disc_from_golden(meta, arr)
+    mode = None if meta["mode"] is None else pkg.SurrogateMode(meta["mode"])
+    A, rep = pkg.build_surrogate_matrix(form_of(meta), disc, pkg.ConstantSampling(meta["M"]), q=meta["q"], mode=mode)
+    m = A.mat
+    assert m.indptr.dtype == np.int32 and m.indices.dtype == np.int32
+    assert np.array_equal(m.indptr, arr["indptr"]), "indptr differs"
+    assert np.array_equal(m.indices, arr["indices"]), "indices differ"
+    err = O.row_scaled_error(arr["indptr"], arr["indices"], arr["data"], m.indptr, m.indices, m.data)
+    assert err <= TOL, err
+    assert A.symmetric == meta["symmetric"]
+    for k, v in meta["report"].items():
+        assert getattr(rep, k) == v, (k, getattr(rep, k), v)
+    if A.symmetric:
+        assert pkg.is_bitwise_symmetric(A)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("M,mode", [(1, None), (3, "general"), (5, None), (2, "symmetric")])
+def test_gpu_surrogate_vs_oracle_3d(M, mode):
+    import paper_1904_06971_b200 as pkg
+
+    disc = pkg.make_discretization(pkg.twisted_cube_standin(), 2, (12, 13, 14))
+    fk = pkg.FormKind.POISSON
+    md = None if mode is None else pkg.SurrogateMode(mode)
+    A, rep = pkg.build_surrogate_matrix(fk, disc, pkg.ConstantSampling(M), mode=md)
+    (ip, ix, d), sym, r2 = O.surrogate(O.problem_from_disc(fk, disc), M, 3, mode)
+    m = A.mat
+    assert np.array_equal(m.indptr, ip) and np.array_equal(m.indices, ix)
+    assert O.row_scaled_error(ip, ix, d, m.indptr, m.indices, m.data) <= TOL
+    assert rep.interp_entries == r2["interp_entries"] and rep.active_elements == r2["active_elements"]
+    if M == 1:
+        full = pkg.assemble(fk, disc)
+        assert pkg.matrices_bitwise_equal(full, A)
+
+
+@pytest.mark.gpu
+def test_gpu_surrogate_skp_kernel_and_symmetry():
+    # SPEC acceptance 7: SKP -> A 1 = 0 to 1e-12 ||A||, bitwise symmetric; GENERAL breaks the kernel
+    import paper_1904_06971_b200 as pkg
+
+    disc = pkg.make_discretization(pkg.builtin_domain("coons_rational"), 2, (40, 40))
+    A, _ = pkg.build_surrogate_matrix(pkg.FormKind.POISSON, disc, pkg.ConstantSampling(5))
+    assert pkg.is_bitwise_symmetric(A)
+    assert np.max(np.abs(A.row_sums())) <= 1e-12 * A.max_abs()
+    G, _ = pkg.build_surrogate_matrix(pkg.FormKind.POISSON, disc, pkg.ConstantSampling(5),
+                                      mode=pkg.SurrogateMode.GENERAL)
+    assert np.max(np.abs(G.row_sums())) > 1e-10 * G.max_abs()
