@@ -12,6 +12,7 @@
 
 #include "../../include/surriga_b200.h"
 #include "sg_common.cuh"
+#include "sg_geom.cuh"
 #include "sg_internal.h"
 
 namespace sg {
@@ -60,7 +61,8 @@ Call::Call(const sg_exec* ex) {
 }
 
 Call::~Call() {
-    for (void* p : temps) cudaFreeAsync(p, stream);
+    for (void* p : temps)
+        if (p) cudaFreeAsync(p, stream);
     for (auto& k : kev) {
         cudaEventDestroy(k.a);
         cudaEventDestroy(k.b);
@@ -79,6 +81,11 @@ void* Call::alloc(size_t bytes, bool temp) {
     if (cudaMallocAsync(&p, bytes, stream) != cudaSuccess) return nullptr;
     if (temp) temps.push_back(p);
     return p;
+}
+
+void Call::release(void* p) {
+    for (auto& t : temps)
+        if (t == p) t = nullptr;
 }
 
 void* Call::upload(const void* host, size_t bytes) {
@@ -278,17 +285,16 @@ static void* get_kernel(int n, int form, int p, bool rat, int* kmax) {
 
 struct Layout {
     int T[3];
-    int ypad, GN[2];
-    size_t off[14];
-    size_t total;  // doubles
+    int ypad;
+    size_t off[6];  // B0, B1, D, T1, T2, misc
+    size_t total;   // doubles
 };
 
 static Layout make_layout(const DevProblem& dp, int T0, int T1, int T2) {
     const int n = dp.n, P = dp.p, g = dp.g;
     const Tables TT = make_tables(n, dp.pr.form, dp.rational);
     const int MS = TT.MS, U = MS * (MS + 1) / 2;
-    const int NU = dp.nu, NUG = dp.nug, pg = dp.pr.geo_p;
-    const int NB = (NU + 1) * (P + 1), NBG = (NUG + 1) * (pg + 1);
+    const int NB = (dp.nu + 1) * (P + 1);
     const int W2P = 2 * P + 1;
     Layout L;
     L.T[0] = T0;
@@ -297,43 +303,18 @@ static Layout make_layout(const DevProblem& dp, int T0, int T1, int T2) {
     const int X0 = (std::min(T0 + P, dp.S[0])) * g;
     const int X1 = n >= 2 ? (std::min(L.T[1] + P, dp.S[1])) * g : 1;
     L.ypad = n >= 2 ? (X1 | 1) : 1;
-    // geometry functions per window: max over windows of span range + pg + 1
-    for (int d = 0; d < 2; ++d) {
-        L.GN[d] = 1;
-        if (d >= n) continue;
-        const int Td = L.T[d];
-        const int tg = (dp.m[d] + Td - 1) / Td;
-        for (int t = 0; t < tg; ++t) {
-            const int b = t * Td;
-            const int lo = std::max(0, b - P), hi = std::min(dp.S[d] - 1, b + Td - 1);
-            const int s0 = dp.hgspan[d][lo * g], s1 = dp.hgspan[d][hi * g + g - 1];
-            L.GN[d] = std::max(L.GN[d], s1 - s0 + pg + 1);
-        }
-    }
-    const int C = n + 1;
-    const int NCg = n == 3 ? (NUG + 1) * (NUG + 2) / 2 : NUG + 1;
-    const int NCw = n == 3 ? (NU + 1) * (NU + 2) / 2 : NU + 1;
-    const int WN0 = L.T[0] + 2 * P, WN1 = L.T[1] + 2 * P;
-    size_t sz[14];
-    sz[0] = (size_t)X0 * NB;                                        // B0
-    sz[1] = n >= 2 ? (size_t)X1 * NB : 0;                            // B1
-    sz[2] = (size_t)X0 * NBG;                                       // G0
-    sz[3] = n >= 2 ? (size_t)X1 * NBG : 0;                           // G1
-    sz[4] = (X0 + 1) / 2 + 1;                                       // gs0 (ints)
-    sz[5] = (X1 + 1) / 2 + 1;                                       // gs1
-    sz[6] = n == 3 ? (size_t)L.GN[0] * L.GN[1] * C * (NUG + 1) : 0;  // Hz
-    sz[7] = n >= 2 ? (size_t)X1 * L.GN[0] * C * NCg : 0;             // Hy
-    sz[8] = (n == 3 && dp.rational) ? (size_t)WN0 * WN1 * (NU + 1) : 0;  // Wz
-    sz[9] = (n >= 2 && dp.rational) ? (size_t)X1 * WN0 * NCw : 0;   // Wy
-    sz[10] = (size_t)U * X0 * L.ypad;                               // D
-    sz[11] = n >= 2 ? (size_t)TT.NG1 * T0 * W2P * L.ypad : 0;       // T1
-    sz[12] = n == 3 ? (size_t)TT.NG2 * T0 * W2P * L.T[1] * W2P : 0; // T2
-    sz[13] = 24 + NB + NBG + (X0 + X1) / 2 + 4;                     // misc
+    size_t sz[6];
+    sz[0] = (size_t)X0 * NB;
+    sz[1] = n >= 2 ? (size_t)X1 * NB : 0;
+    sz[2] = (size_t)U * X0 * L.ypad;
+    sz[3] = n >= 2 ? (size_t)TT.NG1 * T0 * W2P * L.ypad : 0;
+    sz[4] = n == 3 ? (size_t)TT.NG2 * T0 * W2P * L.T[1] * W2P : 0;
+    sz[5] = NB + 8;
     size_t o = 0;
-    for (int k = 0; k < 14; ++k) {
+    for (int k = 0; k < 6; ++k) {
         L.off[k] = o;
         o += sz[k];
-        o = (o + 1) & ~size_t(1);  // 16-byte alignment
+        o = (o + 1) & ~size_t(1);
     }
     L.total = o;
     return L;
@@ -344,18 +325,136 @@ static const size_t kSmemCap = 227 * 1024;
 static int choose_layout(const DevProblem& dp, int kmax, int nthreads, Layout& out) {
     const int n = dp.n, P = dp.p;
     const int W2P = 2 * P + 1;
-    int best = -1;
     for (int T = (n == 1 ? 256 : 16); T >= 1; --T) {
-        if (n == 1 && T > 256) continue;
         const int T2 = n == 3 ? 16 : 1;
         Layout L = make_layout(dp, T, T, T2);
         if (L.total * sizeof(double) > kSmemCap) continue;
         if (n == 3 && (size_t)T * W2P * T * W2P * (P + 1) > (size_t)kmax * nthreads) continue;
-        best = T;
         out = L;
-        break;
+        return 0;
     }
-    if (best < 0) return fail(-2, "no tile configuration fits shared memory for this problem (p=%d, n=%d)", P, n);
+    return fail(-2, "no tile configuration fits shared memory for this problem (p=%d, n=%d)", P, n);
+}
+
+// ------------------------------------------------------------------------------------------
+// K3 launch: per-point form tensor D on the blocks of points the selected tiles read
+// ------------------------------------------------------------------------------------------
+#define SG_DECLG(nd, f) extern void* geom_kernel_##nd##_##f(bool rat);
+SG_DECLG(1, 0) SG_DECLG(1, 1) SG_DECLG(1, 2) SG_DECLG(2, 0) SG_DECLG(2, 1) SG_DECLG(2, 2) SG_DECLG(3, 0) SG_DECLG(3, 1) SG_DECLG(3, 2)
+#undef SG_DECLG
+
+static void* get_geom_kernel(int n, int form, bool rat) {
+    typedef void* (*Fn)(bool);
+    static const Fn tab[3][3] = {{geom_kernel_1_0, geom_kernel_1_1, geom_kernel_1_2},
+                                 {geom_kernel_2_0, geom_kernel_2_1, geom_kernel_2_2},
+                                 {geom_kernel_3_0, geom_kernel_3_1, geom_kernel_3_2}};
+    return tab[n - 1][form](rat);
+}
+
+int compute_D(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* tiles) {
+    const int n = dp.n, g = dp.g, P = dp.p, pg = dp.pr.geo_p;
+    const Tables TT = make_tables(n, dp.pr.form, dp.rational);
+    const int U = TT.MS * (TT.MS + 1) / 2;
+    const int NU = dp.nu, NUG = dp.nug;
+    const int NB = (NU + 1) * (P + 1), NBG = (NUG + 1) * (pg + 1);
+    GeomParams gp;
+    memset(&gp, 0, sizeof(gp));
+    gp.p = P;
+    gp.g = g;
+    gp.pg = pg;
+    for (int d = 0; d < 3; ++d) {
+        gp.m[d] = dp.m[d];
+        gp.mg[d] = dp.mg[d];
+        gp.B[d] = dp.B[d];
+        gp.qw[d] = dp.qw[d];
+        gp.gspan[d] = dp.gspan[d];
+        gp.G[d] = dp.G[d];
+        gp.Gp[d] = d < n ? dp.S[d] * g : 1;
+    }
+    gp.sol_w = dp.sol_w;
+    gp.hom = dp.hom;
+    gp.coef = dp.pr.coefficient;
+    gp.U = U;
+    gp.BX = n == 1 ? 256 : 32;
+    gp.BY = n >= 2 ? 32 : 1;
+    gp.nbx = (gp.Gp[0] + gp.BX - 1) / gp.BX;
+    gp.nby = (gp.Gp[1] + gp.BY - 1) / gp.BY;
+    const int64_t nblk_all = (int64_t)gp.nbx * gp.nby * gp.Gp[2];
+    // function-range bounds per block
+    auto gbound = [&](int d, int B) {
+        int mx = 1;
+        if (d >= n) return 1;
+        for (int s0 = 0; s0 < gp.Gp[d]; s0 += B) {
+            const int s1 = std::min(gp.Gp[d], s0 + B) - 1;
+            mx = std::max(mx, dp.hgspan[d][s1] - dp.hgspan[d][s0] + pg + 1);
+        }
+        return mx;
+    };
+    gp.GN0 = gbound(0, gp.BX);
+    gp.GN1 = gbound(1, gp.BY);
+    gp.WN0 = (gp.BX + g - 1) / g + 1 + P;
+    gp.WN1 = n >= 2 ? (gp.BY + g - 1) / g + 1 + P : 1;
+    const int C = n + 1;
+    const int NCg = n == 3 ? (NUG + 1) * (NUG + 2) / 2 : NUG + 1;
+    const int NCw = n == 3 ? (NU + 1) * (NU + 2) / 2 : NU + 1;
+    size_t sz[13];
+    sz[0] = (size_t)gp.BX * NBG;
+    sz[1] = n >= 2 ? (size_t)gp.BY * NBG : 0;
+    sz[2] = gp.BX / 2 + 1;
+    sz[3] = gp.BY / 2 + 1;
+    sz[4] = dp.rational ? (size_t)gp.BX * NB : 0;
+    sz[5] = (dp.rational && n >= 2) ? (size_t)gp.BY * NB : 0;
+    sz[6] = gp.BX / 2 + 1;
+    sz[7] = gp.BY / 2 + 1;
+    sz[8] = n == 3 ? (size_t)gp.GN0 * gp.GN1 * C * (NUG + 1) : 0;
+    sz[9] = n >= 2 ? (size_t)gp.BY * gp.GN0 * C * NCg : 0;
+    sz[10] = (n == 3 && dp.rational) ? (size_t)gp.WN0 * gp.WN1 * (NU + 1) : 0;
+    sz[11] = (n >= 2 && dp.rational) ? (size_t)gp.BY * gp.WN0 * NCw : 0;
+    sz[12] = 32 + NB + 8;
+    int* offs[13] = {&gp.off_G0, &gp.off_G1, &gp.off_gs0, &gp.off_gs1, &gp.off_B0, &gp.off_B1, &gp.off_ws0,
+                     &gp.off_ws1, &gp.off_Hz, &gp.off_Hy, &gp.off_Wz, &gp.off_Wy, &gp.off_misc};
+    size_t o = 0;
+    for (int k = 0; k < 13; ++k) {
+        *offs[k] = (int)o;
+        o += sz[k];
+        o = (o + 1) & ~size_t(1);
+    }
+    const size_t smem = o * sizeof(double);
+    if (smem > kSmemCap) return fail(-2, "geometry block does not fit shared memory (%zu B)", smem);
+    const size_t npts = (size_t)gp.Gp[0] * gp.Gp[1] * gp.Gp[2];
+    gp.D = (double*)c.alloc(sizeof(double) * npts * U, true);
+    if (!gp.D) return fail(-4, "device allocation of the D tensor failed (%zu MB)", sizeof(double) * npts * U >> 20);
+    dp.D = gp.D;
+    std::vector<int> blocks;
+    if (tiles) {
+        std::vector<uint8_t> mark(nblk_all, 0);
+        for (int t : *tiles) {
+            int64_t lo[3], hi[3];
+            tile_box(pl, dp, t, lo, hi);
+            int64_t plo[3], phi[3];
+            for (int d = 0; d < 3; ++d) {
+                if (d >= n) { plo[d] = 0; phi[d] = 0; continue; }
+                const int64_t e0 = std::max<int64_t>(0, lo[d] - P), e1 = std::min<int64_t>(dp.S[d] - 1, lo[d] + pl.T[d] - 1);
+                plo[d] = e0 * g;
+                phi[d] = (e1 + 1) * g - 1;
+            }
+            for (int64_t z = plo[2]; z <= phi[2]; ++z)
+                for (int64_t by = plo[1] / gp.BY; by <= phi[1] / gp.BY; ++by)
+                    for (int64_t bx = plo[0] / gp.BX; bx <= phi[0] / gp.BX; ++bx) mark[bx + gp.nbx * (by + gp.nby * z)] = 1;
+        }
+        for (int64_t k = 0; k < nblk_all; ++k)
+            if (mark[k]) blocks.push_back((int)k);
+        if (blocks.empty()) return 0;
+        gp.blocks = (const int*)c.upload(blocks.data(), sizeof(int) * blocks.size());
+    }
+    void* kfn = get_geom_kernel(n, dp.pr.form, dp.rational);
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    void* args[] = {&gp};
+    const int64_t nb = tiles ? (int64_t)blocks.size() : nblk_all;
+    c.kbegin("geom_D");
+    cudaError_t e = cudaLaunchKernel(kfn, dim3((unsigned)nb), dim3(256), args, smem, c.stream);
+    c.kend();
+    if (e != cudaSuccess) return fail(-3, "geometry launch failed: %s", cudaGetErrorString(e));
     return 0;
 }
 
@@ -371,9 +470,7 @@ int plan_assembly(DevProblem& dp, Plan& pl) {
         pl.tgrid[d] = (dp.m[d] + L.T[d] - 1) / L.T[d];
     }
     pl.ypad = L.ypad;
-    pl.GN[0] = L.GN[0];
-    pl.GN[1] = L.GN[1];
-    for (int k = 0; k < 14; ++k) pl.off[k] = (int)L.off[k];
+    for (int k = 0; k < 6; ++k) pl.off[k] = (int)L.off[k];
     pl.smem = L.total * sizeof(double);
     pl.ntiles = (int64_t)pl.tgrid[0] * pl.tgrid[1] * pl.tgrid[2];
     return 0;
@@ -395,6 +492,9 @@ int64_t tile_of_row(const Plan& pl, const DevProblem& dp, int64_t r) {
 int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* tiles, const uint8_t* d_rowmask,
                  const int64_t* d_rowstart, int64_t slab_lo, int64_t slab_hi, int* d_indices, double* d_data,
                  unsigned long long* d_zeros) {
+    if (tiles && tiles->empty()) return 0;
+    int rc = compute_D(c, dp, pl, tiles);
+    if (rc) return rc;
     AsmParams prm;
     memset(&prm, 0, sizeof(prm));
     prm.n = dp.n;
@@ -404,23 +504,15 @@ int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>
         prm.m[d] = dp.m[d];
         prm.S[d] = dp.S[d];
         prm.B[d] = dp.B[d];
-        prm.qw[d] = dp.qw[d];
-        prm.mg[d] = dp.mg[d];
-        prm.gspan[d] = dp.gspan[d];
-        prm.G[d] = dp.G[d];
         prm.T[d] = pl.T[d];
         prm.tgrid[d] = pl.tgrid[d];
+        prm.Gp[d] = d < dp.n ? dp.S[d] * dp.g : 1;
     }
     prm.sol_w = dp.sol_w;
-    prm.pg = dp.pr.geo_p;
-    prm.hom = dp.hom;
-    prm.coef = dp.pr.coefficient;
-    prm.GN[0] = pl.GN[0];
-    prm.GN[1] = pl.GN[1];
+    prm.D = dp.D;
     prm.ypad = pl.ypad;
-    int* offs[14] = {&prm.off_B0, &prm.off_B1, &prm.off_G0, &prm.off_G1, &prm.off_gs0, &prm.off_gs1, &prm.off_Hz,
-                     &prm.off_Hy, &prm.off_Wz, &prm.off_Wy, &prm.off_D, &prm.off_T1, &prm.off_T2, &prm.off_misc};
-    for (int k = 0; k < 14; ++k) *offs[k] = pl.off[k];
+    int* offs[6] = {&prm.off_B0, &prm.off_B1, &prm.off_D, &prm.off_T1, &prm.off_T2, &prm.off_misc};
+    for (int k = 0; k < 6; ++k) *offs[k] = pl.off[k];
     prm.rowmask = d_rowmask;
     prm.rowstart = d_rowstart;
     prm.slab_lo = slab_lo;
@@ -430,7 +522,6 @@ int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>
     prm.zeros = d_zeros;
     int64_t nblocks = pl.ntiles;
     if (tiles) {
-        if (tiles->empty()) return 0;
         prm.tiles = (const int*)c.upload(tiles->data(), sizeof(int) * tiles->size());
         nblocks = (int64_t)tiles->size();
     }

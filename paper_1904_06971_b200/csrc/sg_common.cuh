@@ -292,22 +292,15 @@ struct AsmParams {
     int n, p, g;
     int m[3], S[3];              // basis counts, spans (1 for unused directions)
     const double* B[3];          // solution tables  [S*g][nu+1][p+1]
-    const double* qw[3];         // per-direction Gauss weights [g]
     const double* sol_w;         // N (rational) or nullptr
-    int pg;
-    int mg[3];
-    const int* gspan[3];         // geometry span per quadrature point
-    const double* G[3];          // geometry tables [S*g][nug+1][pg+1]
-    const double* hom;           // Ng x (n+1)
-    double coef;
+    const double* D;             // per-point form tensor from K3, [Gp2][U][Gp0][Gp1]
+    int Gp[3];                   // Gauss points per direction
     // tiling
     int T[3];                    // rows per tile per direction
     int tgrid[3];                // tiles per direction
     const int* tiles;            // tile ids to process (colex over tgrid), or nullptr = all
-    int GN[2];                   // max geometry functions per window (dirs 0/1)
     int ypad;                    // padded window size along direction 1
-    // smem layout (offsets in doubles)
-    int off_B0, off_B1, off_G0, off_G1, off_gs0, off_gs1, off_Hz, off_Hy, off_Wz, off_Wy, off_D, off_T1, off_T2, off_misc;
+    int off_B0, off_B1, off_D, off_T1, off_T2, off_misc;   // smem layout (doubles)
     // rows & outputs
     const uint8_t* rowmask;      // per-row selection (nullptr = all rows)
     const int64_t* rowstart;     // output position of each row's first entry

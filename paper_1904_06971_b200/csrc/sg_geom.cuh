@@ -1,0 +1,438 @@
+// K3: geometry at the Gauss points -> per-point form tensor D_{mu nu}(x, y, z).
+//
+// Replaces the reference's full-grid geometry evaluation (geometry.py:185-229 map_grid,
+// :98-131 det/adj; assembly.py:558-576 _geometry_blocks, :402-438 weight function of a rational
+// space) and folds the integrand algebra of assembly.py:531-548 / :496-517 into D, so that
+//     A_ij = s_i s_j sum_q sum_{mu,nu} D_{mu nu}(q) d^mu B_i(q) d^nu B_j(q).
+// Each CTA evaluates one block of points of one z-plane by sum factorisation over the coarse
+// control net (contract z, then y, then x), so every Gauss point is evaluated exactly once.
+// D is stored plane-major, [z][u][x][y] (y fastest), the layout the tile kernel streams.
+#pragma once
+#include "sg_common.cuh"
+
+namespace sg {
+
+template <int NDIM>
+__device__ __forceinline__ int c12(int a1, int a2) {
+    if constexpr (NDIM == 3) return (a1 + a2) * (a1 + a2 + 1) / 2 + a2;
+    else return a1;
+}
+template <int NDIM, int NU>
+struct NC12 { static constexpr int v = NDIM == 3 ? (NU + 1) * (NU + 2) / 2 : NU + 1; };
+
+// ---------------------------------------------------------------------------------------------
+// plane preparation of a tensor field sum_{i} c_i B_i(x) (geometry or weight function):
+//   3D: Hz[i1][i0][c][a2] = sum_r2 tz[a2][r2] coef[i0, i1, sz-deg+r2]
+//       Hy[y][i0][c][c12(a1,a2)] = sum_r1 t1[y][a1][r1] Hz[s1(y)-deg+r1][i0][c][a2]
+//   2D: Hy[y][i0][c][a1]        = sum_r1 t1[y][a1][r1] coef[i0, s1(y)-deg+r1]
+// ---------------------------------------------------------------------------------------------
+template <int NDIM, int NU, int C>
+__device__ void field_plane_prep(const double* __restrict__ coef, int deg, const int* md, const double* t1,
+                                 const int* s1, int Y, const double* tz, int sz, int lo0, int n0, int lo1, int n1,
+                                 double* Hz, double* Hy) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    constexpr int NC = NC12<NDIM, NU>::v;
+    if constexpr (NDIM == 3) {
+        const int items = n0 * n1 * C;
+        for (int it = tid; it < items; it += nt) {
+            const int c = it % C;
+            const int i0 = (it / C) % n0;
+            const int i1 = it / (C * n0);
+            const int g0 = lo0 + i0, g1 = lo1 + i1;
+            double acc[NU + 1];
+#pragma unroll
+            for (int a = 0; a <= NU; ++a) acc[a] = 0.0;
+            if (g0 < md[0] && g1 < md[1]) {
+                for (int r = 0; r <= deg; ++r) {
+                    const double v = coef[((long long)g0 + (long long)md[0] * (g1 + (long long)md[1] * (sz - deg + r))) * C + c];
+#pragma unroll
+                    for (int a = 0; a <= NU; ++a) acc[a] = fma(tz[a * (deg + 1) + r], v, acc[a]);
+                }
+            }
+#pragma unroll
+            for (int a = 0; a <= NU; ++a) Hz[((i1 * n0 + i0) * C + c) * (NU + 1) + a] = acc[a];
+        }
+        __syncthreads();
+    }
+    if constexpr (NDIM >= 2) {
+        const int items = Y * n0 * C;
+        for (int it = tid; it < items; it += nt) {
+            const int c = it % C;
+            const int i0 = (it / C) % n0;
+            const int y = it / (C * n0);
+            const int sy = s1[y];
+            double acc[NC];
+#pragma unroll
+            for (int k = 0; k < NC; ++k) acc[k] = 0.0;
+            for (int r = 0; r <= deg; ++r) {
+                if constexpr (NDIM == 3) {
+                    const double* hz = Hz + (((sy - deg + r - lo1) * n0 + i0) * C + c) * (NU + 1);
+#pragma unroll
+                    for (int a1 = 0; a1 <= NU; ++a1) {
+                        const double b = t1[(y * (NU + 1) + a1) * (deg + 1) + r];
+#pragma unroll
+                        for (int a2 = 0; a2 + a1 <= NU; ++a2) acc[c12<3>(a1, a2)] = fma(b, hz[a2], acc[c12<3>(a1, a2)]);
+                    }
+                } else {
+                    const int g0 = lo0 + i0;
+                    const double v = (g0 < md[0]) ? coef[((long long)g0 + (long long)md[0] * (sy - deg + r)) * C + c] : 0.0;
+#pragma unroll
+                    for (int a1 = 0; a1 <= NU; ++a1) acc[a1] = fma(t1[(y * (NU + 1) + a1) * (deg + 1) + r], v, acc[a1]);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < NC; ++k) Hy[((y * n0 + i0) * C + c) * NC + k] = acc[k];
+        }
+    }
+}
+
+// point evaluation: out[c][code] for all multi-indices with |alpha| <= NU (code = a0+3a1+9a2)
+template <int NDIM, int NU, int C>
+__device__ __forceinline__ void field_point(const double* __restrict__ coef, int deg, const double* t0, int sx,
+                                            const double* Hy, int y, int lo0, int n0, double (&out)[C][27]) {
+    constexpr int NC = NC12<NDIM, NU>::v;
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+#pragma unroll
+        for (int k = 0; k < 27; ++k) out[c][k] = 0.0;
+    for (int r = 0; r <= deg; ++r) {
+        const int i0 = sx - deg + r;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            if constexpr (NDIM == 1) {
+                const double v = coef[(long long)i0 * C + c];
+#pragma unroll
+                for (int a0 = 0; a0 <= NU; ++a0) out[c][a0] = fma(t0[a0 * (deg + 1) + r], v, out[c][a0]);
+            } else {
+                const double* hy = Hy + ((y * n0 + (i0 - lo0)) * C + c) * NC;
+#pragma unroll
+                for (int a0 = 0; a0 <= NU; ++a0) {
+                    const double b = t0[a0 * (deg + 1) + r];
+#pragma unroll
+                    for (int a1 = 0; a1 + a0 <= NU; ++a1) {
+                        if constexpr (NDIM == 3) {
+#pragma unroll
+                            for (int a2 = 0; a2 + a1 + a0 <= NU; ++a2)
+                                out[c][a0 + 3 * a1 + 9 * a2] = fma(b, hy[c12<3>(a1, a2)], out[c][a0 + 3 * a1 + 9 * a2]);
+                        } else {
+                            out[c][a0 + 3 * a1] = fma(b, hy[a1], out[c][a0 + 3 * a1]);
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ constexpr int ucode(int a) { return a == 0 ? 1 : (a == 1 ? 3 : 9); }
+
+// ---------------------------------------------------------------------------------------------
+// per-point physics: D_{mu nu} (packed upper triangle over Mset) from geometry numerators,
+// weight-function values and the tensor Gauss weight.  Reference: geometry.py:185-229 (map,
+// quotient rule), :98-131 (det, adj), assembly.py:558-576 (K, C, hess), :531-548 (integrands),
+// :496-517 (rational basis).
+// ---------------------------------------------------------------------------------------------
+template <int NDIM, int FORM, bool RAT>
+__device__ __forceinline__ void point_D(const double (&num)[NDIM + 1][27], const double (&wf)[1][27], double wq,
+                                        double coefv, double* Dout) {
+    constexpr Tables TT = TermTables<NDIM, FORM, RAT>::T;
+    constexpr int MS = TT.MS;
+    constexpr int NUG = geo_deriv(FORM);
+    const double W = num[NDIM][0];
+    const double iW = 1.0 / W;
+    double phi[NDIM], jac[NDIM][NDIM], dW[NDIM];
+#pragma unroll
+    for (int c = 0; c < NDIM; ++c) phi[c] = num[c][0] * iW;
+#pragma unroll
+    for (int a = 0; a < NDIM; ++a) {
+        dW[a] = num[NDIM][ucode(a)];
+#pragma unroll
+        for (int c = 0; c < NDIM; ++c) jac[c][a] = (num[c][ucode(a)] - phi[c] * num[NDIM][ucode(a)]) * iW;
+    }
+    double det, adj[NDIM][NDIM];
+    if constexpr (NDIM == 1) {
+        det = jac[0][0];
+        adj[0][0] = 1.0;
+    } else if constexpr (NDIM == 2) {
+        det = jac[0][0] * jac[1][1] - jac[0][1] * jac[1][0];
+        adj[0][0] = jac[1][1];
+        adj[0][1] = -jac[0][1];
+        adj[1][0] = -jac[1][0];
+        adj[1][1] = jac[0][0];
+    } else {
+        det = jac[0][0] * (jac[1][1] * jac[2][2] - jac[1][2] * jac[2][1]) -
+              jac[0][1] * (jac[1][0] * jac[2][2] - jac[1][2] * jac[2][0]) +
+              jac[0][2] * (jac[1][0] * jac[2][1] - jac[1][1] * jac[2][0]);
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+                const int r0 = b == 0 ? 1 : 0, r1 = b == 2 ? 1 : 2;
+                const int c0 = a == 0 ? 1 : 0, c1 = a == 2 ? 1 : 2;
+                const double minor = jac[r0][c0] * jac[r1][c1] - jac[r0][c1] * jac[r1][c0];
+                adj[a][b] = ((a + b) & 1) ? -minor : minor;
+            }
+    }
+    // functional coefficient vectors over Mset: f[k][mu], D = sum_k f_k Core_k f_k^T
+    double Dl[MS * (MS + 1) / 2];
+    const double idet = 1.0 / det;
+    if constexpr (FORM == POISSON) {
+        double Kw[NDIM][NDIM];
+#pragma unroll
+        for (int a = 0; a < NDIM; ++a)
+#pragma unroll
+            for (int c = 0; c < NDIM; ++c) {
+                double s = 0.0;
+#pragma unroll
+                for (int b = 0; b < NDIM; ++b) s = fma(adj[a][b], adj[c][b], s);
+                Kw[a][c] = (s * idet) * coefv * wq;
+            }
+        if constexpr (!RAT) {
+            // Mset = {e_a} in code order e0 (1), e1 (3), e2 (9)
+#pragma unroll
+            for (int mu = 0; mu < MS; ++mu)
+#pragma unroll
+                for (int nu = mu; nu < MS; ++nu) Dl[tri_index(mu, nu, MS)] = Kw[mu][nu];
+        } else {
+            const double Ws = wf[0][0];
+            // d_a N = w (d_a B / W - B d_a W / W^2): R[a][mu]
+            double R[NDIM][MS];
+            static_for<0, MS>([&](auto MU) {
+                constexpr int mu = decltype(MU)::value;
+                constexpr int code = TT.mcode[mu];
+#pragma unroll
+                for (int a = 0; a < NDIM; ++a)
+                    R[a][mu] = (code == 0) ? -wf[0][ucode(a)] / (Ws * Ws) : (code == ucode(a) ? 1.0 / Ws : 0.0);
+            });
+#pragma unroll
+            for (int mu = 0; mu < MS; ++mu)
+#pragma unroll
+                for (int nu = mu; nu < MS; ++nu) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int a = 0; a < NDIM; ++a)
+#pragma unroll
+                        for (int b = 0; b < NDIM; ++b) s = fma(R[a][mu] * Kw[a][b], R[b][nu], s);
+                    Dl[tri_index(mu, nu, MS)] = s;
+                }
+        }
+    } else if constexpr (FORM == MASS) {
+        if constexpr (!RAT) Dl[0] = det * wq;
+        else Dl[0] = det * wq / (wf[0][0] * wf[0][0]);
+    } else {
+        // biharmonic: lap N = sum_ab C_ab d_ab N - sum_a g_a d_a N
+        double hess[NDIM][NDIM][NDIM];
+#pragma unroll
+        for (int a = 0; a < NDIM; ++a)
+#pragma unroll
+            for (int b = a; b < NDIM; ++b) {
+                const int cd = ucode(a) + ucode(b);
+#pragma unroll
+                for (int c = 0; c < NDIM; ++c) {
+                    const double v = (num[c][cd] - jac[c][a] * dW[b] - jac[c][b] * dW[a] - phi[c] * num[NDIM][cd]) * iW;
+                    hess[c][a][b] = v;
+                    hess[c][b][a] = v;
+                }
+            }
+        double Cm[NDIM][NDIM];
+        const double idet2 = idet * idet;
+#pragma unroll
+        for (int a = 0; a < NDIM; ++a)
+#pragma unroll
+            for (int b = 0; b < NDIM; ++b) {
+                double s = 0.0;
+#pragma unroll
+                for (int c = 0; c < NDIM; ++c) s = fma(adj[a][c], adj[b][c], s);
+                Cm[a][b] = s * idet2;
+            }
+        double h[NDIM], gv[NDIM];
+#pragma unroll
+        for (int c = 0; c < NDIM; ++c) {
+            double s = 0.0;
+#pragma unroll
+            for (int a = 0; a < NDIM; ++a)
+#pragma unroll
+                for (int b = 0; b < NDIM; ++b) s = fma(hess[c][a][b], Cm[a][b], s);
+            h[c] = s;
+        }
+#pragma unroll
+        for (int a = 0; a < NDIM; ++a) {
+            double s = 0.0;
+#pragma unroll
+            for (int c = 0; c < NDIM; ++c) s = fma(adj[a][c], h[c], s);
+            gv[a] = s * idet;
+        }
+        double f[MS];
+        if constexpr (!RAT) {
+            static_for<0, MS>([&](auto MU) {
+                constexpr int mu = decltype(MU)::value;
+                constexpr int code = TT.mcode[mu];
+                double v = 0.0;
+#pragma unroll
+                for (int a = 0; a < NDIM; ++a) {
+                    if (code == ucode(a)) v = -gv[a];
+#pragma unroll
+                    for (int b = a; b < NDIM; ++b)
+                        if (code == ucode(a) + ucode(b)) v = (a == b) ? Cm[a][a] : 2.0 * Cm[a][b];
+                }
+                f[mu] = v;
+            });
+        } else {
+            const double Ws = wf[0][0];
+            double dWs[NDIM], d2Ws[NDIM][NDIM];
+#pragma unroll
+            for (int a = 0; a < NDIM; ++a) {
+                dWs[a] = wf[0][ucode(a)];
+#pragma unroll
+                for (int b = 0; b < NDIM; ++b) d2Ws[a][b] = wf[0][ucode(a) + ucode(b)];
+            }
+            const double iW = 1.0 / Ws, iW2 = iW * iW, iW3 = iW2 * iW;
+            double cC2W = 0.0, dWCdW = 0.0, gdW = 0.0;
+#pragma unroll
+            for (int a = 0; a < NDIM; ++a) {
+                gdW = fma(gv[a], dWs[a], gdW);
+#pragma unroll
+                for (int c = 0; c < NDIM; ++c) {
+                    cC2W = fma(Cm[a][c], d2Ws[a][c], cC2W);
+                    dWCdW = fma(dWs[a] * Cm[a][c], dWs[c], dWCdW);
+                }
+            }
+            static_for<0, MS>([&](auto MU) {
+                constexpr int mu = decltype(MU)::value;
+                constexpr int code = TT.mcode[mu];
+                double v = 0.0;
+                if (code == 0) v = -cC2W * iW2 + 2.0 * dWCdW * iW3 + gdW * iW2;
+#pragma unroll
+                for (int a = 0; a < NDIM; ++a) {
+                    if (code == ucode(a)) {
+                        double s = 0.0;
+#pragma unroll
+                        for (int c = 0; c < NDIM; ++c) s = fma(Cm[a][c] + Cm[c][a], dWs[c], s);
+                        v = -s * iW2 - gv[a] * iW;
+                    }
+#pragma unroll
+                    for (int b = a; b < NDIM; ++b)
+                        if (code == ucode(a) + ucode(b)) v = ((a == b) ? Cm[a][a] : 2.0 * Cm[a][b]) * iW;
+                }
+                f[mu] = v;
+            });
+        }
+        const double sw = det * wq;
+#pragma unroll
+        for (int mu = 0; mu < MS; ++mu)
+#pragma unroll
+            for (int nu = mu; nu < MS; ++nu) Dl[tri_index(mu, nu, MS)] = (f[mu] * f[nu]) * sw;
+    }
+#pragma unroll
+    for (int k = 0; k < MS * (MS + 1) / 2; ++k) Dout[k] = Dl[k];
+}
+
+
+struct GeomParams {
+    int p, g, pg;
+    int m[3], mg[3];
+    const double* B[3];      // solution tables [S*g][nu+1][p+1]
+    const double* qw[3];
+    const double* sol_w;
+    const int* gspan[3];
+    const double* G[3];      // geometry tables [S*g][nug+1][pg+1]
+    const double* hom;
+    double coef;
+    int Gp[3];               // global Gauss points per direction (1 for unused directions)
+    int BX, BY;              // points per block (x, y)
+    int nbx, nby;            // blocks per plane
+    const int* blocks;       // block ids (bx + nbx*(by + nby*z)) or nullptr = all
+    int GN0, GN1, WN0, WN1;  // smem bounds of function ranges
+    int off_G0, off_G1, off_gs0, off_gs1, off_B0, off_B1, off_ws0, off_ws1, off_Hz, off_Hy, off_Wz, off_Wy, off_misc;
+    int U;
+    double* D;               // [Gp2][U][Gp0][Gp1]
+};
+
+template <int NDIM, int FORM, bool RAT>
+__global__ void __launch_bounds__(256) geom_D_kernel(const GeomParams prm) {
+    constexpr Tables TT = TermTables<NDIM, FORM, RAT>::T;
+    constexpr int MS = TT.MS;
+    constexpr int U = MS * (MS + 1) / 2;
+    constexpr int NU = form_deriv(FORM);
+    constexpr int NUG = geo_deriv(FORM);
+    constexpr int P_ = 0;
+    (void)P_;
+    extern __shared__ double smem[];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int g = prm.g, pg = prm.pg, p = prm.p;
+    const int NB = (NU + 1) * (p + 1), NBG = (NUG + 1) * (pg + 1);
+    const int blk = prm.blocks ? prm.blocks[blockIdx.x] : (int)blockIdx.x;
+    const int bx = blk % prm.nbx, by = (blk / prm.nbx) % prm.nby, z = blk / (prm.nbx * prm.nby);
+    const int x0 = bx * prm.BX, y0 = by * prm.BY;
+    const int X = min(prm.BX, prm.Gp[0] - x0);
+    const int Y = NDIM >= 2 ? min(prm.BY, prm.Gp[1] - y0) : 1;
+    double* G0s = smem + prm.off_G0;
+    double* G1s = smem + prm.off_G1;
+    int* gs0 = reinterpret_cast<int*>(smem + prm.off_gs0);
+    int* gs1 = reinterpret_cast<int*>(smem + prm.off_gs1);
+    double* B0s = smem + prm.off_B0;
+    double* B1s = smem + prm.off_B1;
+    int* ws0 = reinterpret_cast<int*>(smem + prm.off_ws0);
+    int* ws1 = reinterpret_cast<int*>(smem + prm.off_ws1);
+    double* Hz = smem + prm.off_Hz;
+    double* Hy = smem + prm.off_Hy;
+    double* Wz = smem + prm.off_Wz;
+    double* Wy = smem + prm.off_Wy;
+    double* misc = smem + prm.off_misc;
+    double* G2p = misc;
+    double* B2p = misc + 32;
+    for (int it = tid; it < X * NBG; it += nt) G0s[it] = prm.G[0][(long long)x0 * NBG + it];
+    for (int x = tid; x < X; x += nt) gs0[x] = prm.gspan[0][x0 + x];
+    if constexpr (RAT) {
+        for (int it = tid; it < X * NB; it += nt) B0s[it] = prm.B[0][(long long)x0 * NB + it];
+        for (int x = tid; x < X; x += nt) ws0[x] = (x0 + x) / g + p;
+    }
+    if constexpr (NDIM >= 2) {
+        for (int it = tid; it < Y * NBG; it += nt) G1s[it] = prm.G[1][(long long)y0 * NBG + it];
+        for (int y = tid; y < Y; y += nt) gs1[y] = prm.gspan[1][y0 + y];
+        if constexpr (RAT) {
+            for (int it = tid; it < Y * NB; it += nt) B1s[it] = prm.B[1][(long long)y0 * NB + it];
+            for (int y = tid; y < Y; y += nt) ws1[y] = (y0 + y) / g + p;
+        }
+    }
+    int sz = 0, szw = 0;
+    if constexpr (NDIM == 3) {
+        for (int k = tid; k < NBG; k += nt) G2p[k] = prm.G[2][(long long)z * NBG + k];
+        if constexpr (RAT)
+            for (int k = tid; k < NB; k += nt) B2p[k] = prm.B[2][(long long)z * NB + k];
+        sz = prm.gspan[2][z];
+        szw = z / g + p;
+    }
+    __syncthreads();
+    const int glo0 = gs0[0] - pg, gn0 = gs0[X - 1] - gs0[0] + pg + 1;
+    int glo1 = 0, gn1 = 1;
+    if constexpr (NDIM >= 2) { glo1 = gs1[0] - pg; gn1 = gs1[Y - 1] - gs1[0] + pg + 1; }
+    const int wlo0 = x0 / g, wn0 = (x0 + X - 1) / g - x0 / g + 1 + p;
+    int wlo1 = 0, wn1 = 1;
+    if constexpr (NDIM >= 2) { wlo1 = y0 / g; wn1 = (y0 + Y - 1) / g - y0 / g + 1 + p; }
+    field_plane_prep<NDIM, NUG, NDIM + 1>(prm.hom, pg, prm.mg, G1s, gs1, Y, G2p, sz, glo0, gn0, glo1, gn1, Hz, Hy);
+    if constexpr (RAT)
+        field_plane_prep<NDIM, NU, 1>(prm.sol_w, p, prm.m, B1s, ws1, Y, B2p, szw, wlo0, wn0, wlo1, wn1, Wz, Wy);
+    __syncthreads();
+    const double wz = NDIM == 3 ? prm.qw[2][z % g] : 1.0;
+    for (int it = tid; it < X * Y; it += nt) {
+        const int y = it % Y, x = it / Y;
+        double num[NDIM + 1][27];
+        field_point<NDIM, NUG, NDIM + 1>(prm.hom, pg, G0s + x * NBG, gs0[x], Hy, y, glo0, gn0, num);
+        double wf[1][27];
+        if constexpr (RAT) field_point<NDIM, NU, 1>(prm.sol_w, p, B0s + x * NB, ws0[x], Wy, y, wlo0, wn0, wf);
+        else wf[0][0] = 1.0;
+        // tensor weight in the reference order wq = pw2 * (pw1 * pw0)  (assembly.py:120-125)
+        double wq = prm.qw[0][(x0 + x) % g];
+        if constexpr (NDIM >= 2) wq = prm.qw[1][(y0 + y) % g] * wq;
+        if constexpr (NDIM == 3) wq = wz * wq;
+        double Dp[U];
+        point_D<NDIM, FORM, RAT>(num, wf, wq, prm.coef, Dp);
+        const long long plane = (long long)z * U;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            prm.D[((plane + u) * prm.Gp[0] + x0 + x) * (long long)prm.Gp[1] + y0 + y] = Dp[u];
+    }
+}
+
+}  // namespace sg

@@ -1,6 +1,7 @@
 // Kernel instantiations of the tiled assembly kernel for one dimension (SG_INST_NDIM).
 // Compiled once per dimension so the build parallelises.
 #include "sg_assemble.cuh"
+#include "sg_geom.cuh"
 
 #if !defined(SG_INST_NDIM) || !defined(SG_INST_FORM)
 #error "define SG_INST_NDIM and SG_INST_FORM"
@@ -36,6 +37,10 @@ void* SG_CAT(SG_CAT(assemble_kernel_, SG_INST_NDIM), SG_CAT(_, SG_INST_FORM))(in
 #endif
     }
     return nullptr;
+}
+
+void* SG_CAT(SG_CAT(geom_kernel_, SG_INST_NDIM), SG_CAT(_, SG_INST_FORM))(bool rat) {
+    return rat ? (void*)&geom_D_kernel<SG_INST_NDIM, SG_INST_FORM, true> : (void*)&geom_D_kernel<SG_INST_NDIM, SG_INST_FORM, false>;
 }
 
 }  // namespace sg

@@ -41,6 +41,7 @@ struct Call {
     explicit Call(const sg_exec* ex);
     ~Call();
     void* alloc(size_t bytes, bool temp);
+    void release(void* p);  // hand a temporary over to a result (no free at call end)
     void* upload(const void* host, size_t bytes);
     void kbegin(const char* name);
     void kend();
@@ -62,6 +63,7 @@ struct DevProblem {
     std::vector<int> hgspan[3];
     double* hom = nullptr;
     double* sol_w = nullptr;
+    double* D = nullptr;
     int64_t last_tiles = 0;
     int last_T[3];
     size_t last_smem = 0;
@@ -70,7 +72,7 @@ struct DevProblem {
 struct Plan {
     void* kfn = nullptr;
     int kmax = 1, nthreads = 512;
-    int T[3], tgrid[3], ypad, GN[2], off[14];
+    int T[3], tgrid[3], ypad, off[6];
     size_t smem = 0;
     int64_t ntiles = 0;
 };

@@ -554,15 +554,23 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
             c.kend();
         }
         r->nnz = nnz_hi - nnz_lo;
-        r->indices = (int*)c.alloc(sizeof(int) * std::max<int64_t>(r->nnz, 1), false);
-        r->data = (double*)c.alloc(sizeof(double) * std::max<int64_t>(r->nnz, 1), false);
-        if (!r->indices || !r->data) {
-            delete r;
-            return fail(-4, "device allocation failed");
+        if (nnz_lo == 0 && nnz_hi == nnz_all) {
+            // whole matrix: the work arrays become the result (no copy)
+            c.release(indices);
+            c.release(data);
+            r->indices = indices;
+            r->data = data;
+        } else {
+            // row slab: the full-size work arrays are temporaries; the slab portion is the result
+            r->indices = (int*)c.alloc(sizeof(int) * std::max<int64_t>(r->nnz, 1), false);
+            r->data = (double*)c.alloc(sizeof(double) * std::max<int64_t>(r->nnz, 1), false);
+            if (!r->indices || !r->data) {
+                delete r;
+                return fail(-4, "device allocation failed");
+            }
+            cudaMemcpyAsync(r->indices, indices + nnz_lo, sizeof(int) * r->nnz, cudaMemcpyDeviceToDevice, c.stream);
+            cudaMemcpyAsync(r->data, data + nnz_lo, sizeof(double) * r->nnz, cudaMemcpyDeviceToDevice, c.stream);
         }
-        // the full-size work arrays are temporaries; the slab portion is the result
-        cudaMemcpyAsync(r->indices, indices + nnz_lo, sizeof(int) * r->nnz, cudaMemcpyDeviceToDevice, c.stream);
-        cudaMemcpyAsync(r->data, data + nnz_lo, sizeof(double) * r->nnz, cudaMemcpyDeviceToDevice, c.stream);
         cudaMemcpyAsync(r->indptr, rowstart + slab_lo, sizeof(int64_t) * (r->nrows + 1), cudaMemcpyDeviceToDevice, c.stream);
         if (nnz_lo) {
             c.kbegin("rebase");
