@@ -7,12 +7,14 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
 #include "../../include/surriga_b200.h"
 #include "sg_common.cuh"
 #include "sg_geom.cuh"
+#include "sg_tile_mma.cuh"
 #include "sg_internal.h"
 
 namespace sg {
@@ -274,14 +276,28 @@ int prepare_problem(Call& c, const sg_problem* pr, DevProblem& dp) {
 SG_DECL(1, 0) SG_DECL(1, 1) SG_DECL(1, 2) SG_DECL(2, 0) SG_DECL(2, 1) SG_DECL(2, 2) SG_DECL(3, 0) SG_DECL(3, 1) SG_DECL(3, 2)
 #undef SG_DECL
 
-static void* get_kernel(int n, int form, int p, bool rat, int* kmax) {
-    typedef void* (*Fn)(int, bool, int*);
-    static const Fn tab[3][3] = {{assemble_kernel_1_0, assemble_kernel_1_1, assemble_kernel_1_2},
-                                 {assemble_kernel_2_0, assemble_kernel_2_1, assemble_kernel_2_2},
-                                 {assemble_kernel_3_0, assemble_kernel_3_1, assemble_kernel_3_2}};
+#define SG_DECLK(nd, f, r) extern void* kernel_ptr_##nd##_##f##_##r(int which, int p, int* kmax);
+SG_DECLK(1, 0, 0) SG_DECLK(1, 0, 1) SG_DECLK(1, 1, 0) SG_DECLK(1, 1, 1) SG_DECLK(1, 2, 0) SG_DECLK(1, 2, 1)
+SG_DECLK(2, 0, 0) SG_DECLK(2, 0, 1) SG_DECLK(2, 1, 0) SG_DECLK(2, 1, 1) SG_DECLK(2, 2, 0) SG_DECLK(2, 2, 1)
+SG_DECLK(3, 0, 0) SG_DECLK(3, 0, 1) SG_DECLK(3, 1, 0) SG_DECLK(3, 1, 1) SG_DECLK(3, 2, 0) SG_DECLK(3, 2, 1)
+#undef SG_DECLK
+
+static void* kernel_ptr(int n, int form, bool rat, int which, int p, int* kmax) {
+    typedef void* (*Fn)(int, int, int*);
+    static const Fn tab[3][3][2] = {
+        {{kernel_ptr_1_0_0, kernel_ptr_1_0_1}, {kernel_ptr_1_1_0, kernel_ptr_1_1_1}, {kernel_ptr_1_2_0, kernel_ptr_1_2_1}},
+        {{kernel_ptr_2_0_0, kernel_ptr_2_0_1}, {kernel_ptr_2_1_0, kernel_ptr_2_1_1}, {kernel_ptr_2_2_0, kernel_ptr_2_2_1}},
+        {{kernel_ptr_3_0_0, kernel_ptr_3_0_1}, {kernel_ptr_3_1_0, kernel_ptr_3_1_1}, {kernel_ptr_3_2_0, kernel_ptr_3_2_1}}};
     if (n < 1 || n > 3 || form < 0 || form > 2) return nullptr;
-    return tab[n - 1][form](p, rat, kmax);
+    int km = 1;
+    void* f = tab[n - 1][form][rat ? 1 : 0](which, p, &km);
+    if (kmax) *kmax = km;
+    return f;
 }
+
+static void* get_mma_kernel(int n, int form, int p, bool rat) { return kernel_ptr(n, form, rat, 1, p, nullptr); }
+
+static void* get_kernel(int n, int form, int p, bool rat, int* kmax) { return kernel_ptr(n, form, rat, 0, p, kmax); }
 
 struct Layout {
     int T[3];
@@ -339,17 +355,7 @@ static int choose_layout(const DevProblem& dp, int kmax, int nthreads, Layout& o
 // ------------------------------------------------------------------------------------------
 // K3 launch: per-point form tensor D on the blocks of points the selected tiles read
 // ------------------------------------------------------------------------------------------
-#define SG_DECLG(nd, f) extern void* geom_kernel_##nd##_##f(bool rat);
-SG_DECLG(1, 0) SG_DECLG(1, 1) SG_DECLG(1, 2) SG_DECLG(2, 0) SG_DECLG(2, 1) SG_DECLG(2, 2) SG_DECLG(3, 0) SG_DECLG(3, 1) SG_DECLG(3, 2)
-#undef SG_DECLG
-
-static void* get_geom_kernel(int n, int form, bool rat) {
-    typedef void* (*Fn)(bool);
-    static const Fn tab[3][3] = {{geom_kernel_1_0, geom_kernel_1_1, geom_kernel_1_2},
-                                 {geom_kernel_2_0, geom_kernel_2_1, geom_kernel_2_2},
-                                 {geom_kernel_3_0, geom_kernel_3_1, geom_kernel_3_2}};
-    return tab[n - 1][form](rat);
-}
+static void* get_geom_kernel(int n, int form, bool rat) { return kernel_ptr(n, form, rat, 2, 1, nullptr); }
 
 int compute_D(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* tiles) {
     const int n = dp.n, g = dp.g, P = dp.p, pg = dp.pr.geo_p;
@@ -458,7 +464,29 @@ int compute_D(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* t
     return 0;
 }
 
+static bool plan_mma(DevProblem& dp, Plan& pl) {
+    const int n = dp.n, P = dp.p, g = dp.g;
+    if (P > 4 || g != P + 1 || getenv("SG_NO_MMA")) return false;
+    void* kfn = get_mma_kernel(n, dp.pr.form, P, dp.rational);
+    if (!kfn) return false;
+    const TileChoice tc = mma_tile(n, P, dp.pr.form, dp.rational);
+    const MmaGeom M = mma_geom(n, P, dp.pr.form, dp.rational, tc.T0, tc.T1);
+    if (M.total * 8 > (long)kSmemCap) return false;
+    pl.mma = true;
+    pl.kfn = kfn;
+    pl.nthreads = 512;
+    pl.T[0] = M.T0;
+    pl.T[1] = M.T1;
+    pl.T[2] = n == 3 ? 16 : 1;
+    for (int d = 0; d < 3; ++d) pl.tgrid[d] = (dp.m[d] + pl.T[d] - 1) / pl.T[d];
+    pl.smem = M.total * sizeof(double);
+    pl.ntiles = (int64_t)pl.tgrid[0] * pl.tgrid[1] * pl.tgrid[2];
+    return true;
+}
+
 int plan_assembly(DevProblem& dp, Plan& pl) {
+    pl.mma = false;
+    if (plan_mma(dp, pl)) return 0;
     pl.kfn = get_kernel(dp.n, dp.pr.form, dp.p, dp.rational, &pl.kmax);
     if (!pl.kfn) return fail(-2, "no kernel instantiated for n=%d p=%d form=%d", dp.n, dp.p, dp.pr.form);
     pl.nthreads = 512;
@@ -495,6 +523,41 @@ int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>
     if (tiles && tiles->empty()) return 0;
     int rc = compute_D(c, dp, pl, tiles);
     if (rc) return rc;
+    if (pl.mma) {
+        MmaParams mp;
+        memset(&mp, 0, sizeof(mp));
+        for (int d = 0; d < 3; ++d) {
+            mp.m[d] = dp.m[d];
+            mp.S[d] = dp.S[d];
+            mp.B[d] = dp.B[d];
+            mp.tgrid[d] = pl.tgrid[d];
+            mp.Gp[d] = d < dp.n ? dp.S[d] * dp.g : 1;
+        }
+        mp.T2 = pl.T[2];
+        mp.sol_w = dp.sol_w;
+        mp.D = dp.D;
+        mp.rowmask = d_rowmask;
+        mp.rowstart = d_rowstart;
+        mp.slab_lo = slab_lo;
+        mp.slab_hi = slab_hi;
+        mp.indices = d_indices;
+        mp.data = d_data;
+        mp.zeros = d_zeros;
+        int64_t nb = pl.ntiles;
+        if (tiles) {
+            mp.tiles = (const int*)c.upload(tiles->data(), sizeof(int) * tiles->size());
+            nb = (int64_t)tiles->size();
+        }
+        cudaFuncSetAttribute(pl.kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+        void* args[] = {&mp};
+        c.kbegin("assemble_mma");
+        cudaError_t e = cudaLaunchKernel(pl.kfn, dim3((unsigned)nb), dim3(pl.nthreads), args, pl.smem, c.stream);
+        c.kend();
+        if (e != cudaSuccess)
+            return fail(-3, "assembly (mma) launch failed: %s (smem %zu B, %lld tiles)", cudaGetErrorString(e), pl.smem, (long long)nb);
+        dp.last_tiles = nb;
+        return 0;
+    }
     AsmParams prm;
     memset(&prm, 0, sizeof(prm));
     prm.n = dp.n;

@@ -1,46 +1,47 @@
-// Kernel instantiations of the tiled assembly kernel for one dimension (SG_INST_NDIM).
-// Compiled once per dimension so the build parallelises.
+// Kernel instantiations for one (dimension, form, rational) triple; compiled as separate
+// translation units so the build parallelises.  Exposes one pointer getter per triple.
 #include "sg_assemble.cuh"
 #include "sg_geom.cuh"
+#include "sg_tile_mma.cuh"
 
-#if !defined(SG_INST_NDIM) || !defined(SG_INST_FORM)
-#error "define SG_INST_NDIM and SG_INST_FORM"
+#if !defined(SG_INST_NDIM) || !defined(SG_INST_FORM) || !defined(SG_INST_RAT)
+#error "define SG_INST_NDIM, SG_INST_FORM and SG_INST_RAT"
 #endif
 
 namespace sg {
 
 constexpr int kmax_for(int ndim) { return ndim == 3 ? 8 : 1; }
+constexpr bool kRat = SG_INST_RAT != 0;
 
-template <int P, int FORM, bool RAT>
-static void* kptr() {
-    if constexpr (FORM == BIHARMONIC && P < 2) return nullptr;
-    else return (void*)&assemble_tiles<SG_INST_NDIM, P, FORM, RAT, kmax_for(SG_INST_NDIM)>;
+template <int P>
+static void* simt_ptr() {
+    if constexpr (SG_INST_FORM == BIHARMONIC && P < 2) return nullptr;
+    else return (void*)&assemble_tiles<SG_INST_NDIM, P, SG_INST_FORM, kRat, kmax_for(SG_INST_NDIM)>;
 }
 
 template <int P>
-static void* kptr_p(bool rat) {
-    return rat ? kptr<P, SG_INST_FORM, true>() : kptr<P, SG_INST_FORM, false>();
+static void* mma_ptr() {
+    constexpr TileChoice tc = mma_tile(SG_INST_NDIM, P, SG_INST_FORM, kRat);
+    constexpr bool fits = mma_geom(SG_INST_NDIM, P, SG_INST_FORM, kRat, tc.T0, tc.T1).total * 8 <= 227 * 1024;
+    if constexpr ((SG_INST_FORM == BIHARMONIC && P < 2) || !fits) return nullptr;
+    else return (void*)&assemble_mma<SG_INST_NDIM, P, SG_INST_FORM, kRat>;
 }
 
 #define SG_CAT2(a, b) a##b
 #define SG_CAT(a, b) SG_CAT2(a, b)
+#define SG_NAME SG_CAT(SG_CAT(SG_CAT(kernel_ptr_, SG_INST_NDIM), SG_CAT(_, SG_INST_FORM)), SG_CAT(_, SG_INST_RAT))
 
-void* SG_CAT(SG_CAT(assemble_kernel_, SG_INST_NDIM), SG_CAT(_, SG_INST_FORM))(int p, bool rat, int* kmax) {
-    *kmax = kmax_for(SG_INST_NDIM);
+// which: 0 = SIMT tile kernel, 1 = DMMA tile kernel, 2 = geometry (K3)
+void* SG_NAME(int which, int p, int* kmax) {
+    if (kmax) *kmax = kmax_for(SG_INST_NDIM);
+    if (which == 2) return (void*)&geom_D_kernel<SG_INST_NDIM, SG_INST_FORM, kRat>;
     switch (p) {
-        case 1: return kptr_p<1>(rat);
-        case 2: return kptr_p<2>(rat);
-        case 3: return kptr_p<3>(rat);
-        case 4: return kptr_p<4>(rat);
-#if SG_MAX_P >= 5
-        case 5: return kptr_p<5>(rat);
-#endif
+        case 1: return which ? mma_ptr<1>() : simt_ptr<1>();
+        case 2: return which ? mma_ptr<2>() : simt_ptr<2>();
+        case 3: return which ? mma_ptr<3>() : simt_ptr<3>();
+        case 4: return which ? mma_ptr<4>() : simt_ptr<4>();
     }
     return nullptr;
-}
-
-void* SG_CAT(SG_CAT(geom_kernel_, SG_INST_NDIM), SG_CAT(_, SG_INST_FORM))(bool rat) {
-    return rat ? (void*)&geom_D_kernel<SG_INST_NDIM, SG_INST_FORM, true> : (void*)&geom_D_kernel<SG_INST_NDIM, SG_INST_FORM, false>;
 }
 
 }  // namespace sg

@@ -70,6 +70,7 @@ struct DevProblem {
 };
 
 struct Plan {
+    bool mma = false;            // fp64 tensor-core tile kernel (sg_tile_mma.cuh) vs SIMT fallback
     void* kfn = nullptr;
     int kmax = 1, nthreads = 512;
     int T[3], tgrid[3], ypad, off[6];

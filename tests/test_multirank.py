@@ -1,0 +1,84 @@
+"""World-size-2 row-slab path on CPU (gloo): slab cover, stitched CSR == full, checksum all-reduce."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_1904_06971_b200.slabs import allreduce_checksum, csr_checksum, plane_slabs, stitch, weighted_plane_slabs
+
+
+def test_plane_slabs_cover_rows_contiguously():
+    ms = (11, 9, 13)
+    for world in (1, 2, 4, 8):
+        sl = plane_slabs(ms, world)
+        assert sl[0][0] == 0 and sl[-1][1] == int(np.prod(ms))
+        assert all(a[1] == b[0] for a, b in zip(sl, sl[1:]))
+        assert all((hi - lo) % (11 * 9) == 0 for lo, hi in sl)
+    with pytest.raises(ValueError):
+        plane_slabs(ms, 14)
+
+
+def test_weighted_slabs_balance_cost():
+    cost = np.r_[np.full(6, 10.0), np.ones(20), np.full(6, 10.0)]
+    sl = weighted_plane_slabs(cost, 100, 2)
+    assert sl[0][0] == 0 and sl[-1][1] == 3200 and sl[0][1] == sl[1][0]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch.distributed as dist
+
+    from oracle import surriga_oracle as O
+    import paper_1904_06971_b200 as pkg
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    disc = pkg.make_discretization(pkg.twisted_cube_standin(), 2, (5, 4, 6))
+    prob = O.problem_from_disc(pkg.FormKind.POISSON, disc)
+    lo, hi = plane_slabs(prob.ms, world)[rank]
+    ip, ix, d, _, _ = O.assemble(prob, rows=np.arange(lo, hi))
+    sl_ip = ip[lo:hi + 1] - ip[lo]
+    cs = allreduce_checksum(csr_checksum(sl_ip, d), dist)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (sl_ip, ix, d))
+    if rank == 0:
+        q.put((cs, gathered))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_slabs_gloo_equal_full():
+    from oracle import surriga_oracle as O
+    import paper_1904_06971_b200 as pkg
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    cs, parts = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    disc = pkg.make_discretization(pkg.twisted_cube_standin(), 2, (5, 4, 6))
+    ip, ix, d, _, _ = O.assemble(O.problem_from_disc(pkg.FormKind.POISSON, disc))
+    sip, six, sd = stitch(parts)
+    assert np.array_equal(sip, ip) and np.array_equal(six, ix)
+    assert np.array_equal(sd.view(np.int64), d.view(np.int64))  # restricted rows are bitwise the full rows
+    full = csr_checksum(ip, d)
+    assert cs[0] == full[0]
+    assert np.allclose(cs[1:], full[1:], rtol=1e-12, atol=1e-12)

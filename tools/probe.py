@@ -27,7 +27,7 @@ for k in which:
                 cs = res.checksum()
             res.free()
             best = min(best, ms)
-        ka = [v for n, v in kt if n == "assemble_tiles"]
+        ka = [v for n, v in kt if n.startswith("assemble_")]
         print(f"cfg{k} {f:10s} N={nr} nnz={nnz} total {best:.3f} ms  assemble_tiles {ka[0]:.3f} ms  "
               f"nnz/s {nnz / best * 1e3:.3e}  launches {nl}  setup {ts:.1f}s  checksum {cs[1]:.6e} {cs[4]:.3e}", flush=True)
         print("   ", [(n, round(v, 3)) for n, v in kt], flush=True)
