@@ -381,6 +381,8 @@ int compute_D(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* t
     gp.hom = dp.hom;
     gp.coef = dp.pr.coefficient;
     gp.U = U;
+    gp.Dys = n >= 2 ? ((gp.Gp[1] + 1) & ~1) : 1;
+    dp.Dys = gp.Dys;
     gp.BX = n == 1 ? 256 : 32;
     gp.BY = n >= 2 ? 32 : 1;
     gp.nbx = (gp.Gp[0] + gp.BX - 1) / gp.BX;
@@ -427,7 +429,7 @@ int compute_D(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* t
     }
     const size_t smem = o * sizeof(double);
     if (smem > kSmemCap) return fail(-2, "geometry block does not fit shared memory (%zu B)", smem);
-    const size_t npts = (size_t)gp.Gp[0] * gp.Gp[1] * gp.Gp[2];
+    const size_t npts = (size_t)gp.Gp[0] * gp.Dys * gp.Gp[2];
     gp.D = (double*)c.alloc(sizeof(double) * npts * U, true);
     if (!gp.D) return fail(-4, "device allocation of the D tensor failed (%zu MB)", sizeof(double) * npts * U >> 20);
     dp.D = gp.D;
@@ -461,6 +463,30 @@ int compute_D(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* t
     cudaError_t e = cudaLaunchKernel(kfn, dim3((unsigned)nb), dim3(256), args, smem, c.stream);
     c.kend();
     if (e != cudaSuccess) return fail(-3, "geometry launch failed: %s", cudaGetErrorString(e));
+    return 0;
+}
+
+// TMA descriptor of the D tensor [Gp2][U][Gp0][Dys] (fetched through the runtime's driver entry point)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static int encode_dmap(CUtensorMap* map, const double* D, int Dys, const int Gp[3], int U, int DY, int XW) {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+            return fail(-3, "cuTensorMapEncodeTiled unavailable");
+        fn = (EncodeTiledFn)p;
+    }
+    cuuint64_t dims[4] = {(cuuint64_t)Gp[1], (cuuint64_t)Gp[0], (cuuint64_t)U, (cuuint64_t)Gp[2]};
+    cuuint64_t strides[3] = {(cuuint64_t)Dys * 8, (cuuint64_t)Gp[0] * Dys * 8, (cuuint64_t)U * Gp[0] * Dys * 8};
+    cuuint32_t box[4] = {(cuuint32_t)DY, (cuuint32_t)XW, (cuuint32_t)U, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)D, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(-3, "cuTensorMapEncodeTiled failed (%d): box {%d,%d,%d,1}", (int)r, DY, XW, U);
     return 0;
 }
 
@@ -536,6 +562,12 @@ int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>
         mp.T2 = pl.T[2];
         mp.sol_w = dp.sol_w;
         mp.D = dp.D;
+        if (dp.n >= 2) {
+            const TileChoice tc = mma_tile(dp.n, dp.p, dp.pr.form, dp.rational);
+            const MmaGeom M = mma_geom(dp.n, dp.p, dp.pr.form, dp.rational, tc.T0, tc.T1);
+            int rc2 = encode_dmap(&mp.dmap, dp.D, dp.Dys, mp.Gp, M.U, M.DY, M.XW);
+            if (rc2) return rc2;
+        }
         mp.rowmask = d_rowmask;
         mp.rowstart = d_rowstart;
         mp.slab_lo = slab_lo;
@@ -573,6 +605,7 @@ int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>
     }
     prm.sol_w = dp.sol_w;
     prm.D = dp.D;
+    prm.Dys = dp.Dys;
     prm.ypad = pl.ypad;
     int* offs[6] = {&prm.off_B0, &prm.off_B1, &prm.off_D, &prm.off_T1, &prm.off_T2, &prm.off_misc};
     for (int k = 0; k < 6; ++k) *offs[k] = pl.off[k];

@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(512, 1) assemble_tiles(const AsmParams prm) {
     if constexpr (NDIM >= 2)
         for (int it = tid; it < X[1] * NB; it += nt) B1s[it] = prm.B[1][(long long)elo[1] * g * NB + it];
     const long long xw0 = (long long)elo[0] * g, yw0 = (long long)elo[1] * g;
-    const long long G0 = prm.Gp[0], G1 = prm.Gp[1];
+    const long long G0 = prm.Gp[0], G1 = prm.Dys;
 
     const int nlayer = (NDIM == 3) ? NE[2] : 1;
     const int gz = (NDIM == 3) ? g : 1;

@@ -293,8 +293,9 @@ struct AsmParams {
     int m[3], S[3];              // basis counts, spans (1 for unused directions)
     const double* B[3];          // solution tables  [S*g][nu+1][p+1]
     const double* sol_w;         // N (rational) or nullptr
-    const double* D;             // per-point form tensor from K3, [Gp2][U][Gp0][Gp1]
+    const double* D;             // per-point form tensor from K3, [Gp2][U][Gp0][Dys]
     int Gp[3];                   // Gauss points per direction
+    int Dys;                     // y stride of D
     // tiling
     int T[3];                    // rows per tile per direction
     int tgrid[3];                // tiles per direction

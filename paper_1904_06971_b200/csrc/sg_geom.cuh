@@ -345,7 +345,8 @@ struct GeomParams {
     int GN0, GN1, WN0, WN1;  // smem bounds of function ranges
     int off_G0, off_G1, off_gs0, off_gs1, off_B0, off_B1, off_ws0, off_ws1, off_Hz, off_Hy, off_Wz, off_Wy, off_misc;
     int U;
-    double* D;               // [Gp2][U][Gp0][Gp1]
+    int Dys;                 // y stride of D (Gp1 rounded up to even: 16-byte rows for TMA)
+    double* D;               // [Gp2][U][Gp0][Dys]
 };
 
 template <int NDIM, int FORM, bool RAT>
@@ -431,7 +432,7 @@ __global__ void __launch_bounds__(256) geom_D_kernel(const GeomParams prm) {
         const long long plane = (long long)z * U;
 #pragma unroll
         for (int u = 0; u < U; ++u)
-            prm.D[((plane + u) * prm.Gp[0] + x0 + x) * (long long)prm.Gp[1] + y0 + y] = Dp[u];
+            prm.D[((plane + u) * prm.Gp[0] + x0 + x) * (long long)prm.Dys + y0 + y] = Dp[u];
     }
 }
 

@@ -64,6 +64,7 @@ struct DevProblem {
     double* hom = nullptr;
     double* sol_w = nullptr;
     double* D = nullptr;
+    int Dys = 1;
     int64_t last_tiles = 0;
     int last_T[3];
     size_t last_smem = 0;

@@ -19,6 +19,8 @@
 // no atomics).  The Gauss count is a template constant (G = p + 1); other counts use the SIMT
 // kernel (sg_assemble.cuh).
 #pragma once
+#include <cuda.h>
+
 #include "sg_common.cuh"
 
 namespace sg {
@@ -61,6 +63,51 @@ __host__ __device__ constexpr int g1_units(const Tables& T) { return g1_unit_bas
 __host__ __device__ constexpr int kind1(const Tables& T, int ga) { return (T.g1key[ga] % 3) + 3 * ((T.g1key[ga] / 3) % 3); }
 __host__ __device__ constexpr int kind2(const Tables& T, int g2) { return T.g2key[g2]; }  // a2 + 3 b2
 
+// compact slots of the derivative-order kinds actually used (phase-2 / phase-3 fragment tables)
+__host__ __device__ constexpr int kslot1(const Tables& T, int kind) {
+    int slot = 0;
+    for (int k = 0; k < 9; ++k) {
+        bool used = false;
+        for (int g = 0; g < T.NG1; ++g) used = used || kind1(T, g) == k;
+        if (!used) continue;
+        if (k == kind) return slot;
+        ++slot;
+    }
+    return -1;
+}
+__host__ __device__ constexpr int nkind1(const Tables& T) {
+    int n = 0;
+    for (int k = 0; k < 9; ++k) n += kslot1(T, k) >= 0 ? 1 : 0;
+    return n;
+}
+__host__ __device__ constexpr int kslot2(const Tables& T, int kind) {
+    int slot = 0;
+    for (int k = 0; k < 9; ++k) {
+        bool used = false;
+        for (int g = 0; g < T.NG2; ++g) used = used || kind2(T, g) == k;
+        if (!used) continue;
+        if (k == kind) return slot;
+        ++slot;
+    }
+    return -1;
+}
+__host__ __device__ constexpr int nkind2(const Tables& T) {
+    int n = 0;
+    for (int k = 0; k < 9; ++k) n += kslot2(T, k) >= 0 ? 1 : 0;
+    return n;
+}
+__host__ __device__ constexpr int kind_of_slot1(const Tables& T, int slot) {
+    for (int k = 0; k < 9; ++k)
+        if (kslot1(T, k) == slot) return k;
+    return 0;
+}
+__host__ __device__ constexpr int kind_of_slot2(const Tables& T, int slot) {
+    for (int k = 0; k < 9; ++k)
+        if (kslot2(T, k) == slot) return k;
+    return 0;
+}
+__host__ __device__ constexpr long align16(long o) { return (o + 15) & ~15L; }
+
 __host__ __device__ constexpr int pad16_4(int v) {  // smallest w >= v with w % 16 == 4 (conflict-free fragments)
     int w = v;
     while (w % 16 != 4) ++w;
@@ -69,8 +116,8 @@ __host__ __device__ constexpr int pad16_4(int v) {  // smallest w >= v with w % 
 
 // ---- compile-time tile geometry (shared by host planning and the kernel)
 struct MmaGeom {
-    int T0, T1, G, W, MT, KS, KS3, XW, YW, NTY, DY, TY, NCOMBO, NMT, CH, NCH, TC, U, NG1, NG2, NU1, NB;
-    long o_B0, o_B1, o_B2, o_A1, o_B2f, o_B3f, o_cmb, o_D, o_T1, o_T2, total;
+    int T0, T1, G, W, MT, KS, KS3, XW, YW, NTY, DY, TY, NCOMBO, NMT, CH, NCH, TC, U, NG1, NG2, NU1, NB, NK1, NK2;
+    long o_B0, o_B1, o_B2, o_A1, o_B2f, o_B3f, o_cmb, o_bar, o_D, o_D2, o_T1, o_T2, total;
 };
 
 __host__ __device__ constexpr MmaGeom mma_geom(int ndim, int P, int form, bool rat, int T0, int T1) {
@@ -98,15 +145,20 @@ __host__ __device__ constexpr MmaGeom mma_geom(int ndim, int P, int form, bool r
     m.NG2 = ndim == 3 ? T.NG2 : 1;
     m.NU1 = g1_units(T);
     m.NB = (form_deriv(form) + 1) * (P + 1);
+    m.NK1 = nkind1(T);
+    m.NK2 = ndim == 3 ? nkind2(T) : 0;
     long o = 0;
     m.o_B0 = o; o += (long)m.XW * m.NB + 2;
     m.o_B1 = o; o += ndim >= 2 ? (long)m.YW * m.NB + 2 : 0;
     m.o_B2 = o; o += ndim == 3 ? (long)m.G * m.NB + 2 : 0;
     m.o_A1 = o; o += (long)T0 * m.NU1 * m.KS * m.MT * 32;                      // phase-1 A fragments
-    m.o_B2f = o; o += ndim >= 2 ? (long)m.T1 * 9 * m.KS * m.MT * 32 : 0;         // phase-2 B fragments
-    m.o_B3f = o; o += ndim == 3 ? (long)(P + 1) * 9 * m.KS3 * m.MT * 32 : 0;     // phase-3 B fragments
-    m.o_cmb = o; o += ndim == 3 ? (long)m.NCOMBO + 2 : 0;                      // per-combo CSR offsets
-    m.o_D = o; o += (long)m.U * m.XW * m.DY;
+    m.o_B2f = o; o += ndim >= 2 ? (long)m.T1 * m.NK1 * m.KS * m.MT * 32 : 0;     // phase-2 B fragments
+    m.o_B3f = o; o += ndim == 3 ? (long)(P + 1) * m.NK2 * m.KS3 * m.MT * 32 : 0; // phase-3 B fragments
+    m.o_cmb = o; o += ndim == 3 ? (long)m.NCOMBO / 2 + 2 : 0;                  // per-combo CSR offsets (int)
+    m.o_bar = o; o += 2;                                                       // two mbarriers (TMA)
+    o = align16(o);
+    m.o_D = o; o += align16((long)m.U * m.XW * m.DY);                          // D window, double buffered (TMA)
+    m.o_D2 = o; o += align16((long)m.U * m.XW * m.DY);
     m.o_T1 = o; o += ndim >= 2 ? (long)m.NG1 * T0 * m.MT * 8 * m.TY : 0;
     m.o_T2 = o; o += ndim == 3 ? (long)m.NG2 * m.G * m.TC : 0;
     m.total = o;
@@ -130,6 +182,7 @@ __host__ __device__ constexpr TileChoice mma_tile(int ndim, int P, int form, boo
 }
 
 struct MmaParams {
+    CUtensorMap dmap;            // TMA map of D: dims {Gp1, Gp0, U, Gp2} (y fastest), box {DY, XW, U, 1}
     int m[3], S[3];
     const double* B[3];          // solution tables  [S*g][nu+1][p+1]
     const double* sol_w;
@@ -146,7 +199,7 @@ struct MmaParams {
 };
 
 template <int NDIM, int P, int FORM, bool RAT>
-__global__ void __launch_bounds__(512, 1) assemble_mma(const MmaParams prm) {
+__global__ void __launch_bounds__(512, 1) assemble_mma(const __grid_constant__ MmaParams prm) {
     using TTS = TermTables<NDIM, FORM, RAT>;
     constexpr TileChoice TCH = mma_tile(NDIM, P, FORM, RAT);
     constexpr MmaGeom M = mma_geom(NDIM, P, FORM, RAT, TCH.T0, TCH.T1);
@@ -154,6 +207,8 @@ __global__ void __launch_bounds__(512, 1) assemble_mma(const MmaParams prm) {
     constexpr int NB = M.NB, XW = M.XW, YW = M.YW, NTY = M.NTY, DY = M.DY, TY = M.TY, TC = M.TC;
     constexpr int MS = TTS::T.MS;
     constexpr int NW = 16;
+    constexpr int NK1 = M.NK1, NK2 = M.NK2;
+    constexpr unsigned DBYTES = (unsigned)(M.U * XW * DY * 8);
     extern __shared__ double smem[];
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
@@ -173,7 +228,8 @@ __global__ void __launch_bounds__(512, 1) assemble_mma(const MmaParams prm) {
     double* B2f = smem + M.o_B2f;
     double* B3f = smem + M.o_B3f;
     int* cmb = reinterpret_cast<int*>(smem + M.o_cmb);
-    double* Ds = smem + M.o_D;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + M.o_bar);
+    double* Dbuf[2] = {smem + M.o_D, smem + M.o_D2};
     double* T1s = smem + M.o_T1;
     double* T2s = smem + M.o_T2;
 
@@ -223,11 +279,12 @@ __global__ void __launch_bounds__(512, 1) assemble_mma(const MmaParams prm) {
         });
     });
     if constexpr (NDIM >= 2) {
-        // B2f[((i1l*9 + kind)*KS + kk)*MT + c][lane] = Q1(i1, i1+d1, y): d1 = c*8 + lr - P
-        for (int it = warp; it < T1 * 9; it += NW) {
-            const int i1l = it % T1, kind = it / T1;
+        // B2f[((i1l*NK1 + slot)*KS + kk)*MT + c][lane] = Q1(i1, i1+d1, y): d1 = c*8 + lr - P
+        for (int it = warp; it < T1 * NK1; it += NW) {
+            const int i1l = it % T1, slot = it / T1;
+            int kind = 0;
+            static_for<0, NK1>([&](auto SI) { if (slot == decltype(SI)::value) kind = kind_of_slot1(TTS::T, decltype(SI)::value); });
             const int a1 = kind % 3, bb1 = kind / 3;
-            if (a1 > form_deriv(FORM) || bb1 > form_deriv(FORM)) continue;
             for (int kk = 0; kk < KS; ++kk) {
                 const int s = kk * 4 + lk;
                 const int ei = s / G, q = s % G;
@@ -241,7 +298,7 @@ __global__ void __launch_bounds__(512, 1) assemble_mma(const MmaParams prm) {
                         const double* by = B1s + y * NB;
                         v = __dmul_rn(by[a1 * (P + 1) + ri1], by[bb1 * (P + 1) + rj1]);
                     }
-                    B2f[(((i1l * 9 + kind) * KS + kk) * MT + c) * 32 + lane] = v;
+                    B2f[(((i1l * NK1 + slot) * KS + kk) * MT + c) * 32 + lane] = v;
                 }
             }
         }
@@ -261,21 +318,47 @@ __global__ void __launch_bounds__(512, 1) assemble_mma(const MmaParams prm) {
         }
     }
 
-    const long long G0 = prm.Gp[0], G1 = prm.Gp[1];
+    const long long G0 = prm.Gp[0];
     const int elo2 = NDIM == 3 ? max(0, b2 - P) : 0;
     const int ehi2 = NDIM == 3 ? min(prm.S[2] - 1, b2 + prm.T2 - 1) : 0;
     constexpr int GZ = NDIM == 3 ? G : 1;
+    const int nplanes = (ehi2 - elo2 + 1) * GZ;
+    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&bars[0]);
+    // D window of plane `pi` (TMA: one 4D box per plane; out-of-mesh coordinates are zero filled)
+    auto issue_plane = [&](int pi) {
+        const int z = elo2 * G + pi;
+        const uint32_t bar = bar0 + 8u * (uint32_t)(pi & 1);
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(Dbuf[pi & 1]);
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(DBYTES) : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(dst),
+            "l"(reinterpret_cast<uint64_t>(&prm.dmap)), "r"(ew1 * G), "r"(ew0 * G), "r"(0), "r"(z), "r"(bar)
+            : "memory");
+    };
+    if constexpr (NDIM >= 2) {
+        if (tid == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0 + 8u) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncthreads();
+        if (tid == 0) issue_plane(0);
+    }
+    int pidx = 0;
+    (void)nplanes;
 
     for (int e2 = elo2; e2 <= ehi2; ++e2) {
         if constexpr (NDIM == 3) {
             __syncthreads();
             for (int it = tid; it < G * NB; it += blockDim.x) B2s[it] = prm.B[2][(long long)e2 * G * NB + it];
             __syncthreads();
-            // phase-3 B fragments of this layer: B3f[((r2*9 + kind)*KS3 + kk)*MT + c][lane]
-            for (int it = warp; it < (P + 1) * 9; it += NW) {
-                const int r2 = it % (P + 1), kind = it / (P + 1);
+            // phase-3 B fragments of this layer: B3f[((r2*NK2 + slot)*KS3 + kk)*MT + c][lane]
+            for (int it = warp; it < (P + 1) * NK2; it += NW) {
+                const int r2 = it % (P + 1), slot = it / (P + 1);
+                int kind = 0;
+                static_for<0, NK2>([&](auto SI) { if (slot == decltype(SI)::value) kind = kind_of_slot2(TTS::T, decltype(SI)::value); });
                 const int a2 = kind % 3, bb2 = kind / 3;
-                if (a2 > form_deriv(FORM) || bb2 > form_deriv(FORM)) continue;
                 for (int kk = 0; kk < KS3; ++kk) {
                     const int s = kk * 4 + lk;
                     for (int c = 0; c < MT; ++c) {
@@ -286,29 +369,36 @@ __global__ void __launch_bounds__(512, 1) assemble_mma(const MmaParams prm) {
                             const double* bz = B2s + s * NB;
                             v = __dmul_rn(bz[a2 * (P + 1) + r2], bz[bb2 * (P + 1) + rj2]);
                         }
-                        B3f[(((r2 * 9 + kind) * KS3 + kk) * MT + c) * 32 + lane] = v;
+                        B3f[(((r2 * NK2 + slot) * KS3 + kk) * MT + c) * 32 + lane] = v;
                     }
                 }
             }
         }
         for (int q2 = 0; q2 < GZ; ++q2) {
-            // ---------------- D window of this plane (zero outside the mesh / past the window)
-            {
-                const long long z = (long long)e2 * G + q2;
-                const long long gx0 = (long long)ew0 * G, gy0 = (long long)ew1 * G;
-                constexpr int ROWS = M.U * XW;
-                constexpr int YC = NTY * 8;
-                for (int it = tid; it < ROWS * YC; it += blockDim.x) {
-                    const int y = it % YC, r = it / YC;
-                    const int u = r / XW, x = r % XW;
-                    const long long gx = gx0 + x, gy = gy0 + y;
-                    double v = 0.0;
-                    if (y < YW && gx >= 0 && gx < G0 && (NDIM < 2 || (gy >= 0 && gy < G1)))
-                        v = prm.D[((z * M.U + u) * G0 + gx) * G1 + (NDIM >= 2 ? gy : 0)];
-                    Ds[r * DY + y] = v;
+            // ---------------- D window of this plane
+            double* Ds = Dbuf[pidx & 1];
+            if constexpr (NDIM >= 2) {
+                if (tid == 0 && pidx + 1 < nplanes) issue_plane(pidx + 1);  // prefetch the next plane
+                const uint32_t bar = bar0 + 8u * (uint32_t)(pidx & 1);
+                const uint32_t par = (uint32_t)((pidx >> 1) & 1);
+                uint32_t done = 0;
+                while (!done) {
+                    asm volatile(
+                        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                        : "=r"(done)
+                        : "r"(bar), "r"(par)
+                        : "memory");
                 }
+            } else {
+                const long long gx0 = (long long)ew0 * G;
+                for (int it = tid; it < M.U * XW * 8; it += blockDim.x) {
+                    const int y = it % 8, r = it / 8;
+                    const int u = r / XW, x = r % XW;
+                    const long long gx = gx0 + x;
+                    Ds[r * DY + y] = (y == 0 && gx >= 0 && gx < G0) ? prm.D[(long long)u * G0 + gx] : 0.0;
+                }
+                __syncthreads();
             }
-            __syncthreads();
 
             // ---------------- phase 1: items (group, row i0l), statically scheduled over warps
             static_for<0, M.NG1 * T0>([&](auto KI) {
@@ -402,8 +492,8 @@ __global__ void __launch_bounds__(512, 1) assemble_mma(const MmaParams prm) {
                                 }
                     auto block = [&](auto GA, auto& acc) {
                         constexpr int ga = decltype(GA)::value;
-                        constexpr int kd = kind1(TTS::T, ga);
-                        const double* bfp = B2f + ((i1l * 9 + kd) * KS) * MT * 32 + lane;
+                        constexpr int kd = kslot1(TTS::T, kind1(TTS::T, ga));
+                        const double* bfp = B2f + ((i1l * NK1 + kd) * KS) * MT * 32 + lane;
                         // y of support point s of row i1 is i1l*G + s (the support is contiguous)
                         const double* t1 = T1s + ((ga * T0) * MT * 8 + lr) * TY + i1l * G + lk;
 #pragma unroll
@@ -496,6 +586,7 @@ __global__ void __launch_bounds__(512, 1) assemble_mma(const MmaParams prm) {
                 });
             }
             __syncthreads();
+            ++pidx;
         }  // q2
         if constexpr (NDIM == 3) {
             // ---------------- phase 3: items (row offset r2 in the layer, chunk of CH m-tiles)
@@ -507,6 +598,33 @@ __global__ void __launch_bounds__(512, 1) assemble_mma(const MmaParams prm) {
                 const int r2 = item % (P + 1), ch = item / (P + 1);
                 const int i2 = e2 + r2;
                 if (i2 < b2 || i2 >= b2 + prm.T2 || i2 >= prm.m[2]) continue;
+                // CSR position of every output of this item (lane: rows lr of CH m-tiles, columns 2*lk+h)
+                // and the previously accumulated layers' partial sums, loaded before the MMA chain
+                const int lo2 = max(0, i2 - P);
+                int64_t pos[CH][MT][2];
+                double old[CH][MT][2];
+#pragma unroll
+                for (int mm = 0; mm < CH; ++mm) {
+                    const int combo = (ch * CH + mm) * 8 + lr;
+                    const int off = combo < M.NCOMBO ? cmb[combo] : -1;
+                    const int i1l = (combo / (W * W)) % T1, i0l = combo / (W * W * T1);
+                    const int i0 = b0 + i0l, i1 = b1 + i1l;
+                    const int64_t row = (int64_t)i0 + (int64_t)prm.m[0] * i1 + (int64_t)m01 * i2;
+                    bool ok = off >= 0 && row >= prm.slab_lo && row < prm.slab_hi && (!prm.rowmask || prm.rowmask[row]);
+                    const int cnt01 = ok ? (min(prm.m[0] - 1, i0 + P) - max(0, i0 - P) + 1) * (min(prm.m[1] - 1, i1 + P) - max(0, i1 - P) + 1) : 0;
+                    const int64_t base = ok ? prm.rowstart[row] + off : 0;
+#pragma unroll
+                    for (int c = 0; c < MT; ++c)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int d2 = c * 8 + 2 * lk + h - P;
+                            const int rj2 = r2 + d2;
+                            const bool v = ok && d2 <= P && rj2 >= 0 && rj2 <= P;
+                            pos[mm][c][h] = v ? base + (int64_t)cnt01 * (i2 + d2 - lo2) : -1;
+                            const int first = max(0, max(i2, i2 + d2) - P);
+                            old[mm][c][h] = (v && e2 != first) ? prm.data[pos[mm][c][h]] : 0.0;
+                        }
+                }
                 double accS[CH][MT][2];
                 double accA[NA][CH][MT][2];
                 double accB[NA][CH][MT][2];
@@ -522,8 +640,8 @@ __global__ void __launch_bounds__(512, 1) assemble_mma(const MmaParams prm) {
                         }
                 auto block = [&](auto GA, auto& acc) {
                     constexpr int ga = decltype(GA)::value;
-                    constexpr int kd = kind2(TTS::T, ga);
-                    const double* bfp = B3f + ((r2 * 9 + kd) * KS3) * MT * 32 + lane;
+                    constexpr int kd = kslot2(TTS::T, kind2(TTS::T, ga));
+                    const double* bfp = B3f + ((r2 * NK2 + kd) * KS3) * MT * 32 + lane;
 #pragma unroll
                     for (int kk = 0; kk < KS3; ++kk) {
                         double bfs[MT];
@@ -550,44 +668,34 @@ __global__ void __launch_bounds__(512, 1) assemble_mma(const MmaParams prm) {
                         block(std::integral_constant<int, TTS::T.g2T[ga]>{}, accB[pi]);
                     }
                 });
-                const int lo2 = max(0, i2 - P);
 #pragma unroll
                 for (int mm = 0; mm < CH; ++mm) {
                     const int combo = (ch * CH + mm) * 8 + lr;
-                    if (combo >= M.NCOMBO) continue;
-                    const int off = cmb[combo];
-                    if (off < 0) continue;
                     const int i1l = (combo / (W * W)) % T1, i0l = combo / (W * W * T1);
                     const int i0 = b0 + i0l, i1 = b1 + i1l;
-                    const int64_t row = (int64_t)i0 + (int64_t)prm.m[0] * i1 + (int64_t)m01 * i2;
-                    if (row < prm.slab_lo || row >= prm.slab_hi || (prm.rowmask && !prm.rowmask[row])) continue;
-                    const int cnt01 = (min(prm.m[0] - 1, i0 + P) - max(0, i0 - P) + 1) * (min(prm.m[1] - 1, i1 + P) - max(0, i1 - P) + 1);
-                    const int64_t base = prm.rowstart[row] + off;
                     const int d0 = combo % W - P, d1 = (combo / W) % W - P;
+                    const int64_t row = (int64_t)i0 + (int64_t)prm.m[0] * i1 + (int64_t)m01 * i2;
                     const int64_t colb = (int64_t)(i0 + d0) + (int64_t)prm.m[0] * (i1 + d1);
-                    const double si = RAT ? prm.sol_w[row] : 1.0;
 #pragma unroll
                     for (int c = 0; c < MT; ++c)
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
-                            const int d2 = c * 8 + 2 * lk + h - P;
-                            const int rj2 = r2 + d2;
-                            if (d2 > P || rj2 < 0 || rj2 > P) continue;  // j2 not supported on this layer
-                            const int j2 = i2 + d2;
+                            const int64_t p = pos[mm][c][h];
+                            if (p < 0) continue;
+                            const int j2 = i2 + c * 8 + 2 * lk + h - P;
                             double v = accS[mm][c][h];
 #pragma unroll
                             for (int kx = 0; kx < NFP; ++kx) v = __dadd_rn(v, __dadd_rn(accA[kx][mm][c][h], accB[kx][mm][c][h]));
-                            const int64_t pos = base + (int64_t)cnt01 * (j2 - lo2);
                             const int first = max(0, max(i2, j2) - P);
                             const int last = min(min(i2, j2), prm.S[2] - 1);
-                            if (e2 != first) v = prm.data[pos] + v;
+                            if (e2 != first) v = old[mm][c][h] + v;
                             const int64_t col = colb + (int64_t)m01 * j2;
                             if (e2 == last) {
-                                if constexpr (RAT) v = v * (si * prm.sol_w[col]);
+                                if constexpr (RAT) v = v * (prm.sol_w[row] * prm.sol_w[col]);
                                 if (prm.zeros && v == 0.0) atomicAdd(prm.zeros, 1ull);
                             }
-                            if (e2 == first) prm.indices[pos] = (int)col;
-                            prm.data[pos] = v;
+                            if (e2 == first) prm.indices[p] = (int)col;
+                            prm.data[p] = v;
                         }
                 }
             }
