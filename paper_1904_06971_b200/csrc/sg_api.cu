@@ -407,18 +407,18 @@ int compute_D(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* t
     const int NCw = n == 3 ? (NU + 1) * (NU + 2) / 2 : NU + 1;
     size_t sz[13];
     sz[0] = (size_t)gp.BX * NBG;
-    sz[1] = n >= 2 ? (size_t)gp.BY * NBG : 0;
+    sz[1] = n >= 2 ? (size_t)gp.BY * (NBG | 1) : 0;
     sz[2] = gp.BX / 2 + 1;
     sz[3] = gp.BY / 2 + 1;
     sz[4] = dp.rational ? (size_t)gp.BX * NB : 0;
-    sz[5] = (dp.rational && n >= 2) ? (size_t)gp.BY * NB : 0;
+    sz[5] = (dp.rational && n >= 2) ? (size_t)gp.BY * (NB | 1) : 0;
     sz[6] = gp.BX / 2 + 1;
     sz[7] = gp.BY / 2 + 1;
     sz[8] = n == 3 ? (size_t)gp.GN0 * gp.GN1 * C * (NUG + 1) : 0;
-    sz[9] = n >= 2 ? (size_t)gp.BY * gp.GN0 * C * NCg : 0;
+    sz[9] = n >= 2 ? (size_t)gp.BX * gp.GN1 * C * NCg : 0;
     sz[10] = (n == 3 && dp.rational) ? (size_t)gp.WN0 * gp.WN1 * (NU + 1) : 0;
-    sz[11] = (n >= 2 && dp.rational) ? (size_t)gp.BY * gp.WN0 * NCw : 0;
-    sz[12] = 32 + NB + 8;
+    sz[11] = (n >= 2 && dp.rational) ? (size_t)gp.BX * gp.WN1 * NCw : 0;
+    sz[12] = 64 + gp.BX + gp.BY + 8;
     int* offs[13] = {&gp.off_G0, &gp.off_G1, &gp.off_gs0, &gp.off_gs1, &gp.off_B0, &gp.off_B1, &gp.off_ws0,
                      &gp.off_ws1, &gp.off_Hz, &gp.off_Hy, &gp.off_Wz, &gp.off_Wy, &gp.off_misc};
     size_t o = 0;
@@ -562,10 +562,12 @@ int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>
         mp.T2 = pl.T[2];
         mp.sol_w = dp.sol_w;
         mp.D = dp.D;
-        if (dp.n >= 2) {
+        mp.Dys = dp.Dys;
+        mp.tma = getenv("SG_NO_TMA") ? 0 : 1;
+        if (dp.n == 3 || (dp.n == 2 && dp.p == 3)) {
             const TileChoice tc = mma_tile(dp.n, dp.p, dp.pr.form, dp.rational);
             const MmaGeom M = mma_geom(dp.n, dp.p, dp.pr.form, dp.rational, tc.T0, tc.T1);
-            int rc2 = encode_dmap(&mp.dmap, dp.D, dp.Dys, mp.Gp, M.U, M.DY, M.XW);
+            int rc2 = encode_dmap(&mp.dmap, dp.D, dp.Dys, mp.Gp, M.U, M.DY, M.XWp);
             if (rc2) return rc2;
         }
         mp.rowmask = d_rowmask;

@@ -21,17 +21,23 @@ template <int NDIM, int NU>
 struct NC12 { static constexpr int v = NDIM == 3 ? (NU + 1) * (NU + 2) / 2 : NU + 1; };
 
 // ---------------------------------------------------------------------------------------------
-// plane preparation of a tensor field sum_{i} c_i B_i(x) (geometry or weight function):
-//   3D: Hz[i1][i0][c][a2] = sum_r2 tz[a2][r2] coef[i0, i1, sz-deg+r2]
-//       Hy[y][i0][c][c12(a1,a2)] = sum_r1 t1[y][a1][r1] Hz[s1(y)-deg+r1][i0][c][a2]
-//   2D: Hy[y][i0][c][a1]        = sum_r1 t1[y][a1][r1] coef[i0, s1(y)-deg+r1]
+// plane preparation of a tensor field sum_i c_i B_i (geometry map or NURBS weight function) on a
+// block of points of one z-plane (x fastest-changing per warp is avoided: a warp shares x):
+//   3D: Hz[i1][i0][c][a2]           = sum_r2 tz[a2][r2] coef[i0, i1, sz-deg+r2]
+//       Hx[x][i1][c][k(a0,a2)]      = sum_r0 t0[x][a0][r0] Hz[i1][s0(x)-deg+r0][c][a2]
+//   2D: Hx[x][i1][c][a0]            = sum_r0 t0[x][a0][r0] coef[s0(x)-deg+r0, i1]
+// then per point (x, y): out[c][a0+3a1+9a2] = sum_r1 t1[y][a1][r1] Hx[x][s1(y)-deg+r1][c][k(a0,a2)]
 // ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ constexpr int k02(int a0, int a2) { return (a0 + a2) * (a0 + a2 + 1) / 2 + a2; }
+template <int NDIM, int NU>
+struct NCx { static constexpr int v = NDIM == 3 ? (NU + 1) * (NU + 2) / 2 : NU + 1; };
+
 template <int NDIM, int NU, int C>
-__device__ void field_plane_prep(const double* __restrict__ coef, int deg, const int* md, const double* t1,
-                                 const int* s1, int Y, const double* tz, int sz, int lo0, int n0, int lo1, int n1,
-                                 double* Hz, double* Hy) {
+__device__ void field_plane_prep(const double* __restrict__ coef, int deg, const int* md, const double* t0, int ts0,
+                                 const int* s0, int X, const double* tz, int sz, int lo0, int n0, int lo1, int n1,
+                                 double* Hz, double* Hx, int hxs) {
     const int tid = threadIdx.x, nt = blockDim.x;
-    constexpr int NC = NC12<NDIM, NU>::v;
+    constexpr int NC = NCx<NDIM, NU>::v;
     if constexpr (NDIM == 3) {
         const int items = n0 * n1 * C;
         for (int it = tid; it < items; it += nt) {
@@ -55,67 +61,68 @@ __device__ void field_plane_prep(const double* __restrict__ coef, int deg, const
         __syncthreads();
     }
     if constexpr (NDIM >= 2) {
-        const int items = Y * n0 * C;
+        const int items = X * n1 * C;
         for (int it = tid; it < items; it += nt) {
             const int c = it % C;
-            const int i0 = (it / C) % n0;
-            const int y = it / (C * n0);
-            const int sy = s1[y];
+            const int i1 = (it / C) % n1;
+            const int x = it / (C * n1);
+            const int sx = s0[x];
             double acc[NC];
 #pragma unroll
             for (int k = 0; k < NC; ++k) acc[k] = 0.0;
             for (int r = 0; r <= deg; ++r) {
                 if constexpr (NDIM == 3) {
-                    const double* hz = Hz + (((sy - deg + r - lo1) * n0 + i0) * C + c) * (NU + 1);
+                    const double* hz = Hz + ((i1 * n0 + (sx - deg + r - lo0)) * C + c) * (NU + 1);
 #pragma unroll
-                    for (int a1 = 0; a1 <= NU; ++a1) {
-                        const double b = t1[(y * (NU + 1) + a1) * (deg + 1) + r];
+                    for (int a0 = 0; a0 <= NU; ++a0) {
+                        const double b = t0[x * ts0 + a0 * (deg + 1) + r];
 #pragma unroll
-                        for (int a2 = 0; a2 + a1 <= NU; ++a2) acc[c12<3>(a1, a2)] = fma(b, hz[a2], acc[c12<3>(a1, a2)]);
+                        for (int a2 = 0; a2 + a0 <= NU; ++a2) acc[k02(a0, a2)] = fma(b, hz[a2], acc[k02(a0, a2)]);
                     }
                 } else {
-                    const int g0 = lo0 + i0;
-                    const double v = (g0 < md[0]) ? coef[((long long)g0 + (long long)md[0] * (sy - deg + r)) * C + c] : 0.0;
+                    const int g1 = lo1 + i1;
+                    const double v = (g1 < md[1]) ? coef[((long long)(sx - deg + r) + (long long)md[0] * g1) * C + c] : 0.0;
 #pragma unroll
-                    for (int a1 = 0; a1 <= NU; ++a1) acc[a1] = fma(t1[(y * (NU + 1) + a1) * (deg + 1) + r], v, acc[a1]);
+                    for (int a0 = 0; a0 <= NU; ++a0) acc[a0] = fma(t0[x * ts0 + a0 * (deg + 1) + r], v, acc[a0]);
                 }
             }
 #pragma unroll
-            for (int k = 0; k < NC; ++k) Hy[((y * n0 + i0) * C + c) * NC + k] = acc[k];
+            for (int k = 0; k < NC; ++k) Hx[x * hxs + (i1 * C + c) * NC + k] = acc[k];
         }
     }
 }
 
-// point evaluation: out[c][code] for all multi-indices with |alpha| <= NU (code = a0+3a1+9a2)
+// point evaluation: out[c][code] for all multi-indices with |alpha| <= NU (code = a0+3a1+9a2).
+// 2D/3D: t = y table of this point, s = its span, H = Hx + x*hxs.  1D: t = x table, s = x span.
 template <int NDIM, int NU, int C>
-__device__ __forceinline__ void field_point(const double* __restrict__ coef, int deg, const double* t0, int sx,
-                                            const double* Hy, int y, int lo0, int n0, double (&out)[C][27]) {
-    constexpr int NC = NC12<NDIM, NU>::v;
+__device__ __forceinline__ void field_point(const double* __restrict__ coef, int deg, const double* t, int s,
+                                            const double* H, int lo1, double (&out)[C][27]) {
+    constexpr int NC = NCx<NDIM, NU>::v;
 #pragma unroll
     for (int c = 0; c < C; ++c)
 #pragma unroll
         for (int k = 0; k < 27; ++k) out[c][k] = 0.0;
     for (int r = 0; r <= deg; ++r) {
-        const int i0 = sx - deg + r;
+        const int i = s - deg + r;
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             if constexpr (NDIM == 1) {
-                const double v = coef[(long long)i0 * C + c];
+                const double v = coef[(long long)i * C + c];
 #pragma unroll
-                for (int a0 = 0; a0 <= NU; ++a0) out[c][a0] = fma(t0[a0 * (deg + 1) + r], v, out[c][a0]);
+                for (int a0 = 0; a0 <= NU; ++a0) out[c][a0] = fma(t[a0 * (deg + 1) + r], v, out[c][a0]);
             } else {
-                const double* hy = Hy + ((y * n0 + (i0 - lo0)) * C + c) * NC;
+                const double* h = H + ((i - lo1) * C + c) * NC;
 #pragma unroll
-                for (int a0 = 0; a0 <= NU; ++a0) {
-                    const double b = t0[a0 * (deg + 1) + r];
+                for (int a1 = 0; a1 <= NU; ++a1) {
+                    const double b = t[a1 * (deg + 1) + r];
 #pragma unroll
-                    for (int a1 = 0; a1 + a0 <= NU; ++a1) {
+                    for (int a0 = 0; a0 + a1 <= NU; ++a0) {
                         if constexpr (NDIM == 3) {
 #pragma unroll
                             for (int a2 = 0; a2 + a1 + a0 <= NU; ++a2)
-                                out[c][a0 + 3 * a1 + 9 * a2] = fma(b, hy[c12<3>(a1, a2)], out[c][a0 + 3 * a1 + 9 * a2]);
+                                out[c][a0 + 3 * a1 + 9 * a2] = fma(b, h[k02(a0, a2)], out[c][a0 + 3 * a1 + 9 * a2]);
                         } else {
-                            out[c][a0 + 3 * a1] = fma(b, hy[a1], out[c][a0 + 3 * a1]);
+                            out[c][a0 + 3 * a1] = fma(b, h[a0], out[c][a0 + 3 * a1]);
                         }
                     }
                 }
@@ -356,12 +363,11 @@ __global__ void __launch_bounds__(256) geom_D_kernel(const GeomParams prm) {
     constexpr int U = MS * (MS + 1) / 2;
     constexpr int NU = form_deriv(FORM);
     constexpr int NUG = geo_deriv(FORM);
-    constexpr int P_ = 0;
-    (void)P_;
     extern __shared__ double smem[];
     const int tid = threadIdx.x, nt = blockDim.x;
     const int g = prm.g, pg = prm.pg, p = prm.p;
     const int NB = (NU + 1) * (p + 1), NBG = (NUG + 1) * (pg + 1);
+    const int NBp = NB | 1, NBGp = NBG | 1;  // odd per-point strides: per-lane y tables conflict free
     const int blk = prm.blocks ? prm.blocks[blockIdx.x] : (int)blockIdx.x;
     const int bx = blk % prm.nbx, by = (blk / prm.nbx) % prm.nby, z = blk / (prm.nbx * prm.nby);
     const int x0 = bx * prm.BX, y0 = by * prm.BY;
@@ -376,23 +382,31 @@ __global__ void __launch_bounds__(256) geom_D_kernel(const GeomParams prm) {
     int* ws0 = reinterpret_cast<int*>(smem + prm.off_ws0);
     int* ws1 = reinterpret_cast<int*>(smem + prm.off_ws1);
     double* Hz = smem + prm.off_Hz;
-    double* Hy = smem + prm.off_Hy;
+    double* Hx = smem + prm.off_Hy;
     double* Wz = smem + prm.off_Wz;
-    double* Wy = smem + prm.off_Wy;
+    double* Wx = smem + prm.off_Wy;
     double* misc = smem + prm.off_misc;
     double* G2p = misc;
     double* B2p = misc + 32;
+    double* qwx = misc + 64;
+    double* qwy = qwx + prm.BX;
     for (int it = tid; it < X * NBG; it += nt) G0s[it] = prm.G[0][(long long)x0 * NBG + it];
-    for (int x = tid; x < X; x += nt) gs0[x] = prm.gspan[0][x0 + x];
+    for (int x = tid; x < X; x += nt) {
+        gs0[x] = prm.gspan[0][x0 + x];
+        qwx[x] = prm.qw[0][(x0 + x) % g];
+    }
     if constexpr (RAT) {
         for (int it = tid; it < X * NB; it += nt) B0s[it] = prm.B[0][(long long)x0 * NB + it];
         for (int x = tid; x < X; x += nt) ws0[x] = (x0 + x) / g + p;
     }
     if constexpr (NDIM >= 2) {
-        for (int it = tid; it < Y * NBG; it += nt) G1s[it] = prm.G[1][(long long)y0 * NBG + it];
-        for (int y = tid; y < Y; y += nt) gs1[y] = prm.gspan[1][y0 + y];
+        for (int it = tid; it < Y * NBG; it += nt) G1s[(it / NBG) * NBGp + it % NBG] = prm.G[1][(long long)y0 * NBG + it];
+        for (int y = tid; y < Y; y += nt) {
+            gs1[y] = prm.gspan[1][y0 + y];
+            qwy[y] = prm.qw[1][(y0 + y) % g];
+        }
         if constexpr (RAT) {
-            for (int it = tid; it < Y * NB; it += nt) B1s[it] = prm.B[1][(long long)y0 * NB + it];
+            for (int it = tid; it < Y * NB; it += nt) B1s[(it / NB) * NBp + it % NB] = prm.B[1][(long long)y0 * NB + it];
             for (int y = tid; y < Y; y += nt) ws1[y] = (y0 + y) / g + p;
         }
     }
@@ -411,21 +425,29 @@ __global__ void __launch_bounds__(256) geom_D_kernel(const GeomParams prm) {
     const int wlo0 = x0 / g, wn0 = (x0 + X - 1) / g - x0 / g + 1 + p;
     int wlo1 = 0, wn1 = 1;
     if constexpr (NDIM >= 2) { wlo1 = y0 / g; wn1 = (y0 + Y - 1) / g - y0 / g + 1 + p; }
-    field_plane_prep<NDIM, NUG, NDIM + 1>(prm.hom, pg, prm.mg, G1s, gs1, Y, G2p, sz, glo0, gn0, glo1, gn1, Hz, Hy);
+    constexpr int C = NDIM + 1;
+    const int hxs = gn1 * C * NCx<NDIM, NUG>::v;
+    const int wxs = wn1 * NCx<NDIM, NU>::v;
+    field_plane_prep<NDIM, NUG, C>(prm.hom, pg, prm.mg, G0s, NBG, gs0, X, G2p, sz, glo0, gn0, glo1, gn1, Hz, Hx, hxs);
     if constexpr (RAT)
-        field_plane_prep<NDIM, NU, 1>(prm.sol_w, p, prm.m, B1s, ws1, Y, B2p, szw, wlo0, wn0, wlo1, wn1, Wz, Wy);
+        field_plane_prep<NDIM, NU, 1>(prm.sol_w, p, prm.m, B0s, NB, ws0, X, B2p, szw, wlo0, wn0, wlo1, wn1, Wz, Wx, wxs);
     __syncthreads();
     const double wz = NDIM == 3 ? prm.qw[2][z % g] : 1.0;
     for (int it = tid; it < X * Y; it += nt) {
-        const int y = it % Y, x = it / Y;
+        const int y = it % Y, x = it / Y;  // a warp shares x: Hx reads broadcast, y tables per lane
         double num[NDIM + 1][27];
-        field_point<NDIM, NUG, NDIM + 1>(prm.hom, pg, G0s + x * NBG, gs0[x], Hy, y, glo0, gn0, num);
         double wf[1][27];
-        if constexpr (RAT) field_point<NDIM, NU, 1>(prm.sol_w, p, B0s + x * NB, ws0[x], Wy, y, wlo0, wn0, wf);
-        else wf[0][0] = 1.0;
+        if constexpr (NDIM == 1) {
+            field_point<1, NUG, C>(prm.hom, pg, G0s + x * NBG, gs0[x], nullptr, 0, num);
+            if constexpr (RAT) field_point<1, NU, 1>(prm.sol_w, p, B0s + x * NB, ws0[x], nullptr, 0, wf);
+        } else {
+            field_point<NDIM, NUG, C>(prm.hom, pg, G1s + y * NBGp, gs1[y], Hx + x * hxs, glo1, num);
+            if constexpr (RAT) field_point<NDIM, NU, 1>(prm.sol_w, p, B1s + y * NBp, ws1[y], Wx + x * wxs, wlo1, wf);
+        }
+        if constexpr (!RAT) wf[0][0] = 1.0;
         // tensor weight in the reference order wq = pw2 * (pw1 * pw0)  (assembly.py:120-125)
-        double wq = prm.qw[0][(x0 + x) % g];
-        if constexpr (NDIM >= 2) wq = prm.qw[1][(y0 + y) % g] * wq;
+        double wq = qwx[x];
+        if constexpr (NDIM >= 2) wq = qwy[y] * wq;
         if constexpr (NDIM == 3) wq = wz * wq;
         double Dp[U];
         point_D<NDIM, FORM, RAT>(num, wf, wq, prm.coef, Dp);

@@ -116,7 +116,7 @@ __host__ __device__ constexpr int pad16_4(int v) {  // smallest w >= v with w % 
 
 // ---- compile-time tile geometry (shared by host planning and the kernel)
 struct MmaGeom {
-    int T0, T1, G, W, MT, KS, KS3, XW, YW, NTY, DY, TY, NCOMBO, NMT, CH, NCH, TC, U, NG1, NG2, NU1, NB, NK1, NK2;
+    int T0, T1, G, W, MT, KS, KS3, XW, XWp, YW, NTY, DY, TY, NCOMBO, NMT, CH, NCH, TC, U, NG1, NG2, NU1, NB, NK1, NK2;
     long o_B0, o_B1, o_B2, o_A1, o_B2f, o_B3f, o_cmb, o_bar, o_D, o_D2, o_T1, o_T2, total;
 };
 
@@ -131,6 +131,7 @@ __host__ __device__ constexpr MmaGeom mma_geom(int ndim, int P, int form, bool r
     m.KS = ((P + 1) * m.G + 3) / 4;
     m.KS3 = (m.G + 3) / 4;
     m.XW = (T0 + P) * m.G;
+    m.XWp = (m.XW + 3) & ~3;  // TMA: box bytes DY*XWp*8 stay a multiple of 128
     m.YW = ndim >= 2 ? (m.T1 + P) * m.G : 1;
     m.NTY = ndim >= 2 ? (m.YW + 7) / 8 : 1;
     m.DY = pad16_4(m.NTY * 8);
@@ -157,8 +158,9 @@ __host__ __device__ constexpr MmaGeom mma_geom(int ndim, int P, int form, bool r
     m.o_cmb = o; o += ndim == 3 ? (long)m.NCOMBO / 2 + 2 : 0;                  // per-combo CSR offsets (int)
     m.o_bar = o; o += 2;                                                       // two mbarriers (TMA)
     o = align16(o);
-    m.o_D = o; o += align16((long)m.U * m.XW * m.DY);                          // D window, double buffered (TMA)
-    m.o_D2 = o; o += align16((long)m.U * m.XW * m.DY);
+    m.o_D = o; o += align16((long)m.U * m.XWp * m.DY);                          // D window, double buffered (TMA)
+    m.o_D2 = ndim == 3 ? o : m.o_D;                                           // 2D/1D: one plane per tile
+    o += ndim == 3 ? align16((long)m.U * m.XWp * m.DY) : 0;
     m.o_T1 = o; o += ndim >= 2 ? (long)m.NG1 * T0 * m.MT * 8 * m.TY : 0;
     m.o_T2 = o; o += ndim == 3 ? (long)m.NG2 * m.G * m.TC : 0;
     m.total = o;
@@ -196,6 +198,8 @@ struct MmaParams {
     int* indices;
     double* data;
     unsigned long long* zeros;
+    int tma;                     // 1: TMA double-buffered D windows; 0: plain loads (debug / fallback)
+    int Dys;
 };
 
 template <int NDIM, int P, int FORM, bool RAT>
@@ -208,7 +212,8 @@ __global__ void __launch_bounds__(512, 1) assemble_mma(const __grid_constant__ M
     constexpr int MS = TTS::T.MS;
     constexpr int NW = 16;
     constexpr int NK1 = M.NK1, NK2 = M.NK2;
-    constexpr unsigned DBYTES = (unsigned)(M.U * XW * DY * 8);
+    constexpr int XWp = M.XWp;
+    constexpr unsigned DBYTES = (unsigned)(M.U * XWp * DY * 8);
     extern __shared__ double smem[];
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
@@ -336,7 +341,11 @@ __global__ void __launch_bounds__(512, 1) assemble_mma(const __grid_constant__ M
             "l"(reinterpret_cast<uint64_t>(&prm.dmap)), "r"(ew1 * G), "r"(ew0 * G), "r"(0), "r"(z), "r"(bar)
             : "memory");
     };
-    if constexpr (NDIM >= 2) {
+    // TMA D windows: 3D (double-buffered pencil) and 2D p=3 (validated configs); plain loads otherwise.
+    // (2D p=2 bi-Laplacian boxes raised an illegal-instruction fault under TMA -- open item)
+    constexpr bool kTma = NDIM == 3 || (NDIM == 2 && P == 3);
+    const bool use_tma = kTma && prm.tma;
+    if (use_tma) {
         if (tid == 0) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0) : "memory");
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0 + 8u) : "memory");
@@ -377,7 +386,7 @@ __global__ void __launch_bounds__(512, 1) assemble_mma(const __grid_constant__ M
         for (int q2 = 0; q2 < GZ; ++q2) {
             // ---------------- D window of this plane
             double* Ds = Dbuf[pidx & 1];
-            if constexpr (NDIM >= 2) {
+            if (use_tma) {
                 if (tid == 0 && pidx + 1 < nplanes) issue_plane(pidx + 1);  // prefetch the next plane
                 const uint32_t bar = bar0 + 8u * (uint32_t)(pidx & 1);
                 const uint32_t par = (uint32_t)((pidx >> 1) & 1);
@@ -390,12 +399,17 @@ __global__ void __launch_bounds__(512, 1) assemble_mma(const __grid_constant__ M
                         : "memory");
                 }
             } else {
-                const long long gx0 = (long long)ew0 * G;
-                for (int it = tid; it < M.U * XW * 8; it += blockDim.x) {
-                    const int y = it % 8, r = it / 8;
-                    const int u = r / XW, x = r % XW;
-                    const long long gx = gx0 + x;
-                    Ds[r * DY + y] = (y == 0 && gx >= 0 && gx < G0) ? prm.D[(long long)u * G0 + gx] : 0.0;
+                const long long gx0 = (long long)ew0 * G, gy0 = (long long)ew1 * G;
+                const long long z = (long long)elo2 * G + pidx;
+                const long long G1 = NDIM >= 2 ? prm.Gp[1] : 1;
+                for (int it = tid; it < M.U * XWp * DY; it += blockDim.x) {
+                    const int y = it % DY, r = it / DY;
+                    const int u = r / XWp, x = r % XWp;
+                    const long long gx = gx0 + x, gy = gy0 + y;
+                    double v = 0.0;
+                    if (gx >= 0 && gx < G0 && gy >= 0 && gy < G1)
+                        v = prm.D[((z * M.U + u) * G0 + gx) * (long long)prm.Dys + gy];
+                    Ds[r * DY + y] = v;
                 }
                 __syncthreads();
             }
@@ -421,7 +435,7 @@ __global__ void __launch_bounds__(512, 1) assemble_mma(const __grid_constant__ M
                     for (int kk = 0; kk < KS; ++kk) {
                         const int s = kk * 4 + lk;
                         const int x = (s < (P + 1) * G) ? (i0l + s / G) * G + s % G : 0;
-                        const double* drow = Ds + (ud * XW + x) * DY + lr;
+                        const double* drow = Ds + (ud * XWp + x) * DY + lr;
                         double afr[MT];
 #pragma unroll
                         for (int a = 0; a < MT; ++a) afr[a] = af[(kk * MT + a) * 32];
