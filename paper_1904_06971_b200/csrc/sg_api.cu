@@ -9,6 +9,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/surriga_b200.h"
@@ -846,16 +847,87 @@ int sg_result_sizes(const sg_result* r, int64_t* nrows, int64_t* nnz) {
     return 0;
 }
 
+}  // extern "C"
+
+namespace sg {
+// Device -> host copy of large result arrays: pinned staging ring (2 x 64 MB per thread), D2H of
+// chunk k overlapped with a multi-threaded memcpy of chunk k-1 into the caller's (pageable) buffer.
+struct Stager {
+    int dev = -1;
+    cudaStream_t st = nullptr;
+    char* buf[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2];
+    size_t cap = 0;
+};
+static thread_local Stager g_stage;
+
+static void par_memcpy(char* dst, const char* src, size_t n) {
+    const int nt = (int)std::min<size_t>(16, std::max<size_t>(1, n >> 22));  // >= 4 MB per thread
+    if (nt <= 1) {
+        memcpy(dst, src, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    const size_t per = (n + nt - 1) / nt;
+    for (int t = 0; t < nt; ++t) {
+        const size_t lo = t * per, hi = std::min(n, lo + per);
+        if (lo < hi) th.emplace_back([=] { memcpy(dst + lo, src + lo, hi - lo); });
+    }
+    for (auto& x : th) x.join();
+}
+
+static int d2h(void* dst, const void* src, size_t bytes, int dev) {
+    if (bytes == 0) return 0;
+    if (bytes < (8u << 20)) {
+        if (cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) return fail(-3, "D2H copy failed");
+        return 0;
+    }
+    Stager& S = g_stage;
+    const size_t chunk = 64u << 20;
+    if (S.dev != dev || !S.buf[0]) {
+        if (S.buf[0]) {
+            cudaFreeHost(S.buf[0]);
+            cudaFreeHost(S.buf[1]);
+        }
+        if (cudaHostAlloc((void**)&S.buf[0], chunk, cudaHostAllocDefault) != cudaSuccess ||
+            cudaHostAlloc((void**)&S.buf[1], chunk, cudaHostAllocDefault) != cudaSuccess)
+            return fail(-4, "pinned staging allocation failed");
+        if (!S.st) {
+            cudaStreamCreateWithFlags(&S.st, cudaStreamNonBlocking);
+            cudaEventCreateWithFlags(&S.ev[0], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&S.ev[1], cudaEventDisableTiming);
+        }
+        S.dev = dev;
+        S.cap = chunk;
+    }
+    const size_t nch = (bytes + chunk - 1) / chunk;
+    for (size_t k = 0; k <= nch; ++k) {
+        if (k < nch) {
+            const size_t off = k * chunk, len = std::min(chunk, bytes - off);
+            cudaMemcpyAsync(S.buf[k & 1], (const char*)src + off, len, cudaMemcpyDeviceToHost, S.st);
+            cudaEventRecord(S.ev[k & 1], S.st);
+        }
+        if (k > 0) {
+            const size_t pk = k - 1, off = pk * chunk, len = std::min(chunk, bytes - off);
+            if (cudaEventSynchronize(S.ev[pk & 1]) != cudaSuccess) return fail(-3, "D2H copy failed");
+            par_memcpy((char*)dst + off, S.buf[pk & 1], len);
+        }
+    }
+    return 0;
+}
+}  // namespace sg
+
+extern "C" {
+
 int sg_result_copy_i64(const sg_result* r, int64_t* indptr, int32_t* indices, double* data) {
     if (!r) return fail(-1, "null result");
     cudaSetDevice(r->dev);
-    if (indptr && cudaMemcpy(indptr, r->indptr, sizeof(int64_t) * (r->nrows + 1), cudaMemcpyDeviceToHost) != cudaSuccess)
-        return fail(-3, "indptr copy failed");
+    cudaDeviceSynchronize();
+    int rc = 0;
+    if (indptr && (rc = d2h(indptr, r->indptr, sizeof(int64_t) * (r->nrows + 1), r->dev))) return rc;
     if (r->nnz > 0) {
-        if (indices && cudaMemcpy(indices, r->indices, sizeof(int32_t) * r->nnz, cudaMemcpyDeviceToHost) != cudaSuccess)
-            return fail(-3, "indices copy failed");
-        if (data && cudaMemcpy(data, r->data, sizeof(double) * r->nnz, cudaMemcpyDeviceToHost) != cudaSuccess)
-            return fail(-3, "data copy failed");
+        if (indices && (rc = d2h(indices, r->indices, sizeof(int32_t) * r->nnz, r->dev))) return rc;
+        if (data && (rc = d2h(data, r->data, sizeof(double) * r->nnz, r->dev))) return rc;
     }
     return 0;
 }

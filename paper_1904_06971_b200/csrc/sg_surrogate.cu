@@ -89,27 +89,92 @@ __global__ void const_table_kernel(int n, int* sp, double* tab) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// K7: one CTA per tile of box rows; per-warp sum-factorised spline evaluation per offset.
+// K7: one CTA per tile of box rows (64 rows).  Warps split the P offsets; a lane owns two rows of
+// the tile.  Per offset the warp evaluates the offset's tensor spline on the (possibly shifted)
+// tile points by sum factorisation (x, then y, then z taps) from the coefficient tensor, then
+// places each lane's entries (interpolated / symmetric copy / transposed quadrature value,
+// surrogate.py:633-667), writes them straight into the CSR and keeps per-row partial sums for
+// the kernel-preserving diagonal (:673-680).  No row staging: the CTA's rows stay L2 resident
+// while their sectors fill.
 // ---------------------------------------------------------------------------------------------
 template <int NDIM>
-__global__ void __launch_bounds__(512) interp_tiles_kernel(SurrParams s) {
+__global__ void __launch_bounds__(512, 2) interp_tiles_kernel(SurrParams s) {
     extern __shared__ double sm[];
+    constexpr int NR = 64;
     const int P = s.P;
     const int TB0 = s.TB[0], TB1 = NDIM >= 2 ? s.TB[1] : 1, TB2 = NDIM >= 3 ? s.TB[2] : 1;
-    const int NR = TB0 * TB1 * TB2;
-    double* out = sm;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    const int c0 = s.cmax[0], c1 = s.cmax[1], c2 = s.cmax[2];
+    const int c1 = s.cmax[1], c2 = s.cmax[2];
     const int scr = c2 * c1 * TB0 + c2 * TB1 * TB0 + 8;
-    double* A = sm + (size_t)NR * P + (size_t)warp * scr;
+    double* A = sm + (size_t)warp * scr;
     double* Bm = A + c2 * c1 * TB0;
-    (void)c0;
+    double* red = sm + (size_t)nw * scr;                 // [nw][NR] partial row sums
+    double* dgv = red + (size_t)nw * NR;                 // [NR] pre-reset diagonal value
+    int* rcnt = reinterpret_cast<int*>(dgv + NR);        // [nw][NR][3]: off-diag interp, interp, zeros
     const int t = blockIdx.x;
     const int tc0 = t % s.tg[0], tc1 = (t / s.tg[0]) % s.tg[1], tc2 = t / (s.tg[0] * s.tg[1]);
     const int org0 = tc0 * TB0, org1 = tc1 * TB1, org2 = tc2 * TB2;
     const int q0 = s.qd[0], q1 = s.qd[1], q2 = s.qd[2];
+    // stage the evaluation tables and row-class masks of this tile's +-p neighbourhood in smem
+    const int p = s.p;
+    const int L0 = TB0 + 2 * p, L1 = NDIM >= 2 ? TB1 + 2 * p : 1, L2 = NDIM >= 3 ? TB2 + 2 * p : 1;
+    const int base0 = org0 - p, base1 = NDIM >= 2 ? org1 - p : 0, base2 = NDIM >= 3 ? org2 - p : 0;
+    double* tb0 = reinterpret_cast<double*>(rcnt + nw * NR * 3 + 2);
+    double* tb1 = tb0 + L0 * (q0 + 1);
+    double* tb2 = tb1 + L1 * (q1 + 1);
+    int* sp0 = reinterpret_cast<int*>(tb2 + L2 * (q2 + 1));
+    int* sp1 = sp0 + L0;
+    int* sp2 = sp1 + L1;
+    uint8_t* mk0 = reinterpret_cast<uint8_t*>(sp2 + L2);  // bit0 in box, bit1 sampled (index range blo+base..)
+    uint8_t* mk1 = mk0 + L0;
+    uint8_t* mk2 = mk1 + L1;
+    for (int it = threadIdx.x; it < L0 + L1 + L2; it += blockDim.x) {
+        int d = 0, li = it;
+        if (li >= L0) { li -= L0; d = 1; if (li >= L1) { li -= L1; d = 2; } }
+        const int L = d == 0 ? L0 : (d == 1 ? L1 : L2), base = d == 0 ? base0 : (d == 1 ? base1 : base2);
+        const int qq = s.qd[d];
+        (void)L;
+        const int x = min(max(base + li, 0), s.bn[d] - 1);
+        int* spd = d == 0 ? sp0 : (d == 1 ? sp1 : sp2);
+        double* tbd = d == 0 ? tb0 : (d == 1 ? tb1 : tb2);
+        spd[li] = s.esp[d][x];
+        for (int r = 0; r <= qq; ++r) tbd[li * (qq + 1) + r] = s.etab[d][x * (qq + 1) + r];
+        const int j = s.blo[d] + base + li;  // basis index
+        uint8_t mk = 0;
+        if (j >= 0 && j < s.m[d]) mk = (uint8_t)(s.inb[d][j] | (s.smp[d][j] << 1));
+        (d == 0 ? mk0 : (d == 1 ? mk1 : mk2))[li] = mk;
+    }
+    __syncthreads();
+    auto jint_of = [&](int j0, int j1, int j2) {
+        const uint8_t a = mk0[j0 - s.blo[0] - base0];
+        const uint8_t b = NDIM >= 2 ? mk1[j1 - s.blo[1] - base1] : (uint8_t)3;
+        const uint8_t c = NDIM >= 3 ? mk2[j2 - s.blo[2] - base2] : (uint8_t)3;
+        return ((a & b & c) & 1) && !((a & b & c) & 2);
+    };
 
-    // ---- phase A: spline values for every offset on this tile (possibly shifted points)
+    // the lane's two rows
+    int rb0[2], rb1[2], rb2[2], ri0[2], ri1[2], ri2[2];
+    int64_t rrow[2], rbase[2];
+    bool rint[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int r = lane + 32 * k;
+        rb0[k] = r % TB0;
+        rb1[k] = (r / TB0) % TB1;
+        rb2[k] = r / (TB0 * TB1);
+        bool ok = org0 + rb0[k] < s.bn[0] && (NDIM < 2 || org1 + rb1[k] < s.bn[1]) && (NDIM < 3 || org2 + rb2[k] < s.bn[2]);
+        ri0[k] = s.blo[0] + org0 + rb0[k];
+        ri1[k] = NDIM >= 2 ? s.blo[1] + org1 + rb1[k] : 0;
+        ri2[k] = NDIM >= 3 ? s.blo[2] + org2 + rb2[k] : 0;
+        ok = ok && row_interp(s, ri0[k], ri1[k], ri2[k]);
+        rrow[k] = (int64_t)ri0[k] + (int64_t)s.m[0] * ((int64_t)ri1[k] + (int64_t)s.m[1] * ri2[k]);
+        ok = ok && rrow[k] >= s.slab_lo && rrow[k] < s.slab_hi;
+        rint[k] = ok;
+        rbase[k] = ok ? s.rowstart[rrow[k]] : 0;
+    }
+    double psum[2] = {0.0, 0.0};
+    int poff[2] = {0, 0}, pint[2] = {0, 0}, pzero[2] = {0, 0};
+
     for (int o = warp; o < P; o += nw) {
         int op = o, sh0 = 0, sh1 = 0, sh2 = 0;
         if (s.mode != SG_GENERAL && o < s.center) {
@@ -118,146 +183,148 @@ __global__ void __launch_bounds__(512) interp_tiles_kernel(SurrParams s) {
             sh1 = s.shifts[o * 3 + 1];
             sh2 = s.shifts[o * 3 + 2];
         }
+        const int so0 = s.shifts[o * 3 + 0], so1 = s.shifts[o * 3 + 1], so2 = s.shifts[o * 3 + 2];
         const double* cf = s.coef + (int64_t)op * s.nl[0] * s.nl[1] * s.nl[2];
-        // valid point ranges (clamped) -> coefficient windows
-        auto xpt = [&](int d, int org, int b, int sh) { return org + b + sh; };
         int lo1 = 0, lo2 = 0;
-        if (NDIM >= 2) {
-            const int a = min(max(xpt(1, org1, 0, sh1), 0), s.bn[1] - 1);
-            lo1 = s.esp[1][a] - q1;
-        }
-        if (NDIM >= 3) {
-            const int a = min(max(xpt(2, org2, 0, sh2), 0), s.bn[2] - 1);
-            lo2 = s.esp[2][a] - q2;
-        }
+        if (NDIM >= 2) lo1 = sp1[min(max(org1 + sh1, 0), s.bn[1] - 1) - base1] - q1;
+        if (NDIM >= 3) lo2 = sp2[min(max(org2 + sh2, 0), s.bn[2] - 1) - base2] - q2;
+        double V[2];
         if constexpr (NDIM == 1) {
-            for (int b0 = lane; b0 < TB0; b0 += 32) {
-                const int x0 = min(max(org0 + b0 + sh0, 0), s.bn[0] - 1);
-                const int sp = s.esp[0][x0];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int x0 = min(max(org0 + rb0[k] + sh0, 0), s.bn[0] - 1);
+                const int sp = sp0[x0 - base0];
                 double v = 0.0;
-                for (int r = 0; r <= q0; ++r) v = fma(s.etab[0][x0 * (q0 + 1) + r], cf[sp - q0 + r], v);
-                out[b0 * P + o] = v;
+                for (int r = 0; r <= q0; ++r) v = fma(tb0[(x0 - base0) * (q0 + 1) + r], cf[sp - q0 + r], v);
+                V[k] = v;
             }
-        } else if constexpr (NDIM == 2) {
-            // A[t1][b0] = sum_r0 E0 cf[lo1+t1][sp0-q0+r0]
-            for (int it = lane; it < c1 * TB0; it += 32) {
-                const int b0 = it % TB0, t1 = it / TB0;
-                const int x0 = min(max(org0 + b0 + sh0, 0), s.bn[0] - 1);
-                const int sp = s.esp[0][x0];
-                const int row = min(lo1 + t1, s.nl[1] - 1);
-                double v = 0.0;
-                for (int r = 0; r <= q0; ++r) v = fma(s.etab[0][x0 * (q0 + 1) + r], cf[(int64_t)row * s.nl[0] + sp - q0 + r], v);
-                A[t1 * TB0 + b0] = v;
-            }
-            __syncwarp();
-            for (int it = lane; it < TB1 * TB0; it += 32) {
-                const int b0 = it % TB0, b1 = it / TB0;
-                const int x1 = min(max(org1 + b1 + sh1, 0), s.bn[1] - 1);
-                const int sp = s.esp[1][x1];
-                double v = 0.0;
-                for (int r = 0; r <= q1; ++r) {
-                    const int t1 = sp - q1 + r - lo1;
-                    if (t1 >= 0 && t1 < c1) v = fma(s.etab[1][x1 * (q1 + 1) + r], A[t1 * TB0 + b0], v);
-                }
-                out[(b1 * TB0 + b0) * P + o] = v;
-            }
-            __syncwarp();
         } else {
+            // x pass: A[t2][t1][b0]
             for (int it = lane; it < c2 * c1 * TB0; it += 32) {
-                const int b0 = it % TB0, t1 = (it / TB0) % c1, t2 = it / (TB0 * c1);
+                const int b0 = it % TB0, tt1 = (it / TB0) % c1, tt2 = it / (TB0 * c1);
                 const int x0 = min(max(org0 + b0 + sh0, 0), s.bn[0] - 1);
-                const int sp = s.esp[0][x0];
-                const int r1 = min(lo1 + t1, s.nl[1] - 1), r2 = min(lo2 + t2, s.nl[2] - 1);
+                const int sp = sp0[x0 - base0];
+                const int r1 = min(lo1 + tt1, s.nl[1] - 1), r2 = min(lo2 + tt2, s.nl[2] - 1);
                 const double* crow = cf + ((int64_t)r2 * s.nl[1] + r1) * s.nl[0];
                 double v = 0.0;
-                for (int r = 0; r <= q0; ++r) v = fma(s.etab[0][x0 * (q0 + 1) + r], crow[sp - q0 + r], v);
-                A[(t2 * c1 + t1) * TB0 + b0] = v;
+                for (int r = 0; r <= q0; ++r) v = fma(tb0[(x0 - base0) * (q0 + 1) + r], crow[sp - q0 + r], v);
+                A[(tt2 * c1 + tt1) * TB0 + b0] = v;
             }
             __syncwarp();
-            for (int it = lane; it < c2 * TB1 * TB0; it += 32) {
-                const int b0 = it % TB0, b1 = (it / TB0) % TB1, t2 = it / (TB0 * TB1);
-                const int x1 = min(max(org1 + b1 + sh1, 0), s.bn[1] - 1);
-                const int sp = s.esp[1][x1];
-                double v = 0.0;
-                for (int r = 0; r <= q1; ++r) {
-                    const int t1 = sp - q1 + r - lo1;
-                    if (t1 >= 0 && t1 < c1) v = fma(s.etab[1][x1 * (q1 + 1) + r], A[(t2 * c1 + t1) * TB0 + b0], v);
+            if constexpr (NDIM == 2) {
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const int x1 = min(max(org1 + rb1[k] + sh1, 0), s.bn[1] - 1);
+                    const int sp = sp1[x1 - base1];
+                    double v = 0.0;
+                    for (int r = 0; r <= q1; ++r) {
+                        const int tt1 = sp - q1 + r - lo1;
+                        if (tt1 >= 0 && tt1 < c1) v = fma(tb1[(x1 - base1) * (q1 + 1) + r], A[tt1 * TB0 + rb0[k]], v);
+                    }
+                    V[k] = v;
                 }
-                Bm[(t2 * TB1 + b1) * TB0 + b0] = v;
-            }
-            __syncwarp();
-            for (int it = lane; it < TB2 * TB1 * TB0; it += 32) {
-                const int b0 = it % TB0, b1 = (it / TB0) % TB1, b2 = it / (TB0 * TB1);
-                const int x2 = min(max(org2 + b2 + sh2, 0), s.bn[2] - 1);
-                const int sp = s.esp[2][x2];
-                double v = 0.0;
-                for (int r = 0; r <= q2; ++r) {
-                    const int t2 = sp - q2 + r - lo2;
-                    if (t2 >= 0 && t2 < c2) v = fma(s.etab[2][x2 * (q2 + 1) + r], Bm[(t2 * TB1 + b1) * TB0 + b0], v);
+            } else {
+                // y pass: Bm[t2][b1][b0]
+                for (int it = lane; it < c2 * TB1 * TB0; it += 32) {
+                    const int b0 = it % TB0, b1 = (it / TB0) % TB1, tt2 = it / (TB0 * TB1);
+                    const int x1 = min(max(org1 + b1 + sh1, 0), s.bn[1] - 1);
+                    const int sp = sp1[x1 - base1];
+                    double v = 0.0;
+                    for (int r = 0; r <= q1; ++r) {
+                        const int tt1 = sp - q1 + r - lo1;
+                        if (tt1 >= 0 && tt1 < c1) v = fma(tb1[(x1 - base1) * (q1 + 1) + r], A[(tt2 * c1 + tt1) * TB0 + b0], v);
+                    }
+                    Bm[(tt2 * TB1 + b1) * TB0 + b0] = v;
                 }
-                out[((b2 * TB1 + b1) * TB0 + b0) * P + o] = v;
+                __syncwarp();
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const int x2 = min(max(org2 + rb2[k] + sh2, 0), s.bn[2] - 1);
+                    const int sp = sp2[x2 - base2];
+                    double v = 0.0;
+                    for (int r = 0; r <= q2; ++r) {
+                        const int tt2 = sp - q2 + r - lo2;
+                        if (tt2 >= 0 && tt2 < c2) v = fma(tb2[(x2 - base2) * (q2 + 1) + r], Bm[(tt2 * TB1 + rb1[k]) * TB0 + rb0[k]], v);
+                    }
+                    V[k] = v;
+                }
             }
             __syncwarp();
+        }
+        // placement of offset o for the lane's rows
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            if (!rint[k]) continue;
+            const int j0 = ri0[k] + so0, j1 = ri1[k] + so1, j2 = ri2[k] + so2;
+            const int64_t col = (int64_t)j0 + (int64_t)s.m[0] * ((int64_t)j1 + (int64_t)s.m[1] * j2);
+            const bool jint = jint_of(j0, j1, j2);
+            const double v = jint ? V[k] : s.data[s.rowstart[col] + (P - 1 - o)];  // transposed quadrature entry A[j, i]
+            s.data[rbase[k] + o] = v;
+            s.indices[rbase[k] + o] = (int)col;
+            psum[k] += v;
+            if (jint) {
+                pint[k]++;
+                if (o != s.center) poff[k]++;
+            }
+            if (v == 0.0) pzero[k]++;
+            if (o == s.center) dgv[lane + 32 * k] = v;
         }
     }
-    __syncthreads();
-
-    // ---- phase B: placement per interpolated row (warp per row, lanes over offsets)
-    unsigned long long n_int = 0, n_zero = 0, n_reset = 0, n_rows = 0;
-    for (int r = warp; r < NR; r += nw) {
-        const int b0 = r % TB0, b1 = (r / TB0) % TB1, b2 = r / (TB0 * TB1);
-        if (org0 + b0 >= s.bn[0]) continue;
-        if (NDIM >= 2 && org1 + b1 >= s.bn[1]) continue;
-        if (NDIM >= 3 && org2 + b2 >= s.bn[2]) continue;
-        const int i0 = s.blo[0] + org0 + b0;
-        const int i1 = NDIM >= 2 ? s.blo[1] + org1 + b1 : 0;
-        const int i2 = NDIM >= 3 ? s.blo[2] + org2 + b2 : 0;
-        if (!row_interp(s, i0, i1, i2)) continue;
-        const int64_t row = (int64_t)i0 + (int64_t)s.m[0] * ((int64_t)i1 + (int64_t)s.m[1] * i2);
-        if (row < s.slab_lo || row >= s.slab_hi) continue;
-        const int64_t base = s.rowstart[row];
-        double sum = 0.0;
-        int cnt_off = 0, cnt_int = 0, cnt_zero = 0;
-        for (int o = lane; o < P; o += 32) {
-            const int j0 = i0 + s.shifts[o * 3 + 0], j1 = i1 + s.shifts[o * 3 + 1], j2 = i2 + s.shifts[o * 3 + 2];
-            const int64_t col = (int64_t)j0 + (int64_t)s.m[0] * ((int64_t)j1 + (int64_t)s.m[1] * j2);
-            const bool jint = row_interp(s, j0, j1, j2);
-            double v;
-            if (jint) {
-                v = out[r * P + o];
-                cnt_int++;
-                if (o != s.center) cnt_off++;
-            } else {
-                v = s.data[s.rowstart[col] + (P - 1 - o)];  // transposed quadrature entry A[j, i]
-            }
-            s.data[base + o] = v;
-            s.indices[base + o] = (int)col;
-            sum += v;
-            if (v == 0.0) cnt_zero++;
-        }
+    // per-row reduction over warps (fixed order)
 #pragma unroll
-        for (int w = 16; w > 0; w >>= 1) {
-            sum += __shfl_xor_sync(0xffffffffu, sum, w);
-            cnt_off += __shfl_xor_sync(0xffffffffu, cnt_off, w);
-            cnt_int += __shfl_xor_sync(0xffffffffu, cnt_int, w);
-            cnt_zero += __shfl_xor_sync(0xffffffffu, cnt_zero, w);
-        }
-        if (lane == 0) {
-            n_int += cnt_int;
-            n_zero += cnt_zero;
+    for (int k = 0; k < 2; ++k) {
+        const int r = lane + 32 * k;
+        red[warp * NR + r] = psum[k];
+        rcnt[(warp * NR + r) * 3 + 0] = poff[k];
+        rcnt[(warp * NR + r) * 3 + 1] = pint[k];
+        rcnt[(warp * NR + r) * 3 + 2] = pzero[k];
+    }
+    __syncthreads();
+    unsigned long long n_int = 0, n_zero = 0, n_reset = 0, n_rows = 0;
+    if (threadIdx.x < NR) {
+        const int r = threadIdx.x;
+        const int k = r / 32, l = r % 32;
+        (void)l;
+        const int b0 = r % TB0, b1 = (r / TB0) % TB1, b2 = r / (TB0 * TB1);
+        bool ok = org0 + b0 < s.bn[0] && (NDIM < 2 || org1 + b1 < s.bn[1]) && (NDIM < 3 || org2 + b2 < s.bn[2]);
+        const int i0 = s.blo[0] + org0 + b0, i1 = NDIM >= 2 ? s.blo[1] + org1 + b1 : 0, i2 = NDIM >= 3 ? s.blo[2] + org2 + b2 : 0;
+        ok = ok && row_interp(s, i0, i1, i2);
+        const int64_t row = (int64_t)i0 + (int64_t)s.m[0] * ((int64_t)i1 + (int64_t)s.m[1] * i2);
+        ok = ok && row >= s.slab_lo && row < s.slab_hi;
+        (void)k;
+        if (ok) {
+            double sum = 0.0;
+            int off = 0, in = 0, ze = 0;
+            for (int w = 0; w < nw; ++w) {
+                sum += red[w * NR + r];
+                off += rcnt[(w * NR + r) * 3 + 0];
+                in += rcnt[(w * NR + r) * 3 + 1];
+                ze += rcnt[(w * NR + r) * 3 + 2];
+            }
+            n_int += in;
+            n_zero += ze;
             n_rows++;
-            if (s.mode == SG_SYMMETRIC_KERNEL_PRESERVING && cnt_off > 0) {
-                s.newdiag[row] = out[r * P + s.center] - sum;
+            if (s.mode == SG_SYMMETRIC_KERNEL_PRESERVING && off > 0) {
+                s.newdiag[row] = dgv[r] - sum;
                 s.reset[row] = 1;
                 n_reset++;
             }
         }
     }
-    if (lane == 0) {
-        if (n_int) atomicAdd(&s.counters[0], n_int);
-        if (n_zero) atomicAdd(&s.counters[1], n_zero);
-        if (n_reset) atomicAdd(&s.counters[2], n_reset);
-        if (n_rows) atomicAdd(&s.counters[3], n_rows);
+    if (threadIdx.x < NR) {
+#pragma unroll
+        for (int w = 16; w > 0; w >>= 1) {
+            n_int += __shfl_xor_sync(0xffffffffu, n_int, w);
+            n_zero += __shfl_xor_sync(0xffffffffu, n_zero, w);
+            n_reset += __shfl_xor_sync(0xffffffffu, n_reset, w);
+            n_rows += __shfl_xor_sync(0xffffffffu, n_rows, w);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            if (n_int) atomicAdd(&s.counters[0], n_int);
+            if (n_zero) atomicAdd(&s.counters[1], n_zero);
+            if (n_reset) atomicAdd(&s.counters[2], n_reset);
+            if (n_rows) atomicAdd(&s.counters[3], n_rows);
+        }
     }
 }
 
@@ -495,7 +562,7 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
         s.etab[d] = et;
     }
     // coefficient window bounds per direction for a tile (host-side, from the same tables)
-    const int TBdef[3][3] = {{64, 1, 1}, {8, 8, 1}, {4, 4, 2}};
+    const int TBdef[3][3] = {{64, 1, 1}, {8, 8, 1}, {4, 4, 4}};  // 64 rows per tile
     for (int d = 0; d < 3; ++d) {
         s.TB[d] = TBdef[n - 1][d];
         s.tg[d] = (s.bn[d] + s.TB[d] - 1) / s.TB[d];
@@ -521,9 +588,15 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
     }
     // ---- K7
     const int nthreads = 512;
-    const int NR = s.TB[0] * s.TB[1] * s.TB[2];
+    const int NR = 64;
+    const int nw = nthreads / 32;
     const int scr = s.cmax[2] * s.cmax[1] * s.TB[0] + s.cmax[2] * s.TB[1] * s.TB[0] + 8;
-    const size_t smem = sizeof(double) * ((size_t)NR * P + (size_t)(nthreads / 32) * scr);
+    size_t tabs = 0;
+    for (int d = 0; d < 3; ++d) {
+        const int L = (d < n ? s.TB[d] + 2 * p : 1);
+        tabs += (size_t)L * (s.qd[d] + 1) * sizeof(double) + (size_t)L * sizeof(int) + L;
+    }
+    const size_t smem = sizeof(double) * ((size_t)nw * scr + (size_t)nw * NR + NR) + sizeof(int) * ((size_t)nw * NR * 3 + 2) + tabs + 64;
     if (smem > 227 * 1024) return fail(-2, "surrogate tile does not fit shared memory (%zu B)", smem);
     const int ntiles = s.tg[0] * s.tg[1] * s.tg[2];
     void* kfn = n == 1 ? (void*)interp_tiles_kernel<1> : (n == 2 ? (void*)interp_tiles_kernel<2> : (void*)interp_tiles_kernel<3>);
