@@ -97,14 +97,17 @@ __global__ void const_table_kernel(int n, int* sp, double* tab) {
 // the kernel-preserving diagonal (:673-680).  No row staging: the CTA's rows stay L2 resident
 // while their sectors fill.
 // ---------------------------------------------------------------------------------------------
-template <int NDIM>
+template <int NDIM, int QC>
 __global__ void __launch_bounds__(512, 2) interp_tiles_kernel(SurrParams s) {
+    // QC > 0: degree QC in every direction and tile 4x4x4 / 8x8 / 64, coefficient window QC+2
+    constexpr bool FIX = QC > 0;
+    constexpr int FTB0 = NDIM == 1 ? 64 : (NDIM == 2 ? 8 : 4), FTB1 = NDIM == 2 ? 8 : (NDIM == 3 ? 4 : 1), FTB2 = NDIM == 3 ? 4 : 1;
     extern __shared__ double sm[];
     constexpr int NR = 64;
     const int P = s.P;
-    const int TB0 = s.TB[0], TB1 = NDIM >= 2 ? s.TB[1] : 1, TB2 = NDIM >= 3 ? s.TB[2] : 1;
+    const int TB0 = FIX ? FTB0 : s.TB[0], TB1 = FIX ? FTB1 : (NDIM >= 2 ? s.TB[1] : 1), TB2 = FIX ? FTB2 : (NDIM >= 3 ? s.TB[2] : 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    const int c1 = s.cmax[1], c2 = s.cmax[2];
+    const int c1 = FIX ? (NDIM >= 2 ? QC + 2 : 1) : s.cmax[1], c2 = FIX ? (NDIM >= 3 ? QC + 2 : 1) : s.cmax[2];
     const int scr = c2 * c1 * TB0 + c2 * TB1 * TB0 + 8;
     double* A = sm + (size_t)warp * scr;
     double* Bm = A + c2 * c1 * TB0;
@@ -114,7 +117,7 @@ __global__ void __launch_bounds__(512, 2) interp_tiles_kernel(SurrParams s) {
     const int t = blockIdx.x;
     const int tc0 = t % s.tg[0], tc1 = (t / s.tg[0]) % s.tg[1], tc2 = t / (s.tg[0] * s.tg[1]);
     const int org0 = tc0 * TB0, org1 = tc1 * TB1, org2 = tc2 * TB2;
-    const int q0 = s.qd[0], q1 = s.qd[1], q2 = s.qd[2];
+    const int q0 = FIX ? QC : s.qd[0], q1 = FIX ? (NDIM >= 2 ? QC : 0) : s.qd[1], q2 = FIX ? (NDIM >= 3 ? QC : 0) : s.qd[2];
     // stage the evaluation tables and row-class masks of this tile's +-p neighbourhood in smem
     const int p = s.p;
     const int L0 = TB0 + 2 * p, L1 = NDIM >= 2 ? TB1 + 2 * p : 1, L2 = NDIM >= 3 ? TB2 + 2 * p : 1;
@@ -588,6 +591,16 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
     }
     // ---- K7
     const int nthreads = 512;
+    const int ntiles = s.tg[0] * s.tg[1] * s.tg[2];
+    bool fixq = s.qd[0] == 3 && (n < 2 || s.qd[1] == 3) && (n < 3 || s.qd[2] == 3);
+    for (int d = 0; d < n; ++d) fixq = fixq && s.cmax[d] <= 5;
+    void* kfn;
+    if (fixq) {
+        for (int d = 0; d < n; ++d) s.cmax[d] = 5;
+        kfn = n == 1 ? (void*)interp_tiles_kernel<1, 3> : (n == 2 ? (void*)interp_tiles_kernel<2, 3> : (void*)interp_tiles_kernel<3, 3>);
+    } else {
+        kfn = n == 1 ? (void*)interp_tiles_kernel<1, 0> : (n == 2 ? (void*)interp_tiles_kernel<2, 0> : (void*)interp_tiles_kernel<3, 0>);
+    }
     const int NR = 64;
     const int nw = nthreads / 32;
     const int scr = s.cmax[2] * s.cmax[1] * s.TB[0] + s.cmax[2] * s.TB[1] * s.TB[0] + 8;
@@ -598,8 +611,6 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
     }
     const size_t smem = sizeof(double) * ((size_t)nw * scr + (size_t)nw * NR + NR) + sizeof(int) * ((size_t)nw * NR * 3 + 2) + tabs + 64;
     if (smem > 227 * 1024) return fail(-2, "surrogate tile does not fit shared memory (%zu B)", smem);
-    const int ntiles = s.tg[0] * s.tg[1] * s.tg[2];
-    void* kfn = n == 1 ? (void*)interp_tiles_kernel<1> : (n == 2 ? (void*)interp_tiles_kernel<2> : (void*)interp_tiles_kernel<3>);
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     void* args[] = {&s};
     c.kbegin("interp_tiles");
