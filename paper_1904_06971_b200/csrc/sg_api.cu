@@ -296,7 +296,7 @@ static void* kernel_ptr(int n, int form, bool rat, int which, int p, int* kmax) 
     return f;
 }
 
-static void* get_mma_kernel(int n, int form, int p, bool rat) { return kernel_ptr(n, form, rat, 1, p, nullptr); }
+static void* get_mma_kernel(int n, int form, int p, bool rat, int* nthreads) { return kernel_ptr(n, form, rat, 1, p, nthreads); }
 
 static void* get_kernel(int n, int form, int p, bool rat, int* kmax) { return kernel_ptr(n, form, rat, 0, p, kmax); }
 
@@ -494,17 +494,18 @@ static int encode_dmap(CUtensorMap* map, const double* D, int Dys, const int Gp[
 static bool plan_mma(DevProblem& dp, Plan& pl) {
     const int n = dp.n, P = dp.p, g = dp.g;
     if (P > 4 || g != P + 1 || getenv("SG_NO_MMA")) return false;
-    void* kfn = get_mma_kernel(n, dp.pr.form, P, dp.rational);
+    int nthreads = 0;
+    void* kfn = get_mma_kernel(n, dp.pr.form, P, dp.rational, &nthreads);
     if (!kfn) return false;
     const TileChoice tc = mma_tile(n, P, dp.pr.form, dp.rational);
     const MmaGeom M = mma_geom(n, P, dp.pr.form, dp.rational, tc.T0, tc.T1);
     if (M.total * 8 > (long)kSmemCap) return false;
     pl.mma = true;
     pl.kfn = kfn;
-    pl.nthreads = 512;
+    pl.nthreads = nthreads;
     pl.T[0] = M.T0;
     pl.T[1] = M.T1;
-    pl.T[2] = n == 3 ? 16 : 1;
+    pl.T[2] = n == 3 ? kMmaT2 : 1;
     for (int d = 0; d < 3; ++d) pl.tgrid[d] = (dp.m[d] + pl.T[d] - 1) / pl.T[d];
     pl.smem = M.total * sizeof(double);
     pl.ntiles = (int64_t)pl.tgrid[0] * pl.tgrid[1] * pl.tgrid[2];

@@ -277,12 +277,13 @@ struct TermTables {
 };
 
 // compile-time loop helper
+template <int I, class F, int... K>
+__device__ __forceinline__ void static_for_impl(F& f, std::integer_sequence<int, K...>) {
+    (f(std::integral_constant<int, I + K>{}), ...);
+}
 template <int I, int N, class F>
 __device__ __forceinline__ void static_for(F&& f) {
-    if constexpr (I < N) {
-        f(std::integral_constant<int, I>{});
-        static_for<I + 1, N>(f);
-    }
+    if constexpr (I < N) static_for_impl<I>(f, std::make_integer_sequence<int, N - I>{});
 }
 
 // ---------------------------------------------------------------------------------------------

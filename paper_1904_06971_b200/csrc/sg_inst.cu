@@ -33,7 +33,7 @@ static void* mma_ptr() {
 
 // which: 0 = SIMT tile kernel, 1 = DMMA tile kernel, 2 = geometry (K3)
 void* SG_NAME(int which, int p, int* kmax) {
-    if (kmax) *kmax = kmax_for(SG_INST_NDIM);
+    if (kmax) *kmax = which == 1 ? 32 * mma_warps(SG_INST_NDIM, p, SG_INST_FORM, kRat) : kmax_for(SG_INST_NDIM);
     if (which == 2) return (void*)&geom_D_kernel<SG_INST_NDIM, SG_INST_FORM, kRat>;
     switch (p) {
         case 1: return which ? mma_ptr<1>() : simt_ptr<1>();

@@ -108,16 +108,33 @@ __host__ __device__ constexpr int kind_of_slot2(const Tables& T, int slot) {
 }
 __host__ __device__ constexpr long align16(long o) { return (o + 15) & ~15L; }
 
-__host__ __device__ constexpr int pad16_4(int v) {  // smallest w >= v with w % 16 == 4 (conflict-free fragments)
+__host__ __device__ constexpr int pad_dy(int v) {  // w >= v, w % 16 in {4, 8, 12}: conflict-free B-fragment rows
     int w = v;
-    while (w % 16 != 4) ++w;
+    while (w % 16 == 0 || w % 4 != 0) ++w;
+    return w;
+}
+__host__ __device__ constexpr int pad8_4(int v) {  // smallest w >= v with w % 8 == 4 (conflict-free fragment rows)
+    int w = v;
+    while (w % 8 != 4) ++w;
     return w;
 }
 
+// warps per CTA (items are scheduled against it at compile time)
+__host__ __device__ constexpr int mma_warps(int ndim, int P, int form, bool rat) {
+#ifdef SG_MMA_NW
+    return SG_MMA_NW;
+#else
+    return 16;
+#endif
+}
+
 // ---- compile-time tile geometry (shared by host planning and the kernel)
+constexpr int kMmaT2 = 16;  // rows per CTA in z (3D)
+
 struct MmaGeom {
-    int T0, T1, G, W, MT, KS, KS3, XW, XWp, YW, NTY, DY, TY, NCOMBO, NMT, CH, NCH, TC, U, NG1, NG2, NU1, NB, NK1, NK2;
-    long o_B0, o_B1, o_B2, o_A1, o_B2f, o_B3f, o_cmb, o_bar, o_D, o_D2, o_T1, o_T2, total;
+    int NCP, T0, T1, G, W, MT, KS, KS3, XW, XWp, YW, NTY, DY, TY, NCOMBO, NMT, CH, NCH, TC, U, NG1, NG2, NU1, NB, NK1, NK2;
+    int NTAB;
+    long o_B0, o_B1, o_B2, o_A1, o_B2f, o_B3f, o_cmb, o_rb, o_tab, o_bar, o_D, o_D2, o_T1, o_T2, o_O, total;
 };
 
 __host__ __device__ constexpr MmaGeom mma_geom(int ndim, int P, int form, bool rat, int T0, int T1) {
@@ -134,13 +151,14 @@ __host__ __device__ constexpr MmaGeom mma_geom(int ndim, int P, int form, bool r
     m.XWp = (m.XW + 3) & ~3;  // TMA: box bytes DY*XWp*8 stay a multiple of 128
     m.YW = ndim >= 2 ? (m.T1 + P) * m.G : 1;
     m.NTY = ndim >= 2 ? (m.YW + 7) / 8 : 1;
-    m.DY = pad16_4(m.NTY * 8);
-    m.TY = pad16_4(m.NTY * 8 > m.YW + 4 ? m.NTY * 8 : m.YW + 4);
+    m.DY = pad_dy(m.NTY * 8);
+    m.TY = pad8_4(m.NTY * 8 > m.YW + 4 ? m.NTY * 8 : m.YW + 4);
     m.NCOMBO = T0 * m.T1 * m.W * m.W;
     m.NMT = (m.NCOMBO + 7) / 8;
     m.CH = 4;
     m.NCH = (m.NMT + m.CH - 1) / m.CH;
-    m.TC = pad16_4(m.NCH * m.CH * 8);
+    m.TC = pad8_4(m.NCH * m.CH * 8);
+    m.NCP = pad8_4(m.NCH * m.CH * 8);
     m.U = T.MS * (T.MS + 1) / 2;
     m.NG1 = T.NG1;
     m.NG2 = ndim == 3 ? T.NG2 : 1;
@@ -151,25 +169,36 @@ __host__ __device__ constexpr MmaGeom mma_geom(int ndim, int P, int form, bool r
     long o = 0;
     m.o_B0 = o; o += (long)m.XW * m.NB + 2;
     m.o_B1 = o; o += ndim >= 2 ? (long)m.YW * m.NB + 2 : 0;
-    m.o_B2 = o; o += ndim == 3 ? (long)m.G * m.NB + 2 : 0;
+    m.o_B2 = o;
     m.o_A1 = o; o += (long)T0 * m.NU1 * m.KS * m.MT * 32;                      // phase-1 A fragments
     m.o_B2f = o; o += ndim >= 2 ? (long)m.T1 * m.NK1 * m.KS * m.MT * 32 : 0;     // phase-2 B fragments
-    m.o_B3f = o; o += ndim == 3 ? (long)(P + 1) * m.NK2 * m.KS3 * m.MT * 32 : 0; // phase-3 B fragments
-    m.o_cmb = o; o += ndim == 3 ? (long)m.NCOMBO / 2 + 2 : 0;                  // per-combo CSR offsets (int)
+    m.o_B3f = o; o += ndim == 3 ? 2L * (P + 1) * m.NK2 * m.KS3 * m.MT * 32 : 0;  // phase-3 B fragments (2 layers)
+    o = (o + 1) & ~1L;
+    m.o_cmb = o; o += ndim == 3 ? (long)m.NCOMBO * 2 + 2 : 0;                  // per-combo {off, cnt01, row01, col01}
+    {
+        const int NW = mma_warps(ndim, P, form, rat);
+        int nu2 = 0;
+        for (int g = 0; g < (ndim >= 2 ? T.NG2 : 0); ++g) nu2 += T.g2n[g];
+        m.NTAB = 3 * (NW + 1) + m.NG1 * T0 + (ndim >= 2 ? T.NG2 * m.T1 * T0 : 0) + (ndim == 3 ? (P + 1) * m.NCH : 0) +
+                 (m.NG1 + 1) + m.NU1 + (T.NG2 + 1) + nu2 + T.NF;
+    }
+    m.o_rb = o; o += ndim == 3 ? (long)T0 * m.T1 * kMmaT2 : 0;                // CSR start of every tile row (int64, -1: not owned)
+    m.o_tab = o; o += (m.NTAB + 1) / 2;                                        // item schedule + unit tables (int)
     m.o_bar = o; o += 2;                                                       // two mbarriers (TMA)
     o = align16(o);
     m.o_D = o; o += align16((long)m.U * m.XWp * m.DY);                          // D window, double buffered (TMA)
     m.o_D2 = ndim == 3 ? o : m.o_D;                                           // 2D/1D: one plane per tile
     o += ndim == 3 ? align16((long)m.U * m.XWp * m.DY) : 0;
-    m.o_T1 = o; o += ndim >= 2 ? (long)m.NG1 * T0 * m.MT * 8 * m.TY : 0;
-    m.o_T2 = o; o += ndim == 3 ? (long)m.NG2 * m.G * m.TC : 0;
+    m.o_T1 = o; o += ndim >= 2 ? (ndim == 3 ? 2L : 1L) * m.NG1 * T0 * m.MT * 8 * m.TY : 0;  // 3D: 2 planes
+    m.o_T2 = o; o += ndim == 3 ? (long)(m.G + 1) * m.NG2 * m.TC : 0;            // ring of G+1 planes
+    m.o_O = o; o += ndim == 3 ? (long)(P + 1) * (P + 1) * m.NCP : 0;            // live (i2, j2) partial sums
     m.total = o;
     return m;
 }
 
 struct TileChoice { int T0, T1; };
 __host__ __device__ constexpr TileChoice mma_tile(int ndim, int P, int form, bool rat) {
-    const long cap = 200 * 1024 / 8;
+    const long cap = 224 * 1024 / 8;
     if (ndim == 1) return {32, 1};
     if (ndim == 2) {
         const int cand[] = {12, 10, 8, 6, 4, 3, 2, 1};
@@ -182,6 +211,131 @@ __host__ __device__ constexpr TileChoice mma_tile(int ndim, int P, int form, boo
         if (mma_geom(3, P, form, rat, t.T0, t.T1).total <= cap) return t;
     return {1, 1};
 }
+
+// ---- compile-time LPT schedule of the warp items of one barrier interval, emitted as a runtime table
+// phase-1 items (group, i0l), phase-2 items (level-2 group, i1l, i0l), phase-3 items (r2, chunk);
+// cost = DMMAs of the item's chains (+ a small epilogue constant).  3D: phases 1 and 2 share an
+// interval (pipelined over planes) and phase 3 is placed on top of that load.  The item bodies are
+// data driven (one copy of the code per phase: the unrolled-per-item form thrashed the I-cache).
+// Table (ints): off1[NW+1] off2[NW+1] off3[NW+1] | items1 items2 items3 (grouped by warp) |
+//   u1beg[NG1+1] u1ud[NU1] | u2beg[NG2+1] u2[NU2] | u3[NF]
+// packed units: ga | gaT << 8 | kd << 16 | kdT << 20 | pair << 24, non-pair units first.
+constexpr int kTabMax = 1024;
+struct MmaTab {
+    int v[kTabMax];
+    int n;
+    int o_off1, o_off2, o_off3, o_it1, o_it2, o_it3, o_u1b, o_u1ud, o_u2b, o_u2, o_u3;
+};
+__host__ __device__ constexpr int g2_blocks(const Tables& T, int g) { return T.g2n[g] + g2_npairs(T, g); }
+__host__ __device__ constexpr int pack_unit(int ga, int gaT, int kd, int kdT, int pair) {
+    return ga | (gaT << 8) | (kd << 16) | (kdT << 20) | (pair << 24);
+}
+__host__ __device__ constexpr MmaTab mma_tab(int ndim, int P, int form, bool rat) {
+    const Tables T = make_tables(ndim, form, rat);
+    const TileChoice tc = mma_tile(ndim, P, form, rat);
+    const MmaGeom M = mma_geom(ndim, P, form, rat, tc.T0, tc.T1);
+    const int NW = mma_warps(ndim, P, form, rat);
+    MmaTab S{};
+    const int n1 = M.NG1 * M.T0;
+    const int n2 = ndim >= 2 ? T.NG2 * M.T1 * M.T0 : 0;
+    const int n3 = ndim == 3 ? (P + 1) * M.NCH : 0;
+    int w1[512] = {}, w2[512] = {}, w3[512] = {};
+    long load[64] = {};
+    int cost[1024] = {};
+    int kind[1024] = {}, idx[1024] = {};
+    bool done[1024] = {};
+    int n = 0;
+    auto lpt = [&]() {
+        for (int it = 0; it < n; ++it) {
+            int best = -1;
+            for (int k = 0; k < n; ++k)
+                if (!done[k] && (best < 0 || cost[k] > cost[best])) best = k;
+            done[best] = true;
+            int w = 0;
+            for (int v = 1; v < NW; ++v)
+                if (load[v] < load[w]) w = v;
+            load[w] += cost[best];
+            if (kind[best] == 1) w1[idx[best]] = w;
+            else if (kind[best] == 2) w2[idx[best]] = w;
+            else w3[idx[best]] = w;
+        }
+        n = 0;
+    };
+    for (int k = 0; k < n1; ++k) {
+        cost[n] = T.g1n[k / M.T0] * M.KS * M.MT * M.NTY + 2;
+        kind[n] = 1; idx[n] = k; done[n] = false; ++n;
+    }
+    if (ndim != 3) {  // 2D: phase 2 after its own barrier
+        lpt();
+        for (int v = 0; v < NW; ++v) load[v] = 0;
+    }
+    for (int k = 0; k < n2; ++k) {
+        cost[n] = g2_blocks(T, k / (M.T1 * M.T0)) * M.KS * M.MT * M.MT + 2;
+        kind[n] = 2; idx[n] = k; done[n] = false; ++n;
+    }
+    lpt();
+    const int fb = T.NF + f_npairs(T);
+    for (int k = 0; k < n3; ++k) {
+        cost[n] = fb * M.KS3 * M.CH * M.MT + 2;
+        kind[n] = 3; idx[n] = k; done[n] = false; ++n;
+    }
+    lpt();
+    // emit
+    int o = 0;
+    S.o_off1 = o; o += NW + 1;
+    S.o_off2 = o; o += NW + 1;
+    S.o_off3 = o; o += NW + 1;
+    S.o_it1 = o; o += n1;
+    S.o_it2 = o; o += n2;
+    S.o_it3 = o; o += n3;
+    int c1 = 0, c2 = 0, c3 = 0;
+    for (int w = 0; w < NW; ++w) {
+        S.v[S.o_off1 + w] = c1;
+        S.v[S.o_off2 + w] = c2;
+        S.v[S.o_off3 + w] = c3;
+        for (int k = 0; k < n1; ++k) if (w1[k] == w) S.v[S.o_it1 + c1++] = k;
+        for (int k = 0; k < n2; ++k) if (w2[k] == w) S.v[S.o_it2 + c2++] = k;
+        for (int k = 0; k < n3; ++k) if (w3[k] == w) S.v[S.o_it3 + c3++] = k;
+    }
+    S.v[S.o_off1 + NW] = c1;
+    S.v[S.o_off2 + NW] = c2;
+    S.v[S.o_off3 + NW] = c3;
+    S.o_u1b = o; o += M.NG1 + 1;
+    S.o_u1ud = o; o += M.NU1;
+    for (int g = 0; g <= M.NG1; ++g) S.v[S.o_u1b + g] = g1_unit_base(T, g);
+    for (int g = 0; g < M.NG1; ++g)
+        for (int u = 0; u < T.g1n[g]; ++u) S.v[S.o_u1ud + g1_unit_base(T, g) + u] = tri_index(T.g1mu[g][u], T.g1nu[g][u], T.MS);
+    S.o_u2b = o; o += T.NG2 + 1;
+    S.o_u2 = o;
+    int c = 0;
+    for (int g = 0; g < (ndim >= 2 ? T.NG2 : 0); ++g) {
+        S.v[S.o_u2b + g] = c;
+        for (int pass = 0; pass < 2; ++pass)
+            for (int u = 0; u < T.g2n[g]; ++u) {
+                if (T.g2pair[g][u] != pass) continue;
+                const int ga = T.g2u[g][u], gaT = T.g1T[ga];
+                S.v[S.o_u2 + c++] = pack_unit(ga, gaT, kslot1(T, kind1(T, ga)), kslot1(T, kind1(T, gaT)), pass);
+            }
+    }
+    S.v[S.o_u2b + (ndim >= 2 ? T.NG2 : 0)] = c;
+    o += c;
+    S.o_u3 = o;
+    c = 0;
+    if (ndim == 3)
+        for (int pass = 0; pass < 2; ++pass)
+            for (int f = 0; f < T.NF; ++f) {
+                if (T.fpair[f] != pass) continue;
+                const int ga = T.fu[f], gaT = T.g2T[ga];
+                S.v[S.o_u3 + c++] = pack_unit(ga, gaT, kslot2(T, kind2(T, ga)), kslot2(T, kind2(T, gaT)), pass);
+            }
+    o += c;
+    S.n = o;
+    return S;
+}
+template <int NDIM, int P, int FORM, bool RAT>
+struct MmaTabS {
+    static constexpr MmaTab S = mma_tab(NDIM, P, FORM, RAT);
+};
 
 struct MmaParams {
     CUtensorMap dmap;            // TMA map of D: dims {Gp1, Gp0, U, Gp2} (y fastest), box {DY, XW, U, 1}
@@ -203,14 +357,14 @@ struct MmaParams {
 };
 
 template <int NDIM, int P, int FORM, bool RAT>
-__global__ void __launch_bounds__(512, 1) assemble_mma(const __grid_constant__ MmaParams prm) {
+__global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), 1) assemble_mma(const __grid_constant__ MmaParams prm) {
     using TTS = TermTables<NDIM, FORM, RAT>;
     constexpr TileChoice TCH = mma_tile(NDIM, P, FORM, RAT);
     constexpr MmaGeom M = mma_geom(NDIM, P, FORM, RAT, TCH.T0, TCH.T1);
     constexpr int T0 = M.T0, T1 = M.T1, G = M.G, W = M.W, MT = M.MT, KS = M.KS, KS3 = M.KS3;
     constexpr int NB = M.NB, XW = M.XW, YW = M.YW, NTY = M.NTY, DY = M.DY, TY = M.TY, TC = M.TC;
     constexpr int MS = TTS::T.MS;
-    constexpr int NW = 16;
+    constexpr int NW = mma_warps(NDIM, P, FORM, RAT);
     constexpr int NK1 = M.NK1, NK2 = M.NK2;
     constexpr int XWp = M.XWp;
     constexpr unsigned DBYTES = (unsigned)(M.U * XWp * DY * 8);
@@ -228,7 +382,6 @@ __global__ void __launch_bounds__(512, 1) assemble_mma(const __grid_constant__ M
 
     double* B0s = smem + M.o_B0;
     double* B1s = smem + M.o_B1;
-    double* B2s = smem + M.o_B2;
     double* A1f = smem + M.o_A1;
     double* B2f = smem + M.o_B2f;
     double* B3f = smem + M.o_B3f;
@@ -238,6 +391,14 @@ __global__ void __launch_bounds__(512, 1) assemble_mma(const __grid_constant__ M
     double* T1s = smem + M.o_T1;
     double* T2s = smem + M.o_T2;
 
+    // ---- item schedule + unit tables
+    if (tid == 0) {
+        int* tabw = reinterpret_cast<int*>(smem + M.o_tab);
+        static_for<0, MmaTabS<NDIM, P, FORM, RAT>::S.n>([&](auto I) {
+            constexpr int v = MmaTabS<NDIM, P, FORM, RAT>::S.v[decltype(I)::value];
+            tabw[decltype(I)::value] = v;
+        });
+    }
     // ---- zero the staging buffers once (padding columns / rows are read as exact zeros)
     for (long it = tid; it < M.total - M.o_T1; it += blockDim.x) T1s[it] = 0.0;
     // ---- window basis tables (zero outside the mesh)
@@ -309,17 +470,31 @@ __global__ void __launch_bounds__(512, 1) assemble_mma(const __grid_constant__ M
         }
     }
     if constexpr (NDIM == 3) {
-        // per-combo CSR offset inside a row's j2 block: (j0-lo0) + cnt0*(j1-lo1), or -1 (out of range)
+        // per combo: {offset inside a row's j2 block (or -1), cnt0*cnt1, i0 + m0 i1, j0 + m0 j1}
         for (int c = tid; c < M.NCOMBO; c += blockDim.x) {
             const int d0 = c % W - P, d1 = (c / W) % W - P, i1l = (c / (W * W)) % T1, i0l = c / (W * W * T1);
             const int i0 = b0 + i0l, i1 = b1 + i1l, j0 = i0 + d0, j1 = i1 + d1;
-            int off = -1;
+            int off = -1, c01 = 0;
             if (i0 < prm.m[0] && i1 < prm.m[1] && j0 >= 0 && j0 < prm.m[0] && j1 >= 0 && j1 < prm.m[1]) {
                 const int lo0 = max(0, i0 - P), lo1 = max(0, i1 - P);
-                const int cnt0 = min(prm.m[0] - 1, i0 + P) - lo0 + 1;
+                const int cnt0 = min(prm.m[0] - 1, i0 + P) - lo0 + 1, cnt1 = min(prm.m[1] - 1, i1 + P) - lo1 + 1;
                 off = (j0 - lo0) + cnt0 * (j1 - lo1);
+                c01 = cnt0 * cnt1;
             }
-            cmb[c] = off;
+            cmb[4 * c + 0] = off;
+            cmb[4 * c + 1] = c01;
+            cmb[4 * c + 2] = i0 + prm.m[0] * i1;
+            cmb[4 * c + 3] = j0 + prm.m[0] * j1;
+        }
+        int64_t* rb = reinterpret_cast<int64_t*>(smem + M.o_rb);
+        for (int t = tid; t < T0 * T1 * kMmaT2; t += blockDim.x) {
+            const int i2 = b2 + t % kMmaT2, i1 = b1 + (t / kMmaT2) % T1, i0 = b0 + t / (kMmaT2 * T1);
+            int64_t v = -1;
+            if (i0 < prm.m[0] && i1 < prm.m[1] && i2 < prm.m[2] && t % kMmaT2 < prm.T2) {
+                const int64_t row = (int64_t)i0 + (int64_t)prm.m[0] * i1 + (int64_t)prm.m[0] * prm.m[1] * i2;
+                if (row >= prm.slab_lo && row < prm.slab_hi && (!prm.rowmask || prm.rowmask[row])) v = prm.rowstart[row];
+            }
+            rb[t] = v;
         }
     }
 
@@ -354,365 +529,354 @@ __global__ void __launch_bounds__(512, 1) assemble_mma(const __grid_constant__ M
         __syncthreads();
         if (tid == 0) issue_plane(0);
     }
-    int pidx = 0;
-    (void)nplanes;
+    // make the D window of plane j resident in Dbuf[j & 1] (plain path: all threads load, then a barrier)
+    auto get_plane = [&](int j) {
+        double* Ds = Dbuf[j & 1];
+        if (use_tma) {
+            if (tid == 0 && j + 1 < nplanes) issue_plane(j + 1);  // prefetch the next plane
+            const uint32_t bar = bar0 + 8u * (uint32_t)(j & 1);
+            const uint32_t par = (uint32_t)((j >> 1) & 1);
+            uint32_t done = 0;
+            while (!done) {
+                asm volatile(
+                    "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                    : "=r"(done)
+                    : "r"(bar), "r"(par)
+                    : "memory");
+            }
+        } else {
+            const long long gx0 = (long long)ew0 * G, gy0 = (long long)ew1 * G;
+            const long long z = (long long)elo2 * G + j;
+            const long long G1 = NDIM >= 2 ? prm.Gp[1] : 1;
+            for (int it = tid; it < M.U * XWp * DY; it += blockDim.x) {
+                const int y = it % DY, r = it / DY;
+                const int u = r / XWp, x = r % XWp;
+                const long long gx = gx0 + x, gy = gy0 + y;
+                double v = 0.0;
+                if (gx >= 0 && gx < G0 && gy >= 0 && gy < G1)
+                    v = prm.D[((z * M.U + u) * G0 + gx) * (long long)prm.Dys + gy];
+                Ds[r * DY + y] = v;
+            }
+            __syncthreads();
+        }
+        return Ds;
+    };
 
-    for (int e2 = elo2; e2 <= ehi2; ++e2) {
-        if constexpr (NDIM == 3) {
-            __syncthreads();
-            for (int it = tid; it < G * NB; it += blockDim.x) B2s[it] = prm.B[2][(long long)e2 * G * NB + it];
-            __syncthreads();
-            // phase-3 B fragments of this layer: B3f[((r2*NK2 + slot)*KS3 + kk)*MT + c][lane]
-            for (int it = warp; it < (P + 1) * NK2; it += NW) {
-                const int r2 = it % (P + 1), slot = it / (P + 1);
-                int kind = 0;
-                static_for<0, NK2>([&](auto SI) { if (slot == decltype(SI)::value) kind = kind_of_slot2(TTS::T, decltype(SI)::value); });
-                const int a2 = kind % 3, bb2 = kind / 3;
-                for (int kk = 0; kk < KS3; ++kk) {
+    using TAB = MmaTabS<NDIM, P, FORM, RAT>;
+    constexpr long T1SZ = (long)M.NG1 * T0 * MT * 8 * TY;
+    const int* tab = reinterpret_cast<const int*>(smem + M.o_tab);
+
+    // ---------------- phase 1 (x): items (group, row i0l) -> T1[Gc][i0l][d0][y]
+    auto phase1 = [&](const double* Ds, double* T1b) {
+        const int qe = tab[TAB::S.o_off1 + warp + 1];
+        for (int q = tab[TAB::S.o_off1 + warp]; q < qe; ++q) {
+            const int k = tab[TAB::S.o_it1 + q];
+            const int Gc = k / T0, i0l = k - (k / T0) * T0;
+            double acc[MT][NTY][2];
+#pragma unroll
+            for (int a = 0; a < MT; ++a)
+#pragma unroll
+                for (int c = 0; c < NTY; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+            const int ue = tab[TAB::S.o_u1b + Gc + 1];
+            for (int unit = tab[TAB::S.o_u1b + Gc]; unit < ue; ++unit) {
+                const int ud = tab[TAB::S.o_u1ud + unit];
+                const double* af = A1f + ((i0l * M.NU1 + unit) * KS) * MT * 32 + lane;
+                const double* dpl = Ds + (ud * XWp) * DY + lr;
+#pragma unroll
+                for (int kk = 0; kk < KS; ++kk) {
                     const int s = kk * 4 + lk;
-                    for (int c = 0; c < MT; ++c) {
-                        const int d2 = c * 8 + lr - P;
-                        const int rj2 = r2 + d2;
-                        double v = 0.0;
-                        if (s < G && d2 <= P && rj2 >= 0 && rj2 <= P) {
-                            const double* bz = B2s + s * NB;
-                            v = __dmul_rn(bz[a2 * (P + 1) + r2], bz[bb2 * (P + 1) + rj2]);
+                    const int x = (s < (P + 1) * G) ? i0l * G + s : 0;
+                    const double* drow = dpl + x * DY;
+                    double afr[MT];
+#pragma unroll
+                    for (int a = 0; a < MT; ++a) afr[a] = af[(kk * MT + a) * 32];
+#pragma unroll
+                    for (int c = 0; c < NTY; ++c) {
+                        const double bf = drow[c * 8];
+#pragma unroll
+                        for (int a = 0; a < MT; ++a) dmma(acc[a][c][0], acc[a][c][1], afr[a], bf);
+                    }
+                }
+            }
+            if constexpr (NDIM == 1) {
+                const int i0 = b0 + i0l;
+                if (lk == 0 && i0 < prm.m[0]) {
+                    const int64_t row = i0;
+                    if (row >= prm.slab_lo && row < prm.slab_hi && (!prm.rowmask || prm.rowmask[row])) {
+                        const int lo = max(0, i0 - P);
+                        const int64_t base = prm.rowstart[row];
+#pragma unroll
+                        for (int a = 0; a < MT; ++a) {
+                            const int d0 = a * 8 + lr - P;
+                            const int j0 = i0 + d0;
+                            if (d0 > P || j0 < 0 || j0 >= prm.m[0]) continue;
+                            double v = acc[a][0][0];
+                            if constexpr (RAT) v = v * (prm.sol_w[i0] * prm.sol_w[j0]);
+                            prm.data[base + (j0 - lo)] = v;
+                            prm.indices[base + (j0 - lo)] = j0;
+                            if (prm.zeros && v == 0.0) atomicAdd(prm.zeros, 1ull);
                         }
-                        B3f[(((r2 * NK2 + slot) * KS3 + kk) * MT + c) * 32 + lane] = v;
+                    }
+                }
+            } else {
+                double* t1 = T1b + ((Gc * T0 + i0l) * MT * 8) * TY;
+#pragma unroll
+                for (int a = 0; a < MT; ++a)
+#pragma unroll
+                    for (int c = 0; c < NTY; ++c) {
+                        double* dst = t1 + (a * 8 + lr) * TY + c * 8 + 2 * lk;
+                        dst[0] = acc[a][c][0];
+                        dst[1] = acc[a][c][1];
+                    }
+            }
+        }
+    };
+
+    // ---------------- phase 2 (y): items (level-2 group, row i1l, row i0l)
+    // 2D: final values into the CSR; 3D: T2 plane slot [g2][(i0l,i1l,d1,d0)]
+    // Chains: non-pair units into accS in unit order, then each symmetric pair (A, B chains) folded
+    // in as accS + (A + B) in order -- the mirror of the transposed entry's evaluation.
+    auto phase2 = [&](const double* T1b, double* T2b) {
+        if constexpr (NDIM >= 2) {
+            const int qe = tab[TAB::S.o_off2 + warp + 1];
+            for (int q = tab[TAB::S.o_off2 + warp]; q < qe; ++q) {
+                const int k = tab[TAB::S.o_it2 + q];
+                const int Gc = k / (T1 * T0), rem = k - Gc * (T1 * T0);
+                const int i1l = rem / T0, r = rem - (rem / T0) * T0;
+                const int i1 = b1 + i1l, i0 = b0 + r;
+                if (i1 >= prm.m[1] || i0 >= prm.m[0]) continue;
+                auto block = [&](int ga, int kd, double (&acc)[MT][MT][2]) {
+                    const double* bfp = B2f + ((i1l * NK1 + kd) * KS) * MT * 32 + lane;
+                    // y of support point s of row i1 is i1l*G + s (the support is contiguous)
+                    const double* t1 = T1b + ((ga * T0 + r) * MT * 8 + lr) * TY + i1l * G + lk;
+#pragma unroll
+                    for (int kk = 0; kk < KS; ++kk) {
+                        double bfs[MT];
+#pragma unroll
+                        for (int c = 0; c < MT; ++c) bfs[c] = bfp[(kk * MT + c) * 32];
+#pragma unroll
+                        for (int a = 0; a < MT; ++a) {
+                            const double av = t1[a * 8 * TY + kk * 4];
+#pragma unroll
+                            for (int c = 0; c < MT; ++c) dmma(acc[a][c][0], acc[a][c][1], av, bfs[c]);
+                        }
+                    }
+                };
+                double accS[MT][MT][2];
+#pragma unroll
+                for (int a = 0; a < MT; ++a)
+#pragma unroll
+                    for (int c = 0; c < MT; ++c) accS[a][c][0] = accS[a][c][1] = 0.0;
+                const int ue = tab[TAB::S.o_u2b + Gc + 1];
+                for (int u = tab[TAB::S.o_u2b + Gc]; u < ue; ++u) {
+                    const int d = tab[TAB::S.o_u2 + u];
+                    const int ga = d & 255, kd = (d >> 16) & 15;
+                    if (!(d >> 24)) {
+                        block(ga, kd, accS);
+                    } else {
+                        double tA[MT][MT][2], tB[MT][MT][2];
+#pragma unroll
+                        for (int a = 0; a < MT; ++a)
+#pragma unroll
+                            for (int c = 0; c < MT; ++c) tA[a][c][0] = tA[a][c][1] = tB[a][c][0] = tB[a][c][1] = 0.0;
+                        block(ga, kd, tA);
+                        block((d >> 8) & 255, (d >> 20) & 15, tB);
+#pragma unroll
+                        for (int a = 0; a < MT; ++a)
+#pragma unroll
+                            for (int c = 0; c < MT; ++c)
+#pragma unroll
+                                for (int h = 0; h < 2; ++h) accS[a][c][h] = __dadd_rn(accS[a][c][h], __dadd_rn(tA[a][c][h], tB[a][c][h]));
+                    }
+                }
+                if constexpr (NDIM == 2) {
+                    const int64_t row = (int64_t)i0 + (int64_t)prm.m[0] * i1;
+                    if (!(row >= prm.slab_lo && row < prm.slab_hi && (!prm.rowmask || prm.rowmask[row]))) continue;
+                    const int lo0 = max(0, i0 - P), lo1 = max(0, i1 - P);
+                    const int cnt0 = min(prm.m[0] - 1, i0 + P) - lo0 + 1;
+                    const int64_t base = prm.rowstart[row];
+                    const double si = RAT ? prm.sol_w[row] : 1.0;
+#pragma unroll
+                    for (int a = 0; a < MT; ++a) {
+                        const int d0 = a * 8 + lr - P;
+                        const int j0 = i0 + d0;
+                        if (d0 > P || j0 < 0 || j0 >= prm.m[0]) continue;
+#pragma unroll
+                        for (int c = 0; c < MT; ++c)
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                const int d1 = c * 8 + 2 * lk + h - P;
+                                const int j1 = i1 + d1;
+                                if (d1 > P || j1 < 0 || j1 >= prm.m[1]) continue;
+                                double v = accS[a][c][h];
+                                const int64_t col = (int64_t)j0 + (int64_t)prm.m[0] * j1;
+                                if constexpr (RAT) v = v * (si * prm.sol_w[col]);
+                                const int64_t pos = base + (j0 - lo0) + (int64_t)cnt0 * (j1 - lo1);
+                                prm.data[pos] = v;
+                                prm.indices[pos] = (int)col;
+                                if (prm.zeros && v == 0.0) atomicAdd(prm.zeros, 1ull);
+                            }
+                    }
+                } else {
+                    double* t2 = T2b + Gc * TC + (r * T1 + i1l) * W * W;
+#pragma unroll
+                    for (int a = 0; a < MT; ++a) {
+                        const int d0 = a * 8 + lr;
+                        if (d0 >= W) continue;
+#pragma unroll
+                        for (int c = 0; c < MT; ++c)
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                const int d1 = c * 8 + 2 * lk + h;
+                                if (d1 < W) t2[d1 * W + d0] = accS[a][c][h];
+                            }
                     }
                 }
             }
         }
-        for (int q2 = 0; q2 < GZ; ++q2) {
-            // ---------------- D window of this plane
-            double* Ds = Dbuf[pidx & 1];
-            if (use_tma) {
-                if (tid == 0 && pidx + 1 < nplanes) issue_plane(pidx + 1);  // prefetch the next plane
-                const uint32_t bar = bar0 + 8u * (uint32_t)(pidx & 1);
-                const uint32_t par = (uint32_t)((pidx >> 1) & 1);
-                uint32_t done = 0;
-                while (!done) {
-                    asm volatile(
-                        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-                        : "=r"(done)
-                        : "r"(bar), "r"(par)
-                        : "memory");
-                }
-            } else {
-                const long long gx0 = (long long)ew0 * G, gy0 = (long long)ew1 * G;
-                const long long z = (long long)elo2 * G + pidx;
-                const long long G1 = NDIM >= 2 ? prm.Gp[1] : 1;
-                for (int it = tid; it < M.U * XWp * DY; it += blockDim.x) {
-                    const int y = it % DY, r = it / DY;
-                    const int u = r / XWp, x = r % XWp;
-                    const long long gx = gx0 + x, gy = gy0 + y;
-                    double v = 0.0;
-                    if (gx >= 0 && gx < G0 && gy >= 0 && gy < G1)
-                        v = prm.D[((z * M.U + u) * G0 + gx) * (long long)prm.Dys + gy];
-                    Ds[r * DY + y] = v;
-                }
-                __syncthreads();
-            }
+    };
 
-            // ---------------- phase 1: items (group, row i0l), statically scheduled over warps
-            static_for<0, M.NG1 * T0>([&](auto KI) {
-                constexpr int k = decltype(KI)::value;
-                if (warp != k % NW) return;
-                constexpr int Gc = k / T0, i0l = k % T0;
-                const int i0 = b0 + i0l;
-                double acc[MT][NTY][2];
+    if constexpr (NDIM <= 2) {
+        const double* Ds = get_plane(0);
+        phase1(Ds, T1s);
+        if constexpr (NDIM == 2) {
+            __syncthreads();
+            phase2(T1s, nullptr);
+        }
+    } else {
+        // ---------------- 3D: one barrier interval per Gauss plane j (ascending z):
+        //   phase 3(layer finished one interval ago; final entries straight to the CSR)
+        //   | phase 1(plane j) | phase 2(plane j-1) | phase-3 fragments of the layer starting at j
+        // T1 is double buffered by plane parity, T2 is a ring of G+1 plane slots, the phase-3
+        // fragments are double buffered by layer parity.
+        constexpr int NS = G + 1;
+        constexpr int B3SZ = (P + 1) * NK2 * KS3 * MT * 32;
+        constexpr int CH = M.CH;
+        const int m01 = prm.m[0] * prm.m[1];
+        double* Os = smem + M.o_O;
+        for (int j = 0; j <= nplanes + 1; ++j) {
+            const double* Ds = j < nplanes ? get_plane(j) : nullptr;
+            // ---- phase 3 (z) of layer L3: items (row offset r2, chunk of CH m-tiles) -> O
+            if (j >= G + 1 && (j - 1) % G == 0) {
+                const int L3 = (j - 1) / G - 1;
+                const int e2 = elo2 + L3;
+                const double* B3b = B3f + (L3 & 1) * B3SZ;
+                const int qe = tab[TAB::S.o_off3 + warp + 1];
+                for (int q = tab[TAB::S.o_off3 + warp]; q < qe; ++q) {
+                    const int k = tab[TAB::S.o_it3 + q];
+                    const int r2 = k % (P + 1), ch = k / (P + 1);
+                    const int i2 = e2 + r2;
+                    if (i2 < b2 || i2 >= b2 + prm.T2 || i2 >= prm.m[2]) continue;
+                    auto block = [&](int ga, int kd, double (&acc)[CH][MT][2]) {
+                        const double* bfp = B3b + ((r2 * NK2 + kd) * KS3) * MT * 32 + lane;
 #pragma unroll
-                for (int a = 0; a < MT; ++a)
-#pragma unroll
-                    for (int c = 0; c < NTY; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
-                static_for<0, TTS::T.g1n[Gc]>([&](auto UI) {
-                    constexpr int Uc = decltype(UI)::value;
-                    constexpr int mu = TTS::T.g1mu[Gc][Uc], nu = TTS::T.g1nu[Gc][Uc];
-                    constexpr int ud = tri_index(mu, nu, MS);
-                    constexpr int unit = g1_unit_base(TTS::T, Gc) + Uc;
-                    const double* af = A1f + ((i0l * M.NU1 + unit) * KS) * MT * 32 + lane;
-#pragma unroll
-                    for (int kk = 0; kk < KS; ++kk) {
-                        const int s = kk * 4 + lk;
-                        const int x = (s < (P + 1) * G) ? (i0l + s / G) * G + s % G : 0;
-                        const double* drow = Ds + (ud * XWp + x) * DY + lr;
-                        double afr[MT];
-#pragma unroll
-                        for (int a = 0; a < MT; ++a) afr[a] = af[(kk * MT + a) * 32];
-#pragma unroll
-                        for (int c = 0; c < NTY; ++c) {
-                            const double bf = drow[c * 8];
-#pragma unroll
-                            for (int a = 0; a < MT; ++a) dmma(acc[a][c][0], acc[a][c][1], afr[a], bf);
-                        }
-                    }
-                });
-                if constexpr (NDIM == 1) {
-                    if (lk == 0 && i0 < prm.m[0]) {
-                        const int64_t row = i0;
-                        if (row >= prm.slab_lo && row < prm.slab_hi && (!prm.rowmask || prm.rowmask[row])) {
-                            const int lo = max(0, i0 - P);
-                            const int64_t base = prm.rowstart[row];
-#pragma unroll
-                            for (int a = 0; a < MT; ++a) {
-                                const int d0 = a * 8 + lr - P;
-                                const int j0 = i0 + d0;
-                                if (d0 > P || j0 < 0 || j0 >= prm.m[0]) continue;
-                                double v = acc[a][0][0];
-                                if constexpr (RAT) v = v * (prm.sol_w[i0] * prm.sol_w[j0]);
-                                prm.data[base + (j0 - lo)] = v;
-                                prm.indices[base + (j0 - lo)] = j0;
-                                if (prm.zeros && v == 0.0) atomicAdd(prm.zeros, 1ull);
-                            }
-                        }
-                    }
-                } else {
-                    double* t1 = T1s + ((Gc * T0 + i0l) * MT * 8) * TY;
-#pragma unroll
-                    for (int a = 0; a < MT; ++a)
-#pragma unroll
-                        for (int c = 0; c < NTY; ++c) {
-                            double* dst = t1 + (a * 8 + lr) * TY + c * 8 + 2 * lk;
-                            dst[0] = acc[a][c][0];
-                            dst[1] = acc[a][c][1];
-                        }
-                }
-            });
-            if constexpr (NDIM >= 2) {
-                __syncthreads();
-                // ---------------- phase 2: items (level-2 group, row i1l); the T0 rows i0 share Q1
-                static_for<0, M.NG2 * T1>([&](auto KI) {
-                    constexpr int k = decltype(KI)::value;
-                    if (warp != k % NW) return;
-                    constexpr int Gc = k / T1, i1l = k % T1;
-                    const int i1 = b1 + i1l;
-                    if (i1 >= prm.m[1]) return;
-                    constexpr int NPR = g2_npairs(TTS::T, Gc);
-                    constexpr int NA = imax(NPR, 1);
-                    double accS[T0][MT][MT][2];
-                    double accA[NA][T0][MT][MT][2];
-                    double accB[NA][T0][MT][MT][2];
-#pragma unroll
-                    for (int r = 0; r < T0; ++r)
-#pragma unroll
-                        for (int a = 0; a < MT; ++a)
-#pragma unroll
-                            for (int c = 0; c < MT; ++c)
-#pragma unroll
-                                for (int h = 0; h < 2; ++h) {
-                                    accS[r][a][c][h] = 0.0;
-#pragma unroll
-                                    for (int kx = 0; kx < NA; ++kx) accA[kx][r][a][c][h] = accB[kx][r][a][c][h] = 0.0;
-                                }
-                    auto block = [&](auto GA, auto& acc) {
-                        constexpr int ga = decltype(GA)::value;
-                        constexpr int kd = kslot1(TTS::T, kind1(TTS::T, ga));
-                        const double* bfp = B2f + ((i1l * NK1 + kd) * KS) * MT * 32 + lane;
-                        // y of support point s of row i1 is i1l*G + s (the support is contiguous)
-                        const double* t1 = T1s + ((ga * T0) * MT * 8 + lr) * TY + i1l * G + lk;
-#pragma unroll
-                        for (int kk = 0; kk < KS; ++kk) {
+                        for (int kk = 0; kk < KS3; ++kk) {
                             double bfs[MT];
 #pragma unroll
                             for (int c = 0; c < MT; ++c) bfs[c] = bfp[(kk * MT + c) * 32];
+                            const int s = kk * 4 + lk;
+                            const int slot = (L3 * G + (s < G ? s : 0)) % NS;
+                            const double* t2 = T2s + (slot * M.NG2 + ga) * TC + ch * CH * 8 + lr;
 #pragma unroll
-                            for (int r = 0; r < T0; ++r)
+                            for (int mm = 0; mm < CH; ++mm) {
+                                const double av = t2[mm * 8];
 #pragma unroll
-                                for (int a = 0; a < MT; ++a) {
-                                    const double av = t1[(r * MT + a) * 8 * TY + kk * 4];
-#pragma unroll
-                                    for (int c = 0; c < MT; ++c) dmma(acc[r][a][c][0], acc[r][a][c][1], av, bfs[c]);
-                                }
+                                for (int c = 0; c < MT; ++c) dmma(acc[mm][c][0], acc[mm][c][1], av, bfs[c]);
+                            }
                         }
                     };
-                    static_for<0, TTS::T.g2n[Gc]>([&](auto UI) {
-                        constexpr int Uc = decltype(UI)::value;
-                        constexpr int ga = TTS::T.g2u[Gc][Uc];
-                        if constexpr (TTS::T.g2pair[Gc][Uc] == 0) {
-                            block(std::integral_constant<int, ga>{}, accS);
+                    double accS[CH][MT][2];
+#pragma unroll
+                    for (int mm = 0; mm < CH; ++mm)
+#pragma unroll
+                        for (int c = 0; c < MT; ++c) accS[mm][c][0] = accS[mm][c][1] = 0.0;
+                    for (int u = 0; u < TTS::T.NF; ++u) {
+                        const int d = tab[TAB::S.o_u3 + u];
+                        const int ga = d & 255, kd = (d >> 16) & 15;
+                        if (!(d >> 24)) {
+                            block(ga, kd, accS);
                         } else {
-                            constexpr int pi = g2_pairidx(TTS::T, Gc, Uc);
-                            block(std::integral_constant<int, ga>{}, accA[pi]);
-                            block(std::integral_constant<int, TTS::T.g1T[ga]>{}, accB[pi]);
-                        }
-                    });
+                            double tA[CH][MT][2], tB[CH][MT][2];
 #pragma unroll
-                    for (int r = 0; r < T0; ++r)
+                            for (int mm = 0; mm < CH; ++mm)
 #pragma unroll
-                        for (int a = 0; a < MT; ++a)
+                                for (int c = 0; c < MT; ++c) tA[mm][c][0] = tA[mm][c][1] = tB[mm][c][0] = tB[mm][c][1] = 0.0;
+                            block(ga, kd, tA);
+                            block((d >> 8) & 255, (d >> 20) & 15, tB);
 #pragma unroll
-                            for (int c = 0; c < MT; ++c)
-#pragma unroll
-                                for (int h = 0; h < 2; ++h) {
-                                    double v = accS[r][a][c][h];
-#pragma unroll
-                                    for (int kx = 0; kx < NPR; ++kx) v = __dadd_rn(v, __dadd_rn(accA[kx][r][a][c][h], accB[kx][r][a][c][h]));
-                                    accS[r][a][c][h] = v;
-                                }
-#pragma unroll
-                    for (int r = 0; r < T0; ++r) {
-                        const int i0 = b0 + r;
-                        if (i0 >= prm.m[0]) continue;
-                        if constexpr (NDIM == 2) {
-                            const int64_t row = (int64_t)i0 + (int64_t)prm.m[0] * i1;
-                            if (!(row >= prm.slab_lo && row < prm.slab_hi && (!prm.rowmask || prm.rowmask[row]))) continue;
-                            const int lo0 = max(0, i0 - P), lo1 = max(0, i1 - P);
-                            const int cnt0 = min(prm.m[0] - 1, i0 + P) - lo0 + 1;
-                            const int64_t base = prm.rowstart[row];
-                            const double si = RAT ? prm.sol_w[row] : 1.0;
-#pragma unroll
-                            for (int a = 0; a < MT; ++a) {
-                                const int d0 = a * 8 + lr - P;
-                                const int j0 = i0 + d0;
-                                if (d0 > P || j0 < 0 || j0 >= prm.m[0]) continue;
+                            for (int mm = 0; mm < CH; ++mm)
 #pragma unroll
                                 for (int c = 0; c < MT; ++c)
 #pragma unroll
-                                    for (int h = 0; h < 2; ++h) {
-                                        const int d1 = c * 8 + 2 * lk + h - P;
-                                        const int j1 = i1 + d1;
-                                        if (d1 > P || j1 < 0 || j1 >= prm.m[1]) continue;
-                                        double v = accS[r][a][c][h];
-                                        const int64_t col = (int64_t)j0 + (int64_t)prm.m[0] * j1;
-                                        if constexpr (RAT) v = v * (si * prm.sol_w[col]);
-                                        const int64_t pos = base + (j0 - lo0) + (int64_t)cnt0 * (j1 - lo1);
-                                        prm.data[pos] = v;
-                                        prm.indices[pos] = (int)col;
-                                        if (prm.zeros && v == 0.0) atomicAdd(prm.zeros, 1ull);
-                                    }
-                            }
-                        } else {
-                            double* t2 = T2s + (Gc * G + q2) * TC + (r * T1 + i1l) * W * W;
-#pragma unroll
-                            for (int a = 0; a < MT; ++a) {
-                                const int d0 = a * 8 + lr;
-                                if (d0 >= W) continue;
-#pragma unroll
-                                for (int c = 0; c < MT; ++c)
-#pragma unroll
-                                    for (int h = 0; h < 2; ++h) {
-                                        const int d1 = c * 8 + 2 * lk + h;
-                                        if (d1 < W) t2[d1 * W + d0] = accS[r][a][c][h];
-                                    }
-                            }
+                                    for (int h = 0; h < 2; ++h) accS[mm][c][h] = __dadd_rn(accS[mm][c][h], __dadd_rn(tA[mm][c][h], tB[mm][c][h]));
                         }
                     }
-                });
+                    // accumulate the layer into O[(i2 mod G)*G + (j2 mod G)][combo] (the entries live at this
+                    // layer have i2, j2 in [e2, e2+P]: distinct residues); the first layer of an entry
+                    // overwrites, its last layer writes the CSR (once, no read-modify-write in HBM)
+                    const int64_t* rb = reinterpret_cast<const int64_t*>(smem + M.o_rb);
+                    const int i2m = i2 % G;
+#pragma unroll
+                    for (int mm = 0; mm < CH; ++mm) {
+                        const int combo = (ch * CH + mm) * 8 + lr;
+                        if (combo >= M.NCOMBO) continue;
+                        const int4 cb = reinterpret_cast<const int4*>(cmb)[combo];
+                        const int64_t rowb = rb[(combo / (W * W)) * kMmaT2 + (i2 - b2)];
+#pragma unroll
+                        for (int c = 0; c < MT; ++c)
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                const int d2 = c * 8 + 2 * lk + h - P;
+                                const int rj2 = r2 + d2;
+                                if (d2 > P || rj2 < 0 || rj2 > P) continue;
+                                const int j2 = e2 + rj2;
+                                const int first = max(0, max(i2, j2) - P);
+                                const int last = min(min(i2, j2), prm.S[2] - 1);
+                                double* slot = Os + (i2m * G + j2 % G) * M.NCP + combo;
+                                double v = accS[mm][c][h];
+                                if (e2 != first) v = *slot + v;
+                                if (e2 != last) {
+                                    *slot = v;
+                                } else if (cb.x >= 0 && rowb >= 0) {
+                                    const int64_t pos = rowb + cb.x + (int64_t)cb.y * (j2 - max(0, i2 - P));
+                                    const int col = cb.w + m01 * j2;
+                                    if constexpr (RAT) v = v * (prm.sol_w[(int64_t)cb.z + (int64_t)m01 * i2] * prm.sol_w[col]);
+                                    if (prm.zeros && v == 0.0) atomicAdd(prm.zeros, 1ull);
+                                    prm.data[pos] = v;
+                                    prm.indices[pos] = col;
+                                }
+                            }
+                    }
+                }
+            }
+            if (j < nplanes) phase1(Ds, T1s + (j & 1) * T1SZ);
+            if (j >= 1 && j <= nplanes) phase2(T1s + ((j - 1) & 1) * T1SZ, T2s + (long)((j - 1) % NS) * M.NG2 * TC);
+            // ---- phase-3 B fragments of the layer starting at plane j: B3f[L&1][((r2*NK2 + slot)*KS3 + kk)*MT + c][lane]
+            if (j < nplanes && j % G == 0) {
+                const int L = j / G, e2 = elo2 + L;
+                double* B3b = B3f + (L & 1) * B3SZ;
+                const double* bz0 = prm.B[2] + (long long)e2 * G * NB;
+                for (int it = warp; it < (P + 1) * NK2; it += NW) {
+                    const int r2 = it % (P + 1), slot = it / (P + 1);
+                    int kind = 0;
+                    static_for<0, NK2>([&](auto SI) { if (slot == decltype(SI)::value) kind = kind_of_slot2(TTS::T, decltype(SI)::value); });
+                    const int a2 = kind % 3, bb2 = kind / 3;
+                    for (int kk = 0; kk < KS3; ++kk) {
+                        const int s = kk * 4 + lk;
+                        for (int c = 0; c < MT; ++c) {
+                            const int d2 = c * 8 + lr - P;
+                            const int rj2 = r2 + d2;
+                            double v = 0.0;
+                            if (s < G && d2 <= P && rj2 >= 0 && rj2 <= P) {
+                                const double* bz = bz0 + s * NB;
+                                v = __dmul_rn(bz[a2 * (P + 1) + r2], bz[bb2 * (P + 1) + rj2]);
+                            }
+                            B3b[(((r2 * NK2 + slot) * KS3 + kk) * MT + c) * 32 + lane] = v;
+                        }
+                    }
+                }
             }
             __syncthreads();
-            ++pidx;
-        }  // q2
-        if constexpr (NDIM == 3) {
-            // ---------------- phase 3: items (row offset r2 in the layer, chunk of CH m-tiles)
-            constexpr int NFP = f_npairs(TTS::T);
-            constexpr int NA = imax(NFP, 1);
-            constexpr int CH = M.CH;
-            const int m01 = prm.m[0] * prm.m[1];
-            for (int item = warp; item < (P + 1) * M.NCH; item += NW) {
-                const int r2 = item % (P + 1), ch = item / (P + 1);
-                const int i2 = e2 + r2;
-                if (i2 < b2 || i2 >= b2 + prm.T2 || i2 >= prm.m[2]) continue;
-                // CSR position of every output of this item (lane: rows lr of CH m-tiles, columns 2*lk+h)
-                // and the previously accumulated layers' partial sums, loaded before the MMA chain
-                const int lo2 = max(0, i2 - P);
-                int64_t pos[CH][MT][2];
-                double old[CH][MT][2];
-#pragma unroll
-                for (int mm = 0; mm < CH; ++mm) {
-                    const int combo = (ch * CH + mm) * 8 + lr;
-                    const int off = combo < M.NCOMBO ? cmb[combo] : -1;
-                    const int i1l = (combo / (W * W)) % T1, i0l = combo / (W * W * T1);
-                    const int i0 = b0 + i0l, i1 = b1 + i1l;
-                    const int64_t row = (int64_t)i0 + (int64_t)prm.m[0] * i1 + (int64_t)m01 * i2;
-                    bool ok = off >= 0 && row >= prm.slab_lo && row < prm.slab_hi && (!prm.rowmask || prm.rowmask[row]);
-                    const int cnt01 = ok ? (min(prm.m[0] - 1, i0 + P) - max(0, i0 - P) + 1) * (min(prm.m[1] - 1, i1 + P) - max(0, i1 - P) + 1) : 0;
-                    const int64_t base = ok ? prm.rowstart[row] + off : 0;
-#pragma unroll
-                    for (int c = 0; c < MT; ++c)
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            const int d2 = c * 8 + 2 * lk + h - P;
-                            const int rj2 = r2 + d2;
-                            const bool v = ok && d2 <= P && rj2 >= 0 && rj2 <= P;
-                            pos[mm][c][h] = v ? base + (int64_t)cnt01 * (i2 + d2 - lo2) : -1;
-                            const int first = max(0, max(i2, i2 + d2) - P);
-                            old[mm][c][h] = (v && e2 != first) ? prm.data[pos[mm][c][h]] : 0.0;
-                        }
-                }
-                double accS[CH][MT][2];
-                double accA[NA][CH][MT][2];
-                double accB[NA][CH][MT][2];
-#pragma unroll
-                for (int mm = 0; mm < CH; ++mm)
-#pragma unroll
-                    for (int c = 0; c < MT; ++c)
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            accS[mm][c][h] = 0.0;
-#pragma unroll
-                            for (int kx = 0; kx < NA; ++kx) accA[kx][mm][c][h] = accB[kx][mm][c][h] = 0.0;
-                        }
-                auto block = [&](auto GA, auto& acc) {
-                    constexpr int ga = decltype(GA)::value;
-                    constexpr int kd = kslot2(TTS::T, kind2(TTS::T, ga));
-                    const double* bfp = B3f + ((r2 * NK2 + kd) * KS3) * MT * 32 + lane;
-#pragma unroll
-                    for (int kk = 0; kk < KS3; ++kk) {
-                        double bfs[MT];
-#pragma unroll
-                        for (int c = 0; c < MT; ++c) bfs[c] = bfp[(kk * MT + c) * 32];
-                        const int s = kk * 4 + lk;
-                        const double* t2 = T2s + (ga * G + (s < G ? s : 0)) * TC + ch * CH * 8 + lr;
-#pragma unroll
-                        for (int mm = 0; mm < CH; ++mm) {
-                            const double av = t2[mm * 8];
-#pragma unroll
-                            for (int c = 0; c < MT; ++c) dmma(acc[mm][c][0], acc[mm][c][1], av, bfs[c]);
-                        }
-                    }
-                };
-                static_for<0, TTS::T.NF>([&](auto FI) {
-                    constexpr int f = decltype(FI)::value;
-                    constexpr int ga = TTS::T.fu[f];
-                    if constexpr (TTS::T.fpair[f] == 0) {
-                        block(std::integral_constant<int, ga>{}, accS);
-                    } else {
-                        constexpr int pi = f_pairidx(TTS::T, f);
-                        block(std::integral_constant<int, ga>{}, accA[pi]);
-                        block(std::integral_constant<int, TTS::T.g2T[ga]>{}, accB[pi]);
-                    }
-                });
-#pragma unroll
-                for (int mm = 0; mm < CH; ++mm) {
-                    const int combo = (ch * CH + mm) * 8 + lr;
-                    const int i1l = (combo / (W * W)) % T1, i0l = combo / (W * W * T1);
-                    const int i0 = b0 + i0l, i1 = b1 + i1l;
-                    const int d0 = combo % W - P, d1 = (combo / W) % W - P;
-                    const int64_t row = (int64_t)i0 + (int64_t)prm.m[0] * i1 + (int64_t)m01 * i2;
-                    const int64_t colb = (int64_t)(i0 + d0) + (int64_t)prm.m[0] * (i1 + d1);
-#pragma unroll
-                    for (int c = 0; c < MT; ++c)
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            const int64_t p = pos[mm][c][h];
-                            if (p < 0) continue;
-                            const int j2 = i2 + c * 8 + 2 * lk + h - P;
-                            double v = accS[mm][c][h];
-#pragma unroll
-                            for (int kx = 0; kx < NFP; ++kx) v = __dadd_rn(v, __dadd_rn(accA[kx][mm][c][h], accB[kx][mm][c][h]));
-                            const int first = max(0, max(i2, j2) - P);
-                            const int last = min(min(i2, j2), prm.S[2] - 1);
-                            if (e2 != first) v = old[mm][c][h] + v;
-                            const int64_t col = colb + (int64_t)m01 * j2;
-                            if (e2 == last) {
-                                if constexpr (RAT) v = v * (prm.sol_w[row] * prm.sol_w[col]);
-                                if (prm.zeros && v == 0.0) atomicAdd(prm.zeros, 1ull);
-                            }
-                            if (e2 == first) prm.indices[p] = (int)col;
-                            prm.data[p] = v;
-                        }
-                }
-            }
         }
     }
 }
