@@ -387,7 +387,8 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), 1) assembl
     double* B3f = smem + M.o_B3f;
     int* cmb = reinterpret_cast<int*>(smem + M.o_cmb);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + M.o_bar);
-    double* Dbuf[2] = {smem + M.o_D, smem + M.o_D2};
+    // D window buffer of plane parity b (computed from smem so every access stays an LDS)
+    auto Dbuf = [&](int b) -> double* { return smem + (b ? M.o_D2 : M.o_D); };
     double* T1s = smem + M.o_T1;
     double* T2s = smem + M.o_T2;
 
@@ -508,7 +509,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), 1) assembl
     auto issue_plane = [&](int pi) {
         const int z = elo2 * G + pi;
         const uint32_t bar = bar0 + 8u * (uint32_t)(pi & 1);
-        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(Dbuf[pi & 1]);
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(Dbuf(pi & 1));
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(DBYTES) : "memory");
         asm volatile(
@@ -531,7 +532,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), 1) assembl
     }
     // make the D window of plane j resident in Dbuf[j & 1] (plain path: all threads load, then a barrier)
     auto get_plane = [&](int j) {
-        double* Ds = Dbuf[j & 1];
+        double* Ds = Dbuf(j & 1);
         if (use_tma) {
             if (tid == 0 && j + 1 < nplanes) issue_plane(j + 1);  // prefetch the next plane
             const uint32_t bar = bar0 + 8u * (uint32_t)(j & 1);
