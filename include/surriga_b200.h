@@ -99,6 +99,9 @@ int sg_result_sizes(const sg_result* r, int64_t* nrows, int64_t* nnz);
 /* Copy CSR to host: indptr int32[nrows+1] (or int64 if *_i64 variant), indices int32[nnz], data f64[nnz]. */
 int sg_result_copy(const sg_result* r, int32_t* indptr, int32_t* indices, double* data);
 int sg_result_copy_i64(const sg_result* r, int64_t* indptr, int32_t* indices, double* data);
+/* Optional: allocate the calling thread's pinned D2H staging ring and host copy pool for `device` up
+   front (otherwise done by the first large sg_result_copy*; not part of the reference interface). */
+int sg_host_staging_init(int device);
 /* Device pointers (for device-resident consumers and timing). */
 int sg_result_device_ptrs(const sg_result* r, void** indptr_i64, void** indices_i32, void** data_f64);
 /* Deterministic fp64 checksums {nnz, sum a, sum a^2, sum |a|, sum of row sums} of the rows in the result. */

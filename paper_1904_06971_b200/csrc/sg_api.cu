@@ -3,7 +3,13 @@
 // result handles, transfers and checksums.
 #include <cub/cub.cuh>
 
+#include <sys/mman.h>
+
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <deque>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -851,30 +857,103 @@ int sg_result_sizes(const sg_result* r, int64_t* nrows, int64_t* nnz) {
 }  // extern "C"
 
 namespace sg {
-// Device -> host copy of large result arrays: pinned staging ring (2 x 64 MB per thread), D2H of
-// chunk k overlapped with a multi-threaded memcpy of chunk k-1 into the caller's (pageable) buffer.
+// Device -> host copy of large result arrays.  PCIe D2H runs at ~57 GB/s into pinned memory, but
+// pinning the caller's buffer costs more than it saves (2-8 GB/s), so the copy goes through a
+// pinned staging ring (R x 64 MB): the DMA engine fills slot k+1.. while a persistent pool of host
+// threads copies slot k into the caller's pageable buffer (first-touch page faults spread over the
+// pool, transparent huge pages requested on the destination).
+struct CopyPool {
+    std::vector<std::thread> th;
+    std::mutex mu;
+    std::condition_variable cv, done_cv;
+    struct Task { char* dst; const char* src; size_t len; std::atomic<int>* left; };
+    std::deque<Task> q;
+    bool stop = false;
+    explicit CopyPool(int n) {
+        for (int t = 0; t < n; ++t)
+            th.emplace_back([this] {
+                for (;;) {
+                    Task tk;
+                    {
+                        std::unique_lock<std::mutex> lk(mu);
+                        cv.wait(lk, [this] { return stop || !q.empty(); });
+                        if (stop && q.empty()) return;
+                        tk = q.front();
+                        q.pop_front();
+                    }
+                    memcpy(tk.dst, tk.src, tk.len);
+                    if (tk.left->fetch_sub(1) == 1) {
+                        std::lock_guard<std::mutex> lk(mu);
+                        done_cv.notify_all();
+                    }
+                }
+            });
+    }
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            stop = true;
+        }
+        cv.notify_all();
+        for (auto& t : th) t.join();
+    }
+    void submit(char* dst, const char* src, size_t n, std::atomic<int>* left, size_t piece) {
+        const int np = (int)((n + piece - 1) / piece);
+        left->store(np);
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            for (int p = 0; p < np; ++p) {
+                const size_t lo = (size_t)p * piece, len = std::min(piece, n - lo);
+                q.push_back({dst + lo, src + lo, len, left});
+            }
+        }
+        cv.notify_all();
+    }
+    void wait(std::atomic<int>* left) {
+        std::unique_lock<std::mutex> lk(mu);
+        done_cv.wait(lk, [&] { return left->load() == 0; });
+    }
+};
+static CopyPool& copy_pool() {
+    static CopyPool pool((int)std::max(2u, std::min(16u, std::thread::hardware_concurrency())));
+    return pool;
+}
+
+constexpr int kRing = 4;
 struct Stager {
     int dev = -1;
     cudaStream_t st = nullptr;
-    char* buf[2] = {nullptr, nullptr};
-    cudaEvent_t ev[2];
-    size_t cap = 0;
+    char* buf[kRing] = {};
+    cudaEvent_t ev[kRing];
+    std::atomic<int> left[kRing];
 };
 static thread_local Stager g_stage;
 
-static void par_memcpy(char* dst, const char* src, size_t n) {
-    const int nt = (int)std::min<size_t>(16, std::max<size_t>(1, n >> 22));  // >= 4 MB per thread
-    if (nt <= 1) {
-        memcpy(dst, src, n);
-        return;
+static void want_huge_pages(void* p, size_t n) {
+    const uintptr_t a = ((uintptr_t)p + (2u << 20) - 1) & ~(uintptr_t)((2u << 20) - 1);
+    const uintptr_t e = ((uintptr_t)p + n) & ~(uintptr_t)((2u << 20) - 1);
+    if (e > a) madvise((void*)a, e - a, MADV_HUGEPAGE);
+}
+
+constexpr size_t kChunk = 64u << 20;
+static int stager_init(int dev) {
+    Stager& S = g_stage;
+    if (S.dev != dev || !S.buf[0]) {
+        for (int k = 0; k < kRing; ++k)
+            if (S.buf[k]) cudaFreeHost(S.buf[k]);
+        for (int k = 0; k < kRing; ++k)
+            if (cudaHostAlloc((void**)&S.buf[k], kChunk, cudaHostAllocDefault) != cudaSuccess) {
+                S.buf[0] = nullptr;
+                return fail(-4, "pinned staging allocation failed");
+            }
+        if (!S.st) {
+            cudaStreamCreateWithFlags(&S.st, cudaStreamNonBlocking);
+            for (int k = 0; k < kRing; ++k) cudaEventCreateWithFlags(&S.ev[k], cudaEventDisableTiming);
+        }
+        S.dev = dev;
     }
-    std::vector<std::thread> th;
-    const size_t per = (n + nt - 1) / nt;
-    for (int t = 0; t < nt; ++t) {
-        const size_t lo = t * per, hi = std::min(n, lo + per);
-        if (lo < hi) th.emplace_back([=] { memcpy(dst + lo, src + lo, hi - lo); });
-    }
-    for (auto& x : th) x.join();
+    copy_pool();
+    return 0;
 }
 
 static int d2h(void* dst, const void* src, size_t bytes, int dev) {
@@ -883,42 +962,40 @@ static int d2h(void* dst, const void* src, size_t bytes, int dev) {
         if (cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) return fail(-3, "D2H copy failed");
         return 0;
     }
+    if (int rc = stager_init(dev)) return rc;
     Stager& S = g_stage;
-    const size_t chunk = 64u << 20;
-    if (S.dev != dev || !S.buf[0]) {
-        if (S.buf[0]) {
-            cudaFreeHost(S.buf[0]);
-            cudaFreeHost(S.buf[1]);
-        }
-        if (cudaHostAlloc((void**)&S.buf[0], chunk, cudaHostAllocDefault) != cudaSuccess ||
-            cudaHostAlloc((void**)&S.buf[1], chunk, cudaHostAllocDefault) != cudaSuccess)
-            return fail(-4, "pinned staging allocation failed");
-        if (!S.st) {
-            cudaStreamCreateWithFlags(&S.st, cudaStreamNonBlocking);
-            cudaEventCreateWithFlags(&S.ev[0], cudaEventDisableTiming);
-            cudaEventCreateWithFlags(&S.ev[1], cudaEventDisableTiming);
-        }
-        S.dev = dev;
-        S.cap = chunk;
-    }
+    const size_t chunk = kChunk, piece = 4u << 20;
+    want_huge_pages(dst, bytes);
+    CopyPool& pool = copy_pool();
     const size_t nch = (bytes + chunk - 1) / chunk;
-    for (size_t k = 0; k <= nch; ++k) {
-        if (k < nch) {
-            const size_t off = k * chunk, len = std::min(chunk, bytes - off);
-            cudaMemcpyAsync(S.buf[k & 1], (const char*)src + off, len, cudaMemcpyDeviceToHost, S.st);
-            cudaEventRecord(S.ev[k & 1], S.st);
-        }
-        if (k > 0) {
-            const size_t pk = k - 1, off = pk * chunk, len = std::min(chunk, bytes - off);
-            if (cudaEventSynchronize(S.ev[pk & 1]) != cudaSuccess) return fail(-3, "D2H copy failed");
-            par_memcpy((char*)dst + off, S.buf[pk & 1], len);
+    auto issue = [&](size_t k) {
+        const size_t off = k * chunk, len = std::min(chunk, bytes - off);
+        cudaMemcpyAsync(S.buf[k % kRing], (const char*)src + off, len, cudaMemcpyDeviceToHost, S.st);
+        cudaEventRecord(S.ev[k % kRing], S.st);
+    };
+    for (size_t k = 0; k < std::min<size_t>(nch, kRing); ++k) issue(k);
+    for (size_t k = 0; k < nch; ++k) {
+        const int s = (int)(k % kRing);
+        if (cudaEventSynchronize(S.ev[s]) != cudaSuccess) return fail(-3, "D2H copy failed");
+        const size_t off = k * chunk, len = std::min(chunk, bytes - off);
+        pool.submit((char*)dst + off, S.buf[s], len, &S.left[s], piece);
+        if (k >= 1) {  // slot of chunk k-1 is free once its host copy finished: refill it
+            const int ps = (int)((k - 1) % kRing);
+            pool.wait(&S.left[ps]);
+            if (k - 1 + kRing < nch) issue(k - 1 + kRing);
         }
     }
+    pool.wait(&S.left[(nch - 1) % kRing]);
     return 0;
 }
 }  // namespace sg
 
 extern "C" {
+
+int sg_host_staging_init(int device) {
+    cudaSetDevice(device);
+    return sg::stager_init(device);
+}
 
 int sg_result_copy_i64(const sg_result* r, int64_t* indptr, int32_t* indices, double* data) {
     if (!r) return fail(-1, "null result");
