@@ -97,8 +97,12 @@ __global__ void const_table_kernel(int n, int* sp, double* tab) {
 // the kernel-preserving diagonal (:673-680).  No row staging: the CTA's rows stay L2 resident
 // while their sectors fill.
 // ---------------------------------------------------------------------------------------------
-template <int NDIM, int QC>
-__global__ void __launch_bounds__(512, 2) interp_tiles_kernel(SurrParams s) {
+// STAGE (fixed-degree path, V fits in smem): phase A evaluates every offset of the tile into smem
+// V[o][row]; phase B writes each row's P entries with lanes on consecutive offsets (coalesced
+// 256 B data / 128 B index stores instead of one 8 B store per row per offset), reducing the row
+// sums with a fixed shuffle tree.
+template <int NDIM, int QC, bool STAGE>
+__global__ void __launch_bounds__(512, STAGE ? 1 : 2) interp_tiles_kernel(SurrParams s) {
     // QC > 0: degree QC in every direction and tile 4x4x4 / 8x8 / 64, coefficient window QC+2
     constexpr bool FIX = QC > 0;
     constexpr int FTB0 = NDIM == 1 ? 64 : (NDIM == 2 ? 8 : 4), FTB1 = NDIM == 2 ? 8 : (NDIM == 3 ? 4 : 1), FTB2 = NDIM == 3 ? 4 : 1;
@@ -131,6 +135,11 @@ __global__ void __launch_bounds__(512, 2) interp_tiles_kernel(SurrParams s) {
     uint8_t* mk0 = reinterpret_cast<uint8_t*>(sp2 + L2);  // bit0 in box, bit1 sampled (index range blo+base..)
     uint8_t* mk1 = mk0 + L0;
     uint8_t* mk2 = mk1 + L1;
+    constexpr int NRP = NR + 1;  // odd row stride of V: lanes on consecutive offsets hit distinct banks
+    double* Vs = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(mk2 + L2) + 15) & ~(uintptr_t)15);
+    int* shs = reinterpret_cast<int*>(Vs + (STAGE ? (size_t)P * NRP : 0));
+    if constexpr (STAGE)
+        for (int it = threadIdx.x; it < P * 3; it += blockDim.x) shs[it] = s.shifts[it];
     for (int it = threadIdx.x; it < L0 + L1 + L2; it += blockDim.x) {
         int d = 0, li = it;
         if (li >= L0) { li -= L0; d = 1; if (li >= L1) { li -= L1; d = 2; } }
@@ -254,6 +263,11 @@ __global__ void __launch_bounds__(512, 2) interp_tiles_kernel(SurrParams s) {
             }
             __syncwarp();
         }
+        if constexpr (STAGE) {
+            Vs[o * NRP + lane] = V[0];
+            Vs[o * NRP + lane + 32] = V[1];
+            continue;
+        }
         // placement of offset o for the lane's rows
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
@@ -272,6 +286,62 @@ __global__ void __launch_bounds__(512, 2) interp_tiles_kernel(SurrParams s) {
             if (v == 0.0) pzero[k]++;
             if (o == s.center) dgv[lane + 32 * k] = v;
         }
+    }
+    if constexpr (STAGE) {
+        __syncthreads();
+        unsigned long long n_int = 0, n_zero = 0, n_reset = 0, n_rows = 0;
+        for (int r = warp; r < NR; r += nw) {
+            const int b0 = r % TB0, b1 = (r / TB0) % TB1, b2 = r / (TB0 * TB1);
+            bool ok = org0 + b0 < s.bn[0] && (NDIM < 2 || org1 + b1 < s.bn[1]) && (NDIM < 3 || org2 + b2 < s.bn[2]);
+            const int i0 = s.blo[0] + org0 + b0, i1 = NDIM >= 2 ? s.blo[1] + org1 + b1 : 0, i2 = NDIM >= 3 ? s.blo[2] + org2 + b2 : 0;
+            ok = ok && row_interp(s, i0, i1, i2);
+            const int64_t row = (int64_t)i0 + (int64_t)s.m[0] * ((int64_t)i1 + (int64_t)s.m[1] * i2);
+            ok = ok && row >= s.slab_lo && row < s.slab_hi;
+            if (!ok) continue;
+            const int64_t rbs = s.rowstart[row];
+            double sum = 0.0, dg = 0.0;
+            int off = 0, in = 0, ze = 0;
+            for (int o = lane; o < P; o += 32) {
+                const int j0 = i0 + shs[o * 3 + 0], j1 = i1 + shs[o * 3 + 1], j2 = i2 + shs[o * 3 + 2];
+                const int64_t col = (int64_t)j0 + (int64_t)s.m[0] * ((int64_t)j1 + (int64_t)s.m[1] * j2);
+                const bool jint = jint_of(j0, j1, j2);
+                const double v = jint ? Vs[o * NRP + r] : s.data[s.rowstart[col] + (P - 1 - o)];  // transposed quadrature entry A[j, i]
+                s.data[rbs + o] = v;
+                s.indices[rbs + o] = (int)col;
+                sum += v;
+                if (jint) {
+                    in++;
+                    if (o != s.center) off++;
+                }
+                if (v == 0.0) ze++;
+                if (o == s.center) dg = v;
+            }
+#pragma unroll
+            for (int w = 16; w > 0; w >>= 1) {
+                sum += __shfl_xor_sync(0xffffffffu, sum, w);
+                off += __shfl_xor_sync(0xffffffffu, off, w);
+                in += __shfl_xor_sync(0xffffffffu, in, w);
+                ze += __shfl_xor_sync(0xffffffffu, ze, w);
+            }
+            dg = __shfl_sync(0xffffffffu, dg, s.center & 31);
+            if (lane == 0) {
+                n_int += in;
+                n_zero += ze;
+                n_rows++;
+                if (s.mode == SG_SYMMETRIC_KERNEL_PRESERVING && off > 0) {
+                    s.newdiag[row] = dg - sum;
+                    s.reset[row] = 1;
+                    n_reset++;
+                }
+            }
+        }
+        if (lane == 0) {
+            if (n_int) atomicAdd(&s.counters[0], n_int);
+            if (n_zero) atomicAdd(&s.counters[1], n_zero);
+            if (n_reset) atomicAdd(&s.counters[2], n_reset);
+            if (n_rows) atomicAdd(&s.counters[3], n_rows);
+        }
+        return;
     }
     // per-row reduction over warps (fixed order)
 #pragma unroll
@@ -595,13 +665,19 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
     bool fixq = s.qd[0] == 3 && (n < 2 || s.qd[1] == 3) && (n < 3 || s.qd[2] == 3);
     for (int d = 0; d < n; ++d) fixq = fixq && s.cmax[d] <= 5;
     void* kfn;
+    const int NR = 64;
+    const size_t vbytes = sizeof(double) * (size_t)P * (NR + 1) + sizeof(int) * (size_t)P * 3 + 16;
+    bool stage = false;
     if (fixq) {
         for (int d = 0; d < n; ++d) s.cmax[d] = 5;
-        kfn = n == 1 ? (void*)interp_tiles_kernel<1, 3> : (n == 2 ? (void*)interp_tiles_kernel<2, 3> : (void*)interp_tiles_kernel<3, 3>);
+        stage = vbytes <= 170 * 1024 && !getenv("SG_NO_STAGE");
+        if (stage)
+            kfn = n == 1 ? (void*)interp_tiles_kernel<1, 3, true> : (n == 2 ? (void*)interp_tiles_kernel<2, 3, true> : (void*)interp_tiles_kernel<3, 3, true>);
+        else
+            kfn = n == 1 ? (void*)interp_tiles_kernel<1, 3, false> : (n == 2 ? (void*)interp_tiles_kernel<2, 3, false> : (void*)interp_tiles_kernel<3, 3, false>);
     } else {
-        kfn = n == 1 ? (void*)interp_tiles_kernel<1, 0> : (n == 2 ? (void*)interp_tiles_kernel<2, 0> : (void*)interp_tiles_kernel<3, 0>);
+        kfn = n == 1 ? (void*)interp_tiles_kernel<1, 0, false> : (n == 2 ? (void*)interp_tiles_kernel<2, 0, false> : (void*)interp_tiles_kernel<3, 0, false>);
     }
-    const int NR = 64;
     const int nw = nthreads / 32;
     const int scr = s.cmax[2] * s.cmax[1] * s.TB[0] + s.cmax[2] * s.TB[1] * s.TB[0] + 8;
     size_t tabs = 0;
@@ -609,7 +685,8 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
         const int L = (d < n ? s.TB[d] + 2 * p : 1);
         tabs += (size_t)L * (s.qd[d] + 1) * sizeof(double) + (size_t)L * sizeof(int) + L;
     }
-    const size_t smem = sizeof(double) * ((size_t)nw * scr + (size_t)nw * NR + NR) + sizeof(int) * ((size_t)nw * NR * 3 + 2) + tabs + 64;
+    const size_t smem = sizeof(double) * ((size_t)nw * scr + (size_t)nw * NR + NR) + sizeof(int) * ((size_t)nw * NR * 3 + 2) + tabs + 64 +
+                        (stage ? vbytes : 0);
     if (smem > 227 * 1024) return fail(-2, "surrogate tile does not fit shared memory (%zu B)", smem);
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     void* args[] = {&s};

@@ -21,6 +21,8 @@
 #pragma once
 #include <cuda.h>
 
+#include <climits>
+
 #include "sg_common.cuh"
 
 namespace sg {
@@ -182,7 +184,7 @@ __host__ __device__ constexpr MmaGeom mma_geom(int ndim, int P, int form, bool r
         m.NTAB = 3 * (NW + 1) + m.NG1 * T0 + (ndim >= 2 ? T.NG2 * m.T1 * T0 : 0) + (ndim == 3 ? (P + 1) * m.NCH : 0) +
                  (m.NG1 + 1) + m.NU1 + (T.NG2 + 1) + nu2 + T.NF;
     }
-    m.o_rb = o; o += ndim == 3 ? (long)T0 * m.T1 * kMmaT2 : 0;                // CSR start of every tile row (int64, -1: not owned)
+    m.o_rb = o; o += ndim == 3 ? (long)T0 * m.T1 * kMmaT2 + 1 : 0;                // CSR start of every tile row (int64, -1: not owned)
     m.o_tab = o; o += (m.NTAB + 1) / 2;                                        // item schedule + unit tables (int)
     m.o_bar = o; o += 2;                                                       // two mbarriers (TMA)
     o = align16(o);
@@ -399,6 +401,11 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), 1) assembl
             constexpr int v = MmaTabS<NDIM, P, FORM, RAT>::S.v[decltype(I)::value];
             tabw[decltype(I)::value] = v;
         });
+        if constexpr (NDIM == 3) {
+            int* zr = reinterpret_cast<int*>(smem + M.o_rb + T0 * T1 * kMmaT2);
+            zr[0] = INT_MAX;
+            zr[1] = -1;
+        }
     }
     // ---- zero the staging buffers once (padding columns / rows are read as exact zeros)
     for (long it = tid; it < M.total - M.o_T1; it += blockDim.x) T1s[it] = 0.0;
@@ -488,6 +495,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), 1) assembl
             cmb[4 * c + 3] = j0 + prm.m[0] * j1;
         }
         int64_t* rb = reinterpret_cast<int64_t*>(smem + M.o_rb);
+        int zlo = INT_MAX, zhi = -1;
         for (int t = tid; t < T0 * T1 * kMmaT2; t += blockDim.x) {
             const int i2 = b2 + t % kMmaT2, i1 = b1 + (t / kMmaT2) % T1, i0 = b0 + t / (kMmaT2 * T1);
             int64_t v = -1;
@@ -496,12 +504,31 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), 1) assembl
                 if (row >= prm.slab_lo && row < prm.slab_hi && (!prm.rowmask || prm.rowmask[row])) v = prm.rowstart[row];
             }
             rb[t] = v;
+            if (v >= 0) {
+                zlo = min(zlo, b2 + t % kMmaT2);
+                zhi = max(zhi, b2 + t % kMmaT2);
+            }
         }
+        // z range of the rows this tile actually owns (restricted plans: only the needed layers)
+        int* zr = reinterpret_cast<int*>(rb + T0 * T1 * kMmaT2);
+        if (zlo <= zhi) {
+            atomicMin(&zr[0], zlo);
+            atomicMax(&zr[1], zhi);
+        }
+    }
+    if constexpr (NDIM == 3) {
+        __syncthreads();
+        const int* zr = reinterpret_cast<const int*>(smem + M.o_rb + T0 * T1 * kMmaT2);
+        if (zr[1] < zr[0]) return;  // no owned row in this tile
     }
 
     const long long G0 = prm.Gp[0];
-    const int elo2 = NDIM == 3 ? max(0, b2 - P) : 0;
-    const int ehi2 = NDIM == 3 ? min(prm.S[2] - 1, b2 + prm.T2 - 1) : 0;
+    int elo2 = 0, ehi2 = 0;
+    if constexpr (NDIM == 3) {
+        const int* zrng = reinterpret_cast<const int*>(smem + M.o_rb + T0 * T1 * kMmaT2);
+        elo2 = max(0, zrng[0] - P);
+        ehi2 = min(prm.S[2] - 1, zrng[1]);
+    }
     constexpr int GZ = NDIM == 3 ? G : 1;
     const int nplanes = (ehi2 - elo2 + 1) * GZ;
     const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&bars[0]);
