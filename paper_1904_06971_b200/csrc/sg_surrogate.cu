@@ -97,21 +97,14 @@ __global__ void const_table_kernel(int n, int* sp, double* tab) {
 // the kernel-preserving diagonal (:673-680).  No row staging: the CTA's rows stay L2 resident
 // while their sectors fill.
 // ---------------------------------------------------------------------------------------------
-// STAGE (fixed-degree path, V fits in smem): phase A evaluates every offset of the tile into smem
-// V[o][row]; phase B writes each row's P entries with lanes on consecutive offsets (coalesced
-// 256 B data / 128 B index stores instead of one 8 B store per row per offset), reducing the row
-// sums with a fixed shuffle tree.
-template <int NDIM, int QC, bool STAGE>
-__global__ void __launch_bounds__(512, STAGE ? 1 : 2) interp_tiles_kernel(SurrParams s) {
-    // QC > 0: degree QC in every direction and tile 4x4x4 / 8x8 / 64, coefficient window QC+2
-    constexpr bool FIX = QC > 0;
-    constexpr int FTB0 = NDIM == 1 ? 64 : (NDIM == 2 ? 8 : 4), FTB1 = NDIM == 2 ? 8 : (NDIM == 3 ? 4 : 1), FTB2 = NDIM == 3 ? 4 : 1;
+template <int NDIM>
+__global__ void __launch_bounds__(512, 2) interp_tiles_kernel(SurrParams s) {
     extern __shared__ double sm[];
     constexpr int NR = 64;
     const int P = s.P;
-    const int TB0 = FIX ? FTB0 : s.TB[0], TB1 = FIX ? FTB1 : (NDIM >= 2 ? s.TB[1] : 1), TB2 = FIX ? FTB2 : (NDIM >= 3 ? s.TB[2] : 1);
+    const int TB0 = s.TB[0], TB1 = NDIM >= 2 ? s.TB[1] : 1, TB2 = NDIM >= 3 ? s.TB[2] : 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    const int c1 = FIX ? (NDIM >= 2 ? QC + 2 : 1) : s.cmax[1], c2 = FIX ? (NDIM >= 3 ? QC + 2 : 1) : s.cmax[2];
+    const int c1 = s.cmax[1], c2 = s.cmax[2];
     const int scr = c2 * c1 * TB0 + c2 * TB1 * TB0 + 8;
     double* A = sm + (size_t)warp * scr;
     double* Bm = A + c2 * c1 * TB0;
@@ -121,7 +114,7 @@ __global__ void __launch_bounds__(512, STAGE ? 1 : 2) interp_tiles_kernel(SurrPa
     const int t = blockIdx.x;
     const int tc0 = t % s.tg[0], tc1 = (t / s.tg[0]) % s.tg[1], tc2 = t / (s.tg[0] * s.tg[1]);
     const int org0 = tc0 * TB0, org1 = tc1 * TB1, org2 = tc2 * TB2;
-    const int q0 = FIX ? QC : s.qd[0], q1 = FIX ? (NDIM >= 2 ? QC : 0) : s.qd[1], q2 = FIX ? (NDIM >= 3 ? QC : 0) : s.qd[2];
+    const int q0 = s.qd[0], q1 = s.qd[1], q2 = s.qd[2];
     // stage the evaluation tables and row-class masks of this tile's +-p neighbourhood in smem
     const int p = s.p;
     const int L0 = TB0 + 2 * p, L1 = NDIM >= 2 ? TB1 + 2 * p : 1, L2 = NDIM >= 3 ? TB2 + 2 * p : 1;
@@ -135,11 +128,6 @@ __global__ void __launch_bounds__(512, STAGE ? 1 : 2) interp_tiles_kernel(SurrPa
     uint8_t* mk0 = reinterpret_cast<uint8_t*>(sp2 + L2);  // bit0 in box, bit1 sampled (index range blo+base..)
     uint8_t* mk1 = mk0 + L0;
     uint8_t* mk2 = mk1 + L1;
-    constexpr int NRP = NR + 1;  // odd row stride of V: lanes on consecutive offsets hit distinct banks
-    double* Vs = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(mk2 + L2) + 15) & ~(uintptr_t)15);
-    int* shs = reinterpret_cast<int*>(Vs + (STAGE ? (size_t)P * NRP : 0));
-    if constexpr (STAGE)
-        for (int it = threadIdx.x; it < P * 3; it += blockDim.x) shs[it] = s.shifts[it];
     for (int it = threadIdx.x; it < L0 + L1 + L2; it += blockDim.x) {
         int d = 0, li = it;
         if (li >= L0) { li -= L0; d = 1; if (li >= L1) { li -= L1; d = 2; } }
@@ -263,11 +251,6 @@ __global__ void __launch_bounds__(512, STAGE ? 1 : 2) interp_tiles_kernel(SurrPa
             }
             __syncwarp();
         }
-        if constexpr (STAGE) {
-            Vs[o * NRP + lane] = V[0];
-            Vs[o * NRP + lane + 32] = V[1];
-            continue;
-        }
         // placement of offset o for the lane's rows
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
@@ -286,62 +269,6 @@ __global__ void __launch_bounds__(512, STAGE ? 1 : 2) interp_tiles_kernel(SurrPa
             if (v == 0.0) pzero[k]++;
             if (o == s.center) dgv[lane + 32 * k] = v;
         }
-    }
-    if constexpr (STAGE) {
-        __syncthreads();
-        unsigned long long n_int = 0, n_zero = 0, n_reset = 0, n_rows = 0;
-        for (int r = warp; r < NR; r += nw) {
-            const int b0 = r % TB0, b1 = (r / TB0) % TB1, b2 = r / (TB0 * TB1);
-            bool ok = org0 + b0 < s.bn[0] && (NDIM < 2 || org1 + b1 < s.bn[1]) && (NDIM < 3 || org2 + b2 < s.bn[2]);
-            const int i0 = s.blo[0] + org0 + b0, i1 = NDIM >= 2 ? s.blo[1] + org1 + b1 : 0, i2 = NDIM >= 3 ? s.blo[2] + org2 + b2 : 0;
-            ok = ok && row_interp(s, i0, i1, i2);
-            const int64_t row = (int64_t)i0 + (int64_t)s.m[0] * ((int64_t)i1 + (int64_t)s.m[1] * i2);
-            ok = ok && row >= s.slab_lo && row < s.slab_hi;
-            if (!ok) continue;
-            const int64_t rbs = s.rowstart[row];
-            double sum = 0.0, dg = 0.0;
-            int off = 0, in = 0, ze = 0;
-            for (int o = lane; o < P; o += 32) {
-                const int j0 = i0 + shs[o * 3 + 0], j1 = i1 + shs[o * 3 + 1], j2 = i2 + shs[o * 3 + 2];
-                const int64_t col = (int64_t)j0 + (int64_t)s.m[0] * ((int64_t)j1 + (int64_t)s.m[1] * j2);
-                const bool jint = jint_of(j0, j1, j2);
-                const double v = jint ? Vs[o * NRP + r] : s.data[s.rowstart[col] + (P - 1 - o)];  // transposed quadrature entry A[j, i]
-                s.data[rbs + o] = v;
-                s.indices[rbs + o] = (int)col;
-                sum += v;
-                if (jint) {
-                    in++;
-                    if (o != s.center) off++;
-                }
-                if (v == 0.0) ze++;
-                if (o == s.center) dg = v;
-            }
-#pragma unroll
-            for (int w = 16; w > 0; w >>= 1) {
-                sum += __shfl_xor_sync(0xffffffffu, sum, w);
-                off += __shfl_xor_sync(0xffffffffu, off, w);
-                in += __shfl_xor_sync(0xffffffffu, in, w);
-                ze += __shfl_xor_sync(0xffffffffu, ze, w);
-            }
-            dg = __shfl_sync(0xffffffffu, dg, s.center & 31);
-            if (lane == 0) {
-                n_int += in;
-                n_zero += ze;
-                n_rows++;
-                if (s.mode == SG_SYMMETRIC_KERNEL_PRESERVING && off > 0) {
-                    s.newdiag[row] = dg - sum;
-                    s.reset[row] = 1;
-                    n_reset++;
-                }
-            }
-        }
-        if (lane == 0) {
-            if (n_int) atomicAdd(&s.counters[0], n_int);
-            if (n_zero) atomicAdd(&s.counters[1], n_zero);
-            if (n_reset) atomicAdd(&s.counters[2], n_reset);
-            if (n_rows) atomicAdd(&s.counters[3], n_rows);
-        }
-        return;
     }
     // per-row reduction over warps (fixed order)
 #pragma unroll
@@ -399,6 +326,325 @@ __global__ void __launch_bounds__(512, STAGE ? 1 : 2) interp_tiles_kernel(SurrPa
             if (n_rows) atomicAdd(&s.counters[3], n_rows);
         }
     }
+}
+
+// ---------------------------------------------------------------------------------------------
+// K7 fixed-degree path (interpolation degree 3 in every direction, tile 4x4x4 / 8x8 = 64 rows,
+// coefficient window 5 per direction).  Same arithmetic as interp_tiles_kernel (same FMA chains,
+// bit-identical values) with the per-tile work hoisted out of the offset loop:
+//   * per direction and shift sh in [-p, p]: the tap weights, window-relative tap start and window
+//     origin of every tile point (the mirrored offsets of the symmetric modes evaluate at shifted
+//     points, surrogate.py:633-651);
+//   * per offset: the 5^n coefficient window is loaded once (independent loads), then the x, y, z
+//     passes run with compile-time trip counts and no bounds checks.
+// ---------------------------------------------------------------------------------------------
+template <int NDIM>
+__global__ void __launch_bounds__(512, 2) interp_fix_kernel(SurrParams s) {
+    static_assert(NDIM == 2 || NDIM == 3, "fixed path: 2D / 3D");
+    constexpr int Q = 3, CW = Q + 2, NR = 64, MAXSH = 9;  // p <= 4
+    constexpr int TB0 = NDIM == 2 ? 8 : 4, TB1 = NDIM == 2 ? 8 : 4, TB2 = NDIM == 3 ? 4 : 1;
+    constexpr int C2 = NDIM == 3 ? CW : 1;
+    constexpr int NWIN = C2 * CW * CW, NA = C2 * CW * TB0, NB = NDIM == 3 ? C2 * TB1 * TB0 : 0;
+    constexpr int SCR = 128 + NA + NB;
+    extern __shared__ double sm[];
+    const int P = s.P, p = s.p, NSH = 2 * p + 1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    double* Wn = sm + (size_t)warp * SCR;
+    double* A = Wn + 128;
+    double* Bm = A + NA;
+    double* red = sm + (size_t)nw * SCR;                 // [nw][NR] partial row sums
+    double* dgv = red + (size_t)nw * NR;                 // [NR] pre-reset diagonal value
+    double* TW = dgv + NR;                               // [d][sh][b][Q+1] tap weights
+    int* TR = reinterpret_cast<int*>(TW + 3 * MAXSH * 8 * (Q + 1));  // [d][sh][b] window-relative tap start
+    int* TL = TR + 3 * MAXSH * 8;                        // [d][sh] window origin (coefficient index)
+    int* rcnt = TL + 3 * MAXSH;                          // [nw][NR][3]: off-diag interp, interp, zeros
+    uint8_t* mk0 = reinterpret_cast<uint8_t*>(rcnt + nw * NR * 3);
+    const int L0 = TB0 + 2 * p, L1 = TB1 + 2 * p, L2 = NDIM == 3 ? TB2 + 2 * p : 1;
+    uint8_t* mk1 = mk0 + L0;
+    uint8_t* mk2 = mk1 + L1;
+    const int t = blockIdx.x;
+    const int tc0 = t % s.tg[0], tc1 = (t / s.tg[0]) % s.tg[1], tc2 = t / (s.tg[0] * s.tg[1]);
+    const int org[3] = {tc0 * TB0, tc1 * TB1, NDIM == 3 ? tc2 * TB2 : 0};
+    const int TBd[3] = {TB0, TB1, TB2};
+    const int base0 = org[0] - p, base1 = org[1] - p, base2 = NDIM == 3 ? org[2] - p : 0;
+    for (int it = threadIdx.x; it < NDIM * NSH * 8; it += blockDim.x) {
+        const int d = it / (NSH * 8), sh = (it / 8) % NSH - p, b = it % 8;
+        if (b >= TBd[d]) continue;
+        const int x = min(max(org[d] + b + sh, 0), s.bn[d] - 1);
+        const int lo = s.esp[d][min(max(org[d] + sh, 0), s.bn[d] - 1)] - Q;
+        const int k = (d * MAXSH + sh + p) * 8 + b;
+        TR[k] = s.esp[d][x] - Q - lo;
+        if (b == 0) TL[d * MAXSH + sh + p] = lo;
+#pragma unroll
+        for (int r = 0; r <= Q; ++r) TW[k * (Q + 1) + r] = s.etab[d][x * (Q + 1) + r];
+    }
+    for (int it = threadIdx.x; it < L0 + L1 + L2; it += blockDim.x) {
+        int d = 0, li = it;
+        if (li >= L0) { li -= L0; d = 1; if (li >= L1) { li -= L1; d = 2; } }
+        if (d >= NDIM) continue;
+        const int base = d == 0 ? base0 : (d == 1 ? base1 : base2);
+        const int j = s.blo[d] + base + li;  // basis index
+        uint8_t mk = 0;
+        if (j >= 0 && j < s.m[d]) mk = (uint8_t)(s.inb[d][j] | (s.smp[d][j] << 1));
+        (d == 0 ? mk0 : (d == 1 ? mk1 : mk2))[li] = mk;
+    }
+    __syncthreads();
+    auto jint_of = [&](int j0, int j1, int j2) {
+        const uint8_t a = mk0[j0 - s.blo[0] - base0];
+        const uint8_t b = mk1[j1 - s.blo[1] - base1];
+        const uint8_t c = NDIM == 3 ? mk2[j2 - s.blo[2] - base2] : (uint8_t)3;
+        return ((a & b & c) & 1) && !((a & b & c) & 2);
+    };
+
+    // tile rows: CSR start (-1: not an interpolated row of this slab) and basis indices
+    int64_t* rbS = reinterpret_cast<int64_t*>((reinterpret_cast<uintptr_t>(mk2 + L2) + 15) & ~(uintptr_t)15);
+    int* rI = reinterpret_cast<int*>(rbS + NR);
+    double* VB = reinterpret_cast<double*>(rI + 3 * NR) + (size_t)warp * 4 * NR;  // per warp [4][NR] values
+    for (int r = threadIdx.x; r < NR; r += blockDim.x) {
+        const int b0 = r % TB0, b1 = (r / TB0) % TB1, b2 = r / (TB0 * TB1);
+        bool ok = org[0] + b0 < s.bn[0] && org[1] + b1 < s.bn[1] && (NDIM < 3 || org[2] + b2 < s.bn[2]);
+        const int i0 = s.blo[0] + org[0] + b0, i1 = s.blo[1] + org[1] + b1, i2 = NDIM == 3 ? s.blo[2] + org[2] + b2 : 0;
+        ok = ok && row_interp(s, i0, i1, i2);
+        const int64_t row = (int64_t)i0 + (int64_t)s.m[0] * ((int64_t)i1 + (int64_t)s.m[1] * i2);
+        ok = ok && row >= s.slab_lo && row < s.slab_hi;
+        rbS[r] = ok ? s.rowstart[row] : -1;
+        rI[3 * r] = i0;
+        rI[3 * r + 1] = i1;
+        rI[3 * r + 2] = i2;
+    }
+    for (int r = lane; r < NR; r += 32) {
+        red[warp * NR + r] = 0.0;
+        rcnt[(warp * NR + r) * 3 + 0] = rcnt[(warp * NR + r) * 3 + 1] = rcnt[(warp * NR + r) * 3 + 2] = 0;
+    }
+    __syncthreads();
+    // the lane's two rows in the evaluation passes
+    int rb0[2], rb1[2], rb2[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int r = lane + 32 * k;
+        rb0[k] = r % TB0;
+        rb1[k] = (r / TB0) % TB1;
+        rb2[k] = r / (TB0 * TB1);
+    }
+    const int64_t nl01 = (int64_t)s.nl[0] * s.nl[1];
+
+    // offset -> (evaluated offset, evaluation shift): mirrored offsets of the symmetric modes
+    auto offset_of = [&](int o, int& op, int& sh0, int& sh1, int& sh2) {
+        op = o;
+        sh0 = sh1 = sh2 = 0;
+        if (s.mode != SG_GENERAL && o < s.center) {
+            op = P - 1 - o;
+            sh0 = s.shifts[o * 3 + 0];
+            sh1 = s.shifts[o * 3 + 1];
+            sh2 = s.shifts[o * 3 + 2];
+        }
+    };
+    constexpr int NWL = (NWIN + 31) / 32;  // window elements per lane
+    // the lane's share of offset o's coefficient window W[t2][t1][t0] (registers: prefetched one
+    // offset ahead so the L2 latency overlaps the current offset's passes)
+    auto fetch = [&](int o, double (&w)[NWL]) {
+        int op, a0, a1, a2;
+        offset_of(o, op, a0, a1, a2);
+        const double* cf = s.coef + (int64_t)op * nl01 * s.nl[2];
+        const int lo0 = TL[0 * MAXSH + a0 + p], lo1 = TL[1 * MAXSH + a1 + p], lo2 = NDIM == 3 ? TL[2 * MAXSH + a2 + p] : 0;
+#pragma unroll
+        for (int i = 0; i < NWL; ++i) {
+            const int e = i * 32 + lane;
+            w[i] = 0.0;
+            if (e < NWIN) {
+                const int t0 = e % CW, t1 = (e / CW) % CW, t2 = e / (CW * CW);
+                const int r0 = min(lo0 + t0, s.nl[0] - 1), r1 = min(lo1 + t1, s.nl[1] - 1);
+                const int r2 = NDIM == 3 ? min(lo2 + t2, s.nl[2] - 1) : 0;
+                w[i] = __ldg(cf + r2 * nl01 + (int64_t)r1 * s.nl[0] + r0);
+            }
+        }
+    };
+    // the warp's offsets: blocks of 4 consecutive offsets (block b = warp, warp + nw, ...), so the
+    // placement writes 4 consecutive CSR slots per row (32 B data / 16 B index segments)
+    const int nblk = (P + 3) / 4;
+    auto next_offset = [&](int o) {  // offset after o in this warp's sequence (or P)
+        if ((o & 3) != 3 && o + 1 < P) return o + 1;
+        const int nb = (o >> 2) + nw;
+        return nb < nblk ? nb * 4 : P;
+    };
+    double wpre[NWL];
+    if (warp < nblk) fetch(warp * 4, wpre);
+    for (int blk = warp; blk < nblk; blk += nw) {
+        const int ob = blk * 4;
+        for (int oo = 0; oo < 4; ++oo) {
+            const int o = ob + oo;
+            if (o >= P) break;
+            int op, sh0, sh1, sh2;
+            offset_of(o, op, sh0, sh1, sh2);
+            (void)op;
+            const int k0 = (0 * MAXSH + sh0 + p), k1 = (1 * MAXSH + sh1 + p), k2 = (2 * MAXSH + sh2 + p);
+#pragma unroll
+            for (int i = 0; i < NWL; ++i)
+                if (i * 32 + lane < NWIN) Wn[i * 32 + lane] = wpre[i];
+            {
+                const int on = next_offset(o);
+                if (on < P) fetch(on, wpre);
+            }
+            __syncwarp();
+            // x pass: A[t2][t1][b0] = sum_r w0[b0][r] W[t2][t1][rel0(b0) + r]  (b0 = lane % TB0 for
+            // every item of the lane: its weights and tap start are loaded once per offset)
+            {
+                const int kb = k0 * 8 + (lane % TB0);
+                const double2 wa = *reinterpret_cast<const double2*>(TW + kb * (Q + 1));
+                const double2 wb = *reinterpret_cast<const double2*>(TW + kb * (Q + 1) + 2);
+                const double* cb = Wn + TR[kb];
+#pragma unroll
+                for (int i0 = 0; i0 < NA; i0 += 32) {
+                    const int it = i0 + lane;
+                    if (it < NA) {
+                        const double* c = cb + (it / TB0) * CW;  // row t2*CW + t1
+                        double v = 0.0;
+                        v = fma(wa.x, c[0], v);
+                        v = fma(wa.y, c[1], v);
+                        v = fma(wb.x, c[2], v);
+                        v = fma(wb.y, c[3], v);
+                        A[it] = v;
+                    }
+                }
+            }
+            __syncwarp();
+            if constexpr (NDIM == 2) {
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const int kb = k1 * 8 + rb1[k];
+                    const double* w = TW + kb * (Q + 1);
+                    const double* c = A + TR[kb] * TB0 + rb0[k];
+                    double v = 0.0;
+#pragma unroll
+                    for (int r = 0; r <= Q; ++r) v = fma(w[r], c[r * TB0], v);
+                    VB[oo * NR + lane + 32 * k] = v;
+                }
+            } else {
+                // y pass: Bm[t2][b1][b0] = sum_r w1[b1][r] A[t2][rel1(b1) + r][b0]
+                {
+                    // b0 = lane % TB0 and b1 = (lane / TB0) % TB1 for every item of the lane (TB0*TB1 = 16 | 32)
+                    const int b0 = lane % TB0, b1 = (lane / TB0) % TB1;
+                    const int kb = k1 * 8 + b1;
+                    const double2 wa = *reinterpret_cast<const double2*>(TW + kb * (Q + 1));
+                    const double2 wb = *reinterpret_cast<const double2*>(TW + kb * (Q + 1) + 2);
+                    const double* cb = A + TR[kb] * TB0 + b0;
+#pragma unroll
+                    for (int i0 = 0; i0 < NB; i0 += 32) {
+                        const int it = i0 + lane;
+                        if (it < NB) {
+                            const double* c = cb + (it / (TB0 * TB1)) * CW * TB0;  // t2
+                            double v = 0.0;
+                            v = fma(wa.x, c[0], v);
+                            v = fma(wa.y, c[TB0], v);
+                            v = fma(wb.x, c[2 * TB0], v);
+                            v = fma(wb.y, c[3 * TB0], v);
+                            Bm[it] = v;
+                        }
+                    }
+                }
+                __syncwarp();
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const int kb = k2 * 8 + rb2[k];
+                    const double* w = TW + kb * (Q + 1);
+                    const double* c = Bm + (TR[kb] * TB1 + rb1[k]) * TB0 + rb0[k];
+                    double v = 0.0;
+#pragma unroll
+                    for (int r = 0; r <= Q; ++r) v = fma(w[r], c[r * TB1 * TB0], v);
+                    VB[oo * NR + lane + 32 * k] = v;
+                }
+            }
+            __syncwarp();
+        }
+        // placement of the block: lane -> (row rr*8 + lane/4, offset ob + lane%4)
+        const int oo = lane & 3, o = ob + oo;
+        const bool ov = o < P;
+        const int so0 = ov ? s.shifts[o * 3 + 0] : 0, so1 = ov ? s.shifts[o * 3 + 1] : 0, so2 = ov ? s.shifts[o * 3 + 2] : 0;
+#pragma unroll 2
+        for (int rr = 0; rr < NR / 8; ++rr) {
+            const int r = rr * 8 + (lane >> 2);
+            const int64_t rb = rbS[r];
+            double v = 0.0;
+            int in = 0, off = 0, ze = 0;
+            if (rb >= 0 && ov) {
+                const int j0 = rI[3 * r] + so0, j1 = rI[3 * r + 1] + so1, j2 = rI[3 * r + 2] + so2;
+                const int64_t col = (int64_t)j0 + (int64_t)s.m[0] * ((int64_t)j1 + (int64_t)s.m[1] * j2);
+                const bool jint = jint_of(j0, j1, j2);
+                v = jint ? VB[oo * NR + r] : s.data[s.rowstart[col] + (P - 1 - o)];  // transposed quadrature entry A[j, i]
+                s.data[rb + o] = v;
+                s.indices[rb + o] = (int)col;
+                in = jint;
+                off = jint && o != s.center;
+                ze = v == 0.0;
+                if (o == s.center) dgv[r] = v;
+            }
+            // the row's 4 values: ((v0 + v1) + (v2 + v3)) added to this warp's partial row sum
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            v += __shfl_xor_sync(0xffffffffu, v, 2);
+            in += __shfl_xor_sync(0xffffffffu, in, 1);
+            in += __shfl_xor_sync(0xffffffffu, in, 2);
+            off += __shfl_xor_sync(0xffffffffu, off, 1);
+            off += __shfl_xor_sync(0xffffffffu, off, 2);
+            ze += __shfl_xor_sync(0xffffffffu, ze, 1);
+            ze += __shfl_xor_sync(0xffffffffu, ze, 2);
+            if (oo == 0 && rb >= 0) {
+                red[warp * NR + r] += v;
+                rcnt[(warp * NR + r) * 3 + 0] += off;
+                rcnt[(warp * NR + r) * 3 + 1] += in;
+                rcnt[(warp * NR + r) * 3 + 2] += ze;
+            }
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    unsigned long long n_int = 0, n_zero = 0, n_reset = 0, n_rows = 0;
+    if (threadIdx.x < NR) {
+        const int r = threadIdx.x;
+        if (rbS[r] >= 0) {
+            const int64_t row = (int64_t)rI[3 * r] + (int64_t)s.m[0] * ((int64_t)rI[3 * r + 1] + (int64_t)s.m[1] * rI[3 * r + 2]);
+            double sum = 0.0;
+            int off = 0, in = 0, ze = 0;
+            for (int w = 0; w < nw; ++w) {
+                sum += red[w * NR + r];
+                off += rcnt[(w * NR + r) * 3 + 0];
+                in += rcnt[(w * NR + r) * 3 + 1];
+                ze += rcnt[(w * NR + r) * 3 + 2];
+            }
+            n_int += in;
+            n_zero += ze;
+            n_rows++;
+            if (s.mode == SG_SYMMETRIC_KERNEL_PRESERVING && off > 0) {
+                s.newdiag[row] = dgv[r] - sum;
+                s.reset[row] = 1;
+                n_reset++;
+            }
+        }
+    }
+    if (threadIdx.x < NR) {
+#pragma unroll
+        for (int w = 16; w > 0; w >>= 1) {
+            n_int += __shfl_xor_sync(0xffffffffu, n_int, w);
+            n_zero += __shfl_xor_sync(0xffffffffu, n_zero, w);
+            n_reset += __shfl_xor_sync(0xffffffffu, n_reset, w);
+            n_rows += __shfl_xor_sync(0xffffffffu, n_rows, w);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            if (n_int) atomicAdd(&s.counters[0], n_int);
+            if (n_zero) atomicAdd(&s.counters[1], n_zero);
+            if (n_reset) atomicAdd(&s.counters[2], n_reset);
+            if (n_rows) atomicAdd(&s.counters[3], n_rows);
+        }
+    }
+}
+static size_t interp_fix_smem(int n, int p) {
+    const int Q = 3, CW = 5, NR = 64, MAXSH = 9, nw = 16;
+    const int TB0 = n == 2 ? 8 : 4, TB1 = n == 2 ? 8 : 4, TB2 = n == 3 ? 4 : 1;
+    const int C2 = n == 3 ? CW : 1;
+    const int SCR = 128 + C2 * CW * TB0 + (n == 3 ? C2 * TB1 * TB0 : 0);
+    const int L = (TB0 + 2 * p) + (TB1 + 2 * p) + (n == 3 ? TB2 + 2 * p : 1);
+    return sizeof(double) * ((size_t)nw * SCR + (size_t)nw * NR + NR + 3 * MAXSH * 8 * (Q + 1)) +
+           sizeof(int) * (3 * MAXSH * 8 + 3 * MAXSH + (size_t)nw * NR * 3) + L + 16 +
+           sizeof(int64_t) * NR + sizeof(int) * 3 * NR + sizeof(double) * (size_t)nw * 4 * NR;
 }
 
 __global__ void skp_apply_kernel(const uint8_t* __restrict__ reset, const double* __restrict__ newdiag,
@@ -666,27 +912,22 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
     for (int d = 0; d < n; ++d) fixq = fixq && s.cmax[d] <= 5;
     void* kfn;
     const int NR = 64;
-    const size_t vbytes = sizeof(double) * (size_t)P * (NR + 1) + sizeof(int) * (size_t)P * 3 + 16;
-    bool stage = false;
-    if (fixq) {
+    size_t smem;
+    if (fixq && n >= 2 && p <= 4) {
         for (int d = 0; d < n; ++d) s.cmax[d] = 5;
-        stage = vbytes <= 170 * 1024 && !getenv("SG_NO_STAGE");
-        if (stage)
-            kfn = n == 1 ? (void*)interp_tiles_kernel<1, 3, true> : (n == 2 ? (void*)interp_tiles_kernel<2, 3, true> : (void*)interp_tiles_kernel<3, 3, true>);
-        else
-            kfn = n == 1 ? (void*)interp_tiles_kernel<1, 3, false> : (n == 2 ? (void*)interp_tiles_kernel<2, 3, false> : (void*)interp_tiles_kernel<3, 3, false>);
+        kfn = n == 2 ? (void*)interp_fix_kernel<2> : (void*)interp_fix_kernel<3>;
+        smem = interp_fix_smem(n, p);
     } else {
-        kfn = n == 1 ? (void*)interp_tiles_kernel<1, 0, false> : (n == 2 ? (void*)interp_tiles_kernel<2, 0, false> : (void*)interp_tiles_kernel<3, 0, false>);
+        kfn = n == 1 ? (void*)interp_tiles_kernel<1> : (n == 2 ? (void*)interp_tiles_kernel<2> : (void*)interp_tiles_kernel<3>);
+        const int nw = nthreads / 32;
+        const int scr = s.cmax[2] * s.cmax[1] * s.TB[0] + s.cmax[2] * s.TB[1] * s.TB[0] + 8;
+        size_t tabs = 0;
+        for (int d = 0; d < 3; ++d) {
+            const int L = (d < n ? s.TB[d] + 2 * p : 1);
+            tabs += (size_t)L * (s.qd[d] + 1) * sizeof(double) + (size_t)L * sizeof(int) + L;
+        }
+        smem = sizeof(double) * ((size_t)nw * scr + (size_t)nw * NR + NR) + sizeof(int) * ((size_t)nw * NR * 3 + 2) + tabs + 64;
     }
-    const int nw = nthreads / 32;
-    const int scr = s.cmax[2] * s.cmax[1] * s.TB[0] + s.cmax[2] * s.TB[1] * s.TB[0] + 8;
-    size_t tabs = 0;
-    for (int d = 0; d < 3; ++d) {
-        const int L = (d < n ? s.TB[d] + 2 * p : 1);
-        tabs += (size_t)L * (s.qd[d] + 1) * sizeof(double) + (size_t)L * sizeof(int) + L;
-    }
-    const size_t smem = sizeof(double) * ((size_t)nw * scr + (size_t)nw * NR + NR) + sizeof(int) * ((size_t)nw * NR * 3 + 2) + tabs + 64 +
-                        (stage ? vbytes : 0);
     if (smem > 227 * 1024) return fail(-2, "surrogate tile does not fit shared memory (%zu B)", smem);
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     void* args[] = {&s};
