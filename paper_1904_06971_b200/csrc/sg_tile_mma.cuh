@@ -126,7 +126,9 @@ __host__ __device__ constexpr int mma_warps(int ndim, int P, int form, bool rat)
 #ifdef SG_MMA_NW
     return SG_MMA_NW;
 #else
-    return 16;
+    // 3D: 24 warps (6 per sub-partition) hide the smem -> DMMA -> smem latency chains of the
+    // pipelined intervals better than 16 (cfg5 Poisson 52.4 -> 48.2 ms); more spills registers
+    return ndim == 3 ? 24 : 16;
 #endif
 }
 
@@ -178,7 +180,7 @@ __host__ __device__ constexpr MmaGeom mma_geom(int ndim, int P, int form, bool r
     o = (o + 1) & ~1L;
     m.o_cmb = o; o += ndim == 3 ? (long)m.NCOMBO * 2 + 2 : 0;                  // per-combo {off, cnt01, row01, col01}
     {
-        const int NW = mma_warps(ndim, P, form, rat);
+        const int NW = 32;  // table sized for up to 32 warps (host and device layouts agree whatever the warp count)
         int nu2 = 0;
         for (int g = 0; g < (ndim >= 2 ? T.NG2 : 0); ++g) nu2 += T.g2n[g];
         m.NTAB = 3 * (NW + 1) + m.NG1 * T0 + (ndim >= 2 ? T.NG2 * m.T1 * T0 : 0) + (ndim == 3 ? (P + 1) * m.NCH : 0) +
