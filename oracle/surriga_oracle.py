@@ -524,6 +524,122 @@ def assemble(prob: Problem, rows=None, chunk=4096):
 
 
 # ---------------------------------------------------------------------------
+# mixed divergence pairing (assembly.py:180-207, 654-725)
+# ---------------------------------------------------------------------------
+
+def div_col_range(mv, pp, multi):
+    """Velocity columns of pressure row(s) ``multi``: j_d in [2 i_d - 2pp, 2 i_d + pp + 2] (clipped)."""
+    lo = np.maximum(2 * multi - 2 * pp, 0)
+    hi = np.minimum(2 * multi + pp + 2, np.asarray(mv) - 1)
+    return lo, hi
+
+
+def div_pattern(mp, mv, pp, rows=None):
+    """indptr/indices of the pressure x velocity overlap pattern (rows restricted if given)."""
+    mp, mv = tuple(mp), tuple(mv)
+    Np = int(np.prod(mp))
+    rsel = np.arange(Np) if rows is None else np.asarray(rows, dtype=np.int64)
+    multi = np.stack(np.unravel_index(rsel, mp, order="F"), axis=-1)
+    lo, hi = div_col_range(mv, pp, multi)
+    cnt = np.zeros(Np, dtype=np.int64)
+    cnt[rsel] = np.prod(hi - lo + 1, axis=1)
+    indptr = np.zeros(Np + 1, dtype=np.int64)
+    np.cumsum(cnt, out=indptr[1:])
+    vstr = np.cumprod((1,) + mv[:-1])
+    cols = []
+    for r in range(rsel.size):
+        axes = [np.arange(lo[r, d], hi[r, d] + 1) for d in range(len(mv))]
+        grid = np.stack(np.meshgrid(*axes, indexing="ij"), axis=-1).reshape(-1, len(mv), order="F")
+        cols.append((grid * vstr).sum(-1))
+    indices = (np.concatenate(cols) if cols else np.zeros(0, np.int64)).astype(np.int32)
+    return indptr, indices
+
+
+def div_elements_for_rows(mp, pp, sv, rows):
+    """assembly.py:347-360 with ratio 2: velocity elements [2 max(0, i-pp), 2 min(Sp-1, i) + 1] per direction."""
+    mp = tuple(mp)
+    n = len(mp)
+    sp_ = tuple(m - pp for m in mp)
+    mask = np.zeros(tuple(sv), dtype=bool)
+    multi = np.stack(np.unravel_index(np.asarray(rows, dtype=np.int64), mp, order="F"), axis=-1)
+    for mi in multi:
+        sl = tuple(slice(2 * max(0, int(mi[d]) - pp), 2 * (min(sp_[d] - 1, int(mi[d])) + 1)) for d in range(n))
+        mask[sl] = True
+    return np.flatnonzero(mask.ravel(order="F"))
+
+
+def divergence(vel: Problem, pp: int, rows=None, chunk=1024):
+    """Pressure/velocity divergence pairing, one CSR per component c (assembly.py:654-725).
+
+    ``vel`` describes the velocity discretisation (degree pp+1 on the halved mesh, Gauss order,
+    geometry); the pressure space has degree ``pp`` and half the velocity spans.  Entry (i, j) of
+    component c is  sum_q w_q P_i(x_q) sum_a d_a V_j(x_q) adj(J)[a, c]  (no determinant: the
+    adjugate folds it).  Non-rational spaces (unit weights) only.
+    Returns ``(indptr, indices, [data_c for c < n], populated_rows)``.
+    """
+    n, pv, g = vel.n, vel.p, vel.g
+    if pv != pp + 1:
+        raise ValueError("velocity degree must be pressure degree + 1")
+    sv = vel.spans
+    if any(s % 2 for s in sv):
+        raise ValueError("velocity spans must be twice the pressure spans")
+    spn = tuple(s // 2 for s in sv)
+    mp = tuple(s + pp for s in spn)
+    mv = vel.ms
+    Np = int(np.prod(mp))
+    tabs_v, axes, pws = _dir_tables(vel, 1)
+    tabs_p = []
+    for d in range(n):
+        span, ders = basis_ders(open_uniform_knots(pp, mp[d]), pp, axes[d], 0)
+        assert np.array_equal(span.reshape(sv[d], g), (np.arange(sv[d]) // 2 + pp)[:, None].repeat(g, 1))
+        tabs_p.append(ders.reshape(sv[d], g, 1, pp + 1))
+    wq = pws[0]
+    for d in range(1, n):
+        wq = (pws[d][:, None] * wq[None, :]).ravel()
+    geo = geometry_on_grid(vel, axes, 1)
+    jacE = _to_elements(geo["jac"], sv, g)
+    if rows is None:
+        eids = np.arange(int(np.prod(sv)))
+        rowsel = None
+    else:
+        rowsel = np.unique(np.asarray(rows, dtype=np.int64))
+        if rowsel.size and (rowsel[0] < 0 or rowsel[-1] >= Np):
+            raise ValueError("pressure row index out of range")
+        eids = div_elements_for_rows(mp, pp, sv, rowsel) if rowsel.size else np.zeros(0, np.int64)
+        keep = np.zeros(Np, dtype=bool)
+        keep[rowsel] = True
+    indptr, indices = div_pattern(mp, mv, pp, rowsel)
+    data = [np.zeros(indices.size) for _ in range(n)]
+    Lp, Lv = (pp + 1) ** n, (pv + 1) ** n
+    Ip = np.stack(np.unravel_index(np.arange(Lp), (pp + 1,) * n, order="F"), axis=-1)
+    Iv = np.stack(np.unravel_index(np.arange(Lv), (pv + 1,) * n, order="F"), axis=-1)
+    pstr = np.cumprod((1,) + mp[:-1])
+    for s0 in range(0, eids.size, chunk):
+        ce = eids[s0:s0 + chunk]
+        et = np.stack(np.unravel_index(ce, sv, order="F"), axis=-1)
+        A = adj(jacE[ce])                                    # (E, Q, a, c)
+        Bp = _local_tensor(tabs_p, et, (0,) * n, pp, g)      # (E, Q, Lp)
+        dV = np.stack([_local_tensor(tabs_v, et, _unit(n, a), pv, g) for a in range(n)], axis=-1)  # (E,Q,Lv,a)
+        Pw = Bp * wq[None, :, None]
+        gp = et[:, None, :] // 2 + Ip[None, :, :]           # pressure multi (E, Lp, n)
+        gv = et[:, None, :] + Iv[None, :, :]                # velocity multi (E, Lv, n)
+        rflat = (gp * pstr).sum(-1)
+        lo, hi = div_col_range(mv, pp, gp)
+        cnt = hi - lo + 1
+        rel = gv[:, None, :, :] - lo[:, :, None, :]          # (E, Lp, Lv, n)
+        cstr = np.concatenate([np.ones(cnt.shape[:2] + (1,), np.int64), np.cumprod(cnt[..., :-1], -1)], -1)
+        colpos = (rel * cstr[:, :, None, :]).sum(-1)
+        rr = np.broadcast_to(rflat[:, :, None], colpos.shape)
+        sel = keep[rr] if rowsel is not None else np.ones(rr.shape, dtype=bool)
+        pos = indptr[rr[sel]] + colpos[sel]
+        for c in range(n):
+            t = np.einsum("eqka,eqa->eqk", dV, A[..., :, c])
+            loc = np.einsum("eql,eqk->elk", Pw, t)
+            data[c] += np.bincount(pos, weights=loc[sel], minlength=indices.size)
+    return indptr, indices, data, rowsel
+
+
+# ---------------------------------------------------------------------------
 # surrogate (surrogate.py:36-691)
 # ---------------------------------------------------------------------------
 
