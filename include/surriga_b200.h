@@ -99,6 +99,14 @@ int sg_result_sizes(const sg_result* r, int64_t* nrows, int64_t* nnz);
 /* Copy CSR to host: indptr int32[nrows+1] (or int64 if *_i64 variant), indices int32[nnz], data f64[nnz]. */
 int sg_result_copy(const sg_result* r, int32_t* indptr, int32_t* indices, double* data);
 int sg_result_copy_i64(const sg_result* r, int64_t* indptr, int32_t* indices, double* data);
+/* Mixed divergence pairing (replaces surriga/assembly.py:654-725 `assemble_divergence(stokes, rows=None)`):
+   `velocity` describes the velocity discretisation (degree pp+1 on the halved mesh, its Gauss points and weights,
+   the geometry), `pressure` the pressure space (degree pp; only n, p, m and knots are read).  Writes n results,
+   one per velocity component c (out[0..n-1]): rows = pressure functions, columns = velocity functions, entry
+   sum_q w_q P_i sum_a d_a V_j adj(J)[a][c].  `rows` (sorted, unique) restricts to pressure rows as the reference's
+   `rows=` (bitwise equal to the full assembly).  Non-rational spaces only; no row slabs. */
+int sg_assemble_divergence(const sg_problem* velocity, const sg_problem* pressure, const int64_t* rows, int64_t nrows,
+                           const sg_exec* exec, sg_result** out);
 /* Optional: allocate the calling thread's pinned D2H staging ring and host copy pool for `device` up
    front (otherwise done by the first large sg_result_copy*; not part of the reference interface). */
 int sg_host_staging_init(int device);

@@ -11,7 +11,10 @@ from .assembly import (  # noqa: F401
     Discretization,
     FormKind,
     SparseMatrix,
+    StokesSpaces,
     assemble,
+    assemble_divergence,
+    assemble_divergence_device,
     assemble_device,
     elements_for_rows,
     form_is_symmetric,
@@ -20,6 +23,7 @@ from .assembly import (  # noqa: F401
     make_discretization,
     matrices_bitwise_equal,
     set_device,
+    stokes_subgrid_spaces,
 )
 from .geometry import (  # noqa: F401
     BUILTIN_NAMES,

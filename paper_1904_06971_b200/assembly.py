@@ -23,7 +23,7 @@ from .spaces import NurbsWeights, TensorSpace, make_open_uniform_knots, make_ten
 __all__ = [
     "FormKind", "Discretization", "SparseMatrix", "gauss_rule", "make_discretization", "assemble", "assemble_device",
     "elements_for_rows", "is_bitwise_symmetric", "matrices_bitwise_equal", "form_is_symmetric", "set_device",
-    "problem_arrays",
+    "problem_arrays", "StokesSpaces", "stokes_subgrid_spaces", "assemble_divergence", "assemble_divergence_device",
 ]
 
 
@@ -297,3 +297,80 @@ def assemble(form, disc, rows=None, coefficient: float = 1.0) -> SparseMatrix:
     mat = sp.csr_matrix((data, indices, indptr), shape=(N, N))
     mat.has_sorted_indices = True
     return SparseMatrix(mat=mat, symmetric=sym, populated_rows=None if rows is None else rsel)
+
+
+# ---------------------------------------------------------------------------------------
+# mixed divergence pairing (assembly.py:180-207, 654-725)
+# ---------------------------------------------------------------------------------------
+
+@dataclass
+class StokesSpaces:
+    """assembly.py:180-194: inf-sup stable velocity/pressure pair on nested meshes (velocity degree
+    one higher, every pressure element halved)."""
+
+    geom: GeometryMap
+    velocity: Discretization
+    pressure: Discretization
+
+    @property
+    def n(self) -> int:
+        return self.geom.n
+
+
+def stokes_subgrid_spaces(geom: GeometryMap, p_pressure: int, spans, gauss: int | None = None) -> StokesSpaces:
+    """assembly.py:197-207; ``spans`` counts pressure elements."""
+    if p_pressure < 1:
+        raise ValueError("pressure degree must be at least 1")
+    n = geom.n
+    if np.isscalar(spans):
+        spans = (int(spans),) * n
+    spans = tuple(int(s) for s in spans)
+    pressure = make_discretization(geom, p_pressure, spans)
+    velocity = make_discretization(geom, p_pressure + 1, tuple(2 * s for s in spans), gauss=gauss)
+    return StokesSpaces(geom=geom, velocity=velocity, pressure=pressure)
+
+
+def assemble_divergence_device(stokes, rows=None, *, device=None, stream=None):
+    """Divergence pairing on the GPU, CSRs kept in HBM: ``([_lib.Result per component], rows)``."""
+    vel, prs = stokes.velocity, stokes.pressure
+    n = len(vel.space.kvs)
+    vpr, vkeep, _, _ = problem_arrays(FormKind.POISSON, vel)
+    pspace = prs.space
+    pp = int(pspace.kvs[0].p)
+    pkeep = _Keep()
+    ppr = _lib.SgProblem()
+    ppr.n = n
+    ppr.p = pp
+    ppr.g = int(prs.gauss)
+    for d, kv in enumerate(pspace.kvs):
+        ppr.m[d] = int(kv.m)
+        ppr.knots[d] = pkeep.ptr(make_open_uniform_knots(pp, int(kv.m)).knots)
+    pw = np.asarray(prs.weights.weights, dtype=float)
+    ppr.sol_w = None if bool(np.all(pw == pw[0])) else pkeep.ptr(pw)
+    Np = int(np.prod([kv.m for kv in pspace.kvs]))
+    rsel, rptr, nr = None, None, 0
+    if rows is not None:
+        rsel = np.unique(np.asarray(rows, dtype=np.int64))
+        if rsel.size and (rsel[0] < 0 or rsel[-1] >= Np):
+            raise ValueError("pressure row index out of range")
+        rptr, nr = rsel.ctypes.data_as(_lib._i64), rsel.size
+    ex = _exec(device, stream, None)
+    hs = (C.c_void_p * 3)()
+    _lib.check(_lib.lib().sg_assemble_divergence(C.byref(vpr), C.byref(ppr), rptr, nr, C.byref(ex), hs))
+    del vkeep, pkeep
+    return [_lib.Result(hs[c]) for c in range(n)], rsel
+
+
+def assemble_divergence(stokes, rows=None) -> list:
+    """Pressure/velocity divergence pairing, one matrix per velocity component (assembly.py:654-725)."""
+    res, rsel = assemble_divergence_device(stokes, rows=rows)
+    Np = int(np.prod([kv.m for kv in stokes.pressure.space.kvs]))
+    Nv = int(np.prod([kv.m for kv in stokes.velocity.space.kvs]))
+    out = []
+    for r in res:
+        indptr, indices, data = r.to_host()
+        r.free()
+        mat = sp.csr_matrix((data, indices, indptr), shape=(Np, Nv))
+        mat.has_sorted_indices = True
+        out.append(SparseMatrix(mat=mat, symmetric=False, populated_rows=None if rows is None else rsel))
+    return out

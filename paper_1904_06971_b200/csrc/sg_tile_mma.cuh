@@ -692,6 +692,31 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), 1) assembl
                         }
                     }
                 };
+                // a symmetric pair's two chains, interleaved (independent accumulators)
+                auto block2 = [&](int ga, int kd, int gb, int kb, double (&accA)[MT][MT][2], double (&accB)[MT][MT][2]) {
+                    const double* bfa = B2f + ((i1l * NK1 + kd) * KS) * MT * 32 + lane;
+                    const double* bfb = B2f + ((i1l * NK1 + kb) * KS) * MT * 32 + lane;
+                    const double* ta = T1b + ((ga * T0 + r) * MT * 8 + lr) * TY + i1l * G + lk;
+                    const double* tb = T1b + ((gb * T0 + r) * MT * 8 + lr) * TY + i1l * G + lk;
+#pragma unroll
+                    for (int kk = 0; kk < KS; ++kk) {
+                        double fa[MT], fb[MT];
+#pragma unroll
+                        for (int c = 0; c < MT; ++c) {
+                            fa[c] = bfa[(kk * MT + c) * 32];
+                            fb[c] = bfb[(kk * MT + c) * 32];
+                        }
+#pragma unroll
+                        for (int a = 0; a < MT; ++a) {
+                            const double va = ta[a * 8 * TY + kk * 4], vb = tb[a * 8 * TY + kk * 4];
+#pragma unroll
+                            for (int c = 0; c < MT; ++c) {
+                                dmma(accA[a][c][0], accA[a][c][1], va, fa[c]);
+                                dmma(accB[a][c][0], accB[a][c][1], vb, fb[c]);
+                            }
+                        }
+                    }
+                };
                 double accS[MT][MT][2];
 #pragma unroll
                 for (int a = 0; a < MT; ++a)
@@ -709,8 +734,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), 1) assembl
                         for (int a = 0; a < MT; ++a)
 #pragma unroll
                             for (int c = 0; c < MT; ++c) tA[a][c][0] = tA[a][c][1] = tB[a][c][0] = tB[a][c][1] = 0.0;
-                        block(ga, kd, tA);
-                        block((d >> 8) & 255, (d >> 20) & 15, tB);
+                        block2(ga, kd, (d >> 8) & 255, (d >> 20) & 15, tA, tB);
 #pragma unroll
                         for (int a = 0; a < MT; ++a)
 #pragma unroll

@@ -1,0 +1,82 @@
+"""GPU parity of the mixed divergence pairing (assembly.py:654-725) against the reference's goldens
+(tests/golden/div) and the oracle; properties of test_assembly.py:154-178."""
+import numpy as np
+import pytest
+
+from oracle import surriga_oracle as O
+from test_oracle_divergence import div_cases, load_div, vel_problem
+
+TOL = 1e-12
+
+
+def stokes_from_golden(meta, arr):
+    import paper_1904_06971_b200 as pkg
+    from paper_1904_06971_b200.geometry import GeometryMap
+    from paper_1904_06971_b200.spaces import NurbsWeights, make_tensor_space
+
+    gsp = make_tensor_space(meta["geo_p"], meta["geo_ms"])
+    geom = GeometryMap(space=gsp, weights=NurbsWeights(arr["geo_w"], polynomial_weight=True), control=arr["geo_ctrl"])
+    st = pkg.stokes_subgrid_spaces(geom, meta["pp"], tuple(meta["spans"]))
+    if st.velocity.gauss != meta["gauss"]:
+        st = pkg.stokes_subgrid_spaces(geom, meta["pp"], tuple(meta["spans"]), gauss=meta["gauss"])
+    return st
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", div_cases())
+def test_gpu_divergence_matches_reference_golden(case):
+    import paper_1904_06971_b200 as pkg
+
+    meta, arr = load_div(case)
+    st = stokes_from_golden(meta, arr)
+    rows = arr.get("rows")
+    D = pkg.assemble_divergence(st, rows=rows)
+    assert len(D) == meta["n"]
+    for c, Dc in enumerate(D):
+        m = Dc.mat
+        assert m.indptr.dtype == np.int32 and m.indices.dtype == np.int32 and m.data.dtype == np.float64
+        assert np.array_equal(m.indptr, arr["indptr"]), "indptr differs"
+        assert np.array_equal(m.indices, arr["indices"]), "indices differ"
+        err = O.row_scaled_error(arr["indptr"], arr["indices"], arr[f"data_{c}"], m.indptr, m.indices, m.data)
+        assert err <= TOL, (c, err)
+        assert Dc.symmetric is False
+        if rows is not None:
+            assert np.array_equal(Dc.populated_rows, arr["populated_rows"])
+
+
+@pytest.mark.gpu
+def test_gpu_divergence_matches_oracle_larger_3d():
+    import paper_1904_06971_b200 as pkg
+
+    st = pkg.stokes_subgrid_spaces(pkg.twisted_cube_standin(), 2, (4, 3, 5))
+    D = pkg.assemble_divergence(st)
+    vel = O.problem_from_disc("stokes_divergence", st.velocity)
+    ip, ix, data, _ = O.divergence(vel, 2)
+    for c, Dc in enumerate(D):
+        assert np.array_equal(Dc.mat.indptr, ip) and np.array_equal(Dc.mat.indices, ix)
+        assert O.row_scaled_error(ip, ix, data[c], Dc.mat.indptr, Dc.mat.indices, Dc.mat.data) <= TOL
+
+
+@pytest.mark.gpu
+def test_gpu_divergence_rows_bitwise_and_constant_field():
+    # test_assembly.py:154-160 and :173-178 on the GPU path
+    import paper_1904_06971_b200 as pkg
+
+    st = pkg.stokes_subgrid_spaces(pkg.builtin_domain("coons_quadratic"), 2, (6, 6))
+    full = pkg.assemble_divergence(st)
+    ones = np.ones(st.velocity.space.N)
+    for Dc in full:
+        assert np.max(np.abs(Dc.mat @ ones)) < 1e-13
+    rows = np.array([0, 5, 17, 40])
+    part = pkg.assemble_divergence(st, rows=rows)
+    for Df, Dp in zip(full, part):
+        assert pkg.matrices_bitwise_equal(Df, Dp, rows=rows)
+
+
+@pytest.mark.gpu
+def test_gpu_divergence_rejects_rational_spaces():
+    import paper_1904_06971_b200 as pkg
+
+    st = pkg.stokes_subgrid_spaces(pkg.quarter_annulus(1.0, 2.0), 2, (4, 4))
+    with pytest.raises((NotImplementedError, ValueError, RuntimeError)):
+        pkg.assemble_divergence(st)
