@@ -821,6 +821,115 @@ def surrogate(prob: Problem, M: int, q: int = 3, mode=None):
     return (indptr, indices, data), mode in ("symmetric", "symmetric_kernel_preserving"), rep
 
 
+def surrogate_divergence(vel: Problem, pp: int, M: int, q: int = 3):
+    """Surrogate divergence pairing, general mode only (surrogate.py:702-819).
+
+    Returns ``([(indptr, indices, data) per component], report dict)``.
+    """
+    from scipy.linalg import solve
+
+    n, pv = vel.n, vel.p
+    sv = vel.spans
+    mp = tuple(s // 2 + pp for s in sv)
+    mv = vel.ms
+    Np = int(np.prod(mp))
+    h0 = 1.0 / (mp[0] - pp)
+    if any(m <= 4 * pp for m in mp):
+        ip, ix, data, _ = divergence(vel, pp)
+        rep = dict(N=Np, p=pp, q=q, M=M, H=M * h0, quad_entries=ix.size * n, interp_entries=0, quad_fraction=1.0,
+                   active_elements=int(np.prod(sv)), flags=["surrogate=disabled"])
+        return [(ip, ix, d) for d in data], rep
+    lat = [lattice_indices(pp, m, M) for m in mp]
+    core, smp = [], []
+    for d, m in enumerate(mp):
+        lo, hi = box_range(pp, m)
+        a = np.zeros(m, bool)
+        if lo + 1 <= hi - 1:
+            a[lo + 1:hi] = True
+        sm_ = np.zeros(m, bool)
+        sm_[lat[d]] = True
+        core.append(a)
+        smp.append(sm_)
+
+    def flat(masks):
+        acc = np.ones(1, bool)
+        for mk in masks[::-1]:
+            acc = (acc[:, None] & mk[None, :]).ravel()
+        return acc
+
+    core_flat, samp_flat = flat(core), flat(smp)
+    quad_rows = np.flatnonzero(~core_flat | samp_flat)
+    interp_rows = np.flatnonzero(core_flat & ~samp_flat)
+    ipq, ixq, dq, _ = divergence(vel, pp, rows=quad_rows)
+    active = div_elements_for_rows(mp, pp, sv, quad_rows).size
+    H = M * h0
+    nI = interp_rows.size
+    if nI == 0:
+        rep = dict(N=Np, p=pp, q=q, M=M, H=H, quad_entries=ixq.size * n, interp_entries=0, quad_fraction=1.0,
+                   active_elements=int(active), flags=[])
+        return [(ipq, ixq, d) for d in dq], rep
+    rng = np.arange(-2 * pp, pp + 3)
+    k = rng.size
+    offs = np.stack([rng[g] for g in np.unravel_index(np.arange(k ** n), (k,) * n, order="F")], -1)
+    P = offs.shape[0]
+    pstr = np.cumprod((1,) + mp[:-1])
+    vstr = np.cumprod((1,) + tuple(mv[:-1]))
+    lat_grid = np.stack([g.ravel(order="F") for g in np.meshgrid(*lat, indexing="ij")], -1)
+    lat_rows = lat_grid @ pstr
+    assert np.all(np.diff(ipq)[lat_rows] == P)
+    lat_shape = tuple(x.size for x in lat)
+    flags = []
+    qd, kn, Es = [], [], []
+    box_n = []
+    for d in range(n):
+        sites = midpoints(pp, mp[d], lat[d])
+        qq = min(q, sites.size - 1)
+        if qq < q and "interpolation-order-lowered" not in flags:
+            flags.append("interpolation-order-lowered")
+        qd.append(qq)
+        kn.append(averaging_knots(sites, qq) if qq >= 1 else None)
+        lo, hi = box_range(pp, mp[d])
+        pts = midpoints(pp, mp[d], np.arange(lo, hi + 1))
+        box_n.append(pts.size)
+        Es.append(np.ones((pts.size, 1)) if kn[d] is None else collocation_matrix(kn[d], qq, pts))
+    box_str = np.cumprod((1,) + tuple(box_n[:-1]))
+    Im = np.stack(np.unravel_index(interp_rows, mp, order="F"), -1)
+    Ib = (Im - 2 * pp) @ box_str
+    indptr, indices = div_pattern(mp, mv, pp)
+    rowid = np.repeat(np.arange(Np), np.diff(indptr))
+    isq = np.zeros(Np, dtype=bool)
+    isq[quad_rows] = True
+    out = []
+    for c in range(n):
+        coef = dq[c][ipq[lat_rows][:, None] + np.arange(P)[None, :]].T.reshape((P,) + lat_shape, order="F")
+        for d in range(n):
+            if qd[d] >= 1:
+                sites = midpoints(pp, mp[d], lat[d])
+                C = collocation_matrix(kn[d], qd[d], sites)
+                moved = np.moveaxis(coef, 1 + d, 0)
+                coef = np.moveaxis(solve(C, moved.reshape(sites.size, -1)).reshape(moved.shape), 0, 1 + d)
+        V = coef
+        for d in range(n):
+            V = np.moveaxis(np.tensordot(Es[d], np.moveaxis(V, 1 + d, 0), axes=(1, 0)), 0, 1 + d)
+        VF = V.reshape(P, -1, order="F")
+        data = np.zeros(indices.size)
+        data[isq[rowid]] = dq[c]
+        data[indptr[interp_rows][:, None] + np.arange(P)[None, :]] = VF[:, Ib].T
+        ip_c, ix_c = indptr, indices
+        nz = data != 0.0                       # scipy CSR add drops exact zeros (surrogate.py:810)
+        if not np.all(nz):
+            cnt = np.add.reduceat(nz.astype(np.int64), indptr[:-1]) * (np.diff(indptr) > 0)
+            ip_c = np.zeros_like(indptr)
+            np.cumsum(cnt, out=ip_c[1:])
+            ix_c, data = indices[nz], data[nz]
+        out.append((ip_c, ix_c, data))
+    quad_entries = int(ixq.size * n)
+    n_interp = int(nI * P * n)
+    rep = dict(N=Np, p=pp, q=q, M=M, H=H, quad_entries=quad_entries, interp_entries=n_interp,
+               quad_fraction=quad_entries / (quad_entries + n_interp), active_elements=int(active), flags=flags)
+    return out, rep
+
+
 # ---------------------------------------------------------------------------
 # comparisons
 # ---------------------------------------------------------------------------

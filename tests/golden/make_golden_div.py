@@ -14,6 +14,7 @@ import numpy as np
 import scipy
 
 from surriga.assembly import assemble_divergence, stokes_subgrid_spaces
+from surriga.surrogate import ConstantSampling, build_surrogate_divergence
 
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from make_golden import geo  # noqa: E402
@@ -29,6 +30,11 @@ CASES = [
     ("div_tri3d_p1", "trivariate_polynomial_3d", 1, (2, 3, 2), {}),
     ("div_twisted_p2", "twisted_cube_p3_m12.geo", 2, (3, 3, 3), {}),
     ("div_twisted_p2_rows", "twisted_cube_p3_m12.geo", 2, (3, 4, 3), {"rows": [0, 11, 30, 74, 149]}),
+    ("sdiv_coons_quad_p2", "coons_quadratic", 2, (20, 22), {"M": 4}),
+    ("sdiv_coons_quad_p1_lowered", "coons_quadratic", 1, (12, 12), {"M": 5}),
+    ("sdiv_unit_square_p1", "unit_square", 1, (14, 12), {"M": 3}),
+    ("sdiv_twisted_p1", "twisted_cube_p3_m12.geo", 1, (9, 10, 9), {"M": 3}),
+    ("sdiv_coons_quad_disabled", "coons_quadratic", 2, (7, 7), {"M": 2}),
 ]
 
 
@@ -36,13 +42,22 @@ def run_case(case, gname, pp, spans, extra):
     g = geo(gname)
     st = stokes_subgrid_spaces(g, pp, spans, gauss=extra.get("gauss"))
     rows = extra.get("rows")
-    D = assemble_divergence(st, rows=None if rows is None else np.asarray(rows))
     meta = dict(case=case, geometry=gname, pp=pp, spans=list(spans), gauss=st.velocity.gauss, geo_p=g.space.p,
                 geo_ms=[kv.m for kv in g.space.kvs], n=st.n, numpy=np.__version__, scipy=scipy.__version__)
+    if "M" in extra:
+        D, rep = build_surrogate_divergence(st, ConstantSampling(extra["M"]), q=extra.get("q", 3))
+        meta.update(kind="surrogate", M=extra["M"], q=extra.get("q", 3),
+                    report={k: getattr(rep, k) for k in ("N", "p", "q", "M", "H", "quad_entries", "interp_entries",
+                                                         "quad_fraction", "active_elements", "flags")})
+    else:
+        D = assemble_divergence(st, rows=None if rows is None else np.asarray(rows))
+        meta.update(kind="full" if rows is None else "rows")
     arrays = dict(geo_w=g.weights.weights, geo_ctrl=g.control, vel_w=st.velocity.weights.weights,
-                  prs_w=st.pressure.weights.weights, indptr=D[0].mat.indptr, indices=D[0].mat.indices)
+                  prs_w=st.pressure.weights.weights)
     for c, Dc in enumerate(D):
-        assert np.array_equal(Dc.mat.indptr, D[0].mat.indptr) and np.array_equal(Dc.mat.indices, D[0].mat.indices)
+        # surrogate components may differ in pattern (exact zeros dropped by the CSR add)
+        arrays[f"indptr_{c}"] = Dc.mat.indptr
+        arrays[f"indices_{c}"] = Dc.mat.indices
         arrays[f"data_{c}"] = Dc.mat.data
     if rows is not None:
         arrays["rows"] = np.asarray(rows)

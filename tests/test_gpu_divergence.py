@@ -4,7 +4,7 @@ import numpy as np
 import pytest
 
 from oracle import surriga_oracle as O
-from test_oracle_divergence import div_cases, load_div, vel_problem
+from test_oracle_divergence import check_component, div_cases, load_div, vel_problem
 
 TOL = 1e-12
 
@@ -23,7 +23,7 @@ def stokes_from_golden(meta, arr):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", div_cases())
+@pytest.mark.parametrize("case", [c for c in div_cases() if not c.startswith("sdiv_")])
 def test_gpu_divergence_matches_reference_golden(case):
     import paper_1904_06971_b200 as pkg
 
@@ -35,10 +35,7 @@ def test_gpu_divergence_matches_reference_golden(case):
     for c, Dc in enumerate(D):
         m = Dc.mat
         assert m.indptr.dtype == np.int32 and m.indices.dtype == np.int32 and m.data.dtype == np.float64
-        assert np.array_equal(m.indptr, arr["indptr"]), "indptr differs"
-        assert np.array_equal(m.indices, arr["indices"]), "indices differ"
-        err = O.row_scaled_error(arr["indptr"], arr["indices"], arr[f"data_{c}"], m.indptr, m.indices, m.data)
-        assert err <= TOL, (c, err)
+        check_component(arr, c, m.indptr.astype(np.int64), m.indices, m.data)
         assert Dc.symmetric is False
         if rows is not None:
             assert np.array_equal(Dc.populated_rows, arr["populated_rows"])

@@ -33,18 +33,32 @@ def vel_problem(meta, arr):
                      geo_ctrl=arr["geo_ctrl"])
 
 
-@pytest.mark.parametrize("case", div_cases())
+def check_component(arr, c, ip, ix, d):
+    assert np.array_equal(ip, arr[f"indptr_{c}"].astype(np.int64)), f"indptr differs (component {c})"
+    assert np.array_equal(ix, arr[f"indices_{c}"]), f"indices differ (component {c})"
+    err = O.row_scaled_error(arr[f"indptr_{c}"], arr[f"indices_{c}"], arr[f"data_{c}"], ip, ix, d)
+    assert err <= TOL, (c, err)
+
+
+@pytest.mark.parametrize("case", [c for c in div_cases() if not c.startswith("sdiv_")])
 def test_oracle_divergence_matches_reference(case):
     meta, arr = load_div(case)
     vel = vel_problem(meta, arr)
     ip, ix, data, pop = O.divergence(vel, meta["pp"], rows=arr.get("rows"))
-    assert np.array_equal(ip, arr["indptr"].astype(np.int64))
-    assert np.array_equal(ix, arr["indices"])
     if "rows" in arr:
         assert np.array_equal(pop, arr["populated_rows"])
     for c in range(meta["n"]):
-        err = O.row_scaled_error(arr["indptr"], arr["indices"], arr[f"data_{c}"], ip, ix, data[c])
-        assert err <= TOL, (c, err)
+        check_component(arr, c, ip, ix, data[c])
+
+
+@pytest.mark.parametrize("case", [c for c in div_cases() if c.startswith("sdiv_")])
+def test_oracle_surrogate_divergence_matches_reference(case):
+    meta, arr = load_div(case)
+    mats, rep = O.surrogate_divergence(vel_problem(meta, arr), meta["pp"], meta["M"], meta["q"])
+    for k, v in meta["report"].items():
+        assert rep[k] == v, (k, rep[k], v)
+    for c, (ip, ix, d) in enumerate(mats):
+        check_component(arr, c, ip, ix, d)
 
 
 def test_oracle_divergence_constant_field_vanishes():
