@@ -107,6 +107,14 @@ int sg_result_copy_i64(const sg_result* r, int64_t* indptr, int32_t* indices, do
    `rows=` (bitwise equal to the full assembly).  Non-rational spaces only; no row slabs. */
 int sg_assemble_divergence(const sg_problem* velocity, const sg_problem* pressure, const int64_t* rows, int64_t nrows,
                            const sg_exec* exec, sg_result** out);
+/* Surrogate divergence pairing, general mode (replaces surriga/surrogate.py:702-819 `build_surrogate_divergence`):
+   `params` as for sg_surrogate over the pressure space (lattice, per-direction degree, averaged knots, inverse
+   collocation matrices, in-box midpoints); `shifts` the P mixed offsets [-2pp, pp+2]^n (colex, n ints each);
+   `quad_rows` the host-classified quadrature rows (not in the one-index-shrunk box, or on the lattice).  Quadrature
+   rows by quadrature, the others interpolated per offset; exact zeros dropped per component. */
+int sg_surrogate_divergence(const sg_problem* velocity, const sg_problem* pressure, const sg_surrogate_params* params,
+                            const int32_t* shifts, const int64_t* quad_rows, int64_t nquad, const sg_exec* exec,
+                            sg_result** out, sg_surrogate_stats* stats);
 /* Optional: allocate the calling thread's pinned D2H staging ring and host copy pool for `device` up
    front (otherwise done by the first large sg_result_copy*; not part of the reference interface). */
 int sg_host_staging_init(int device);

@@ -47,6 +47,7 @@ try:  # surrogate host layer (added with its kernels)
         ConstantSampling,
         MeshDependentSampling,
         SurrogateMode,
+        build_surrogate_divergence,
         build_surrogate_matrix,
         surrogate_plan,
     )

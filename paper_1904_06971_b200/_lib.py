@@ -74,6 +74,9 @@ def lib():
         L.sg_host_staging_init.argtypes = [C.c_int]
         L.sg_assemble_divergence.argtypes = [C.POINTER(SgProblem), C.POINTER(SgProblem), _i64, C.c_int64,
                                              C.POINTER(SgExec), C.POINTER(C.c_void_p)]
+        L.sg_surrogate_divergence.argtypes = [C.POINTER(SgProblem), C.POINTER(SgProblem), C.POINTER(SgSurrogateParams),
+                                              C.POINTER(C.c_int32), _i64, C.c_int64, C.POINTER(SgExec),
+                                              C.POINTER(C.c_void_p), C.POINTER(SgSurrogateStats)]
         L.sg_result_device_ptrs.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]
         L.sg_result_checksum.argtypes = [C.c_void_p, _d]
         L.sg_result_free.argtypes = [C.c_void_p]
@@ -86,7 +89,7 @@ def lib():
 SYMBOLS = ("sg_assemble", "sg_surrogate", "sg_result_sizes", "sg_result_copy", "sg_result_copy_i64",
            "sg_result_device_ptrs", "sg_result_checksum", "sg_result_free", "sg_last_timing",
            "sg_last_kernel_times", "sg_last_error", "sg_version", "sg_max_degree", "sg_host_staging_init",
-           "sg_assemble_divergence")
+           "sg_assemble_divergence", "sg_surrogate_divergence")
 
 
 def check(rc):

@@ -40,6 +40,7 @@ struct DivParams {
     const int* eslot;              // element id -> slot (-1: not computed); nullptr = identity
     double* eloc;                  // [slot][c][Lp][Lv]
     const uint8_t* rowmask;        // pressure rows to assemble (nullptr = all)
+    const uint8_t* countmask;      // rows present in the CSR pattern (nullptr = all)
     const int64_t* rowstart;
     int* indices[3];
     double* data[3];
@@ -208,7 +209,7 @@ template <int NDIM>
 __global__ void div_counts_kernel(DivParams s, int64_t* counts) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r > s.Np) return;
-    if (r == s.Np || (s.rowmask && !s.rowmask[r])) {
+    if (r == s.Np || (s.countmask && !s.countmask[r])) {
         counts[r] = 0;
         return;
     }
@@ -306,36 +307,155 @@ static int run_divergence(Call& c, DivParams& s, int64_t npts, size_t local_smem
     return 0;
 }
 
-}  // namespace sg
 
-using namespace sg;
+// ---- surrogate pieces (surrogate.py:702-819): samples, coefficient solve, interpolant evaluation
+__global__ void div_samples_kernel(const int64_t* __restrict__ rowstart, const double* __restrict__ data,
+                                   const int64_t* __restrict__ latrows, int64_t nlat, int P, double* __restrict__ S) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nlat * P) return;
+    const int64_t t = k / P;
+    const int o = (int)(k % P);
+    S[(int64_t)o * nlat + t] = data[rowstart[latrows[t]] + o];
+}
 
-extern "C" int sg_assemble_divergence(const sg_problem* vel, const sg_problem* prs, const int64_t* rows, int64_t nrows,
-                                      const sg_exec* ex, sg_result** out) {
-    if (!out) return fail(-1, "null output handles");
-    if (!vel || !prs) return fail(-1, "null problem");
+// out[a][s][b] = sum_t Cinv[s][t] in[a][t][b]  (one direction of the tensor collocation solve)
+__global__ void div_apply_dir_kernel(const double* __restrict__ in, double* __restrict__ out, const double* __restrict__ Cinv,
+                                     int64_t outer, int len, int64_t inner) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= outer * len * inner) return;
+    const int64_t a = k / (len * inner), rem = k % (len * inner);
+    const int sidx = (int)(rem / inner);
+    const int64_t b = rem % inner;
+    double acc = 0.0;
+    for (int t = 0; t < len; ++t) acc = fma(Cinv[(int64_t)sidx * len + t], in[(a * len + t) * inner + b], acc);
+    out[k] = acc;
+}
+
+struct DivInterp {
+    int n, P, pp;
+    int mp[3], mv[3], blo[3], nl[3], qd[3];
+    const uint8_t* core[3];        // pressure index in the shrunk box (one index of margin)
+    const uint8_t* smp[3];         // pressure index on the lattice
+    const int* esp[3];             // interpolant spans at the box points
+    const double* etab[3];         // interpolant basis values at the box points [nbox][qd+1]
+    const double* coef[3];         // per component [P][nl2][nl1][nl0]
+    const int* shifts;             // [P][3] mixed offsets
+    const int64_t* rowstart;
+    int* indices[3];
+    double* data[3];
+    int64_t Np;
+    unsigned long long* counters;  // 0 interp rows, 1 zeros
+};
+
+// one warp per interpolated pressure row, lanes on offsets: the row's P columns 2 i + shift(o)
+template <int NDIM>
+__global__ void div_interp_kernel(DivInterp s) {
+    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= s.Np) return;
+    int i[3] = {0, 0, 0};
+    int64_t rem = r;
+    bool core = true, samp = true;
+    for (int d = 0; d < NDIM; ++d) {
+        i[d] = (int)(rem % s.mp[d]);
+        rem /= s.mp[d];
+        core = core && s.core[d][i[d]];
+        samp = samp && s.smp[d][i[d]];
+    }
+    if (!core || samp) return;
+    if (lane == 0) atomicAdd(&s.counters[0], 1ull);
+    const double* e[3];
+    int lo[3] = {0, 0, 0}, q[3] = {0, 0, 0};
+    for (int d = 0; d < 3; ++d) {
+        if (d < NDIM) {
+            const int b = i[d] - s.blo[d];
+            q[d] = s.qd[d];
+            e[d] = s.etab[d] + (int64_t)b * (q[d] + 1);
+            lo[d] = s.esp[d][b] - q[d];
+        } else {
+            e[d] = nullptr;
+        }
+    }
+    const int64_t base = s.rowstart[r];
+    unsigned long long zeros = 0;
+    for (int o = lane; o < s.P; o += 32) {
+        int j[3] = {0, 0, 0};
+        for (int d = 0; d < NDIM; ++d) j[d] = 2 * i[d] + s.shifts[o * 3 + d];
+        const int64_t col = (int64_t)j[0] + (int64_t)s.mv[0] * ((int64_t)j[1] + (int64_t)s.mv[1] * j[2]);
+        for (int c = 0; c < NDIM; ++c) {
+            const double* cf = s.coef[c] + (int64_t)o * s.nl[0] * s.nl[1] * s.nl[2];
+            double v = 0.0;
+            for (int r2 = 0; r2 <= (NDIM >= 3 ? q[2] : 0); ++r2) {
+                const double w2 = NDIM >= 3 ? e[2][r2] : 1.0;
+                const int64_t c2 = NDIM >= 3 ? (int64_t)(lo[2] + r2) * s.nl[1] * s.nl[0] : 0;
+                double v1 = 0.0;
+                for (int r1 = 0; r1 <= (NDIM >= 2 ? q[1] : 0); ++r1) {
+                    const double w1 = NDIM >= 2 ? e[1][r1] : 1.0;
+                    const double* row = cf + c2 + (NDIM >= 2 ? (int64_t)(lo[1] + r1) * s.nl[0] : 0) + lo[0];
+                    double v0 = 0.0;
+                    for (int r0 = 0; r0 <= q[0]; ++r0) v0 = fma(e[0][r0], row[r0], v0);
+                    v1 = fma(w1, v0, v1);
+                }
+                v = fma(w2, v1, v);
+            }
+            s.data[c][base + o] = v;
+            s.indices[c][base + o] = (int)col;
+            zeros += (v == 0.0);
+        }
+    }
+    if (zeros) atomicAdd(&s.counters[1], zeros);
+}
+
+__global__ void div_nz_count_kernel(const int64_t* __restrict__ rowstart, const double* __restrict__ data, int64_t N,
+                                    int64_t* __restrict__ cnt) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > N) return;
+    if (i == N) {
+        cnt[i] = 0;
+        return;
+    }
+    int64_t c = 0;
+    for (int64_t k = rowstart[i]; k < rowstart[i + 1]; ++k) c += (data[k] != 0.0);
+    cnt[i] = c;
+}
+
+__global__ void div_compact_kernel(const int64_t* __restrict__ rowstart, const double* __restrict__ data,
+                                   const int* __restrict__ indices, int64_t N, const int64_t* __restrict__ newptr,
+                                   double* __restrict__ ndata, int* __restrict__ nind) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    int64_t w = newptr[i];
+    for (int64_t k = rowstart[i]; k < rowstart[i + 1]; ++k)
+        if (data[k] != 0.0) {
+            ndata[w] = data[k];
+            nind[w] = indices[k];
+            ++w;
+        }
+}
+
+// shared set-up of both entry points: validation, velocity tables + geometry, pressure tables
+static int div_setup(Call& c, const sg_problem* vel, const sg_problem* prs, DevProblem& dp, DivParams& s, int64_t& npts,
+                     int64_t& Ev) {
     const int n = vel->n;
-    for (int c = 0; c < n && c < 3; ++c) out[c] = nullptr;
     if (prs->n != n || n < 1 || n > 3) return fail(-1, "velocity/pressure dimension mismatch");
     if (vel->p != prs->p + 1) return fail(-1, "velocity degree must be the pressure degree + 1");
     for (int d = 0; d < n; ++d)
         if (vel->m[d] - vel->p != 2 * (prs->m[d] - prs->p))
             return fail(-1, "velocity mesh must halve every pressure element (subgrid pair)");
     if (vel->sol_w || prs->sol_w) return fail(-2, "rational (NURBS) Stokes spaces are not supported by the divergence kernels");
-    if (ex && (ex->slab_lo != 0 || ex->slab_hi != 0)) return fail(-2, "row slabs are not supported for the divergence pairing");
-    Call c(ex);
     sg_problem vp = *vel;
     vp.form = POISSON;  // velocity tables with first derivatives, geometry with first derivatives
-    DevProblem dp;
     int rc = prepare_problem(c, &vp, dp);
     if (rc) return rc;
-    DivParams s{};
+    s = DivParams{};
     s.n = n;
     s.pv = vel->p;
     s.pp = prs->p;
     s.pg = vel->geo_p;
     s.g = vel->g;
-    int64_t Np = 1, Ev = 1, npts = 1;
+    int64_t Np = 1;
+    Ev = 1;
+    npts = 1;
     for (int d = 0; d < 3; ++d) {
         if (d < n) {
             s.Sv[d] = dp.S[d];
@@ -368,12 +488,15 @@ extern "C" int sg_assemble_divergence(const sg_problem* vel, const sg_problem* p
         s.Pt[d] = tab;
     }
     s.Dg = (double*)c.alloc(sizeof(double) * npts * n * n, true);
-    // elements and rows
-    std::vector<int64_t> elist;
-    uint8_t* rowmask = nullptr;
+    return s.Dg ? 0 : fail(-4, "device allocation failed");
+}
+
+// elements supporting the listed pressure rows (assembly.py:347-360, ratio 2) + gather row mask
+static int div_elements(Call& c, DivParams& s, const int64_t* rows, int64_t nrows, int64_t Ev, std::vector<int64_t>& elist) {
+    const int n = s.n;
     if (rows) {
         for (int64_t k = 0; k < nrows; ++k) {
-            if (rows[k] < 0 || rows[k] >= Np) return fail(-1, "pressure row index out of range");
+            if (rows[k] < 0 || rows[k] >= s.Np) return fail(-1, "pressure row index out of range");
             if (k && rows[k] <= rows[k - 1]) return fail(-1, "rows must be sorted and unique");
         }
         std::vector<uint8_t> emask(Ev, 0);
@@ -388,8 +511,7 @@ extern "C" int sg_assemble_divergence(const sg_problem* vel, const sg_problem* p
             }
             for (int e2 = elo[2]; e2 <= ehi[2]; ++e2)
                 for (int e1 = elo[1]; e1 <= ehi[1]; ++e1)
-                    for (int e0 = elo[0]; e0 <= ehi[0]; ++e0)
-                        emask[e0 + (int64_t)s.Sv[0] * (e1 + (int64_t)s.Sv[1] * e2)] = 1;
+                    for (int e0 = elo[0]; e0 <= ehi[0]; ++e0) emask[e0 + (int64_t)s.Sv[0] * (e1 + (int64_t)s.Sv[1] * e2)] = 1;
         }
         std::vector<int> slot(Ev, -1);
         for (int64_t e = 0; e < Ev; ++e)
@@ -398,18 +520,19 @@ extern "C" int sg_assemble_divergence(const sg_problem* vel, const sg_problem* p
                 elist.push_back(e);
             }
         s.eslot = (const int*)c.upload(slot.data(), sizeof(int) * Ev);
-        rowmask = (uint8_t*)c.alloc(Np + 1, true);
-        cudaMemsetAsync(rowmask, 0, Np + 1, c.stream);
+        uint8_t* rowmask = (uint8_t*)c.alloc(s.Np + 1, true);
+        cudaMemsetAsync(rowmask, 0, s.Np + 1, c.stream);
         if (nrows > 0) {
             int64_t* dr = (int64_t*)c.upload(rows, sizeof(int64_t) * nrows);
             div_mask_kernel<<<(unsigned)((nrows + 255) / 256), 256, 0, c.stream>>>(dr, nrows, rowmask);
         }
+        s.rowmask = rowmask;
     } else {
         elist.resize(Ev);
         for (int64_t e = 0; e < Ev; ++e) elist[e] = e;
         s.eslot = nullptr;
+        s.rowmask = nullptr;
     }
-    s.rowmask = rowmask;
     s.nelem = (int64_t)elist.size();
     s.elems = s.nelem ? (const int64_t*)c.upload(elist.data(), sizeof(int64_t) * elist.size()) : nullptr;
     int64_t Lp = 1, Lv = 1;
@@ -420,65 +543,281 @@ extern "C" int sg_assemble_divergence(const sg_problem* vel, const sg_problem* p
     const double loc_bytes = (double)s.nelem * n * Lp * Lv * sizeof(double);
     if (loc_bytes > 32e9) return fail(-4, "divergence element matrices need %.1f GB of device memory", loc_bytes / 1e9);
     s.eloc = (double*)c.alloc(std::max<size_t>((size_t)loc_bytes, 8), true);
-    if (!s.eloc || !s.Dg) return fail(-4, "device allocation failed");
-    // row pointers
+    return s.eloc ? 0 : fail(-4, "device allocation failed");
+}
+
+static int div_rowstart(Call& c, DivParams& s, int64_t*& rowstart, int64_t& nnz) {
+    const int64_t Np = s.Np;
     int64_t* counts = (int64_t*)c.alloc(sizeof(int64_t) * (Np + 1), true);
-    int64_t* rowstart = (int64_t*)c.alloc(sizeof(int64_t) * (Np + 1), true);
+    rowstart = (int64_t*)c.alloc(sizeof(int64_t) * (Np + 1), true);
     c.kbegin("div_counts");
-    if (n == 1) div_counts_kernel<1><<<(unsigned)((Np + 256) / 256), 256, 0, c.stream>>>(s, counts);
-    if (n == 2) div_counts_kernel<2><<<(unsigned)((Np + 256) / 256), 256, 0, c.stream>>>(s, counts);
-    if (n == 3) div_counts_kernel<3><<<(unsigned)((Np + 256) / 256), 256, 0, c.stream>>>(s, counts);
+    if (s.n == 1) div_counts_kernel<1><<<(unsigned)((Np + 256) / 256), 256, 0, c.stream>>>(s, counts);
+    if (s.n == 2) div_counts_kernel<2><<<(unsigned)((Np + 256) / 256), 256, 0, c.stream>>>(s, counts);
+    if (s.n == 3) div_counts_kernel<3><<<(unsigned)((Np + 256) / 256), 256, 0, c.stream>>>(s, counts);
     c.kend();
     size_t tb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tb, counts, rowstart, Np + 1, c.stream);
     void* tmp = c.alloc(tb, true);
     cub::DeviceScan::ExclusiveSum(tmp, tb, counts, rowstart, Np + 1, c.stream);
-    int64_t nnz = 0;
+    nnz = 0;
     cudaMemcpyAsync(&nnz, rowstart + Np, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream);
     cudaStreamSynchronize(c.stream);
     s.rowstart = rowstart;
-    sg_result* res[3] = {nullptr, nullptr, nullptr};
-    for (int k = 0; k < n; ++k) {
-        sg_result* r = new sg_result();
-        r->dev = c.dev;
-        r->nrows = Np;
-        r->nrows_global = Np;
-        r->row_lo = 0;
-        r->nnz = nnz;
-        r->indptr = (int64_t*)c.alloc(sizeof(int64_t) * (Np + 1), false);
+    return 0;
+}
+
+static size_t div_local_smem(const DivParams& s) {
+    int Q = 1;
+    for (int d = 0; d < s.n; ++d) Q *= s.g;
+    return sizeof(double) * ((size_t)s.n * s.g * (s.pp + 1) + (size_t)s.n * s.g * 2 * (s.pv + 1) + (size_t)Q * s.n * s.n);
+}
+
+static int div_run(Call& c, DivParams& s, int64_t npts) {
+    const size_t local_smem = div_local_smem(s);
+    if (local_smem > 227 * 1024) return fail(-2, "divergence element tables do not fit shared memory");
+    if (s.n == 1) return run_divergence<1>(c, s, npts, local_smem);
+    if (s.n == 2) return run_divergence<2>(c, s, npts, local_smem);
+    return run_divergence<3>(c, s, npts, local_smem);
+}
+
+static sg_result* new_result(Call& c, int64_t Np, int64_t nnz, bool with_arrays) {
+    sg_result* r = new sg_result();
+    r->dev = c.dev;
+    r->nrows = Np;
+    r->nrows_global = Np;
+    r->row_lo = 0;
+    r->nnz = nnz;
+    r->indptr = (int64_t*)c.alloc(sizeof(int64_t) * (Np + 1), false);
+    if (with_arrays) {
         r->indices = (int*)c.alloc(sizeof(int) * std::max<int64_t>(nnz, 1), false);
         r->data = (double*)c.alloc(sizeof(double) * std::max<int64_t>(nnz, 1), false);
-        res[k] = r;
-        if (!r->indptr || !r->indices || !r->data) {
-            for (int q = 0; q <= k; ++q) sg_result_free(res[q]);
-            return fail(-4, "device allocation failed (nnz=%lld)", (long long)nnz);
-        }
-        cudaMemcpyAsync(r->indptr, rowstart, sizeof(int64_t) * (Np + 1), cudaMemcpyDeviceToDevice, c.stream);
-        s.indices[k] = r->indices;
-        s.data[k] = r->data;
     }
-    // local kernel shared memory: tables + the element's point tensors
-    int Q = 1;
-    for (int d = 0; d < n; ++d) Q *= s.g;
-    const size_t local_smem = sizeof(double) * ((size_t)n * s.g * (s.pp + 1) + (size_t)n * s.g * 2 * (s.pv + 1) + (size_t)Q * n * n);
-    if (local_smem > 227 * 1024) {
-        for (int q = 0; q < n; ++q) sg_result_free(res[q]);
-        return fail(-2, "divergence element tables do not fit shared memory");
-    }
-    if (n == 1) rc = run_divergence<1>(c, s, npts, local_smem);
-    if (n == 2) rc = run_divergence<2>(c, s, npts, local_smem);
-    if (n == 3) rc = run_divergence<3>(c, s, npts, local_smem);
-    if (!rc) rc = c.finish();
+    return r;
+}
+
+static int div_finish(Call& c, sg_result** res, int n, sg_result** out) {
+    int rc = c.finish();
     if (!rc) {
         cudaStreamSynchronize(c.stream);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) rc = fail(-3, "CUDA error in the divergence assembly: %s", cudaGetErrorString(e));
     }
     if (rc) {
-        for (int q = 0; q < n; ++q) sg_result_free(res[q]);
+        for (int q = 0; q < n; ++q)
+            if (res[q]) sg_result_free(res[q]);
         return rc;
     }
     c.record_timing();
     for (int k = 0; k < n; ++k) out[k] = res[k];
     return 0;
+}
+
+}  // namespace sg
+
+using namespace sg;
+
+extern "C" int sg_assemble_divergence(const sg_problem* vel, const sg_problem* prs, const int64_t* rows, int64_t nrows,
+                                      const sg_exec* ex, sg_result** out) {
+    if (!out) return fail(-1, "null output handles");
+    if (!vel || !prs) return fail(-1, "null problem");
+    for (int k = 0; k < 3 && k < vel->n; ++k) out[k] = nullptr;
+    if (ex && (ex->slab_lo != 0 || ex->slab_hi != 0)) return fail(-2, "row slabs are not supported for the divergence pairing");
+    Call c(ex);
+    DevProblem dp;
+    DivParams s;
+    int64_t npts = 0, Ev = 0;
+    int rc = div_setup(c, vel, prs, dp, s, npts, Ev);
+    if (rc) return rc;
+    std::vector<int64_t> elist;
+    if ((rc = div_elements(c, s, rows, nrows, Ev, elist))) return rc;
+    s.countmask = s.rowmask;  // restricted rows: only those rows are present
+    int64_t* rowstart = nullptr;
+    int64_t nnz = 0;
+    div_rowstart(c, s, rowstart, nnz);
+    const int n = s.n;
+    sg_result* res[3] = {nullptr, nullptr, nullptr};
+    for (int k = 0; k < n; ++k) {
+        res[k] = new_result(c, s.Np, nnz, true);
+        if (!res[k]->indptr || !res[k]->indices || !res[k]->data) {
+            for (int q = 0; q <= k; ++q) sg_result_free(res[q]);
+            return fail(-4, "device allocation failed (nnz=%lld)", (long long)nnz);
+        }
+        cudaMemcpyAsync(res[k]->indptr, rowstart, sizeof(int64_t) * (s.Np + 1), cudaMemcpyDeviceToDevice, c.stream);
+        s.indices[k] = res[k]->indices;
+        s.data[k] = res[k]->data;
+    }
+    rc = div_run(c, s, npts);
+    if (rc) {
+        for (int q = 0; q < n; ++q) sg_result_free(res[q]);
+        return rc;
+    }
+    return div_finish(c, res, n, out);
+}
+
+extern "C" int sg_surrogate_divergence(const sg_problem* vel, const sg_problem* prs, const sg_surrogate_params* sp,
+                                       const int32_t* shifts, const int64_t* quad_rows, int64_t nquad, const sg_exec* ex,
+                                       sg_result** out, sg_surrogate_stats* stats) {
+    if (!out || !vel || !prs || !sp || !shifts) return fail(-1, "null argument");
+    for (int k = 0; k < 3 && k < vel->n; ++k) out[k] = nullptr;
+    if (sp->mode != SG_GENERAL) return fail(-1, "the divergence pairing only supports the general mode");
+    if (ex && (ex->slab_lo != 0 || ex->slab_hi != 0)) return fail(-2, "row slabs are not supported for the divergence pairing");
+    Call c(ex);
+    DevProblem dp;
+    DivParams s;
+    int64_t npts = 0, Ev = 0;
+    int rc = div_setup(c, vel, prs, dp, s, npts, Ev);
+    if (rc) return rc;
+    const int n = s.n, pp = s.pp;
+    // quadrature rows by quadrature (elements supporting them); every row present in the pattern
+    std::vector<int64_t> elist;
+    if ((rc = div_elements(c, s, quad_rows, nquad, Ev, elist))) return rc;
+    s.countmask = nullptr;
+    int64_t* rowstart = nullptr;
+    int64_t nnz = 0;
+    div_rowstart(c, s, rowstart, nnz);
+    int* wind[3] = {nullptr, nullptr, nullptr};
+    double* wdat[3] = {nullptr, nullptr, nullptr};
+    for (int k = 0; k < n; ++k) {
+        wind[k] = (int*)c.alloc(sizeof(int) * std::max<int64_t>(nnz, 1), true);
+        wdat[k] = (double*)c.alloc(sizeof(double) * std::max<int64_t>(nnz, 1), true);
+        if (!wind[k] || !wdat[k]) return fail(-4, "device allocation failed (nnz=%lld)", (long long)nnz);
+        s.indices[k] = wind[k];
+        s.data[k] = wdat[k];
+    }
+    if ((rc = div_run(c, s, npts))) return rc;
+    // samples S[o][lattice colex] from the quadrature rows (surrogate.py:336-379), per component
+    int P = 1;
+    for (int d = 0; d < n; ++d) P *= 3 * pp + 3;
+    int64_t nlat = 1;
+    for (int d = 0; d < n; ++d) nlat *= sp->nlat[d];
+    std::vector<int64_t> latrows(nlat);
+    for (int64_t t = 0; t < nlat; ++t) {
+        int64_t rem = t, row = 0, str = 1;
+        for (int d = 0; d < n; ++d) {
+            const int a = (int)(rem % sp->nlat[d]);
+            rem /= sp->nlat[d];
+            row += sp->lat_idx[d][a] * str;
+            str *= s.mp[d];
+        }
+        latrows[t] = row;
+    }
+    const int64_t* dlat = (const int64_t*)c.upload(latrows.data(), sizeof(int64_t) * nlat);
+    DivInterp I{};
+    I.n = n;
+    I.P = P;
+    I.pp = pp;
+    I.Np = s.Np;
+    I.rowstart = rowstart;
+    for (int d = 0; d < 3; ++d) {
+        I.mp[d] = s.mp[d];
+        I.mv[d] = s.mv[d];
+        I.nl[d] = d < n ? sp->nlat[d] : 1;
+        I.qd[d] = d < n ? sp->qd[d] : 0;
+        I.blo[d] = 2 * pp;
+    }
+    const double* cinv[3];
+    for (int d = 0; d < n; ++d) cinv[d] = (const double*)c.upload(sp->colloc_inv[d], sizeof(double) * sp->nlat[d] * sp->nlat[d]);
+    for (int k = 0; k < n; ++k) {
+        double* S0 = (double*)c.alloc(sizeof(double) * P * nlat, true);
+        double* S1 = (double*)c.alloc(sizeof(double) * P * nlat, true);
+        c.kbegin("div_samples");
+        div_samples_kernel<<<(unsigned)((nlat * P + 255) / 256), 256, 0, c.stream>>>(rowstart, wdat[k], dlat, nlat, P, S0);
+        c.kend();
+        // coefficient solve per direction (surrogate.py:430-471): S[P][l2][l1][l0]
+        for (int d = 0; d < n; ++d) {
+            if (sp->qd[d] < 1) continue;
+            int64_t inner = 1, outer = P;
+            for (int e = 0; e < d; ++e) inner *= sp->nlat[e];
+            for (int e = d + 1; e < n; ++e) outer *= sp->nlat[e];
+            c.kbegin("div_coef_solve");
+            div_apply_dir_kernel<<<(unsigned)((P * nlat + 255) / 256), 256, 0, c.stream>>>(S0, S1, cinv[d], outer, sp->nlat[d], inner);
+            c.kend();
+            std::swap(S0, S1);
+        }
+        I.coef[k] = S0;
+        I.indices[k] = wind[k];
+        I.data[k] = wdat[k];
+    }
+    // interpolant tables at the box points, masks
+    for (int d = 0; d < n; ++d) {
+        const int nbox = s.mp[d] - 4 * pp;
+        int* esp = (int*)c.alloc(sizeof(int) * std::max(nbox, 1), true);
+        double* et = (double*)c.alloc(sizeof(double) * std::max(nbox, 1) * (sp->qd[d] + 1), true);
+        if (sp->qd[d] >= 1) {
+            double* kn = (double*)c.upload(sp->interp_knots[d], sizeof(double) * (sp->nlat[d] + sp->qd[d] + 1));
+            double* bp = (double*)c.upload(sp->box_pts[d], sizeof(double) * nbox);
+            tabulate(c, kn, sp->nlat[d] + sp->qd[d] + 1, sp->qd[d], bp, nbox, 0, esp, et);
+        } else {
+            std::vector<int> z(nbox, 0);
+            std::vector<double> one(nbox, 1.0);
+            cudaMemcpyAsync(esp, z.data(), sizeof(int) * nbox, cudaMemcpyHostToDevice, c.stream);
+            cudaMemcpyAsync(et, one.data(), sizeof(double) * nbox, cudaMemcpyHostToDevice, c.stream);
+            cudaStreamSynchronize(c.stream);
+        }
+        I.esp[d] = esp;
+        I.etab[d] = et;
+        std::vector<uint8_t> core(s.mp[d], 0), smp(s.mp[d], 0);
+        const int lo = 2 * pp, hi = s.mp[d] - 2 * pp - 1;
+        for (int i = lo + 1; i <= hi - 1; ++i) core[i] = 1;
+        for (int a = 0; a < sp->nlat[d]; ++a) smp[sp->lat_idx[d][a]] = 1;
+        I.core[d] = (const uint8_t*)c.upload(core.data(), s.mp[d]);
+        I.smp[d] = (const uint8_t*)c.upload(smp.data(), s.mp[d]);
+    }
+    std::vector<int> sh3((size_t)P * 3, 0);
+    for (int o = 0; o < P; ++o)
+        for (int d = 0; d < n; ++d) sh3[(size_t)o * 3 + d] = shifts[(size_t)o * n + d];
+    I.shifts = (const int*)c.upload(sh3.data(), sizeof(int) * P * 3);
+    unsigned long long* counters = (unsigned long long*)c.alloc(sizeof(unsigned long long) * 2, true);
+    cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * 2, c.stream);
+    I.counters = counters;
+    c.kbegin("div_interp");
+    const unsigned nb = (unsigned)((s.Np * 32 + 255) / 256);
+    if (n == 1) div_interp_kernel<1><<<nb, 256, 0, c.stream>>>(I);
+    if (n == 2) div_interp_kernel<2><<<nb, 256, 0, c.stream>>>(I);
+    if (n == 3) div_interp_kernel<3><<<nb, 256, 0, c.stream>>>(I);
+    c.kend();
+    unsigned long long hc[2] = {0, 0};
+    cudaMemcpyAsync(hc, counters, sizeof(hc), cudaMemcpyDeviceToHost, c.stream);
+    cudaStreamSynchronize(c.stream);
+    // merge: exact zeros dropped (scipy CSR add, surrogate.py:810), per component
+    sg_result* res[3] = {nullptr, nullptr, nullptr};
+    int64_t dropped = 0;
+    for (int k = 0; k < n; ++k) {
+        int64_t* cnt = (int64_t*)c.alloc(sizeof(int64_t) * (s.Np + 1), true);
+        c.kbegin("div_nz_count");
+        div_nz_count_kernel<<<(unsigned)((s.Np + 256) / 256), 256, 0, c.stream>>>(rowstart, wdat[k], s.Np, cnt);
+        c.kend();
+        sg_result* r = new_result(c, s.Np, 0, false);
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, r->indptr, s.Np + 1, c.stream);
+        void* tmp = c.alloc(tb, true);
+        cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, r->indptr, s.Np + 1, c.stream);
+        int64_t nz = 0;
+        cudaMemcpyAsync(&nz, r->indptr + s.Np, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream);
+        cudaStreamSynchronize(c.stream);
+        r->nnz = nz;
+        dropped += nnz - nz;
+        if (nz == nnz) {
+            c.release(wind[k]);
+            c.release(wdat[k]);
+            r->indices = wind[k];
+            r->data = wdat[k];
+        } else {
+            r->indices = (int*)c.alloc(sizeof(int) * std::max<int64_t>(nz, 1), false);
+            r->data = (double*)c.alloc(sizeof(double) * std::max<int64_t>(nz, 1), false);
+            c.kbegin("div_compact");
+            div_compact_kernel<<<(unsigned)((s.Np + 255) / 256), 256, 0, c.stream>>>(rowstart, wdat[k], wind[k], s.Np, r->indptr,
+                                                                                     r->data, r->indices);
+            c.kend();
+        }
+        res[k] = r;
+    }
+    if (stats) {
+        stats->n_interp_rows = (int64_t)hc[0];
+        stats->n_quad_rows = nquad;
+        stats->n_interp_entries = (int64_t)hc[0] * P * n;
+        stats->n_zero_dropped = dropped;
+        stats->n_reset_rows = 0;
+    }
+    return div_finish(c, res, n, out);
 }

@@ -19,10 +19,23 @@ import numpy as np
 import scipy.sparse as sp
 
 from . import _lib
-from .assembly import SparseMatrix, _elements_for_rows, _exec, _fname, assemble, form_is_symmetric, problem_arrays
+from .assembly import (
+    FormKind,
+    SparseMatrix,
+    _elements_for_rows,
+    _exec,
+    _fname,
+    _Keep as _AKeep,
+    assemble,
+    assemble_divergence,
+    form_is_symmetric,
+    problem_arrays,
+)
+from .spaces import make_open_uniform_knots
 from .spaces import collocation_matrix
 
 __all__ = [
+    "build_surrogate_divergence",
     "SurrogateMode", "DEFAULT_MODE", "OffsetSet", "build_offsets", "TildeDomain", "tilde_domain", "SamplingLattice",
     "build_sampling_lattice", "ConstantSampling", "MeshDependentSampling", "mesh_dependent_M", "AssemblyReport",
     "REPORT_CSV_HEADER", "build_surrogate_matrix", "surrogate_plan", "SurrogatePlan",
@@ -467,3 +480,121 @@ def surrogate_plan(disc, strategy=None, q: int = 3) -> SurrogatePlan:
                          quad_entries=int(total_entries - interp_entries), interp_entries=int(interp_entries),
                          active_elements=int(active), total_elements=total,
                          gauss_points_surrogate=int(active) * g ** n, gauss_points_full=total * g ** n)
+
+
+# ---------------------------------------------------------------------------------------
+# surrogate divergence pairing (surrogate.py:699-819)
+# ---------------------------------------------------------------------------------------
+
+def _div_elements_for_rows(mp, pp, sv, rows) -> int:
+    """Count of velocity elements supporting the pressure rows (assembly.py:347-360, ratio 2)."""
+    n = len(mp)
+    sp_ = tuple(m - pp for m in mp)
+    mask = np.zeros(tuple(sv), dtype=bool)
+    multi = np.stack(np.unravel_index(np.asarray(rows, dtype=np.int64), tuple(mp), order="F"), axis=-1)
+    lo = 2 * np.maximum(0, multi - pp)
+    hi = 2 * (np.minimum(np.asarray(sp_) - 1, multi) + 1)
+    for a, b in zip(lo, hi):
+        mask[tuple(slice(int(a[d]), int(b[d])) for d in range(n))] = True
+    return int(mask.sum())
+
+
+def build_surrogate_divergence(stokes, strategy=None, q: int = 3, mode=None):
+    """Surrogate assembly of the divergence pairing, one matrix per component (surrogate.py:702-819).
+
+    Only the general placement applies (the matrix is rectangular); a pressure row is interpolated
+    when it lies in the pressure box shrunk by one index and is not on the sampling lattice.
+    Returns ``(list of SparseMatrix, AssemblyReport)``.
+    """
+    mode = SurrogateMode.GENERAL if mode is None else mode
+    if getattr(mode, "value", mode) != "general":
+        raise ValueError("the divergence pairing only supports the general mode")
+    if strategy is None:
+        strategy = ConstantSampling(1)
+    t0 = time.perf_counter()
+    prs, vel = stokes.pressure, stokes.velocity
+    n = stokes.n
+    pp = int(prs.space.kvs[0].p)
+    mp = tuple(int(kv.m) for kv in prs.space.kvs)
+    sv = tuple(int(kv.m - kv.p) for kv in vel.space.kvs)
+    h = 1.0 / (mp[0] - pp)
+    tilde = tilde_domain(pp, mp)
+    M = mesh_dependent_M(strategy, h, pp, q)
+    Np = int(np.prod(mp))
+
+    if tilde.is_empty:
+        D = assemble_divergence(stokes)
+        dt = time.perf_counter() - t0
+        nnz = sum(Dc.nnz for Dc in D)
+        return D, AssemblyReport(N=Np, p=pp, q=q, M=M, H=M * h, quad_entries=nnz, interp_entries=0,
+                                 quad_fraction=1.0, active_elements=int(np.prod(sv)), assembly_seconds=dt,
+                                 flags=["surrogate=disabled"])
+    lattice = build_sampling_lattice(prs.space.kvs, M, tilde)
+    inb, smp = _masks(tilde, lattice)
+    core = []
+    for d in range(n):
+        lo, hi = tilde.index_range(d)
+        a = np.zeros(mp[d], dtype=bool)
+        if lo + 1 <= hi - 1:
+            a[lo + 1:hi] = True
+        core.append(a)
+    core_flat, samp_flat = _flat(core), _flat(smp)
+    quad_rows = np.flatnonzero(~core_flat | samp_flat)
+    nI = Np - quad_rows.size
+    active = _div_elements_for_rows(mp, pp, sv, quad_rows)
+    if nI == 0:
+        Dq = assemble_divergence(stokes, rows=quad_rows)
+        dt = time.perf_counter() - t0
+        nnz = sum(Dc.nnz for Dc in Dq)
+        return ([SparseMatrix(mat=Dc.mat, symmetric=False) for Dc in Dq],
+                AssemblyReport(N=Np, p=pp, q=q, M=M, H=lattice.H, quad_entries=nnz, interp_entries=0,
+                               quad_fraction=1.0, active_elements=active, assembly_seconds=dt, flags=[]))
+    # device call
+    vpr, vkeep, _, _ = problem_arrays(FormKind.POISSON, vel)
+    pkeep = _AKeep()
+    ppr = _lib.SgProblem()
+    ppr.n = n
+    ppr.p = pp
+    ppr.g = int(prs.gauss)
+    for d, kv in enumerate(prs.space.kvs):
+        ppr.m[d] = int(kv.m)
+        ppr.knots[d] = pkeep.ptr(make_open_uniform_knots(pp, int(kv.m)).knots)
+    pw = np.asarray(prs.weights.weights, dtype=float)
+    ppr.sol_w = None if bool(np.all(pw == pw[0])) else pkeep.ptr(pw)
+    spp, fkeep, lowered = _fit_params(prs, lattice, tilde, q, "general", M)
+    offs = build_offsets(pp, n, mixed=True)
+    shifts = np.ascontiguousarray(offs.shifts, dtype=np.int32)
+    qr = np.ascontiguousarray(quad_rows, dtype=np.int64)
+    hs = (C.c_void_p * 3)()
+    st = _lib.SgSurrogateStats()
+    ex = _exec(None, None, None)
+    _lib.check(_lib.lib().sg_surrogate_divergence(C.byref(vpr), C.byref(ppr), C.byref(spp),
+                                                  shifts.ctypes.data_as(C.POINTER(C.c_int32)),
+                                                  qr.ctypes.data_as(_lib._i64), qr.size, C.byref(ex), hs, C.byref(st)))
+    del vkeep, pkeep, fkeep
+    Nv = int(np.prod([kv.m for kv in vel.space.kvs]))
+    out = []
+    quad_entries = 0
+    for c in range(n):
+        r = _lib.Result(hs[c])
+        indptr, indices, data = r.to_host()
+        r.free()
+        mat = sp.csr_matrix((data, indices, indptr), shape=(Np, Nv))
+        mat.has_sorted_indices = True
+        out.append(SparseMatrix(mat=mat, symmetric=False))
+    # quadrature entries = the restricted assembly's pattern size per component (explicit zeros included)
+    quad_entries = n * int(_div_pattern_rows_nnz(mp, tuple(int(kv.m) for kv in vel.space.kvs), pp, quad_rows))
+    n_interp = int(st.n_interp_entries)
+    dt = time.perf_counter() - t0
+    flags = ["interpolation-order-lowered"] if lowered else []
+    rep = AssemblyReport(N=Np, p=pp, q=q, M=M, H=lattice.H, quad_entries=quad_entries, interp_entries=n_interp,
+                         quad_fraction=quad_entries / (quad_entries + n_interp), active_elements=int(active),
+                         assembly_seconds=dt, flags=flags)
+    return out, rep
+
+
+def _div_pattern_rows_nnz(mp, mv, pp, rows) -> int:
+    multi = np.stack(np.unravel_index(np.asarray(rows, dtype=np.int64), tuple(mp), order="F"), axis=-1)
+    lo = np.maximum(2 * multi - 2 * pp, 0)
+    hi = np.minimum(2 * multi + pp + 2, np.asarray(mv) - 1)
+    return int(np.prod(hi - lo + 1, axis=1).sum())
