@@ -23,6 +23,7 @@
 #ifndef SURRIGA_B200_H
 #define SURRIGA_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -118,6 +119,10 @@ int sg_surrogate_divergence(const sg_problem* velocity, const sg_problem* pressu
 /* Optional: allocate the calling thread's pinned D2H staging ring and host copy pool for `device` up
    front (otherwise done by the first large sg_result_copy*; not part of the reference interface). */
 int sg_host_staging_init(int device);
+/* Optional: pin / unpin a host range with the driver (cudaHostRegister); sg_result_copy* DMAs straight into
+   registered destinations.  Used by the Python layer for reused result buffers. */
+int sg_host_register(void* ptr, size_t bytes);
+int sg_host_unregister(void* ptr);
 /* Device pointers (for device-resident consumers and timing). */
 int sg_result_device_ptrs(const sg_result* r, void** indptr_i64, void** indices_i32, void** data_f64);
 /* Deterministic fp64 checksums {nnz, sum a, sum a^2, sum |a|, sum of row sums} of the rows in the result. */

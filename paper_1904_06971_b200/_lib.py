@@ -72,6 +72,8 @@ def lib():
         L.sg_result_copy.argtypes = [C.c_void_p, _i32, _i32, _d]
         L.sg_result_copy_i64.argtypes = [C.c_void_p, _i64, _i32, _d]
         L.sg_host_staging_init.argtypes = [C.c_int]
+        L.sg_host_register.argtypes = [C.c_void_p, C.c_size_t]
+        L.sg_host_unregister.argtypes = [C.c_void_p]
         L.sg_assemble_divergence.argtypes = [C.POINTER(SgProblem), C.POINTER(SgProblem), _i64, C.c_int64,
                                              C.POINTER(SgExec), C.POINTER(C.c_void_p)]
         L.sg_surrogate_divergence.argtypes = [C.POINTER(SgProblem), C.POINTER(SgProblem), C.POINTER(SgSurrogateParams),
@@ -89,7 +91,7 @@ def lib():
 SYMBOLS = ("sg_assemble", "sg_surrogate", "sg_result_sizes", "sg_result_copy", "sg_result_copy_i64",
            "sg_result_device_ptrs", "sg_result_checksum", "sg_result_free", "sg_last_timing",
            "sg_last_kernel_times", "sg_last_error", "sg_version", "sg_max_degree", "sg_host_staging_init",
-           "sg_assemble_divergence", "sg_surrogate_divergence")
+           "sg_assemble_divergence", "sg_surrogate_divergence", "sg_host_register", "sg_host_unregister")
 
 
 def check(rc):
@@ -109,9 +111,11 @@ class _HostPool:
 
     A result array is a view of a pooled base buffer; the base is reused once no view of it is alive
     (its reference count drops back to the pool's own), so repeated assemblies copy into memory whose
-    pages are already mapped instead of paying first-touch page faults on every D2H (~40 vs ~75 GB/s
-    host copy rate on the B200 host).  At most ``keep`` idle bases per dtype are retained.
-    SG_HOST_POOL=0 disables it (plain np.empty)."""
+    pages are already mapped instead of paying first-touch page faults on every D2H.  Bases that get
+    reused are registered with the driver (cudaHostRegister, ~13 GB/s, done by a background thread
+    after the base's first copy), after which the D2H runs straight into them at the PCIe rate
+    (57 GB/s) instead of through the staging ring (~36 GB/s, host-memory bound).  At most ``keep``
+    idle bases per dtype are retained.  SG_HOST_POOL=0 disables the pool (plain np.empty)."""
 
     MIN_BYTES = 64 << 20
 
@@ -120,10 +124,42 @@ class _HostPool:
         self.bases = {}
         self.lock = threading.Lock()
         self.enabled = os.environ.get("SG_HOST_POOL", "1") != "0"
+        self.registered = {}     # id(base) -> True once pinned
+        self.fresh = []          # bases created by the last take(): registered at the next take()
+        self.jobs = []
+        self.worker = None
 
     @staticmethod
     def _idle(b):
         return sys.getrefcount(b) <= 4  # pool list + caller loop variable + parameter + getrefcount argument
+
+    def _register_async(self, bases):
+        def run(items):
+            for b in items:
+                if check_quiet(lib().sg_host_register(C.c_void_p(b.ctypes.data), C.c_size_t(b.nbytes))):
+                    with self.lock:
+                        self.registered[id(b)] = True
+
+        t = threading.Thread(target=run, args=(list(bases),), daemon=True)
+        t.start()
+        self.jobs.append(t)
+
+    def sync(self):
+        """Wait for pending registrations (call outside timed regions)."""
+        for t in self.jobs:
+            t.join()
+        self.jobs = []
+
+    def _drop(self, lst, x):
+        if self.registered.pop(id(x), False):
+            lib().sg_host_unregister(C.c_void_p(x.ctypes.data))
+        lst.remove(x)
+
+    def begin(self):
+        """Start of a result copy: bases created by earlier copies are filled -> pin them now."""
+        if self.fresh:
+            fresh, self.fresh = self.fresh, []
+            self._register_async(fresh)
 
     def take(self, n, dtype):
         dtype = np.dtype(dtype)
@@ -139,11 +175,19 @@ class _HostPool:
             if best is None:
                 best = np.empty(n, dtype=dtype)
                 lst.append(best)
+                self.fresh.append(best)
             idle = [x for x in lst if x is not best and self._idle(x)]
             x = None
-            for x in sorted(idle, key=lambda a: a.size)[:max(0, len(idle) - self.keep)]:
-                lst.remove(x)
+            if len(idle) > self.keep:
+                self.sync()
+                for x in sorted(idle, key=lambda a: a.size)[:len(idle) - self.keep]:
+                    self._drop(lst, x)
+                x = None
             return best[:n]
+
+
+def check_quiet(rc):
+    return rc == 0
 
 
 _pool = _HostPool()
@@ -163,6 +207,7 @@ class Result:
     def to_host(self):
         """D2H copy -> (indptr, indices, data) with scipy's index dtype (int32 when it fits)."""
         nrows, nnz = self.sizes()
+        _pool.begin()
         indices = _pool.take(nnz, np.int32)
         data = _pool.take(nnz, np.float64)
         if nnz < 2**31 - 1:
@@ -198,6 +243,11 @@ class Result:
 def host_staging_init(device=0):
     """Allocate the pinned D2H staging ring + host copy pool now (else on the first large copy)."""
     check(lib().sg_host_staging_init(int(device)))
+
+
+def host_pool_sync():
+    """Finish pending registrations of reused host result buffers (call outside timed regions)."""
+    _pool.sync()
 
 
 def last_timing():

@@ -919,13 +919,15 @@ static CopyPool& copy_pool() {
     return pool;
 }
 
-constexpr int kRing = 4;
+constexpr int kRingMax = 16;
 struct Stager {
     int dev = -1;
     cudaStream_t st = nullptr;
-    char* buf[kRing] = {};
-    cudaEvent_t ev[kRing];
-    std::atomic<int> left[kRing];
+    char* buf[kRingMax] = {};
+    cudaEvent_t ev[kRingMax];
+    std::atomic<int> left[kRingMax];
+    int ring = 0;
+    size_t chunk = 0, piece = 0;
 };
 static thread_local Stager g_stage;
 
@@ -935,20 +937,27 @@ static void want_huge_pages(void* p, size_t n) {
     if (e > a) madvise((void*)a, e - a, MADV_HUGEPAGE);
 }
 
-constexpr size_t kChunk = 64u << 20;
+static size_t env_size(const char* name, size_t dflt) {
+    const char* v = getenv(name);
+    return v ? (size_t)atof(v) : dflt;
+}
 static int stager_init(int dev) {
     Stager& S = g_stage;
     if (S.dev != dev || !S.buf[0]) {
-        for (int k = 0; k < kRing; ++k)
-            if (S.buf[k]) cudaFreeHost(S.buf[k]);
-        for (int k = 0; k < kRing; ++k)
-            if (cudaHostAlloc((void**)&S.buf[k], kChunk, cudaHostAllocDefault) != cudaSuccess) {
+        for (int k = 0; k < kRingMax; ++k)
+            if (S.buf[k]) cudaFreeHost(S.buf[k]), S.buf[k] = nullptr;
+        // ring geometry (tunable for experiments; defaults measured on the B200 host)
+        S.chunk = env_size("SG_D2H_CHUNK_KB", 64 * 1024) << 10;
+        S.ring = (int)std::min<size_t>(kRingMax, std::max<size_t>(2, env_size("SG_D2H_RING", 4)));
+        S.piece = std::max<size_t>(64 << 10, env_size("SG_D2H_PIECE_KB", 4096) << 10);
+        for (int k = 0; k < S.ring; ++k)
+            if (cudaHostAlloc((void**)&S.buf[k], S.chunk, cudaHostAllocDefault) != cudaSuccess) {
                 S.buf[0] = nullptr;
                 return fail(-4, "pinned staging allocation failed");
             }
         if (!S.st) {
             cudaStreamCreateWithFlags(&S.st, cudaStreamNonBlocking);
-            for (int k = 0; k < kRing; ++k) cudaEventCreateWithFlags(&S.ev[k], cudaEventDisableTiming);
+            for (int k = 0; k < kRingMax; ++k) cudaEventCreateWithFlags(&S.ev[k], cudaEventDisableTiming);
         }
         S.dev = dev;
     }
@@ -962,9 +971,23 @@ static int d2h(void* dst, const void* src, size_t bytes, int dev) {
         if (cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) return fail(-3, "D2H copy failed");
         return 0;
     }
+    // destinations registered with the driver (reused host result buffers, _lib._HostPool): DMA
+    // straight into them, no staging copy
+    cudaPointerAttributes pa;
+    if (cudaPointerGetAttributes(&pa, dst) == cudaSuccess && pa.type == cudaMemoryTypeHost) {
+        cudaStream_t st = nullptr;
+        cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+        const cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st);
+        const cudaError_t e2 = cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
+        if (e != cudaSuccess || e2 != cudaSuccess) return fail(-3, "D2H copy failed");
+        return 0;
+    }
+    cudaGetLastError();  // clear a possible "invalid value" from the attribute query
     if (int rc = stager_init(dev)) return rc;
     Stager& S = g_stage;
-    const size_t chunk = kChunk, piece = 4u << 20;
+    const size_t chunk = S.chunk, piece = S.piece;
+    const int kRing = S.ring;
     want_huge_pages(dst, bytes);
     CopyPool& pool = copy_pool();
     const size_t nch = (bytes + chunk - 1) / chunk;
@@ -991,6 +1014,26 @@ static int d2h(void* dst, const void* src, size_t bytes, int dev) {
 }  // namespace sg
 
 extern "C" {
+
+int sg_host_register(void* ptr, size_t bytes) {
+    if (!ptr || !bytes) return 0;
+    const cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterDefault);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(-3, "cudaHostRegister failed: %s", cudaGetErrorString(e));
+    }
+    return 0;
+}
+
+int sg_host_unregister(void* ptr) {
+    if (!ptr) return 0;
+    const cudaError_t e = cudaHostUnregister(ptr);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(-3, "cudaHostUnregister failed: %s", cudaGetErrorString(e));
+    }
+    return 0;
+}
 
 int sg_host_staging_init(int device) {
     cudaSetDevice(device);

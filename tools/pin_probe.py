@@ -28,3 +28,11 @@ for huge in (False, True):
     t = time.time(); rt.cudaMemcpy(ctypes.c_void_p(a.ctypes.data), ctypes.c_void_p(d.data_ptr()), ctypes.c_size_t(n), 2); dt = time.time() - t
     print(f"  D2H into registered: {n / dt / 1e9:.1f} GB/s")
     t = time.time(); rt.cudaHostUnregister(ctypes.c_void_p(a.ctypes.data)); print(f"  unregister {1e3*(time.time()-t):.0f} ms")
+# pre-faulted buffer (pages already mapped): registration cost alone
+a = np.empty(n, dtype=np.uint8)
+a[::4096] = 1
+t = time.time(); rc = rt.cudaHostRegister(ctypes.c_void_p(a.ctypes.data), ctypes.c_size_t(n), 0); dt = time.time() - t
+print(f"cudaHostRegister pre-faulted 2 GiB: rc={rc} {n / dt / 1e9:.1f} GB/s ({dt*1e3:.0f} ms)")
+rt.cudaHostUnregister(ctypes.c_void_p(a.ctypes.data))
+t = time.time(); rc = rt.cudaHostRegister(ctypes.c_void_p(a.ctypes.data), ctypes.c_size_t(n), 0); dt = time.time() - t
+print(f"cudaHostRegister again (re-register) 2 GiB: rc={rc} {n / dt / 1e9:.1f} GB/s ({dt*1e3:.0f} ms)")
