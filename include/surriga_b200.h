@@ -116,6 +116,12 @@ int sg_assemble_divergence(const sg_problem* velocity, const sg_problem* pressur
 int sg_surrogate_divergence(const sg_problem* velocity, const sg_problem* pressure, const sg_surrogate_params* params,
                             const int32_t* shifts, const int64_t* quad_rows, int64_t nquad, const sg_exec* exec,
                             sg_result** out, sg_surrogate_stats* stats);
+/* Load vector (replaces surriga/assembly.py:728-759 `assemble_load(disc, f)`), split at the caller's callable f:
+   sg_map_points writes the physical quadrature points phi(x_q) element-major, shape (E, Q, n) with E colex elements
+   and Q colex points per element (the array the reference passes to f); sg_assemble_load takes f's values (E, Q)
+   and writes vec[N] = sum_e sum_q f det(J) w_q N_i (rational N_i for non-unit sol_w). */
+int sg_map_points(const sg_problem* problem, const sg_exec* exec, double* phi_out);
+int sg_assemble_load(const sg_problem* problem, const double* fvals, const sg_exec* exec, double* vec_out);
 /* Optional: allocate the calling thread's pinned D2H staging ring and host copy pool for `device` up
    front (otherwise done by the first large sg_result_copy*; not part of the reference interface). */
 int sg_host_staging_init(int device);

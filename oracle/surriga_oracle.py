@@ -524,6 +524,44 @@ def assemble(prob: Problem, rows=None, chunk=4096):
 
 
 # ---------------------------------------------------------------------------
+# load vector (assembly.py:728-759)
+# ---------------------------------------------------------------------------
+
+def load_vector(prob: Problem, f):
+    """vec_i = sum_e sum_q f(phi(x_q)) det J(x_q) w_q N_i(x_q), N rational when the weights are not unit.
+
+    ``f`` receives the physical points per element, shape (E, Q, n), and returns (E, Q).
+    """
+    n, p, g = prob.n, prob.p, prob.g
+    tabs, axes, pws = _dir_tables(prob, 0)
+    wq = pws[0]
+    for d in range(1, n):
+        wq = (pws[d][:, None] * wq[None, :]).ravel()
+    spans = prob.spans
+    geo = geometry_on_grid(prob, axes, 1)
+    phiE = _to_elements(geo["phi"], spans, g)
+    detE = _to_elements(geo["det"], spans, g)
+    fb = np.asarray(f(phiE), dtype=float)
+    if fb.shape != detE.shape:
+        raise ValueError("load callable returned a mismatched shape")
+    E = int(np.prod(spans))
+    et = np.stack(np.unravel_index(np.arange(E), spans, order="F"), axis=-1)
+    B = _local_tensor(tabs, et, (0,) * n, p, g)
+    L = (p + 1) ** n
+    Il = np.stack(np.unravel_index(np.arange(L), (p + 1,) * n, order="F"), axis=-1)
+    strides = np.cumprod((1,) + tuple(prob.ms[:-1]))
+    cols = ((et[:, None, :] + Il[None, :, :]) * strides).sum(-1)
+    if prob.rational:
+        Wf = field_on_grid(p, prob.ms, prob.sol_w[:, None], axes, 0)
+        W = _to_elements(Wf[(0,) * n][..., 0], spans, g)[..., None]
+        B = prob.sol_w[cols][:, None, :] * B / W
+    lv = np.einsum("eq,eql->el", fb * detE * wq[None, :], B)
+    vec = np.zeros(prob.N)
+    np.add.at(vec, cols.ravel(), lv.ravel())
+    return vec
+
+
+# ---------------------------------------------------------------------------
 # mixed divergence pairing (assembly.py:180-207, 654-725)
 # ---------------------------------------------------------------------------
 

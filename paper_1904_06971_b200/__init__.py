@@ -15,6 +15,7 @@ from .assembly import (  # noqa: F401
     assemble,
     assemble_divergence,
     assemble_divergence_device,
+    assemble_load,
     assemble_device,
     elements_for_rows,
     form_is_symmetric,

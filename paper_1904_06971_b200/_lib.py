@@ -73,6 +73,8 @@ def lib():
         L.sg_result_copy_i64.argtypes = [C.c_void_p, _i64, _i32, _d]
         L.sg_host_staging_init.argtypes = [C.c_int]
         L.sg_host_register.argtypes = [C.c_void_p, C.c_size_t]
+        L.sg_map_points.argtypes = [C.POINTER(SgProblem), C.POINTER(SgExec), _d]
+        L.sg_assemble_load.argtypes = [C.POINTER(SgProblem), _d, C.POINTER(SgExec), _d]
         L.sg_host_unregister.argtypes = [C.c_void_p]
         L.sg_assemble_divergence.argtypes = [C.POINTER(SgProblem), C.POINTER(SgProblem), _i64, C.c_int64,
                                              C.POINTER(SgExec), C.POINTER(C.c_void_p)]
@@ -91,7 +93,8 @@ def lib():
 SYMBOLS = ("sg_assemble", "sg_surrogate", "sg_result_sizes", "sg_result_copy", "sg_result_copy_i64",
            "sg_result_device_ptrs", "sg_result_checksum", "sg_result_free", "sg_last_timing",
            "sg_last_kernel_times", "sg_last_error", "sg_version", "sg_max_degree", "sg_host_staging_init",
-           "sg_assemble_divergence", "sg_surrogate_divergence", "sg_host_register", "sg_host_unregister")
+           "sg_assemble_divergence", "sg_surrogate_divergence", "sg_host_register", "sg_host_unregister",
+           "sg_map_points", "sg_assemble_load")
 
 
 def check(rc):

@@ -24,6 +24,7 @@ __all__ = [
     "FormKind", "Discretization", "SparseMatrix", "gauss_rule", "make_discretization", "assemble", "assemble_device",
     "elements_for_rows", "is_bitwise_symmetric", "matrices_bitwise_equal", "form_is_symmetric", "set_device",
     "problem_arrays", "StokesSpaces", "stokes_subgrid_spaces", "assemble_divergence", "assemble_divergence_device",
+    "assemble_load",
 ]
 
 
@@ -374,3 +375,32 @@ def assemble_divergence(stokes, rows=None) -> list:
         mat.has_sorted_indices = True
         out.append(SparseMatrix(mat=mat, symmetric=False, populated_rows=None if rows is None else rsel))
     return out
+
+
+# ---------------------------------------------------------------------------------------
+# load vector (assembly.py:728-759)
+# ---------------------------------------------------------------------------------------
+
+def assemble_load(disc, f, *, device=None, stream=None) -> np.ndarray:
+    """Load vector of a callable ``f`` of physical coordinates (assembly.py:728-759).
+
+    ``f`` receives the physical quadrature points per element, shape ``(E, Q, n)`` (elements and
+    in-element points colex, as the reference passes them) and must return ``(E, Q)``.  The points
+    come from the GPU (``sg_map_points``), ``f`` runs on the host, the quadrature sum runs on the GPU
+    (``sg_assemble_load``).
+    """
+    pr, keep, _, N = problem_arrays(FormKind.MASS, disc)
+    n = len(disc.space.kvs)
+    g = int(disc.gauss)
+    E = int(np.prod([kv.m - kv.p for kv in disc.space.kvs]))
+    Q = g ** n
+    ex = _exec(device, stream, None)
+    phi = np.empty((E, Q, n))
+    _lib.check(_lib.lib().sg_map_points(C.byref(pr), C.byref(ex), _lib.dptr(phi)))
+    fb = np.ascontiguousarray(np.asarray(f(phi), dtype=float))
+    if fb.shape != (E, Q):
+        raise ValueError("load callable returned a mismatched shape")
+    vec = np.empty(N)
+    _lib.check(_lib.lib().sg_assemble_load(C.byref(pr), _lib.dptr(fb), C.byref(ex), _lib.dptr(vec)))
+    del keep
+    return vec
