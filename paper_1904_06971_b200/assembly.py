@@ -9,7 +9,9 @@ element quadrature and CSR emission all run on the GPU.  Both the reference's ow
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import os
+import weakref
 from dataclasses import dataclass
 from enum import Enum
 
@@ -68,16 +70,50 @@ def gauss_rule(g: int) -> QuadratureRule:
     return QuadratureRule(g=g, nodes=x, weights=w)
 
 
+@functools.lru_cache(maxsize=64)
+def _axis_1d(p: int, m: int, g: int):
+    """One direction of assembly.py:108-117 (pure function of (p, m, g); read-only, cached)."""
+    rule = gauss_rule(g)
+    h = 1.0 / (m - p)
+    offs = (rule.nodes + 1.0) * (0.5 * h)
+    br = make_open_uniform_knots(p, m).span_breaks()[:-1]
+    ax = np.ascontiguousarray((br[:, None] + offs[None, :]).ravel())
+    pw = np.ascontiguousarray(rule.weights * (0.5 * h))
+    ax.flags.writeable = False
+    pw.flags.writeable = False
+    return ax, pw
+
+
+@functools.lru_cache(maxsize=64)
+def _knots_1d(p: int, m: int) -> np.ndarray:
+    kn = np.ascontiguousarray(make_open_uniform_knots(p, m).knots, dtype=np.float64)
+    kn.flags.writeable = False
+    return kn
+
+
+_UNIT = {}
+
+
+def _is_unit(w: np.ndarray) -> bool:
+    """weights.is_unit (all equal), remembered per weights array (the O(N) scan is ~1 ms at config 5)."""
+    hit = _UNIT.get(id(w))
+    if hit is not None and hit[0]() is w:
+        return hit[1]
+    r = bool(np.all(w == w[0]))
+    try:
+        _UNIT[id(w)] = (weakref.ref(w), r)
+    except TypeError:
+        pass
+    return r
+
+
 def _quad_axes(kvs, g: int):
     """assembly.py:108-117: points break_k + (x+1) h/2, weights w h/2."""
-    rule = gauss_rule(g)
     axes, pw = [], []
     for kv in kvs:
-        h = 1.0 / (kv.m - kv.p)
-        offs = (rule.nodes + 1.0) * (0.5 * h)
-        br = make_open_uniform_knots(kv.p, kv.m).span_breaks()[:-1]
-        axes.append(np.ascontiguousarray((br[:, None] + offs[None, :]).ravel()))
-        pw.append(np.ascontiguousarray(rule.weights * (0.5 * h)))
+        a, w = _axis_1d(int(kv.p), int(kv.m), int(g))
+        axes.append(a)
+        pw.append(w)
     return axes, pw
 
 
@@ -241,17 +277,17 @@ def problem_arrays(form, disc, coefficient: float = 1.0):
     pr.g = g
     for d, kv in enumerate(space.kvs):
         pr.m[d] = int(kv.m)
-        pr.knots[d] = keep.ptr(make_open_uniform_knots(p, int(kv.m)).knots)
+        pr.knots[d] = keep.ptr(_knots_1d(p, int(kv.m)))
         pr.qpts[d] = keep.ptr(axes[d])
         pr.qwts[d] = keep.ptr(pw[d])
     w = np.asarray(disc.weights.weights, dtype=float)
-    pr.sol_w = None if bool(np.all(w == w[0])) else keep.ptr(w)     # weights.is_unit (assembly.py:418)
+    pr.sol_w = None if _is_unit(w) else keep.ptr(w)     # weights.is_unit (assembly.py:418)
     gs = disc.geom.space
     pg = int(gs.kvs[0].p)
     pr.geo_p = pg
     for d, kv in enumerate(gs.kvs):
         pr.geo_m[d] = int(kv.m)
-        pr.geo_knots[d] = keep.ptr(make_open_uniform_knots(pg, int(kv.m)).knots)
+        pr.geo_knots[d] = keep.ptr(_knots_1d(pg, int(kv.m)))
     gw = np.asarray(disc.geom.weights.weights, dtype=float)
     hom = np.concatenate([np.asarray(disc.geom.control, float) * gw[:, None], gw[:, None]], axis=1)
     pr.geo_hom = keep.ptr(hom)

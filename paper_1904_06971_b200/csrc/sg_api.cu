@@ -364,6 +364,27 @@ static int choose_layout(const DevProblem& dp, int kmax, int nthreads, Layout& o
 // ------------------------------------------------------------------------------------------
 static void* get_geom_kernel(int n, int form, bool rat) { return kernel_ptr(n, form, rat, 2, 1, nullptr); }
 
+struct GeomMark {
+    int n, P, g, T[3], tg[3], S[3], BX, BY, nbx, nby;
+};
+// geometry blocks needed by a tile list: the element window [lo - P, lo + T - 1] of every tile
+__global__ void geom_mark_kernel(GeomMark m, const int* __restrict__ tiles, int64_t ntiles, uint8_t* __restrict__ mask) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ntiles) return;
+    const int t = tiles[i];
+    const int tc[3] = {t % m.tg[0], (t / m.tg[0]) % m.tg[1], t / (m.tg[0] * m.tg[1])};
+    int64_t plo[3] = {0, 0, 0}, phi[3] = {0, 0, 0};
+    for (int d = 0; d < m.n; ++d) {
+        const int64_t lo = (int64_t)tc[d] * m.T[d];
+        const int64_t e0 = max((int64_t)0, lo - m.P), e1 = min((int64_t)m.S[d] - 1, lo + m.T[d] - 1);
+        plo[d] = e0 * m.g;
+        phi[d] = (e1 + 1) * m.g - 1;
+    }
+    for (int64_t z = plo[2]; z <= phi[2]; ++z)
+        for (int64_t by = plo[1] / m.BY; by <= phi[1] / m.BY; ++by)
+            for (int64_t bx = plo[0] / m.BX; bx <= phi[0] / m.BX; ++bx) mask[bx + m.nbx * (by + m.nby * z)] = 1;
+}
+
 int compute_D(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* tiles) {
     const int n = dp.n, g = dp.g, P = dp.p, pg = dp.pr.geo_p;
     const Tables TT = make_tables(n, dp.pr.form, dp.rational);
@@ -440,32 +461,34 @@ int compute_D(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* t
     gp.D = (double*)c.alloc(sizeof(double) * npts * U, true);
     if (!gp.D) return fail(-4, "device allocation of the D tensor failed (%zu MB)", sizeof(double) * npts * U >> 20);
     dp.D = gp.D;
-    std::vector<int> blocks;
     if (tiles) {
-        std::vector<uint8_t> mark(nblk_all, 0);
-        for (int t : *tiles) {
-            int64_t lo[3], hi[3];
-            tile_box(pl, dp, t, lo, hi);
-            int64_t plo[3], phi[3];
-            for (int d = 0; d < 3; ++d) {
-                if (d >= n) { plo[d] = 0; phi[d] = 0; continue; }
-                const int64_t e0 = std::max<int64_t>(0, lo[d] - P), e1 = std::min<int64_t>(dp.S[d] - 1, lo[d] + pl.T[d] - 1);
-                plo[d] = e0 * g;
-                phi[d] = (e1 + 1) * g - 1;
-            }
-            for (int64_t z = plo[2]; z <= phi[2]; ++z)
-                for (int64_t by = plo[1] / gp.BY; by <= phi[1] / gp.BY; ++by)
-                    for (int64_t bx = plo[0] / gp.BX; bx <= phi[0] / gp.BX; ++bx) mark[bx + gp.nbx * (by + gp.nby * z)] = 1;
+        // blocks touched by the tiles' element windows, marked on the device (no host loop)
+        if (tiles->empty()) return 0;
+        const int* dt = (const int*)c.upload(tiles->data(), sizeof(int) * tiles->size());
+        uint8_t* mask = (uint8_t*)c.alloc(nblk_all, true);
+        cudaMemsetAsync(mask, 0, nblk_all, c.stream);
+        GeomMark gm;
+        gm.n = n;
+        gm.P = P;
+        gm.g = g;
+        for (int d = 0; d < 3; ++d) {
+            gm.T[d] = pl.T[d];
+            gm.tg[d] = pl.tgrid[d];
+            gm.S[d] = dp.S[d];
         }
-        for (int64_t k = 0; k < nblk_all; ++k)
-            if (mark[k]) blocks.push_back((int)k);
-        if (blocks.empty()) return 0;
-        gp.blocks = (const int*)c.upload(blocks.data(), sizeof(int) * blocks.size());
+        gm.BX = gp.BX;
+        gm.BY = gp.BY;
+        gm.nbx = gp.nbx;
+        gm.nby = gp.nby;
+        c.kbegin("geom_mark");
+        geom_mark_kernel<<<(unsigned)((tiles->size() + 127) / 128), 128, 0, c.stream>>>(gm, dt, (int64_t)tiles->size(), mask);
+        c.kend();
+        gp.blockmask = mask;
     }
     void* kfn = get_geom_kernel(n, dp.pr.form, dp.rational);
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     void* args[] = {&gp};
-    const int64_t nb = tiles ? (int64_t)blocks.size() : nblk_all;
+    const int64_t nb = nblk_all;
     c.kbegin("geom_D");
     cudaError_t e = cudaLaunchKernel(kfn, dim3((unsigned)nb), dim3(256), args, smem, c.stream);
     c.kend();

@@ -349,6 +349,7 @@ struct GeomParams {
     int BX, BY;              // points per block (x, y)
     int nbx, nby;            // blocks per plane
     const int* blocks;       // block ids (bx + nbx*(by + nby*z)) or nullptr = all
+    const uint8_t* blockmask; // restricted plans: blocks to compute (others exit), or nullptr
     int GN0, GN1, WN0, WN1;  // smem bounds of function ranges
     int off_G0, off_G1, off_gs0, off_gs1, off_B0, off_B1, off_ws0, off_ws1, off_Hz, off_Hy, off_Wz, off_Wy, off_misc;
     int U;
@@ -369,6 +370,7 @@ __global__ void __launch_bounds__(256) geom_D_kernel(const GeomParams prm) {
     const int NB = (NU + 1) * (p + 1), NBG = (NUG + 1) * (pg + 1);
     const int NBp = NB | 1, NBGp = NBG | 1;  // odd per-point strides: per-lane y tables conflict free
     const int blk = prm.blocks ? prm.blocks[blockIdx.x] : (int)blockIdx.x;
+    if (prm.blockmask && !prm.blockmask[blk]) return;
     const int bx = blk % prm.nbx, by = (blk / prm.nbx) % prm.nby, z = blk / (prm.nbx * prm.nby);
     const int x0 = bx * prm.BX, y0 = by * prm.BY;
     const int X = min(prm.BX, prm.Gp[0] - x0);
