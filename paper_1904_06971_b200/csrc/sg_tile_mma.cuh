@@ -136,7 +136,7 @@ __host__ __device__ constexpr int mma_warps(int ndim, int P, int form, bool rat)
 constexpr int kMmaT2 = 16;  // rows per CTA in z (3D)
 
 struct MmaGeom {
-    int NCP, T0, T1, G, W, MT, KS, KS3, XW, XWp, YW, NTY, DY, TY, NCOMBO, NMT, CH, NCH, TC, U, NG1, NG2, NU1, NB, NK1, NK2;
+    int NC1, NCP, T0, T1, G, W, MT, KS, KS3, XW, XWp, YW, NTY, DY, TY, NCOMBO, NMT, CH, NCH, TC, U, NG1, NG2, NU1, NB, NK1, NK2;
     int NTAB;
     long o_B0, o_B1, o_B2, o_A1, o_B2f, o_B3f, o_cmb, o_rb, o_tab, o_bar, o_D, o_D2, o_T1, o_T2, o_O, total;
 };
@@ -155,6 +155,13 @@ __host__ __device__ constexpr MmaGeom mma_geom(int ndim, int P, int form, bool r
     m.XWp = (m.XW + 3) & ~3;  // TMA: box bytes DY*XWp*8 stay a multiple of 128
     m.YW = ndim >= 2 ? (m.T1 + P) * m.G : 1;
     m.NTY = ndim >= 2 ? (m.YW + 7) / 8 : 1;
+    // phase-1 items may be split by y n-tile (NC1 > 1); measured slower for Poisson and mass (the
+    // A fragments are then reloaded per n-tile), so one item covers all n-tiles unless forced
+#ifdef SG_NC1_FORCE
+    m.NC1 = ndim >= 2 ? SG_NC1_FORCE : 1;
+#else
+    m.NC1 = 1;
+#endif
     m.DY = pad_dy(m.NTY * 8);
     m.TY = pad8_4(m.NTY * 8 > m.YW + 4 ? m.NTY * 8 : m.YW + 4);
     m.NCOMBO = T0 * m.T1 * m.W * m.W;
@@ -183,7 +190,7 @@ __host__ __device__ constexpr MmaGeom mma_geom(int ndim, int P, int form, bool r
         const int NW = 32;  // table sized for up to 32 warps (host and device layouts agree whatever the warp count)
         int nu2 = 0;
         for (int g = 0; g < (ndim >= 2 ? T.NG2 : 0); ++g) nu2 += T.g2n[g];
-        m.NTAB = 3 * (NW + 1) + m.NG1 * T0 + (ndim >= 2 ? T.NG2 * m.T1 * T0 : 0) + (ndim == 3 ? (P + 1) * m.NCH : 0) +
+        m.NTAB = 3 * (NW + 1) + m.NG1 * T0 * m.NC1 + (ndim >= 2 ? T.NG2 * m.T1 * T0 : 0) + (ndim == 3 ? (P + 1) * m.NCH : 0) +
                  (m.NG1 + 1) + m.NU1 + (T.NG2 + 1) + nu2 + T.NF;
     }
     m.o_rb = o; o += ndim == 3 ? (long)T0 * m.T1 * kMmaT2 + 1 : 0;                // CSR start of every tile row (int64, -1: not owned)
@@ -240,7 +247,7 @@ __host__ __device__ constexpr MmaTab mma_tab(int ndim, int P, int form, bool rat
     const MmaGeom M = mma_geom(ndim, P, form, rat, tc.T0, tc.T1);
     const int NW = mma_warps(ndim, P, form, rat);
     MmaTab S{};
-    const int n1 = M.NG1 * M.T0;
+    const int n1 = M.NG1 * M.T0 * M.NC1;
     const int n2 = ndim >= 2 ? T.NG2 * M.T1 * M.T0 : 0;
     const int n3 = ndim == 3 ? (P + 1) * M.NCH : 0;
     int w1[512] = {}, w2[512] = {}, w3[512] = {};
@@ -266,7 +273,7 @@ __host__ __device__ constexpr MmaTab mma_tab(int ndim, int P, int form, bool rat
         n = 0;
     };
     for (int k = 0; k < n1; ++k) {
-        cost[n] = T.g1n[k / M.T0] * M.KS * M.MT * M.NTY + 2;
+        cost[n] = T.g1n[k / (M.T0 * M.NC1)] * M.KS * M.MT * (M.NTY / M.NC1) + 2;
         kind[n] = 1; idx[n] = k; done[n] = false; ++n;
     }
     if (ndim != 3) {  // 2D: phase 2 after its own barrier
@@ -601,17 +608,18 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), 1) assembl
         const int qe = tab[TAB::S.o_off1 + warp + 1];
         for (int q = tab[TAB::S.o_off1 + warp]; q < qe; ++q) {
             const int k = tab[TAB::S.o_it1 + q];
-            const int Gc = k / T0, i0l = k - (k / T0) * T0;
-            double acc[MT][NTY][2];
+            constexpr int NC1 = M.NC1, NTI = NTY / NC1;
+            const int cc = k % NC1, Gc = k / (T0 * NC1), i0l = (k / NC1) % T0;
+            double acc[MT][NTI][2];
 #pragma unroll
             for (int a = 0; a < MT; ++a)
 #pragma unroll
-                for (int c = 0; c < NTY; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+                for (int c = 0; c < NTI; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
             const int ue = tab[TAB::S.o_u1b + Gc + 1];
             for (int unit = tab[TAB::S.o_u1b + Gc]; unit < ue; ++unit) {
                 const int ud = tab[TAB::S.o_u1ud + unit];
                 const double* af = A1f + ((i0l * M.NU1 + unit) * KS) * MT * 32 + lane;
-                const double* dpl = Ds + (ud * XWp) * DY + lr;
+                const double* dpl = Ds + (ud * XWp) * DY + lr + cc * NTI * 8;
 #pragma unroll
                 for (int kk = 0; kk < KS; ++kk) {
                     const int s = kk * 4 + lk;
@@ -621,7 +629,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), 1) assembl
 #pragma unroll
                     for (int a = 0; a < MT; ++a) afr[a] = af[(kk * MT + a) * 32];
 #pragma unroll
-                    for (int c = 0; c < NTY; ++c) {
+                    for (int c = 0; c < NTI; ++c) {
                         const double bf = drow[c * 8];
 #pragma unroll
                         for (int a = 0; a < MT; ++a) dmma(acc[a][c][0], acc[a][c][1], afr[a], bf);
@@ -653,8 +661,8 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), 1) assembl
 #pragma unroll
                 for (int a = 0; a < MT; ++a)
 #pragma unroll
-                    for (int c = 0; c < NTY; ++c) {
-                        double* dst = t1 + (a * 8 + lr) * TY + c * 8 + 2 * lk;
+                    for (int c = 0; c < NTI; ++c) {
+                        double* dst = t1 + (a * 8 + lr) * TY + (cc * NTI + c) * 8 + 2 * lk;
                         dst[0] = acc[a][c][0];
                         dst[1] = acc[a][c][1];
                     }
