@@ -313,6 +313,7 @@ def run_ours(args):
             dist.all_reduce(tt[0:1], op=dist.ReduceOp.MAX)
             dist.all_reduce(tt[1:2])
             t_e2e, nnz_e = float(tt[0].item()), float(tt[1].item())
+        _lib.host_pool_release()  # unpin and drop the reused host result buffers before anything else
         e2e = {"value": nnz_e / t_e2e, "unit": "nnz/s", "h2d_bytes_per_step": int(h2d // e2e_steps),
                "d2h_bytes_per_step": int(d2h // e2e_steps), "steps": e2e_steps,
                "api": "assemble_device/surrogate_device + Result.to_host (the calls behind assemble / build_surrogate_matrix)"}
@@ -448,7 +449,12 @@ def cpu_baseline(cfg, forms, paths, budget_s=60.0):
     rep = max(1, cores // len(base))
     jobs = base * rep
     workers = max(1, min(len(jobs), cores))
-    with ProcessPoolExecutor(max_workers=workers, initializer=_cpu_init, initargs=(use_ref,)) as ex:
+    import multiprocessing as mp
+
+    # spawn, not fork: the parent may hold a CUDA context and driver-pinned host buffers (a fork would
+    # copy every pinned page into each child)
+    with ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("spawn"), initializer=_cpu_init,
+                             initargs=(use_ref,)) as ex:
         list(ex.map(_cpu_warm, range(2 * workers)))
         t0 = time.perf_counter()
         res = list(ex.map(_cpu_job, jobs))

@@ -153,6 +153,16 @@ class _HostPool:
             t.join()
         self.jobs = []
 
+    def release(self):
+        self.sync()
+        self.fresh = []
+        with self.lock:
+            for lst in self.bases.values():
+                x = None
+                for x in [b for b in lst if self._idle(b)]:
+                    self._drop(lst, x)
+                x = None
+
     def _drop(self, lst, x):
         if self.registered.pop(id(x), False):
             lib().sg_host_unregister(C.c_void_p(x.ctypes.data))
@@ -251,6 +261,11 @@ def host_staging_init(device=0):
 def host_pool_sync():
     """Finish pending registrations of reused host result buffers (call outside timed regions)."""
     _pool.sync()
+
+
+def host_pool_release():
+    """Unpin and drop every idle pooled host buffer (e.g. before forking worker processes)."""
+    _pool.release()
 
 
 def last_timing():
