@@ -12,6 +12,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -37,7 +38,8 @@ struct SurrParams {
     double* data;
     double* newdiag;
     uint8_t* reset;
-    unsigned long long* counters;  // 0 interp entries, 1 zeros (interp rows), 2 resets, 3 interp rows
+    unsigned long long* counters;  // 0 interp entries, 1 zeros (interp rows), 2 resets, 3 interp rows, 6 slow rows
+    int* slow;                     // interpolated rows with a non-interpolated neighbour (row-staged path)
     int TB[3], tg[3];
     int cmax[3];  // max coefficient rows per direction touched by a (shifted) tile
     int64_t slab_lo, slab_hi;
@@ -636,6 +638,352 @@ __global__ void __launch_bounds__(512, 2) interp_fix_kernel(SurrParams s) {
         }
     }
 }
+// ---------------------------------------------------------------------------------------------
+// K7 3D row-staged path (interpolation degree 3, coefficient window 5 per direction, p <= 4).
+// One CTA (8 warps) owns a 4 x 8 x 4 tile of box rows (128 rows).  The P offsets are processed in
+// chunks of K = (2p+1)^2 consecutive offsets (one z-plane of the stencil, i.e. K consecutive CSR
+// slots of every row).  Per chunk:
+//   compute : each warp takes a contiguous run of the chunk's offsets; per offset the 5x5x5
+//             coefficient window is loaded straight into registers (lane = window row, prefetched
+//             one offset ahead), the x pass runs in registers (4 outputs per lane), y and z passes
+//             go through a small per-warp scratch (8 and 4 outputs per lane), and the 128 values
+//             land in a row-major stage [128][K];
+//   write   : a warp per row writes the row's K values and column indices as one contiguous
+//             segment (placement: interpolated / symmetric copy / transposed quadrature entry,
+//             surrogate.py:633-667), and folds the row's K values into its SKP row sum (:673-680).
+// Tap weights are padded to the 5-wide window (one zero tap; adding the +-0 product leaves the
+// 4-tap FMA chain's value unchanged); every lane reads the same weights (broadcast loads).
+// ---------------------------------------------------------------------------------------------
+#ifndef SG_EXP
+#define SG_EXP 0
+#endif
+namespace rows3 {
+constexpr int TB0 = 4, TB1 = 8, TB2 = 4, NR = TB0 * TB1 * TB2, CW = 5, MAXSH = 9, NWARP = 8;
+constexpr int AS = 6;             // scratch A row stride (doubles): [25][AS]
+constexpr int BS = 10;            // scratch B row stride: [(t2, b0)][BS] holding b1 = 0..7
+constexpr int SCR = 25 * AS + 20 * BS + 2;  // per-warp scratch (doubles)
+}  // namespace rows3
+
+template <int NS>
+__global__ void __launch_bounds__(256, 2) interp_rows3_kernel(SurrParams s) {
+    using namespace rows3;
+    extern __shared__ double sm[];
+    constexpr int p = (NS - 1) / 2, K = NS * NS, RPW = NR / NWARP;  // rows per warp (write phase)
+    const int P = s.P;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // smem: W5 [3][MAXSH][8][CW] | scratch [NWARP][SCR] | stage [NR][K] | rbS [NR] (int64) |
+    //       rowid [NR] | shl [P] | LO [3][MAXSH] | rfast [NR] | masks
+    double* W5 = sm;
+    double* scr = W5 + 3 * MAXSH * 8 * CW;
+    double* Aw = scr + (size_t)warp * SCR;
+    double* Bw = Aw + 25 * AS;
+    double* stage = scr + NWARP * SCR;
+    int64_t* rbS = reinterpret_cast<int64_t*>(stage + (size_t)NR * K);
+    int* rbr = reinterpret_cast<int*>(rbS + NR);  // CSR start relative to the tile's first row start
+    int* rowid = rbr + NR;
+    int* shl = rowid + NR;
+    int* oinf = shl + P;  // per offset: evaluated offset | evaluation shift (+p) << 16, 20, 24
+    int* LO = oinf + P;
+    uint8_t* rfast = reinterpret_cast<uint8_t*>(LO + 3 * MAXSH);
+    uint8_t* mk0 = rfast + NR;
+    constexpr int L0 = TB0 + 2 * p, L1 = TB1 + 2 * p, L2 = TB2 + 2 * p;
+    uint8_t* mk1 = mk0 + L0;
+    uint8_t* mk2 = mk1 + L1;
+    const int t = blockIdx.x;
+    const int tc0 = t % s.tg[0], tc1 = (t / s.tg[0]) % s.tg[1], tc2 = t / (s.tg[0] * s.tg[1]);
+    const int org[3] = {tc0 * TB0, tc1 * TB1, tc2 * TB2};
+    const int TBd[3] = {TB0, TB1, TB2};
+    const int base0 = org[0] - p, base1 = org[1] - p, base2 = org[2] - p;
+    // padded tap weights W5[d][sh][r][b] (tile point b contiguous) and window origins per
+    // (direction, evaluation shift)
+    for (int it = threadIdx.x; it < 3 * NS * 8; it += blockDim.x) {
+        const int d = it / (NS * 8), sh = (it / 8) % NS - p, b = it % 8;
+        double* w = W5 + (d * MAXSH + sh + p) * CW * 8 + b;
+        if (b >= TBd[d]) {
+#pragma unroll
+            for (int r = 0; r < CW; ++r) w[r * 8] = 0.0;
+            continue;
+        }
+        const int x = min(max(org[d] + b + sh, 0), s.bn[d] - 1);
+        const int lo_ = s.esp[d][min(max(org[d] + sh, 0), s.bn[d] - 1)] - 3;
+        // window origin kept inside the coefficient rows when there are >= 5 sites (the shifted taps stay
+        // inside the window: points at the last interval then sit at rel = 1)
+        const int lo = s.nl[d] >= CW ? min(lo_, s.nl[d] - CW) : lo_;
+        const int rel = s.esp[d][x] - 3 - lo;  // 0 or 1 (host checked the 5-wide window)
+#pragma unroll
+        for (int r = 0; r < CW; ++r) {
+            const int tap = r - rel;
+            w[r * 8] = (tap >= 0 && tap <= 3) ? s.etab[d][x * 4 + tap] : 0.0;
+        }
+        if (b == 0) LO[d * MAXSH + sh + p] = lo;
+    }
+    for (int it = threadIdx.x; it < L0 + L1 + L2; it += blockDim.x) {
+        int d = 0, li = it;
+        if (li >= L0) { li -= L0; d = 1; if (li >= L1) { li -= L1; d = 2; } }
+        const int base = d == 0 ? base0 : (d == 1 ? base1 : base2);
+        const int j = s.blo[d] + base + li;
+        uint8_t mk = 0;
+        if (j >= 0 && j < s.m[d]) mk = (uint8_t)(s.inb[d][j] | (s.smp[d][j] << 1));
+        (d == 0 ? mk0 : (d == 1 ? mk1 : mk2))[li] = mk;
+    }
+    // column shift of every offset (colex), in flat row index units
+    for (int o = threadIdx.x; o < P; o += blockDim.x) {
+        shl[o] = (o % NS - p) + s.m[0] * ((o / NS) % NS - p + s.m[1] * (o / K - p));
+        // mirrored offsets of the symmetric modes evaluate offset P-1-o at the shifted point
+        const bool mir = s.mode != SG_GENERAL && o < s.center;
+        oinf[o] = mir ? ((P - 1 - o) | ((o % NS) << 16) | (((o / NS) % NS) << 20) | ((o / K) << 24)) : (o | (p << 16) | (p << 20) | (p << 24));
+    }
+    __syncthreads();
+    const int64_t tile_row0 = (int64_t)(s.blo[0] + org[0]) + (int64_t)s.m[0] * ((int64_t)(s.blo[1] + org[1]) + (int64_t)s.m[1] * (s.blo[2] + org[2]));
+    double* const tdata = s.data + s.rowstart[tile_row0];
+    int* const tidx = s.indices + s.rowstart[tile_row0];
+    // tile rows: CSR start (-1: not an interpolated row of this slab), flat index, and whether every
+    // neighbour within +-p is an interpolated row (then every entry is the evaluated value)
+    for (int r = threadIdx.x; r < NR; r += blockDim.x) {
+        const int b0 = r % TB0, b1 = (r / TB0) % TB1, b2 = r / (TB0 * TB1);
+        bool ok = org[0] + b0 < s.bn[0] && org[1] + b1 < s.bn[1] && org[2] + b2 < s.bn[2];
+        const int i0 = s.blo[0] + org[0] + b0, i1 = s.blo[1] + org[1] + b1, i2 = s.blo[2] + org[2] + b2;
+        ok = ok && row_interp(s, i0, i1, i2);
+        const int64_t row = (int64_t)i0 + (int64_t)s.m[0] * ((int64_t)i1 + (int64_t)s.m[1] * i2);
+        ok = ok && row >= s.slab_lo && row < s.slab_hi;
+        rbS[r] = ok ? s.rowstart[row] : -1;
+        rbr[r] = ok ? (int)(s.rowstart[row] - s.rowstart[tile_row0]) : -1;
+        rowid[r] = (int)row;
+        uint8_t all0 = 1, all1 = 1, all2 = 1, any0 = 0, any1 = 0, any2 = 0;
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+            const uint8_t a0 = mk0[b0 + q], a1 = mk1[b1 + q], a2 = mk2[b2 + q];
+            all0 &= a0;
+            all1 &= a1;
+            all2 &= a2;
+            any0 |= a0 >> 1;
+            any1 |= a1 >> 1;
+            any2 |= a2 >> 1;
+        }
+        rfast[r] = (all0 & all1 & all2 & 1) && !(any0 & any1 & any2 & 1);
+    }
+    __syncthreads();
+    // window row of this lane (lanes 0..24): t1 = lane % 5, t2 = lane / 5
+    const int wt1 = lane % 5, wt2 = lane / 5;
+    const int nl0 = s.nl[0], nl01 = s.nl[0] * s.nl[1], nl012 = nl01 * s.nl[2];
+    // the lane's window row of offset o (5 coefficients, unclamped: zero-weight taps may read the
+    // zeroed tail of the coefficient buffer)
+    auto fetch = [&](int o, double (&w)[CW]) {
+        if (lane < 25) {
+            const int oi = oinf[o];
+            const int op = oi & 0xffff, a0 = (oi >> 16) & 15, a1 = (oi >> 20) & 15, a2 = oi >> 24;
+            const double* cf = s.coef + (op * nl012 + (LO[2 * MAXSH + a2] + wt2) * nl01 + (LO[MAXSH + a1] + wt1) * nl0 + LO[a0]);
+#pragma unroll
+            for (int r = 0; r < CW; ++r) w[r] = __ldg(cf + r);
+        }
+    };
+    // this warp's run of offsets in every chunk
+    const int kb = (warp * K) / NWARP, ke = ((warp + 1) * K) / NWARP;
+    double wpre[CW] = {0, 0, 0, 0, 0};
+    if (kb < ke) fetch(kb, wpre);
+    unsigned n_int = 0, n_zero = 0;
+    const int yb0 = lane % 4, yt2 = lane / 4;  // y pass lane (lanes 0..19)
+    const int zb0 = lane % 4, zb1 = lane / 4;  // z pass lane
+    // write phase: warp owns rows [RPW*warp, RPW*warp + RPW); lane < RPW keeps row RPW*warp+lane's sums
+    const int rsl = RPW * warp + (lane < RPW ? lane : 0);
+    double rsum = 0.0, dg = 0.0;
+    for (int c = 0; c < NS; ++c) {
+        // ---- compute the chunk's values into the stage
+        for (int k = kb; k < (SG_EXP == 2 ? kb : ke); ++k) {
+            const int o = c * K + k;
+            const int oi = oinf[o];
+            const int sh0 = (oi >> 16) & 15, sh1 = (oi >> 20) & 15, sh2 = oi >> 24;  // shift + p
+            double w[CW];
+#pragma unroll
+            for (int r = 0; r < CW; ++r) w[r] = wpre[r];
+            {
+                const int on = (k + 1 < ke) ? o + 1 : ((c + 1 < NS) ? (c + 1) * K + kb : -1);
+                if (on >= 0) fetch(on, wpre);
+            }
+            const double2* wx = reinterpret_cast<const double2*>(W5 + (0 * MAXSH + sh0) * CW * 8);
+            const double2* wy = reinterpret_cast<const double2*>(W5 + (1 * MAXSH + sh1) * CW * 8);
+            const double2* wz = reinterpret_cast<const double2*>(W5 + (2 * MAXSH + sh2) * CW * 8);
+            // x pass: A[t2][t1][b0] (independent chains over b0, taps ascending)
+            if (lane < 25) {
+                double a[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                for (int r = 0; r < CW; ++r) {
+                    const double2 u0 = wx[r * 4], u1 = wx[r * 4 + 1];
+                    a[0] = fma(u0.x, w[r], a[0]);
+                    a[1] = fma(u0.y, w[r], a[1]);
+                    a[2] = fma(u1.x, w[r], a[2]);
+                    a[3] = fma(u1.y, w[r], a[3]);
+                }
+                *reinterpret_cast<double2*>(Aw + lane * AS) = make_double2(a[0], a[1]);
+                *reinterpret_cast<double2*>(Aw + lane * AS + 2) = make_double2(a[2], a[3]);
+            }
+            __syncwarp();
+            // y pass: B[t2][b0][b1]
+            if (lane < 20) {
+                double a[CW];
+#pragma unroll
+                for (int r = 0; r < CW; ++r) a[r] = Aw[(yt2 * 5 + r) * AS + yb0];
+                double bv[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                for (int r = 0; r < CW; ++r) {
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        const double2 u = wy[r * 4 + h];
+                        bv[2 * h] = fma(u.x, a[r], bv[2 * h]);
+                        bv[2 * h + 1] = fma(u.y, a[r], bv[2 * h + 1]);
+                    }
+                }
+                double* dst = Bw + lane * BS;  // lane = yt2 * 4 + yb0
+#pragma unroll
+                for (int b = 0; b < 8; b += 2) *reinterpret_cast<double2*>(dst + b) = make_double2(bv[b], bv[b + 1]);
+            }
+            __syncwarp();
+            // z pass: V[b2][b1][b0] -> stage[row][k]
+            {
+                double bb[CW];
+#pragma unroll
+                for (int r = 0; r < CW; ++r) bb[r] = Bw[(r * 4 + zb0) * BS + zb1];
+                double v[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                for (int r = 0; r < CW; ++r) {
+                    const double2 u0 = wz[r * 4], u1 = wz[r * 4 + 1];
+                    v[0] = fma(u0.x, bb[r], v[0]);
+                    v[1] = fma(u0.y, bb[r], v[1]);
+                    v[2] = fma(u1.x, bb[r], v[2]);
+                    v[3] = fma(u1.y, bb[r], v[3]);
+                }
+#pragma unroll
+                for (int b = 0; b < 4; ++b) stage[(lane + 32 * b) * K + k] = v[b];
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+        // ---- write the warp's row segments of the chunk: entries flattened over (row, k) so the
+        //      lanes stay busy; consecutive lanes write consecutive CSR slots of a row
+        int rl = SG_EXP == 3 ? RPW : lane / K, k = lane - (lane / K) * K;
+        for (; rl < RPW; k += 32, rl += k / K, k %= K) {
+            const int r = RPW * warp + rl;
+            const int rb = rbr[r];
+            if (rb < 0) continue;
+            const int o = c * K + k;
+            const int col = rowid[r] + shl[o];
+            const double v = stage[r * K + k];
+            n_int++;  // provisional for slow rows (corrected by slow_rows_kernel)
+            n_zero += v == 0.0;
+            if (SG_EXP != 1) {
+                tdata[rb + o] = v;
+                tidx[rb + o] = col;
+            }
+        }
+        __syncwarp();
+        // ---- SKP row sums of the warp's rows (lane = row; ascending offsets)
+        if (lane < RPW && rbS[rsl] >= 0) {
+            const double* sr = stage + (size_t)rsl * K;
+#pragma unroll 7
+            for (int k = 0; k < K; ++k) rsum += sr[k];
+            if (c == p) dg = sr[(K - 1) / 2];
+        }
+        __syncthreads();
+    }
+    // ---- SKP diagonal values and counters
+    unsigned n_reset = 0, n_rows = 0;
+    if (lane < RPW && rbS[rsl] >= 0) {
+        n_rows = 1;
+        if (s.mode == SG_SYMMETRIC_KERNEL_PRESERVING) s.newdiag[rowid[rsl]] = dg - rsum;
+        if (!rfast[rsl]) {
+            s.slow[atomicAdd(&s.counters[6], 1ull)] = rowid[rsl];  // finished by slow_rows_kernel
+        } else if (s.mode == SG_SYMMETRIC_KERNEL_PRESERVING) {
+            // every neighbour is interpolated: the row has interpolated off-diagonal entries
+            s.reset[rowid[rsl]] = 1;
+            n_reset = 1;
+        }
+    }
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) {
+        n_int += __shfl_xor_sync(0xffffffffu, n_int, m);
+        n_zero += __shfl_xor_sync(0xffffffffu, n_zero, m);
+        n_reset += __shfl_xor_sync(0xffffffffu, n_reset, m);
+        n_rows += __shfl_xor_sync(0xffffffffu, n_rows, m);
+    }
+    if (lane == 0) {
+        if (n_int) atomicAdd(&s.counters[0], n_int);
+        if (n_zero) atomicAdd(&s.counters[1], n_zero);
+        if (n_reset) atomicAdd(&s.counters[2], n_reset);
+        if (n_rows) atomicAdd(&s.counters[3], n_rows);
+    }
+}
+// Rows of the row-staged path with a non-interpolated neighbour (box boundary band, neighbours of
+// fully sampled rows).  interp_rows3_kernel wrote the interpolant into every slot of these rows,
+// counted every slot as interpolated and stored the provisional SKP diagonal (centre - row sum);
+// here the non-interpolated slots get the transposed quadrature entry A[j, i] (surrogate.py:633-667)
+// and the counts, the row sum and the reset flag (:673-680) are corrected.  One warp per row; the row's neighbour classes
+// come from per-direction bit masks (no per-entry mask loads).
+template <int NS>
+__global__ void __launch_bounds__(256) slow_rows_kernel(SurrParams s) {
+    constexpr int p = (NS - 1) / 2, K = NS * NS, P = K * NS;
+    const int lane = threadIdx.x & 31;
+    const int64_t nslow = (int64_t)s.counters[6];
+    int n_int = 0, n_zero = 0, n_reset = 0;
+    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nslow; w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t row = s.slow[w];
+        const int i0 = (int)(row % s.m[0]), i1 = (int)((row / s.m[0]) % s.m[1]), i2 = (int)(row / ((int64_t)s.m[0] * s.m[1]));
+        // bit q of ib_d / sm_d: neighbour index i_d + q - p in the box / sampled
+        unsigned ib[3], sm[3];
+        {
+            const int id[3] = {i0, i1, i2};
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                const int j = id[d] + lane - p;
+                const bool ok = lane < NS;
+                ib[d] = __ballot_sync(0xffffffffu, ok && s.inb[d][j]);
+                sm[d] = __ballot_sync(0xffffffffu, ok && s.smp[d][j]);
+            }
+        }
+        const int64_t rb = s.rowstart[row];
+        double corr = 0.0;
+        int nq = 0;
+        for (int k = lane; k < P; k += 32) {
+            const int q0 = k % NS, q1 = (k / NS) % NS, q2 = k / K;
+            const unsigned a = (ib[0] >> q0) & (ib[1] >> q1) & (ib[2] >> q2) & 1u;
+            const unsigned b = (sm[0] >> q0) & (sm[1] >> q1) & (sm[2] >> q2) & 1u;
+            if (a && !b) continue;  // interpolated neighbour: the slot is final
+            const int64_t col = row + (q0 - p) + (int64_t)s.m[0] * ((q1 - p) + (int64_t)s.m[1] * (q2 - p));
+            const double old = s.data[rb + k];
+            const double v = s.data[s.rowstart[col] + (P - 1 - k)];  // transposed quadrature entry A[j, i]
+            s.data[rb + k] = v;
+            corr += v - old;
+            nq++;
+            n_zero += (v == 0.0) - (old == 0.0);
+        }
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) {
+            corr += __shfl_xor_sync(0xffffffffu, corr, m);
+            nq += __shfl_xor_sync(0xffffffffu, nq, m);
+        }
+        n_int -= nq;
+        if (lane == 0 && s.mode == SG_SYMMETRIC_KERNEL_PRESERVING && nq < P - 1) {
+            s.newdiag[row] -= corr;  // centre - row sum with the transposed entries
+            s.reset[row] = 1;
+            n_reset++;
+        }
+    }
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) n_zero += __shfl_xor_sync(0xffffffffu, n_zero, m);
+    if (lane == 0) {
+        // two's-complement adds: the corrections of the counts may be negative
+        if (n_int) atomicAdd(&s.counters[0], (unsigned long long)(long long)n_int);
+        if (n_zero) atomicAdd(&s.counters[1], (unsigned long long)(long long)n_zero);
+        if (n_reset) atomicAdd(&s.counters[2], (unsigned long long)n_reset);
+    }
+}
+
+static size_t interp_rows3_smem(int p) {
+    using namespace rows3;
+    const int NS = 2 * p + 1, K = NS * NS, P = K * NS;
+    return sizeof(double) * (3 * MAXSH * 8 * CW + NWARP * SCR + (size_t)NR * K) + sizeof(int64_t) * NR +
+           sizeof(int) * (2 * NR + 2 * P + 3 * MAXSH) + 2 * NR + 3 * (8 + 2 * p) + 16;
+}
+
 static size_t interp_fix_smem(int n, int p) {
     const int Q = 3, CW = 5, NR = 64, MAXSH = 9, nw = 16;
     const int TB0 = n == 2 ? 8 : 4, TB1 = n == 2 ? 8 : 4, TB2 = n == 3 ? 4 : 1;
@@ -795,6 +1143,7 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
     s.newdiag = newdiag;
     s.reset = reset;
     s.counters = counters;
+    s.slow = nullptr;
     c.kbegin("classify");
     classify_kernel<<<nblk(N, 256), 256, 0, c.stream>>>(s, N, quadmask);
     c.kend();
@@ -841,8 +1190,13 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
         latrows[t] = idx[0] + dp.m[0] * (idx[1] + (int64_t)dp.m[1] * idx[2]);
     }
     int64_t* dlat = (int64_t*)c.upload(latrows.data(), sizeof(int64_t) * nlat_tot);
-    double* bufA = (double*)c.alloc(sizeof(double) * P * nlat_tot, true);
-    double* bufB = (double*)c.alloc(sizeof(double) * P * nlat_tot, true);
+    // a zeroed tail of one lattice plane + row behind the coefficients: the row-staged K7 kernel
+    // reads whole 5-wide windows without clamping (the taps past the last site have weight 0)
+    const int64_t cpad = (int64_t)s.nl[0] * s.nl[1] + s.nl[0] + 16;
+    double* bufA = (double*)c.alloc(sizeof(double) * (P * nlat_tot + cpad), true);
+    double* bufB = (double*)c.alloc(sizeof(double) * (P * nlat_tot + cpad), true);
+    cudaMemsetAsync(bufA + P * nlat_tot, 0, sizeof(double) * cpad, c.stream);
+    cudaMemsetAsync(bufB + P * nlat_tot, 0, sizeof(double) * cpad, c.stream);
     c.kbegin("gather_samples");
     gather_samples_kernel<<<nblk(nlat_tot * P, 256), 256, 0, c.stream>>>(rowstart, data, dlat, nlat_tot, P, bufA);
     c.kend();
@@ -882,8 +1236,10 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
     }
     // coefficient window bounds per direction for a tile (host-side, from the same tables)
     const int TBdef[3][3] = {{64, 1, 1}, {8, 8, 1}, {4, 4, 4}};  // 64 rows per tile
+    // 3D, interpolation degree 3: the row-staged kernel (4 x 8 x 4 tiles) when every tile's window fits
+    bool rows3 = n == 3 && p <= 4 && s.qd[0] == 3 && s.qd[1] == 3 && s.qd[2] == 3 && !getenv("SG_INTERP_FIX");
     for (int d = 0; d < 3; ++d) {
-        s.TB[d] = TBdef[n - 1][d];
+        s.TB[d] = rows3 ? (d == 1 ? rows3::TB1 : rows3::TB0) : TBdef[n - 1][d];
         s.tg[d] = (s.bn[d] + s.TB[d] - 1) / s.TB[d];
     }
     {
@@ -907,13 +1263,31 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
     }
     // ---- K7
     const int nthreads = 512;
-    const int ntiles = s.tg[0] * s.tg[1] * s.tg[2];
     bool fixq = s.qd[0] == 3 && (n < 2 || s.qd[1] == 3) && (n < 3 || s.qd[2] == 3);
     for (int d = 0; d < n; ++d) fixq = fixq && s.cmax[d] <= 5;
     void* kfn;
     const int NR = 64;
     size_t smem;
-    if (fixq && n >= 2 && p <= 4) {
+    int nthr = nthreads;
+    if (rows3 && !fixq) {
+        // a 4 x 8 x 4 tile's window exceeds 5 coefficients: generic kernel on 64-row tiles (the
+        // window bounds computed for the larger tiles are upper bounds for these)
+        rows3 = false;
+        fixq = false;
+        for (int d = 0; d < 3; ++d) {
+            s.TB[d] = TBdef[n - 1][d];
+            s.tg[d] = (s.bn[d] + s.TB[d] - 1) / s.TB[d];
+        }
+    }
+    if (rows3) {
+        s.slow = (int*)c.alloc(sizeof(int) * N, true);
+        if (!s.slow) return fail(-4, "device allocation failed");
+        for (int d = 0; d < n; ++d) s.cmax[d] = 5;
+        kfn = p == 1 ? (void*)interp_rows3_kernel<3>
+                     : (p == 2 ? (void*)interp_rows3_kernel<5> : (p == 3 ? (void*)interp_rows3_kernel<7> : (void*)interp_rows3_kernel<9>));
+        smem = interp_rows3_smem(p);
+        nthr = rows3::NWARP * 32;
+    } else if (fixq && n >= 2 && p <= 4) {
         for (int d = 0; d < n; ++d) s.cmax[d] = 5;
         kfn = n == 2 ? (void*)interp_fix_kernel<2> : (void*)interp_fix_kernel<3>;
         smem = interp_fix_smem(n, p);
@@ -928,13 +1302,22 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
         }
         smem = sizeof(double) * ((size_t)nw * scr + (size_t)nw * NR + NR) + sizeof(int) * ((size_t)nw * NR * 3 + 2) + tabs + 64;
     }
+    const int ntiles = s.tg[0] * s.tg[1] * s.tg[2];
     if (smem > 227 * 1024) return fail(-2, "surrogate tile does not fit shared memory (%zu B)", smem);
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     void* args[] = {&s};
-    c.kbegin("interp_tiles");
-    cudaError_t e = cudaLaunchKernel(kfn, dim3(ntiles), dim3(nthreads), args, smem, c.stream);
+    c.kbegin(rows3 ? "interp_rows3" : "interp_tiles");
+    cudaError_t e = cudaLaunchKernel(kfn, dim3(ntiles), dim3(nthr), args, smem, c.stream);
     c.kend();
     if (e != cudaSuccess) return fail(-3, "interp launch failed: %s", cudaGetErrorString(e));
+    if (rows3) {
+        void* sk = p == 1 ? (void*)slow_rows_kernel<3>
+                          : (p == 2 ? (void*)slow_rows_kernel<5> : (p == 3 ? (void*)slow_rows_kernel<7> : (void*)slow_rows_kernel<9>));
+        c.kbegin("interp_slow_rows");
+        e = cudaLaunchKernel(sk, dim3(148 * 8), dim3(256), args, 0, c.stream);
+        c.kend();
+        if (e != cudaSuccess) return fail(-3, "slow-row launch failed: %s", cudaGetErrorString(e));
+    }
 
     // ---- merge: zero check
     unsigned long long hc[8];

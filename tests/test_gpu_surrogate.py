@@ -63,3 +63,29 @@ def test_gpu_surrogate_skp_kernel_and_symmetry():
     G, _ = pkg.build_surrogate_matrix(pkg.FormKind.POISSON, disc, pkg.ConstantSampling(5),
                                       mode=pkg.SurrogateMode.GENERAL)
     assert np.max(np.abs(G.row_sums())) > 1e-10 * G.max_abs()
+
+
+ROWS3 = [(2, (26, 27, 25), 8, "poisson", None), (2, (26, 27, 25), 8, "poisson", "general"),
+         (3, (28, 29, 27), 8, "mass", None)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p,spans,M,form,mode", ROWS3)
+def test_gpu_surrogate_rows3_kernel_vs_oracle(p, spans, M, form, mode):
+    # 3D interpolation degree 3 with M >= 8 runs the row-staged K7 kernel (interp_rows3)
+    import paper_1904_06971_b200 as pkg
+    from paper_1904_06971_b200 import _lib
+
+    disc = pkg.make_discretization(pkg.twisted_cube_standin(), p, spans)
+    fk = pkg.FormKind(form)
+    md = None if mode is None else pkg.SurrogateMode(mode)
+    A, rep = pkg.build_surrogate_matrix(fk, disc, pkg.ConstantSampling(M), mode=md)
+    assert "interp_rows3" in [n for n, _ in _lib.last_kernel_times()]
+    (ip, ix, d), sym, r2 = O.surrogate(O.problem_from_disc(fk, disc), M, 3, mode)
+    m = A.mat
+    assert np.array_equal(m.indptr, ip) and np.array_equal(m.indices, ix)
+    assert O.row_scaled_error(ip, ix, d, m.indptr, m.indices, m.data) <= TOL
+    assert rep.interp_entries == r2["interp_entries"] and rep.quad_entries == r2["quad_entries"]
+    assert A.symmetric == sym
+    if sym:
+        assert pkg.is_bitwise_symmetric(A)
