@@ -169,18 +169,20 @@ def run_ours(args):
 
     def one(f, path, checksum=False):
         fk = pkg.FormKind(f)
+        n_irows = 0
         if path == "full":
             res, _, _ = pkg.assemble_device(fk, disc, stream=sptr, slab=slab)
         else:
             mode = pkg.surrogate.DEFAULT_MODE[f].value
-            res, _, _ = surrogate_device(fk, disc, cfg.M, cfg.q, mode, stream=sptr, slab=slab, lattice=lattice,
-                                         tilde=tilde)
+            res, st, _ = surrogate_device(fk, disc, cfg.M, cfg.q, mode, stream=sptr, slab=slab, lattice=lattice,
+                                          tilde=tilde)
+            n_irows = int(st.n_interp_rows)
         ms_, nl = _lib.last_timing()
         kt = _lib.last_kernel_times()
         nrows, nnz = res.sizes()
         cs = res.checksum() if checksum else np.zeros(5)
         res.free()
-        return nnz, nrows, nl, kt, cs
+        return nnz, nrows, nl, kt, cs, n_irows
 
     for _ in range(args.warmup):
         for f, path in jobs:
@@ -203,10 +205,10 @@ def run_ours(args):
     checks = np.zeros(5)
     for _ in range(args.steps):
         for f, path in jobs:
-            nnz, nrows, nl, kt, cs = one(f, path)
+            nnz, nrows, nl, kt, cs, n_irows = one(f, path)
             nnz_tot += nnz
             launches += nl
-            per_job[(f, path)] = (nnz, nrows)
+            per_job[(f, path)] = (nnz, nrows, n_irows)
             for name, t in kt:
                 key = (f, path, name)
                 ktimes.setdefault(key, []).append(t)
@@ -238,7 +240,7 @@ def run_ours(args):
     rows = []
     for (f, path, name), ts in ktimes.items():
         avg = sum(ts) / len(ts)
-        nnz, nrows = per_job[(f, path)]
+        nnz, nrows, n_irows = per_job[(f, path)]
         if name in ("assemble_tiles", "assemble_mma"):
             if path == "full":
                 flops = f_elem(f, n, cfg.p, g) * E
@@ -254,11 +256,14 @@ def run_ours(args):
                          "ms": avg, "flops": flops, "share": sum(ts)})
         elif name == "geom_D":
             rows.append({"kernel": f"geom_D[{f},{path}]", "bound": None, "ms": avg, "share": sum(ts)})
-        elif name == "interp_tiles":
-            b = csr_bytes(nnz, nrows)
+        elif name in ("interp_tiles", "interp_rows3"):
+            # the kernel's own output: value + column of every slot of the interpolated rows
+            b = 12 * n_irows * (2 * cfg.p + 1) ** n
             ach = b / (avg / 1e3) / 1e9
-            rows.append({"kernel": f"interp_tiles[{f}]", "bound": "hbm", "achieved": ach, "peak": hbm,
+            rows.append({"kernel": f"{name}[{f}]", "bound": "hbm", "achieved": ach, "peak": hbm,
                          "unit": "GB/s", "frac": ach / hbm, "ms": avg, "bytes": b, "share": sum(ts)})
+        elif name == "interp_slow_rows":
+            rows.append({"kernel": f"interp_slow_rows[{f}]", "bound": None, "ms": avg, "share": sum(ts)})
     total_k = sum(sum(ts) for ts in ktimes.values())
     rows.sort(key=lambda r: -r["share"])
     for r in rows:
