@@ -135,6 +135,32 @@ int sg_result_device_ptrs(const sg_result* r, void** indptr_i64, void** indices_
 int sg_result_checksum(const sg_result* r, double out[5]);
 int sg_result_free(sg_result* r);
 
+/* ---- Device-resident consumer of the CSR (surriga/solvers.py:74-155) ---- */
+/* Upload a host CSR (e.g. a SparseMatrix built elsewhere) into a result handle on `device`. */
+int sg_result_from_host(int32_t device, int64_t nrows, int64_t nnz, const int64_t* indptr, const int32_t* indices,
+                        const double* data, sg_result** out);
+/* y = A x for a whole square result (host x, y of nrows doubles); replaces scipy's `mat @ x`. */
+int sg_spmv(const sg_result* A, const double* x, double* y, const sg_exec* exec);
+
+enum sg_cg_status {
+    SG_CG_CONVERGED = 0,             /* |r| <= tol |b| (solvers.py:144-145)                      */
+    SG_CG_NEGATIVE_CURVATURE = 1,    /* d.Ad <= 0 at `iterations` (solvers.py:138-141)           */
+    SG_CG_NONPOSITIVE_DIAGONAL = 2,  /* diagonal preconditioner with a diagonal entry <= 0 (:123) */
+    SG_CG_MAX_ITERATIONS = 3         /* no convergence in max_iterations (solvers.py:146-155)     */
+};
+typedef struct sg_cg_stats {
+    int32_t status;          /* enum sg_cg_status                                         */
+    int64_t iterations;      /* iterations run (the failing one for NEGATIVE_CURVATURE)   */
+    double norm_b;           /* |b|                                                       */
+    double rel_residual;     /* |A x - b| / |b| of the returned x (solvers.py:108-110,151) */
+} sg_cg_stats;
+/* Conjugate gradient of solvers.py:118-155 on a device-resident square CSR: x0 = 0, relative
+   tolerance `tol`, at most `maxit` iterations, precond 0 = "none", 1 = "diagonal" (Jacobi).  b, x are
+   host arrays of nrows doubles; x receives the final iterate.  The caller maps the status to the
+   reference's RuntimeError messages. */
+int sg_cg_solve(const sg_result* A, const double* b, double* x, double tol, int64_t maxit, int32_t precond,
+                const sg_exec* exec, sg_cg_stats* stats);
+
 /* Device-time of the kernels of the last call on this thread (ms), and their launch count. */
 int sg_last_timing(double* ms_total, int32_t* launches);
 /* Per-kernel breakdown of the last call: name list (comma separated) and ms values. */

@@ -984,3 +984,49 @@ def row_scaled_error(ipA, ixA, dA, ipB, ixB, dB):
     np.maximum.at(scale, rows, np.abs(dA))
     err = np.abs(dA - dB) / np.where(scale[rows] > 0, scale[rows], 1.0)
     return float(err.max())
+
+
+# ---------------------------------------------------------------------------
+# conjugate gradient (the device-resident consumer of the CSR)
+# ---------------------------------------------------------------------------
+
+def conjugate_gradient(indptr, indices, data, rhs, tol, maxit=None, preconditioner="none"):
+    """solvers.py:118-155 restated: x0 = 0, stop when |r| <= tol |b|.
+
+    Returns ``(x, status, iterations)`` with status "converged", "negative-curvature" (at
+    ``iterations``), "non-positive-diagonal" or "max-iterations" instead of raising, so the GPU
+    tests can compare the outcome as well as the iterate.
+    """
+    import scipy.sparse as sp
+
+    n = rhs.size
+    mat = sp.csr_matrix((data, indices, indptr), shape=(n, n))
+    maxit = 10 * n if maxit is None else maxit
+    if preconditioner == "diagonal":
+        diag = mat.diagonal()
+        if np.any(diag <= 0.0):
+            return np.zeros(n), "non-positive-diagonal", 0
+        prec = lambda r: r / diag  # noqa: E731
+    else:
+        prec = lambda r: r  # noqa: E731
+    target = tol * np.linalg.norm(rhs)
+    x = np.zeros(n)
+    r = rhs.copy()
+    z = prec(r)
+    d = z.copy()
+    rz = r @ z
+    for it in range(1, maxit + 1):
+        Ad = mat @ d
+        curv = d @ Ad
+        if curv <= 0.0:
+            return x, "negative-curvature", it
+        alpha = rz / curv
+        x += alpha * d
+        r -= alpha * Ad
+        if np.linalg.norm(r) <= target:
+            return x, "converged", it
+        z = prec(r)
+        rz_new = r @ z
+        d = z + (rz_new / rz) * d
+        rz = rz_new
+    return x, "max-iterations", maxit

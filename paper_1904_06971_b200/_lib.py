@@ -44,6 +44,10 @@ class SgSurrogateStats(C.Structure):
                 ("n_zero_dropped", C.c_int64), ("n_reset_rows", C.c_int64)]
 
 
+class SgCgStats(C.Structure):
+    _fields_ = [("status", C.c_int32), ("iterations", C.c_int64), ("norm_b", C.c_double), ("rel_residual", C.c_double)]
+
+
 class NativeError(RuntimeError):
     pass
 
@@ -86,6 +90,10 @@ def lib():
         L.sg_result_free.argtypes = [C.c_void_p]
         L.sg_last_timing.argtypes = [_d, _i32]
         L.sg_last_kernel_times.argtypes = [C.c_char_p, C.c_int32, _d, C.c_int32, _i32]
+        L.sg_result_from_host.argtypes = [C.c_int32, C.c_int64, C.c_int64, _i64, _i32, _d, C.POINTER(C.c_void_p)]
+        L.sg_spmv.argtypes = [C.c_void_p, _d, _d, C.POINTER(SgExec)]
+        L.sg_cg_solve.argtypes = [C.c_void_p, _d, _d, C.c_double, C.c_int64, C.c_int32, C.POINTER(SgExec),
+                                  C.POINTER(SgCgStats)]
         _lib = L
     return _lib
 
@@ -94,7 +102,7 @@ SYMBOLS = ("sg_assemble", "sg_surrogate", "sg_result_sizes", "sg_result_copy", "
            "sg_result_device_ptrs", "sg_result_checksum", "sg_result_free", "sg_last_timing",
            "sg_last_kernel_times", "sg_last_error", "sg_version", "sg_max_degree", "sg_host_staging_init",
            "sg_assemble_divergence", "sg_surrogate_divergence", "sg_host_register", "sg_host_unregister",
-           "sg_map_points", "sg_assemble_load")
+           "sg_map_points", "sg_assemble_load", "sg_result_from_host", "sg_spmv", "sg_cg_solve")
 
 
 def check(rc):
