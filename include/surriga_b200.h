@@ -122,6 +122,13 @@ int sg_surrogate_divergence(const sg_problem* velocity, const sg_problem* pressu
    and writes vec[N] = sum_e sum_q f det(J) w_q N_i (rational N_i for non-unit sol_w). */
 int sg_map_points(const sg_problem* problem, const sg_exec* exec, double* phi_out);
 int sg_assemble_load(const sg_problem* problem, const double* fvals, const sg_exec* exec, double* vec_out);
+/* Quadrature fields (replaces surriga/assembly.py:839-907 `quadrature_fields(disc, coefs, nu, gauss)`): for the
+   coefficient vector coefs[N] of the problem's space, writes at every element quadrature point (element-major,
+   T = E * g^n points): x_out[T][n] physical points, w_out[T] = w_q det J, val_out[T] field values and, for nu >= 1,
+   grad_out[T][n] physical gradients, for nu >= 2, hess_out[T][n][n] physical Hessians (NULL when not requested).
+   The problem's `form` is ignored; rational solution spaces use the NURBS basis. */
+int sg_quadrature_fields(const sg_problem* problem, const double* coefs, int32_t nu, const sg_exec* exec, double* x_out,
+                         double* w_out, double* val_out, double* grad_out, double* hess_out);
 /* Optional: allocate the calling thread's pinned D2H staging ring and host copy pool for `device` up
    front (otherwise done by the first large sg_result_copy*; not part of the reference interface). */
 int sg_host_staging_init(int device);

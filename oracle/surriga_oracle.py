@@ -1030,3 +1030,50 @@ def conjugate_gradient(indptr, indices, data, rhs, tol, maxit=None, precondition
         d = z + (rz_new / rz) * d
         rz = rz_new
     return x, "max-iterations", maxit
+
+
+# ---------------------------------------------------------------------------
+# quadrature fields (assembly.py:839-907)
+# ---------------------------------------------------------------------------
+
+def quadrature_fields(prob: Problem, coefs, nu=0):
+    """(x, w, vals, grads, hesses) element-major, as assembly.py:839-907 returns them.
+
+    The field is evaluated as the weighted numerator over the weight function (the reference's
+    rational basis contracted with the coefficients, assembly.py:496-517, 891-903).
+    """
+    n, p, g = prob.n, prob.p, prob.g
+    _, axes, pws = _dir_tables(prob, 0)
+    wq = pws[0]
+    for d in range(1, n):
+        wq = (pws[d][:, None] * wq[None, :]).ravel()
+    spans = prob.spans
+    geo = geometry_on_grid(prob, axes, 2 if nu >= 2 else 1)
+    coefs = np.asarray(coefs, dtype=float).ravel()
+    w = prob.sol_w if prob.rational else np.ones(prob.N)
+    f = field_on_grid(p, prob.ms, np.stack([coefs * w, w], axis=1), axes, nu)
+    z = (0,) * n
+    U, W = f[z][..., 0], f[z][..., 1]
+    u = U / W
+    E = lambda a: _to_elements(a, spans, g)  # noqa: E731
+    detg = geo["det"]
+    x = E(geo["phi"]).reshape(-1, n)
+    wts = (wq[None, :] * E(detg)).ravel()
+    vals = E(u).ravel()
+    grads = hesses = None
+    if nu >= 1:
+        du = np.stack([(f[_unit(n, a)][..., 0] - u * f[_unit(n, a)][..., 1]) / W for a in range(n)], axis=-1)
+        A = adj(geo["jac"])
+        gph = np.einsum("...a,...ac->...c", du, A) / detg[..., None]
+        grads = E(gph).reshape(-1, n)
+    if nu >= 2:
+        d2u = np.empty(u.shape + (n, n))
+        for a in range(n):
+            for b in range(n):
+                fab = f[_pair(n, a, b)]
+                d2u[..., a, b] = (fab[..., 0] - du[..., a] * f[_unit(n, b)][..., 1] - du[..., b] * f[_unit(n, a)][..., 1]
+                                  - u * fab[..., 1]) / W
+        T = d2u - np.einsum("...c,...cab->...ab", gph, geo["hess"])
+        H = np.einsum("...ac,...ab,...bd->...cd", A, T, A) / (detg ** 2)[..., None, None]
+        hesses = E(H).reshape(-1, n, n)
+    return x, wts, vals, grads, hesses

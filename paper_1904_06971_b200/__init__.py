@@ -23,6 +23,7 @@ from .assembly import (  # noqa: F401
     is_bitwise_symmetric,
     make_discretization,
     matrices_bitwise_equal,
+    quadrature_fields,
     set_device,
     stokes_subgrid_spaces,
 )

@@ -440,3 +440,37 @@ def assemble_load(disc, f, *, device=None, stream=None) -> np.ndarray:
     _lib.check(_lib.lib().sg_assemble_load(C.byref(pr), _lib.dptr(fb), C.byref(ex), _lib.dptr(vec)))
     del keep
     return vec
+
+
+def quadrature_fields(disc, coefs, nu: int = 0, gauss: int | None = None, *, device=None, stream=None):
+    """Physical samples of a coefficient field at the element quadrature points (assembly.py:839-907).
+
+    Returns ``(x, w, vals, grads, hesses)``: physical points ``(T, n)``, quadrature weights times
+    det J ``(T,)``, values ``(T,)``, physical gradients ``(T, n)`` (nu >= 1, else None) and physical
+    Hessians ``(T, n, n)`` (nu >= 2, else None), element-major (``T = E * g**n``), all evaluated on
+    the GPU (``sg_quadrature_fields``).
+    """
+    import dataclasses
+
+    d = disc if gauss is None else dataclasses.replace(disc, gauss=int(gauss))
+    pr, keep, _, N = problem_arrays(FormKind.MASS, d)
+    n = len(d.space.kvs)
+    coefs = np.ascontiguousarray(np.asarray(coefs, dtype=float).ravel())
+    if coefs.size != N:
+        raise ValueError("coefficient vector does not match the space")
+    nu = int(nu)
+    if nu not in (0, 1, 2):
+        raise ValueError("nu must be 0, 1 or 2")
+    E = int(np.prod([kv.m - kv.p for kv in d.space.kvs]))
+    T = E * int(d.gauss) ** n
+    x = np.empty((T, n))
+    w = np.empty(T)
+    vals = np.empty(T)
+    grads = np.empty((T, n)) if nu >= 1 else None
+    hesses = np.empty((T, n, n)) if nu >= 2 else None
+    ex = _exec(device, stream, None)
+    _lib.check(_lib.lib().sg_quadrature_fields(C.byref(pr), _lib.dptr(coefs), nu, C.byref(ex), _lib.dptr(x), _lib.dptr(w),
+                                               _lib.dptr(vals), _lib.dptr(grads) if grads is not None else None,
+                                               _lib.dptr(hesses) if hesses is not None else None))
+    del keep
+    return x, w, vals, grads, hesses
