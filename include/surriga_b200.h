@@ -129,6 +129,14 @@ int sg_assemble_load(const sg_problem* problem, const double* fvals, const sg_ex
    The problem's `form` is ignored; rational solution spaces use the NURBS basis. */
 int sg_quadrature_fields(const sg_problem* problem, const double* coefs, int32_t nu, const sg_exec* exec, double* x_out,
                          double* w_out, double* val_out, double* grad_out, double* hess_out);
+/* MatrixMarket coordinate output (replaces surriga/assembly.py:304-312 `save_matrix_market(path, A)`): header,
+   "%", "nrows ncols count", 1-based "i j value" lines; symmetric != 0 writes the lower triangle under the
+   `symmetric` tag as scipy's mmwrite does.  Values are printed in the shortest form that reads back to the same
+   double (the reference's 16 digits do not always round-trip).  Rows are formatted by `nthreads` host threads
+   (<= 0: all cores).  The device variant copies the result to the host first; ncols <= 0 means square. */
+int sg_write_matrix_market_host(const char* path, int64_t nrows, int64_t ncols, const int64_t* indptr, const int32_t* indices,
+                                const double* data, int32_t symmetric, int32_t nthreads);
+int sg_write_matrix_market(const sg_result* A, int64_t ncols, const char* path, int32_t symmetric, int32_t nthreads);
 /* Optional: allocate the calling thread's pinned D2H staging ring and host copy pool for `device` up
    front (otherwise done by the first large sg_result_copy*; not part of the reference interface). */
 int sg_host_staging_init(int device);

@@ -24,6 +24,8 @@ from .assembly import (  # noqa: F401
     make_discretization,
     matrices_bitwise_equal,
     quadrature_fields,
+    save_matrix_market,
+    load_matrix_market,
     set_device,
     stokes_subgrid_spaces,
 )

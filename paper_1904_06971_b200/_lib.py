@@ -93,6 +93,8 @@ def lib():
         L.sg_result_from_host.argtypes = [C.c_int32, C.c_int64, C.c_int64, _i64, _i32, _d, C.POINTER(C.c_void_p)]
         L.sg_spmv.argtypes = [C.c_void_p, _d, _d, C.POINTER(SgExec)]
         L.sg_quadrature_fields.argtypes = [C.POINTER(SgProblem), _d, C.c_int32, C.POINTER(SgExec), _d, _d, _d, _d, _d]
+        L.sg_write_matrix_market_host.argtypes = [C.c_char_p, C.c_int64, C.c_int64, _i64, _i32, _d, C.c_int32, C.c_int32]
+        L.sg_write_matrix_market.argtypes = [C.c_void_p, C.c_int64, C.c_char_p, C.c_int32, C.c_int32]
         L.sg_cg_solve.argtypes = [C.c_void_p, _d, _d, C.c_double, C.c_int64, C.c_int32, C.POINTER(SgExec),
                                   C.POINTER(SgCgStats)]
         _lib = L
@@ -104,7 +106,7 @@ SYMBOLS = ("sg_assemble", "sg_surrogate", "sg_result_sizes", "sg_result_copy", "
            "sg_last_kernel_times", "sg_last_error", "sg_version", "sg_max_degree", "sg_host_staging_init",
            "sg_assemble_divergence", "sg_surrogate_divergence", "sg_host_register", "sg_host_unregister",
            "sg_map_points", "sg_assemble_load", "sg_result_from_host", "sg_spmv", "sg_cg_solve",
-           "sg_quadrature_fields")
+           "sg_quadrature_fields", "sg_write_matrix_market_host", "sg_write_matrix_market")
 
 
 def check(rc):

@@ -474,3 +474,40 @@ def quadrature_fields(disc, coefs, nu: int = 0, gauss: int | None = None, *, dev
                                                _lib.dptr(hesses) if hesses is not None else None))
     del keep
     return x, w, vals, grads, hesses
+
+
+def save_matrix_market(path, A, *, ncols=None, symmetric=None, threads: int = 0) -> None:
+    """Write ``A`` in MatrixMarket coordinate format (assembly.py:304-312).
+
+    ``A`` is a ``SparseMatrix`` (host CSR) or a device ``_lib.Result`` (then ``symmetric`` and, for a
+    rectangular matrix, ``ncols`` are given by the caller).  Symmetric matrices are tagged
+    ``symmetric`` with the lower triangle stored, as the reference's mmwrite call does; values are
+    written in the shortest form that reads back bit-exactly (the reference's 16 digits do not
+    always).  Formatting runs on ``threads`` native threads (0: all cores).
+    """
+    L = _lib.lib()
+    p = os.fspath(path).encode()
+    if isinstance(A, _lib.Result):
+        _lib.check(L.sg_write_matrix_market(A.h, int(ncols or 0), p, int(bool(symmetric)), int(threads)))
+        return
+    mat = A.mat.tocsr()
+    mat.sort_indices()
+    sym = A.symmetric if symmetric is None else bool(symmetric)
+    ip = np.ascontiguousarray(mat.indptr, dtype=np.int64)
+    ix = np.ascontiguousarray(mat.indices, dtype=np.int32)
+    d = np.ascontiguousarray(mat.data, dtype=np.float64)
+    _lib.check(L.sg_write_matrix_market_host(p, mat.shape[0], mat.shape[1], ip.ctypes.data_as(_lib._i64),
+                                             ix.ctypes.data_as(_lib._i32), _lib.dptr(d), int(sym), int(threads)))
+
+
+def load_matrix_market(path) -> "SparseMatrix":
+    """Read a MatrixMarket file back into a ``SparseMatrix`` (assembly.py:315-320; host file IO)."""
+    from scipy.io import mminfo, mmread
+
+    info = mminfo(str(path))
+    try:
+        mat = mmread(str(path), spmatrix=True).tocsr()
+    except TypeError:  # scipy without the spmatrix switch
+        mat = mmread(str(path)).tocsr()
+    mat.sort_indices()
+    return SparseMatrix(mat=mat, symmetric=(info[5] == "symmetric"))

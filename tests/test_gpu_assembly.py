@@ -75,3 +75,20 @@ def test_gpu_surrogate_row_slabs():
     ip, ix, d = stitch(parts)
     assert np.array_equal(ip, A.mat.indptr) and np.array_equal(ix, A.mat.indices)
     assert np.array_equal(d.view(np.int64), A.mat.data.view(np.int64))
+
+
+@pytest.mark.gpu
+def test_gpu_matrix_market_from_device_result(tmp_path):
+    # the device-resident result writes the same file as its host copy
+    import paper_1904_06971_b200 as pkg
+
+    disc = pkg.make_discretization(pkg.twisted_cube_standin(), 2, (6, 5, 4))
+    res, sym, _ = pkg.assemble_device(pkg.FormKind.POISSON, disc)
+    try:
+        pkg.save_matrix_market(tmp_path / "dev.mtx", res, symmetric=sym)
+    finally:
+        res.free()
+    A = pkg.assemble(pkg.FormKind.POISSON, disc)
+    pkg.save_matrix_market(tmp_path / "host.mtx", A)
+    assert (tmp_path / "dev.mtx").read_bytes() == (tmp_path / "host.mtx").read_bytes()
+    assert pkg.matrices_bitwise_equal(A, pkg.load_matrix_market(tmp_path / "dev.mtx"))
