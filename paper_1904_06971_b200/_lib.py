@@ -182,8 +182,9 @@ class _HostPool:
 
     def begin(self):
         """Start of a result copy: bases created by earlier copies are filled -> pin them now."""
-        if self.fresh:
+        with self.lock:
             fresh, self.fresh = self.fresh, []
+        if fresh:
             self._register_async(fresh)
 
     def take(self, n, dtype):

@@ -121,15 +121,36 @@ __host__ __device__ constexpr int pad8_4(int v) {  // smallest w >= v with w % 8
     return w;
 }
 
+#ifndef SG_3D_NW
+#define SG_3D_NW 24
+#endif
+#ifndef SG_MASS_NW
+#define SG_MASS_NW 16
+#endif
+#ifndef SG_MASS_MINB
+#define SG_MASS_MINB 2
+#endif
+#ifndef SG_MASS_T0
+#define SG_MASS_T0 2
+#endif
+#ifndef SG_MASS_T1
+#define SG_MASS_T1 4
+#endif
 // warps per CTA (items are scheduled against it at compile time)
 __host__ __device__ constexpr int mma_warps(int ndim, int P, int form, bool rat) {
 #ifdef SG_MMA_NW
     return SG_MMA_NW;
 #else
     // 3D: 24 warps (6 per sub-partition) hide the smem -> DMMA -> smem latency chains of the
-    // pipelined intervals better than 16 (cfg5 Poisson 52.4 -> 48.2 ms); more spills registers
-    return ndim == 3 ? 24 : 16;
+    // pipelined intervals better than 16 (cfg5 Poisson 52.4 -> 48.2 ms); more spills registers.
+    // 3D mass: two CTAs of SG_MASS_NW warps per SM on half-size tiles (the barrier waits of one CTA
+    // overlap the other's work)
+    return ndim == 3 ? (form == 1 ? SG_MASS_NW : SG_3D_NW) : 16;
 #endif
+}
+// CTAs per SM the kernel is compiled for (register budget of __launch_bounds__)
+__host__ __device__ constexpr int mma_minb(int ndim, int P, int form, bool rat) {
+    return ndim == 3 && form == 1 ? SG_MASS_MINB : 1;
 }
 
 // ---- compile-time tile geometry (shared by host planning and the kernel)
@@ -217,6 +238,8 @@ __host__ __device__ constexpr TileChoice mma_tile(int ndim, int P, int form, boo
             if (mma_geom(2, P, form, rat, t, t).total <= cap) return {t, t};
         return {1, 1};
     }
+    if (form == 1 && mma_minb(3, P, form, rat) > 1 && mma_geom(3, P, form, rat, SG_MASS_T0, SG_MASS_T1).total <= cap / mma_minb(3, P, form, rat))
+        return {SG_MASS_T0, SG_MASS_T1};
     const TileChoice cand[] = {{4, 4}, {2, 4}, {2, 2}, {1, 2}, {1, 1}};
     for (TileChoice t : cand)
         if (mma_geom(3, P, form, rat, t.T0, t.T1).total <= cap) return t;
@@ -368,7 +391,7 @@ struct MmaParams {
 };
 
 template <int NDIM, int P, int FORM, bool RAT>
-__global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), 1) assemble_mma(const __grid_constant__ MmaParams prm) {
+__global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(NDIM, P, FORM, RAT)) assemble_mma(const __grid_constant__ MmaParams prm) {
     using TTS = TermTables<NDIM, FORM, RAT>;
     constexpr TileChoice TCH = mma_tile(NDIM, P, FORM, RAT);
     constexpr MmaGeom M = mma_geom(NDIM, P, FORM, RAT, TCH.T0, TCH.T1);
