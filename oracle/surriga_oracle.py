@@ -383,10 +383,17 @@ def element_matrices(prob: Problem, eids):
     for d in range(1, n):
         wq = (pws[d][:, None] * wq[None, :]).ravel()
     spans = prob.spans
-    geo = geometry_on_grid(prob, axes, gnu)
     et = np.stack(np.unravel_index(eids, spans, order="F"), axis=-1)
-    detE = _to_elements(geo["det"], spans, g)[eids]
-    jacE = _to_elements(geo["jac"], spans, g)[eids]
+    # the geometry (and weight function) is evaluated on the sub-grid of the elements' bounding box
+    # only: pointwise the same values as the full grid, without the full-grid cost at large meshes
+    lo = et.min(axis=0) if et.size else np.zeros(n, np.int64)
+    hi = et.max(axis=0) if et.size else np.zeros(n, np.int64)
+    sub_spans = tuple(int(h - l + 1) for l, h in zip(lo, hi))
+    sub_axes = [axes[d][lo[d] * g:(hi[d] + 1) * g] for d in range(n)]
+    sub_eids = np.ravel_multi_index(tuple((et - lo).T), sub_spans, order="F") if et.size else eids
+    geo = geometry_on_grid(prob, sub_axes, gnu)
+    detE = _to_elements(geo["det"], sub_spans, g)[sub_eids]
+    jacE = _to_elements(geo["jac"], sub_spans, g)[sub_eids]
     A = adj(jacE)
 
     B = _local_tensor(tabs, et, (0,) * n, p, g)
@@ -400,8 +407,8 @@ def element_matrices(prob: Problem, eids):
                 d2B[..., a, b] = _local_tensor(tabs, et, _pair(n, a, b), p, g)
 
     if prob.rational:
-        Wf = field_on_grid(p, prob.ms, prob.sol_w[:, None], axes, nu)
-        W = _to_elements(Wf[(0,) * n][..., 0], spans, g)[eids][..., None]
+        Wf = field_on_grid(p, prob.ms, prob.sol_w[:, None], sub_axes, nu)
+        W = _to_elements(Wf[(0,) * n][..., 0], sub_spans, g)[sub_eids][..., None]
         # local weights per element function (colex)
         L = (p + 1) ** n
         Il = np.stack(np.unravel_index(np.arange(L), (p + 1,) * n, order="F"), axis=-1)
@@ -410,7 +417,7 @@ def element_matrices(prob: Problem, eids):
         wl = prob.sol_w[cols][:, None, :]
         N = wl * B / W
         if nu >= 1:
-            dW = np.stack([_to_elements(Wf[_unit(n, a)][..., 0], spans, g)[eids] for a in range(n)], axis=-1)
+            dW = np.stack([_to_elements(Wf[_unit(n, a)][..., 0], sub_spans, g)[sub_eids] for a in range(n)], axis=-1)
             dN = np.empty_like(dB)
             for a in range(n):
                 dN[..., a] = (wl * dB[..., a] - N * dW[..., a][..., None]) / W
@@ -418,7 +425,7 @@ def element_matrices(prob: Problem, eids):
             d2N = np.empty_like(d2B)
             for a in range(n):
                 for b in range(n):
-                    d2W = _to_elements(Wf[_pair(n, a, b)][..., 0], spans, g)[eids][..., None]
+                    d2W = _to_elements(Wf[_pair(n, a, b)][..., 0], sub_spans, g)[sub_eids][..., None]
                     d2N[..., a, b] = (wl * d2B[..., a, b] - dN[..., a] * dW[..., b][..., None]
                                       - dN[..., b] * dW[..., a][..., None] - N * d2W) / W
         B = N
@@ -436,7 +443,7 @@ def element_matrices(prob: Problem, eids):
         s = detE * wq[None, :]
         loc = np.einsum("eql,eq,eqk->elk", B, s, B)
     elif form == "biharmonic":
-        hessE = _to_elements(geo["hess"], spans, g)[eids]
+        hessE = _to_elements(geo["hess"], sub_spans, g)[sub_eids]
         C = np.einsum("eqac,eqbc->eqab", A, A) / (detE ** 2)[..., None, None]
         pg = np.einsum("eqla,eqac->eqlc", dB, A) / detE[..., None, None]
         T = d2B - np.einsum("eqlc,eqcab->eqlab", pg, hessE)

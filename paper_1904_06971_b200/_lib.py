@@ -152,8 +152,9 @@ class _HostPool:
         def run(items):
             for b in items:
                 if check_quiet(lib().sg_host_register(C.c_void_p(b.ctypes.data), C.c_size_t(b.nbytes))):
-                    with self.lock:
-                        self.registered[id(b)] = True
+                    # no pool lock here: take() may hold it while it joins this thread (sync());
+                    # a single dict store is atomic under the GIL
+                    self.registered[id(b)] = True
 
         t = threading.Thread(target=run, args=(list(bases),), daemon=True)
         t.start()
@@ -178,7 +179,10 @@ class _HostPool:
     def _drop(self, lst, x):
         if self.registered.pop(id(x), False):
             lib().sg_host_unregister(C.c_void_p(x.ctypes.data))
-        lst.remove(x)
+        for i, b in enumerate(lst):  # by identity (list.remove would compare arrays elementwise)
+            if b is x:
+                del lst[i]
+                break
 
     def begin(self):
         """Start of a result copy: bases created by earlier copies are filled -> pin them now."""
