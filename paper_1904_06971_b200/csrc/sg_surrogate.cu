@@ -658,10 +658,12 @@ __global__ void __launch_bounds__(512, 2) interp_fix_kernel(SurrParams s) {
 #define SG_EXP 0
 #endif
 namespace rows3 {
-constexpr int TB0 = 4, TB1 = 8, TB2 = 4, NR = TB0 * TB1 * TB2, CW = 5, MAXSH = 9, NWARP = 8;
-constexpr int AS = 6;             // scratch A row stride (doubles): [25][AS]
-constexpr int BS = 10;            // scratch B row stride: [(t2, b0)][BS] holding b1 = 0..7
+constexpr int TB0 = 4, TB1 = 4, TB2 = 8, NR = TB0 * TB1 * TB2, CW = 5, MAXSH = 9, NWARP = 8;
+constexpr int AS = 6;             // scratch A row stride (doubles): [(t2, t1)][AS] holding b0 = 0..3
+constexpr int BS = 6;             // scratch B row stride: [(t2, b1)][BS] holding b0 = 0..3
+constexpr int WS = 6;             // lane-specific weight rows [d][sh][b][WS] (5 taps + pad)
 constexpr int SCR = 25 * AS + 20 * BS + 2;  // per-warp scratch (doubles)
+// stage row of tile point (b0, b1, b2): rho = (b1 + 4 b2) + 32 b0 (the z-pass lane is b1 + 4 b2)
 }  // namespace rows3
 
 template <int NS>
@@ -673,8 +675,9 @@ __global__ void __launch_bounds__(256, 2) interp_rows3_kernel(SurrParams s) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // smem: W5 [3][MAXSH][8][CW] | scratch [NWARP][SCR] | stage [NR][K] | rbS [NR] (int64) |
     //       rowid [NR] | shl [P] | LO [3][MAXSH] | rfast [NR] | masks
-    double* W5 = sm;
-    double* scr = W5 + 3 * MAXSH * 8 * CW;
+    double* W5 = sm;                          // x taps, uniform over lanes: [d][sh][r][b]
+    double* WT = W5 + 3 * MAXSH * 8 * CW;     // y / z taps, one row per lane: [d][sh][b][WS]
+    double* scr = WT + 3 * MAXSH * 8 * WS;
     double* Aw = scr + (size_t)warp * SCR;
     double* Bw = Aw + 25 * AS;
     double* stage = scr + NWARP * SCR;
@@ -699,9 +702,11 @@ __global__ void __launch_bounds__(256, 2) interp_rows3_kernel(SurrParams s) {
     for (int it = threadIdx.x; it < 3 * NS * 8; it += blockDim.x) {
         const int d = it / (NS * 8), sh = (it / 8) % NS - p, b = it % 8;
         double* w = W5 + (d * MAXSH + sh + p) * CW * 8 + b;
+        double* wt = WT + ((d * MAXSH + sh + p) * 8 + b) * WS;
         if (b >= TBd[d]) {
 #pragma unroll
-            for (int r = 0; r < CW; ++r) w[r * 8] = 0.0;
+            for (int r = 0; r < CW; ++r) w[r * 8] = wt[r] = 0.0;
+            wt[CW] = 0.0;
             continue;
         }
         const int x = min(max(org[d] + b + sh, 0), s.bn[d] - 1);
@@ -713,8 +718,9 @@ __global__ void __launch_bounds__(256, 2) interp_rows3_kernel(SurrParams s) {
 #pragma unroll
         for (int r = 0; r < CW; ++r) {
             const int tap = r - rel;
-            w[r * 8] = (tap >= 0 && tap <= 3) ? s.etab[d][x * 4 + tap] : 0.0;
+            w[r * 8] = wt[r] = (tap >= 0 && tap <= 3) ? s.etab[d][x * 4 + tap] : 0.0;
         }
+        wt[CW] = 0.0;
         if (b == 0) LO[d * MAXSH + sh + p] = lo;
     }
     for (int it = threadIdx.x; it < L0 + L1 + L2; it += blockDim.x) {
@@ -740,7 +746,7 @@ __global__ void __launch_bounds__(256, 2) interp_rows3_kernel(SurrParams s) {
     // tile rows: CSR start (-1: not an interpolated row of this slab), flat index, and whether every
     // neighbour within +-p is an interpolated row (then every entry is the evaluated value)
     for (int r = threadIdx.x; r < NR; r += blockDim.x) {
-        const int b0 = r % TB0, b1 = (r / TB0) % TB1, b2 = r / (TB0 * TB1);
+        const int b0 = r / 32, b1 = r % 4, b2 = (r % 32) / 4;
         bool ok = org[0] + b0 < s.bn[0] && org[1] + b1 < s.bn[1] && org[2] + b2 < s.bn[2];
         const int i0 = s.blo[0] + org[0] + b0, i1 = s.blo[1] + org[1] + b1, i2 = s.blo[2] + org[2] + b2;
         ok = ok && row_interp(s, i0, i1, i2);
@@ -782,8 +788,11 @@ __global__ void __launch_bounds__(256, 2) interp_rows3_kernel(SurrParams s) {
     double wpre[CW] = {0, 0, 0, 0, 0};
     if (kb < ke) fetch(kb, wpre);
     unsigned n_int = 0, n_zero = 0;
-    const int yb0 = lane % 4, yt2 = lane / 4;  // y pass lane (lanes 0..19)
-    const int zb0 = lane % 4, zb1 = lane / 4;  // z pass lane
+    const int yb1 = lane % 4, yt2 = lane / 4;  // y pass lane (lanes 0..19)
+    const int zb1 = lane % 4, zb2 = lane / 4;  // z pass lane
+    // the lane's y and z tap rows, reloaded only when the evaluation shift changes (z: per chunk)
+    double wyr[CW], wzr[CW];
+    int cur1 = -1, cur2 = -1;
     // write phase: warp owns rows [RPW*warp, RPW*warp + RPW); lane < RPW keeps row RPW*warp+lane's sums
     const int rsl = RPW * warp + (lane < RPW ? lane : 0);
     double rsum = 0.0, dg = 0.0;
@@ -801,8 +810,18 @@ __global__ void __launch_bounds__(256, 2) interp_rows3_kernel(SurrParams s) {
                 if (on >= 0) fetch(on, wpre);
             }
             const double2* wx = reinterpret_cast<const double2*>(W5 + (0 * MAXSH + sh0) * CW * 8);
-            const double2* wy = reinterpret_cast<const double2*>(W5 + (1 * MAXSH + sh1) * CW * 8);
-            const double2* wz = reinterpret_cast<const double2*>(W5 + (2 * MAXSH + sh2) * CW * 8);
+            if (sh1 != cur1) {
+                const double2* q = reinterpret_cast<const double2*>(WT + ((1 * MAXSH + sh1) * 8 + yb1) * WS);
+                const double2 u0 = q[0], u1 = q[1], u2 = q[2];
+                wyr[0] = u0.x, wyr[1] = u0.y, wyr[2] = u1.x, wyr[3] = u1.y, wyr[4] = u2.x;
+                cur1 = sh1;
+            }
+            if (sh2 != cur2) {
+                const double2* q = reinterpret_cast<const double2*>(WT + ((2 * MAXSH + sh2) * 8 + zb2) * WS);
+                const double2 u0 = q[0], u1 = q[1], u2 = q[2];
+                wzr[0] = u0.x, wzr[1] = u0.y, wzr[2] = u1.x, wzr[3] = u1.y, wzr[4] = u2.x;
+                cur2 = sh2;
+            }
             // x pass: A[t2][t1][b0] (independent chains over b0, taps ascending)
             if (lane < 25) {
                 double a[4] = {0.0, 0.0, 0.0, 0.0};
@@ -818,39 +837,34 @@ __global__ void __launch_bounds__(256, 2) interp_rows3_kernel(SurrParams s) {
                 *reinterpret_cast<double2*>(Aw + lane * AS + 2) = make_double2(a[2], a[3]);
             }
             __syncwarp();
-            // y pass: B[t2][b0][b1]
+            // y pass: B[t2][b1][b0] for the lane's (b1, t2), b0 = 0..3 (taps t1 ascending)
             if (lane < 20) {
-                double a[CW];
-#pragma unroll
-                for (int r = 0; r < CW; ++r) a[r] = Aw[(yt2 * 5 + r) * AS + yb0];
-                double bv[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+                double bv[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
                 for (int r = 0; r < CW; ++r) {
-#pragma unroll
-                    for (int h = 0; h < 4; ++h) {
-                        const double2 u = wy[r * 4 + h];
-                        bv[2 * h] = fma(u.x, a[r], bv[2 * h]);
-                        bv[2 * h + 1] = fma(u.y, a[r], bv[2 * h + 1]);
-                    }
+                    const double2* q = reinterpret_cast<const double2*>(Aw + (yt2 * 5 + r) * AS);
+                    const double2 u0 = q[0], u1 = q[1];
+                    bv[0] = fma(wyr[r], u0.x, bv[0]);
+                    bv[1] = fma(wyr[r], u0.y, bv[1]);
+                    bv[2] = fma(wyr[r], u1.x, bv[2]);
+                    bv[3] = fma(wyr[r], u1.y, bv[3]);
                 }
-                double* dst = Bw + lane * BS;  // lane = yt2 * 4 + yb0
-#pragma unroll
-                for (int b = 0; b < 8; b += 2) *reinterpret_cast<double2*>(dst + b) = make_double2(bv[b], bv[b + 1]);
+                double* dst = Bw + (yt2 * 4 + yb1) * BS;
+                *reinterpret_cast<double2*>(dst) = make_double2(bv[0], bv[1]);
+                *reinterpret_cast<double2*>(dst + 2) = make_double2(bv[2], bv[3]);
             }
             __syncwarp();
-            // z pass: V[b2][b1][b0] -> stage[row][k]
+            // z pass: V[b2][b1][b0] for the lane's (b1, b2), b0 = 0..3 -> stage rows lane + 32 b0
             {
-                double bb[CW];
-#pragma unroll
-                for (int r = 0; r < CW; ++r) bb[r] = Bw[(r * 4 + zb0) * BS + zb1];
                 double v[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
                 for (int r = 0; r < CW; ++r) {
-                    const double2 u0 = wz[r * 4], u1 = wz[r * 4 + 1];
-                    v[0] = fma(u0.x, bb[r], v[0]);
-                    v[1] = fma(u0.y, bb[r], v[1]);
-                    v[2] = fma(u1.x, bb[r], v[2]);
-                    v[3] = fma(u1.y, bb[r], v[3]);
+                    const double2* q = reinterpret_cast<const double2*>(Bw + (r * 4 + zb1) * BS);
+                    const double2 u0 = q[0], u1 = q[1];
+                    v[0] = fma(wzr[r], u0.x, v[0]);
+                    v[1] = fma(wzr[r], u0.y, v[1]);
+                    v[2] = fma(wzr[r], u1.x, v[2]);
+                    v[3] = fma(wzr[r], u1.y, v[3]);
                 }
 #pragma unroll
                 for (int b = 0; b < 4; ++b) stage[(lane + 32 * b) * K + k] = v[b];
@@ -980,7 +994,7 @@ __global__ void __launch_bounds__(256) slow_rows_kernel(SurrParams s) {
 static size_t interp_rows3_smem(int p) {
     using namespace rows3;
     const int NS = 2 * p + 1, K = NS * NS, P = K * NS;
-    return sizeof(double) * (3 * MAXSH * 8 * CW + NWARP * SCR + (size_t)NR * K) + sizeof(int64_t) * NR +
+    return sizeof(double) * (3 * MAXSH * 8 * CW + 3 * MAXSH * 8 * WS + NWARP * SCR + (size_t)NR * K) + sizeof(int64_t) * NR +
            sizeof(int) * (2 * NR + 2 * P + 3 * MAXSH) + 2 * NR + 3 * (8 + 2 * p) + 16;
 }
 
@@ -1239,7 +1253,7 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
     // 3D, interpolation degree 3: the row-staged kernel (4 x 8 x 4 tiles) when every tile's window fits
     bool rows3 = n == 3 && p <= 4 && s.qd[0] == 3 && s.qd[1] == 3 && s.qd[2] == 3 && !getenv("SG_INTERP_FIX");
     for (int d = 0; d < 3; ++d) {
-        s.TB[d] = rows3 ? (d == 1 ? rows3::TB1 : rows3::TB0) : TBdef[n - 1][d];
+        s.TB[d] = rows3 ? (d == 0 ? rows3::TB0 : (d == 1 ? rows3::TB1 : rows3::TB2)) : TBdef[n - 1][d];
         s.tg[d] = (s.bn[d] + s.TB[d] - 1) / s.TB[d];
     }
     {
