@@ -310,14 +310,37 @@ class _Keep:
         return x.ctypes.data_as(_lib._i64)
 
 
+_FIT_CACHE: dict = {}
+
+
 def _fit_params(disc, lattice: SamplingLattice, tilde: TildeDomain, q: int, mode_name: str, M: int):
     """Host-side interpolation setup: per-direction degree (lowered if needed), averaged knots,
-    inverse collocation matrix at the lattice sites, in-box midpoints (surrogate.py:430-471, 612)."""
+    inverse collocation matrix at the lattice sites, in-box midpoints (surrogate.py:430-471, 612).
+
+    The arrays depend only on the knot vectors, the lattice and q, so they are built once per such
+    key (exact-rational midpoints and collocation inverses cost ~2 ms a call) and reused; the mode
+    is set on a copy of the cached parameter block."""
+    key = (tuple((int(kv.p), int(kv.m)) for kv in disc.space.kvs), int(M), int(q),
+           tuple(tuple(int(i) for i in ix) for ix in lattice.indices),
+           tuple(tuple(float(x) for x in st) for st in lattice.sites),
+           tuple(tilde.index_range(d) for d in range(len(disc.space.kvs))))
+    hit = _FIT_CACHE.get(key)
+    if hit is None:
+        hit = _fit_params_build(disc, lattice, tilde, q, M)
+        if len(_FIT_CACHE) > 16:
+            _FIT_CACHE.clear()
+        _FIT_CACHE[key] = hit
+    base, keep, lowered = hit
+    spp = type(base).from_buffer_copy(base)
+    spp.mode = _NATIVE_MODE[mode_name]
+    return spp, keep, lowered
+
+
+def _fit_params_build(disc, lattice: SamplingLattice, tilde: TildeDomain, q: int, M: int):
     keep = _Keep()
     spp = _lib.SgSurrogateParams()
     spp.M = int(M)
     spp.q = int(q)
-    spp.mode = _NATIVE_MODE[mode_name]
     lowered = False
     for d, kv in enumerate(disc.space.kvs):
         sites = lattice.sites[d]
