@@ -220,7 +220,7 @@ def check_quiet(rc):
     return rc == 0
 
 
-_pool = _HostPool()
+_pool = _HostPool(keep=int(os.environ.get("SG_HOST_POOL_KEEP", "2")))
 
 
 class Result:
