@@ -159,8 +159,13 @@ def run_ours(args):
     n = len(cfg.spans)
     ms = tuple(kv.m for kv in disc.space.kvs)
     N = int(np.prod(ms))
-    slab = plane_slabs(ms, world)[rank] if world > 1 else None
     lattice = build_sampling_lattice(disc.space.kvs, cfg.M)
+    # per call: equal plane slabs for the full assembly, cost-weighted plane slabs for the surrogate
+    # (its box-boundary quadrature layers make the outer slabs heavy)
+    from paper_1904_06971_b200.slabs import job_slabs
+
+    slabs = {(f, path): job_slabs(ms, cfg.p, world, path, f, lattice.indices)[rank if world > 1 else 0]
+             for f in (args.forms.split(",") if args.forms else list(cfg.forms)) for path in args.paths.split(",")}
     tilde = tilde_domain(cfg.p, ms)
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
@@ -170,6 +175,7 @@ def run_ours(args):
     def one(f, path, checksum=False):
         fk = pkg.FormKind(f)
         n_irows = 0
+        slab = slabs[(f, path)]
         if path == "full":
             res, _, _ = pkg.assemble_device(fk, disc, stream=sptr, slab=slab)
         else:
@@ -285,6 +291,7 @@ def run_ours(args):
 
         def e2e_job(f, path):
             fk = pkg.FormKind(f)
+            slab = slabs[(f, path)]
             if path == "full":
                 res, _, _ = pkg.assemble_device(fk, disc, slab=slab)
             else:

@@ -11,7 +11,14 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["plane_slabs", "weighted_plane_slabs", "csr_checksum", "stitch", "allreduce_checksum"]
+__all__ = ["plane_slabs", "weighted_plane_slabs", "surrogate_plane_cost", "job_slabs", "csr_checksum", "stitch",
+           "allreduce_checksum"]
+
+# Relative device cost per row of the surrogate's parts (measured on one B200 at config 5, p=3,
+# DESIGN.md §8): quadrature row (K4 on the quadrature tiles), interpolated row (K7), any row (K3
+# geometry of the needed planes, row pointers).  Only the ratios matter.
+SURROGATE_ROW_COST = {"poisson": (24.7, 2.8, 0.84), "stokes_velocity": (24.7, 2.8, 0.84),
+                      "mass": (6.2, 2.8, 0.77), "biharmonic": (24.7, 2.8, 0.84)}
 
 
 def plane_slabs(ms, world: int):
@@ -27,14 +34,51 @@ def plane_slabs(ms, world: int):
 
 def weighted_plane_slabs(plane_cost, per: int, world: int):
     """Slabs balancing a per-plane cost (e.g. quadrature rows per plane for the surrogate)."""
-    c = np.cumsum(np.asarray(plane_cost, dtype=float))
+    c = np.r_[0.0, np.cumsum(np.asarray(plane_cost, dtype=float))]  # c[k] = cost of planes [0, k)
     tot = c[-1]
     cuts = [0]
     for r in range(1, world):
-        k = int(np.searchsorted(c, tot * r / world)) + 1
-        cuts.append(max(cuts[-1] + 1, min(k, len(c) - (world - r))))
-    cuts.append(len(c))
+        t = tot * r / world
+        k = int(np.searchsorted(c, t))  # c[k-1] < t <= c[k]: cut at whichever side is nearer
+        if k > 0 and t - c[k - 1] < c[k] - t:
+            k -= 1
+        cuts.append(max(cuts[-1] + 1, min(k, len(c) - 1 - (world - r))))
+    cuts.append(len(c) - 1)
     return [(cuts[r] * per, cuts[r + 1] * per) for r in range(world)]
+
+
+def surrogate_plane_cost(ms, p, lattice_indices, form: str) -> np.ndarray:
+    """Estimated surrogate cost of every slowest-direction plane (quadrature rows are ~9x dearer
+    than interpolated rows for Poisson): the boundary layers of the box make the first and last
+    slabs heavy, so equal plane counts do not balance the surrogate."""
+    ms = tuple(int(m) for m in ms)
+    n = len(ms)
+    box, smp = [], []
+    for d in range(n):
+        b = np.zeros(ms[d], bool)
+        b[2 * p:ms[d] - 2 * p] = True
+        sm = np.zeros(ms[d], bool)
+        sm[np.asarray(lattice_indices[d], dtype=np.int64)] = True
+        box.append(b)
+        smp.append(sm)
+    per = int(np.prod(ms[:-1]))
+    inner_box = int(np.prod([box[d].sum() for d in range(n - 1)]))
+    inner_smp = int(np.prod([(box[d] & smp[d]).sum() for d in range(n - 1)]))
+    interp = np.where(~box[-1], 0, np.where(smp[-1], inner_box - inner_smp, inner_box)).astype(float)
+    quad = per - interp
+    cq, ci, c0 = SURROGATE_ROW_COST.get(form, SURROGATE_ROW_COST["poisson"])
+    return cq * quad + ci * interp + c0 * per
+
+
+def job_slabs(ms, p, world: int, path: str, form: str, lattice_indices=None):
+    """Row slabs of one assembly call: equal planes for the full assembly, cost-weighted planes
+    for the surrogate."""
+    if world <= 1:
+        return [None]
+    if path == "full" or lattice_indices is None:
+        return plane_slabs(ms, world)
+    cost = surrogate_plane_cost(ms, p, lattice_indices, form)
+    return weighted_plane_slabs(cost, int(np.prod(ms[:-1])), world)
 
 
 def csr_checksum(indptr, data) -> np.ndarray:

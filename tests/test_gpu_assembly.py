@@ -92,3 +92,29 @@ def test_gpu_matrix_market_from_device_result(tmp_path):
     pkg.save_matrix_market(tmp_path / "host.mtx", A)
     assert (tmp_path / "dev.mtx").read_bytes() == (tmp_path / "host.mtx").read_bytes()
     assert pkg.matrices_bitwise_equal(A, pkg.load_matrix_market(tmp_path / "dev.mtx"))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("form", ["poisson", "mass"])
+def test_gpu_surrogate_weighted_slabs_rows3(form):
+    # cost-weighted slabs (bench.py's surrogate split) on the row-staged K7 path stitch bitwise
+    import paper_1904_06971_b200 as pkg
+    from paper_1904_06971_b200.slabs import job_slabs, stitch
+    from paper_1904_06971_b200.surrogate import DEFAULT_MODE, build_sampling_lattice, surrogate_device
+
+    disc = pkg.make_discretization(pkg.twisted_cube_standin(), 3, (28, 29, 27))
+    fk = pkg.FormKind(form)
+    mode = DEFAULT_MODE[form].value
+    full, _, _ = surrogate_device(fk, disc, 8, 3, mode)
+    fip, fix, fd = full.to_host()
+    full.free()
+    ms = tuple(kv.m for kv in disc.space.kvs)
+    lat = build_sampling_lattice(disc.space.kvs, 8)
+    parts = []
+    for lo, hi in job_slabs(ms, 3, 3, "surrogate", form, lat.indices):
+        res, _, _ = surrogate_device(fk, disc, 8, 3, mode, slab=(lo, hi))
+        parts.append(res.to_host())
+        res.free()
+    ip, ix, d = stitch(parts)
+    assert np.array_equal(ip, fip) and np.array_equal(ix, fix)
+    assert np.array_equal(d.view(np.int64), fd.view(np.int64))

@@ -82,3 +82,28 @@ def test_two_rank_slabs_gloo_equal_full():
     full = csr_checksum(ip, d)
     assert cs[0] == full[0]
     assert np.allclose(cs[1:], full[1:], rtol=1e-12, atol=1e-12)
+
+
+def test_surrogate_plane_cost_rows_and_balance():
+    # the per-plane row classes of the cost model add up to the exact plan (surrogate_plan), and
+    # cost-weighted slabs balance the surrogate of config 5 across 8 ranks better than equal planes
+    import paper_1904_06971_b200 as pkg
+    from paper_1904_06971_b200.configs import CONFIGS
+    from paper_1904_06971_b200.slabs import SURROGATE_ROW_COST, surrogate_plane_cost
+    from paper_1904_06971_b200.surrogate import build_sampling_lattice
+
+    cfg = CONFIGS[5]
+    disc = pkg.make_discretization(cfg.geom(), cfg.p, cfg.spans)
+    ms = tuple(kv.m for kv in disc.space.kvs)
+    lat = build_sampling_lattice(disc.space.kvs, cfg.M)
+    per = int(np.prod(ms[:-1]))
+    cq, ci, c0 = SURROGATE_ROW_COST["poisson"]
+    cost = surrogate_plane_cost(ms, cfg.p, lat.indices, "poisson")
+    interp = (cost - c0 * per - cq * per) / (ci - cq)  # invert cost = cq quad + ci interp + c0 per
+    plan = pkg.surrogate_plan(disc, pkg.ConstantSampling(cfg.M), cfg.q)
+    assert round(interp.sum()) == plan.interp_rows
+    def imbalance(sl):
+        c = [cost[lo // per:hi // per].sum() for lo, hi in sl]
+        return max(c) / np.mean(c)
+    assert imbalance(weighted_plane_slabs(cost, per, 8)) < 1.08 < 1.3 < imbalance(plane_slabs(ms, 8))
+    assert imbalance(weighted_plane_slabs(cost, per, 4)) < 1.05
