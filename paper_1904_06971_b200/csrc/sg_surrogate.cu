@@ -1169,20 +1169,30 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
     const int64_t halo = (int64_t)p * (1 + dp.m[0] + (int64_t)dp.m[0] * dp.m[1]);
     const int64_t qlo = std::max<int64_t>(0, slab_lo - halo), qhi = std::min<int64_t>(N, slab_hi + halo);
     std::vector<int> tiles;
+    // per direction and tile coordinate: every index in the box / some index sampled (the tile
+    // grid is a tensor product, so a tile's classes are ANDs of three per-direction flags)
+    std::vector<uint8_t> fin[3], fsm[3];
+    for (int d = 0; d < 3; ++d) {
+        fin[d].assign(pl.tgrid[d], 1);
+        fsm[d].assign(pl.tgrid[d], d < n ? 0 : 1);
+        if (d >= n) continue;
+        for (int tc = 0; tc < pl.tgrid[d]; ++tc) {
+            const int64_t lo = (int64_t)tc * pl.T[d], hi = std::min<int64_t>(lo + pl.T[d], dp.m[d]) - 1;
+            for (int64_t k = lo; k <= hi; ++k) {
+                fin[d][tc] = fin[d][tc] && inb[d][k];
+                fsm[d][tc] = fsm[d][tc] || smp[d][k];
+            }
+        }
+    }
     for (int64_t t = 0; t < pl.ntiles; ++t) {
         int64_t lo[3], hi[3];
         tile_box(pl, dp, t, lo, hi);
+        const int64_t tc[3] = {t % pl.tgrid[0], (t / pl.tgrid[0]) % pl.tgrid[1], t / ((int64_t)pl.tgrid[0] * pl.tgrid[1])};
         bool all_in = true, any_samp_all = true, any_lat = true;
         for (int d = 0; d < n; ++d) {
-            bool din = true, dsm = false, dlat = false;
-            for (int64_t k = lo[d]; k <= hi[d]; ++k) {
-                din = din && inb[d][k];
-                dsm = dsm || smp[d][k];
-                dlat = dlat || smp[d][k];
-            }
-            all_in = all_in && din;
-            any_samp_all = any_samp_all && dsm;
-            any_lat = any_lat && dlat;
+            all_in = all_in && fin[d][tc[d]];
+            any_samp_all = any_samp_all && fsm[d][tc[d]];
+            any_lat = any_lat && fsm[d][tc[d]];
         }
         const bool has_quad = !all_in || any_samp_all;
         if (!has_quad) continue;
