@@ -47,19 +47,8 @@ __global__ void __launch_bounds__(kThreads) spmv_dot_kernel(int64_t nrows, const
         const int64_t row = base + sub;
         const bool ok = row < nrows;
         const int64_t b = ok ? ip[row] : 0, e = ok ? ip[row + 1] : 0;
-        // four independent partial chains per lane (more loads in flight), joined in a fixed order
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        int64_t k = b + lane;
-        for (; k + 3 * VS < e; k += 4 * VS) {
-            const double a0 = __ldcs(a + k), a1 = __ldcs(a + k + VS), a2 = __ldcs(a + k + 2 * VS), a3 = __ldcs(a + k + 3 * VS);
-            const int c0 = __ldcs(ix + k), c1 = __ldcs(ix + k + VS), c2 = __ldcs(ix + k + 2 * VS), c3 = __ldcs(ix + k + 3 * VS);
-            s0 = fma(a0, x[c0], s0);
-            s1 = fma(a1, x[c1], s1);
-            s2 = fma(a2, x[c2], s2);
-            s3 = fma(a3, x[c3], s3);
-        }
-        for (; k < e; k += VS) s0 = fma(__ldcs(a + k), x[__ldcs(ix + k)], s0);
-        double s = (s0 + s1) + (s2 + s3);
+        double s = 0.0;
+        for (int64_t k = b + lane; k < e; k += VS) s = fma(__ldcs(a + k), x[__ldcs(ix + k)], s);
 #pragma unroll
         for (int m = VS / 2; m > 0; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m, VS);
         if (lane == 0 && ok) {
