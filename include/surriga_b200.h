@@ -178,6 +178,9 @@ int sg_cg_solve(const sg_result* A, const double* b, double* x, double tol, int6
 
 /* Device-time of the kernels of the last call on this thread (ms), and their launch count. */
 int sg_last_timing(double* ms_total, int32_t* launches);
+/* fp64 tensor-core (DMMA m8n8k4, 512 flops each) instructions the assembly kernel executed in the last
+   call on this thread: the hardware-work figure next to the reference-algorithm flop count. */
+int sg_last_dmma_count(int64_t* count);
 /* Per-kernel breakdown of the last call: name list (comma separated) and ms values. */
 int sg_last_kernel_times(char* names, int32_t names_cap, double* ms, int32_t cap, int32_t* count);
 

@@ -92,6 +92,7 @@ def lib():
         L.sg_last_kernel_times.argtypes = [C.c_char_p, C.c_int32, _d, C.c_int32, _i32]
         L.sg_result_from_host.argtypes = [C.c_int32, C.c_int64, C.c_int64, _i64, _i32, _d, C.POINTER(C.c_void_p)]
         L.sg_spmv.argtypes = [C.c_void_p, _d, _d, C.POINTER(SgExec)]
+        L.sg_last_dmma_count.argtypes = [_i64]
         L.sg_quadrature_fields.argtypes = [C.POINTER(SgProblem), _d, C.c_int32, C.POINTER(SgExec), _d, _d, _d, _d, _d]
         L.sg_write_matrix_market_host.argtypes = [C.c_char_p, C.c_int64, C.c_int64, _i64, _i32, _d, C.c_int32, C.c_int32]
         L.sg_write_matrix_market.argtypes = [C.c_void_p, C.c_int64, C.c_char_p, C.c_int32, C.c_int32]
@@ -106,7 +107,7 @@ SYMBOLS = ("sg_assemble", "sg_surrogate", "sg_result_sizes", "sg_result_copy", "
            "sg_last_kernel_times", "sg_last_error", "sg_version", "sg_max_degree", "sg_host_staging_init",
            "sg_assemble_divergence", "sg_surrogate_divergence", "sg_host_register", "sg_host_unregister",
            "sg_map_points", "sg_assemble_load", "sg_result_from_host", "sg_spmv", "sg_cg_solve",
-           "sg_quadrature_fields", "sg_write_matrix_market_host", "sg_write_matrix_market")
+           "sg_quadrature_fields", "sg_write_matrix_market_host", "sg_write_matrix_market", "sg_last_dmma_count")
 
 
 def check(rc):
@@ -290,6 +291,13 @@ def last_timing():
     n = C.c_int32()
     lib().sg_last_timing(C.byref(ms), C.byref(n))
     return ms.value, n.value
+
+
+def last_dmma_count():
+    """DMMA (m8n8k4 f64, 512 flops) instructions executed by the assembly kernel in the last call."""
+    c = C.c_int64()
+    lib().sg_last_dmma_count(C.byref(c))
+    return c.value
 
 
 def last_kernel_times():

@@ -33,6 +33,7 @@ static thread_local std::string g_err;
 static thread_local double g_last_ms = 0.0;
 static thread_local int g_last_launches = 0;
 static thread_local std::vector<std::pair<std::string, double>> g_ktimes;
+static thread_local unsigned long long g_last_dmma = 0;
 
 int fail(int code, const char* fmt, ...) {
     char buf[1024];
@@ -126,6 +127,8 @@ void Call::record_timing() {
     float ms = 0.f;
     if (cudaEventSynchronize(ev1) == cudaSuccess && cudaEventElapsedTime(&ms, ev0, ev1) == cudaSuccess) g_last_ms = ms;
     g_last_launches = launches;
+    g_last_dmma = 0;
+    if (dmma) cudaMemcpy(&g_last_dmma, dmma, sizeof(g_last_dmma), cudaMemcpyDeviceToHost);
     g_ktimes.clear();
     for (auto& k : kev) {
         float t = 0.f;
@@ -608,6 +611,11 @@ int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>
         mp.indices = d_indices;
         mp.data = d_data;
         mp.zeros = d_zeros;
+        if (!c.dmma) {
+            c.dmma = (unsigned long long*)c.alloc(sizeof(unsigned long long), true);
+            if (c.dmma) cudaMemsetAsync(c.dmma, 0, sizeof(unsigned long long), c.stream);
+        }
+        mp.dmma = c.dmma;
         int64_t nb = pl.ntiles;
         if (tiles) {
             mp.tiles = (const int*)c.upload(tiles->data(), sizeof(int) * tiles->size());
@@ -736,6 +744,12 @@ extern "C" {
 const char* sg_last_error(void) { return g_err.c_str(); }
 const char* sg_version(void) { return "surriga_b200 0.1.0 (sm_100a)"; }
 int sg_max_degree(void) { return SG_MAX_P; }
+
+int sg_last_dmma_count(int64_t* count) {
+    if (!count) return fail(-1, "null argument");
+    *count = (int64_t)g_last_dmma;
+    return 0;
+}
 
 int sg_last_timing(double* ms_total, int32_t* launches) {
     if (ms_total) *ms_total = g_last_ms;

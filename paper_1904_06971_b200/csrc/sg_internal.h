@@ -38,6 +38,7 @@ struct Call {
     };
     std::vector<KEv> kev;
     int launches = 0;
+    unsigned long long* dmma = nullptr;  // device counter of executed DMMA instructions (K4)
     explicit Call(const sg_exec* ex);
     ~Call();
     void* alloc(size_t bytes, bool temp);

@@ -388,6 +388,7 @@ struct MmaParams {
     unsigned long long* zeros;
     int tma;                     // 1: TMA double-buffered D windows; 0: plain loads (debug / fallback)
     int Dys;
+    unsigned long long* dmma;    // executed DMMA instructions (per warp, summed per launch), or nullptr
 };
 
 template <int NDIM, int P, int FORM, bool RAT>
@@ -405,6 +406,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
     extern __shared__ double smem[];
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
+    unsigned long long ndmma = 0;  // DMMA instructions this warp issues (reported per launch)
     const int lr = lane >> 2, lk = lane & 3;
 
     const int tile = prm.tiles ? prm.tiles[blockIdx.x] : (int)blockIdx.x;
@@ -639,6 +641,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
 #pragma unroll
                 for (int c = 0; c < NTI; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
             const int ue = tab[TAB::S.o_u1b + Gc + 1];
+            ndmma += (unsigned long long)(ue - tab[TAB::S.o_u1b + Gc]) * KS * NTI * MT;
             for (int unit = tab[TAB::S.o_u1b + Gc]; unit < ue; ++unit) {
                 const int ud = tab[TAB::S.o_u1ud + unit];
                 const double* af = A1f + ((i0l * M.NU1 + unit) * KS) * MT * 32 + lane;
@@ -754,6 +757,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
 #pragma unroll
                     for (int c = 0; c < MT; ++c) accS[a][c][0] = accS[a][c][1] = 0.0;
                 const int ue = tab[TAB::S.o_u2b + Gc + 1];
+                ndmma += (unsigned long long)(ue - tab[TAB::S.o_u2b + Gc]) * KS * MT * MT;  // + one more per pair below
                 for (int u = tab[TAB::S.o_u2b + Gc]; u < ue; ++u) {
                     const int d = tab[TAB::S.o_u2 + u];
                     const int ga = d & 255, kd = (d >> 16) & 15;
@@ -761,6 +765,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
                         block(ga, kd, accS);
                     } else {
                         double tA[MT][MT][2], tB[MT][MT][2];
+                        ndmma += KS * MT * MT;
 #pragma unroll
                         for (int a = 0; a < MT; ++a)
 #pragma unroll
@@ -875,6 +880,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
                     for (int mm = 0; mm < CH; ++mm)
 #pragma unroll
                         for (int c = 0; c < MT; ++c) accS[mm][c][0] = accS[mm][c][1] = 0.0;
+                    ndmma += (unsigned long long)(TTS::T.NF + f_npairs(TTS::T)) * KS3 * CH * MT;  // compile-time per item
                     for (int u = 0; u < TTS::T.NF; ++u) {
                         const int d = tab[TAB::S.o_u3 + u];
                         const int ga = d & 255, kd = (d >> 16) & 15;
@@ -964,6 +970,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
             __syncthreads();
         }
     }
+    if (prm.dmma && lane == 0 && ndmma) atomicAdd(prm.dmma, ndmma);  // all lanes of a warp run the same items
 }
 
 }  // namespace sg
