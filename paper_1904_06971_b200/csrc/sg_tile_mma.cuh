@@ -121,6 +121,15 @@ __host__ __device__ constexpr int pad8_4(int v) {  // smallest w >= v with w % 8
     return w;
 }
 
+#ifndef SG_CH_MASS
+#define SG_CH_MASS 4
+#endif
+#ifndef SG_P12_EPI
+#define SG_P12_EPI 0
+#endif
+#ifndef SG_P3_EPI
+#define SG_P3_EPI 3
+#endif
 #ifndef SG_3D_NW
 #define SG_3D_NW 24
 #endif
@@ -187,7 +196,7 @@ __host__ __device__ constexpr MmaGeom mma_geom(int ndim, int P, int form, bool r
     m.TY = pad8_4(m.NTY * 8 > m.YW + 4 ? m.NTY * 8 : m.YW + 4);
     m.NCOMBO = T0 * m.T1 * m.W * m.W;
     m.NMT = (m.NCOMBO + 7) / 8;
-    m.CH = 4;
+    m.CH = form == 1 ? SG_CH_MASS : 4;  // mass: finer phase-3 items (its epilogue, not DMMA, dominates)
     m.NCH = (m.NMT + m.CH - 1) / m.CH;
     m.TC = pad8_4(m.NCH * m.CH * 8);
     m.NCP = pad8_4(m.NCH * m.CH * 8);
@@ -296,7 +305,7 @@ __host__ __device__ constexpr MmaTab mma_tab(int ndim, int P, int form, bool rat
         n = 0;
     };
     for (int k = 0; k < n1; ++k) {
-        cost[n] = T.g1n[k / (M.T0 * M.NC1)] * M.KS * M.MT * (M.NTY / M.NC1) + 2;
+        cost[n] = T.g1n[k / (M.T0 * M.NC1)] * M.KS * M.MT * (M.NTY / M.NC1) + 2 + SG_P12_EPI * M.MT * (M.NTY / M.NC1);
         kind[n] = 1; idx[n] = k; done[n] = false; ++n;
     }
     if (ndim != 3) {  // 2D: phase 2 after its own barrier
@@ -304,13 +313,13 @@ __host__ __device__ constexpr MmaTab mma_tab(int ndim, int P, int form, bool rat
         for (int v = 0; v < NW; ++v) load[v] = 0;
     }
     for (int k = 0; k < n2; ++k) {
-        cost[n] = g2_blocks(T, k / (M.T1 * M.T0)) * M.KS * M.MT * M.MT + 2;
+        cost[n] = g2_blocks(T, k / (M.T1 * M.T0)) * M.KS * M.MT * M.MT + 2 + SG_P12_EPI * M.MT * M.MT;
         kind[n] = 2; idx[n] = k; done[n] = false; ++n;
     }
     lpt();
     const int fb = T.NF + f_npairs(T);
     for (int k = 0; k < n3; ++k) {
-        cost[n] = fb * M.KS3 * M.CH * M.MT + 2;
+        cost[n] = fb * M.KS3 * M.CH * M.MT + 2 + SG_P3_EPI * M.CH;  // + epilogue (live-sum update / CSR write)
         kind[n] = 3; idx[n] = k; done[n] = false; ++n;
     }
     lpt();
