@@ -119,18 +119,6 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------------------------------
-# slabs
-# ---------------------------------------------------------------------------------------------
-
-def plane_slabs(ms, world):
-    """Contiguous row slabs cut on slowest-direction planes."""
-    planes = ms[-1]
-    per = int(np.prod(ms[:-1]))
-    cuts = [round(planes * r / world) for r in range(world + 1)]
-    return [(cuts[r] * per, cuts[r + 1] * per) for r in range(world)]
-
-
-# ---------------------------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------------------------
 

@@ -654,9 +654,6 @@ __global__ void __launch_bounds__(512, 2) interp_fix_kernel(SurrParams s) {
 // Tap weights are padded to the 5-wide window (one zero tap; adding the +-0 product leaves the
 // 4-tap FMA chain's value unchanged); every lane reads the same weights (broadcast loads).
 // ---------------------------------------------------------------------------------------------
-#ifndef SG_EXP
-#define SG_EXP 0
-#endif
 namespace rows3 {
 constexpr int TB0 = 4, TB1 = 4, TB2 = 8, NR = TB0 * TB1 * TB2, CW = 5, MAXSH = 9, NWARP = 8;
 constexpr int AS = 6;             // scratch A row stride (doubles): [(t2, t1)][AS] holding b0 = 0..3
@@ -798,7 +795,7 @@ __global__ void __launch_bounds__(256, 2) interp_rows3_kernel(SurrParams s) {
     double rsum = 0.0, dg = 0.0;
     for (int c = 0; c < NS; ++c) {
         // ---- compute the chunk's values into the stage
-        for (int k = kb; k < (SG_EXP == 2 ? kb : ke); ++k) {
+        for (int k = kb; k < ke; ++k) {
             const int o = c * K + k;
             const int oi = oinf[o];
             const int sh0 = (oi >> 16) & 15, sh1 = (oi >> 20) & 15, sh2 = oi >> 24;  // shift + p
@@ -874,7 +871,7 @@ __global__ void __launch_bounds__(256, 2) interp_rows3_kernel(SurrParams s) {
         __syncthreads();
         // ---- write the warp's row segments of the chunk: entries flattened over (row, k) so the
         //      lanes stay busy; consecutive lanes write consecutive CSR slots of a row
-        int rl = SG_EXP == 3 ? RPW : lane / K, k = lane - (lane / K) * K;
+        int rl = lane / K, k = lane - (lane / K) * K;
         for (; rl < RPW; k += 32, rl += k / K, k %= K) {
             const int r = RPW * warp + rl;
             const int rb = rbr[r];
@@ -884,10 +881,8 @@ __global__ void __launch_bounds__(256, 2) interp_rows3_kernel(SurrParams s) {
             const double v = stage[r * K + k];
             n_int++;  // provisional for slow rows (corrected by slow_rows_kernel)
             n_zero += v == 0.0;
-            if (SG_EXP != 1) {
-                tdata[rb + o] = v;
-                tidx[rb + o] = col;
-            }
+            tdata[rb + o] = v;
+            tidx[rb + o] = col;
         }
         __syncwarp();
         // ---- SKP row sums of the warp's rows (lane = row; ascending offsets)
