@@ -270,7 +270,16 @@ def run_ours(args):
     ranked = [r for r in rows if r.get("bound")]
     dom = dict(ranked[0]) if ranked else {}
     roof = {k: dom.get(k) for k in ("bound", "achieved", "peak", "unit", "frac", "issued_tflops", "issued_frac")}
-    roof.update({"traffic": None, "kernel": dom.get("kernel"), "peak_source": "measured fp64 microbenchmark"
+    traffic = None
+    try:  # DRAM bytes of the dominant kernel from its committed ncu --set full capture (per launch)
+        tr = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")))
+        t = tr.get(dom.get("kernel") or "")
+        if t and world == 1:
+            traffic = {"bytes": t["dram_bytes_read"] + t["dram_bytes_write"], "read": t["dram_bytes_read"],
+                       "write": t["dram_bytes_write"], "source": t["source"]}
+    except (OSError, ValueError, KeyError):
+        traffic = None
+    roof.update({"traffic": traffic, "kernel": dom.get("kernel"), "peak_source": "measured fp64 microbenchmark"
                  if dom.get("unit") == "TFLOP/s" else hbm_src,
                  "algorithmic": "SURVEY §8d reference-algorithm flops (F_elem x elements); the kernel is sum-factorised",
                  "issued": "issued_tflops / issued_frac: the fp64 tensor-core work the kernel actually executed "
