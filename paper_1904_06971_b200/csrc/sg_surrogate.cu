@@ -870,26 +870,44 @@ __global__ void __launch_bounds__(256, 2) interp_rows3_kernel(SurrParams s) {
         }
         __syncthreads();
         // ---- write the warp's row segments of the chunk: entries flattened over (row, k) so the
-        //      lanes stay busy; consecutive lanes write consecutive CSR slots of a row
-        int rl = lane / K, k = lane - (lane / K) * K;
-        for (; rl < RPW; k += 32, rl += k / K, k %= K) {
-            const int r = RPW * warp + rl;
-            const int rb = rbr[r];
-            if (rb < 0) continue;
-            const int o = c * K + k;
-            const int col = rowid[r] + shl[o];
-            const double v = stage[r * K + k];
-            n_int++;  // provisional for slow rows (corrected by slow_rows_kernel)
-            n_zero += v == 0.0;
-            tdata[rb + o] = v;
-            tidx[rb + o] = col;
+        //      lanes stay busy; consecutive lanes write consecutive CSR slots of a row.  The trip
+        //      count is a compile-time constant, so unrolled iterations issue their shared loads
+        //      together (the loop was bound by shared-load latency)
+        constexpr int NE = RPW * K, NIT = (NE + 31) / 32;
+#pragma unroll 5
+        for (int it = 0; it < NIT; ++it) {
+            const int e = it * 32 + lane;
+            if (e < NE) {
+                const int rl = e / K, k = e - rl * K;
+                const int r = RPW * warp + rl;
+                const int rb = rbr[r];
+                const int o = c * K + k;
+                const int col = rowid[r] + shl[o];
+                const double v = stage[r * K + k];
+                if (rb >= 0) {
+                    n_int++;  // provisional for slow rows (corrected by slow_rows_kernel)
+                    n_zero += v == 0.0;
+                    tdata[rb + o] = v;
+                    tidx[rb + o] = col;
+                }
+            }
         }
         __syncwarp();
-        // ---- SKP row sums of the warp's rows (lane = row; ascending offsets)
+        // ---- SKP row sums of the warp's rows (lane = row; ascending offsets in four interleaved
+        //      partial sums, joined in a fixed order)
         if (lane < RPW && rbS[rsl] >= 0) {
             const double* sr = stage + (size_t)rsl * K;
-#pragma unroll 7
-            for (int k = 0; k < K; ++k) rsum += sr[k];
+            double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0;
+#pragma unroll
+            for (int k = 0; k + 3 < K; k += 4) {
+                q0 += sr[k];
+                q1 += sr[k + 1];
+                q2 += sr[k + 2];
+                q3 += sr[k + 3];
+            }
+#pragma unroll
+            for (int k = K & ~3; k < K; ++k) q0 += sr[k];
+            rsum += (q0 + q1) + (q2 + q3);
             if (c == p) dg = sr[(K - 1) / 2];
         }
         __syncthreads();
