@@ -89,3 +89,26 @@ def test_gpu_surrogate_rows3_kernel_vs_oracle(p, spans, M, form, mode):
     assert A.symmetric == sym
     if sym:
         assert pkg.is_bitwise_symmetric(A)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p,spans,form", [(1, (30, 29, 31), "poisson"), (4, (37, 38, 36), "mass"), (4, (37, 38, 36), "poisson")])
+def test_gpu_rows3_kernel_matches_64row_kernel(p, spans, form, monkeypatch):
+    # degrees 1 and 4 of the row-staged kernel against the 64-row-tile kernel (SG_INTERP_FIX=1) on
+    # the same surrogate: identical pattern and counts, values within 1e-12 row-scaled
+    import paper_1904_06971_b200 as pkg
+    from paper_1904_06971_b200 import _lib
+
+    disc = pkg.make_discretization(pkg.twisted_cube_standin(), p, spans)
+    fk = pkg.FormKind(form)
+    A, rep = pkg.build_surrogate_matrix(fk, disc, pkg.ConstantSampling(8))
+    assert "interp_rows3" in [n for n, _ in _lib.last_kernel_times()]
+    monkeypatch.setenv("SG_INTERP_FIX", "1")
+    B, rep2 = pkg.build_surrogate_matrix(fk, disc, pkg.ConstantSampling(8))
+    assert "interp_rows3" not in [n for n, _ in _lib.last_kernel_times()]
+    a, b = A.mat, B.mat
+    assert np.array_equal(a.indptr, b.indptr) and np.array_equal(a.indices, b.indices)
+    assert O.row_scaled_error(b.indptr, b.indices, b.data, a.indptr, a.indices, a.data) <= TOL
+    assert rep.interp_entries == rep2.interp_entries and rep.quad_entries == rep2.quad_entries
+    if A.symmetric:
+        assert pkg.is_bitwise_symmetric(A)
