@@ -1080,7 +1080,8 @@ int sg_host_staging_init(int device) {
 int sg_result_copy_i64(const sg_result* r, int64_t* indptr, int32_t* indices, double* data) {
     if (!r) return fail(-1, "null result");
     cudaSetDevice(r->dev);
-    cudaDeviceSynchronize();
+    // every call that creates a result synchronises its stream before returning the handle, so no
+    // device-wide synchronisation here: a copy can overlap the next assembly on the same device
     int rc = 0;
     if (indptr && (rc = d2h(indptr, r->indptr, sizeof(int64_t) * (r->nrows + 1), r->dev))) return rc;
     if (r->nnz > 0) {
