@@ -118,3 +118,33 @@ def test_gpu_surrogate_weighted_slabs_rows3(form):
     ip, ix, d = stitch(parts)
     assert np.array_equal(ip, fip) and np.array_equal(ix, fix)
     assert np.array_equal(d.view(np.int64), fd.view(np.int64))
+
+
+@pytest.mark.gpu
+def test_gpu_concurrent_calls_are_reentrant():
+    # studies call the entry points from a ThreadPoolExecutor (studies.py:89-95); ctypes
+    # releases the GIL, so calls overlap in the library: results equal the sequential ones bit for bit
+    from concurrent.futures import ThreadPoolExecutor
+
+    import paper_1904_06971_b200 as pkg
+
+    jobs = [(pkg.twisted_cube_standin(), 2, (9, 8, 10), "poisson", "full"),
+            (pkg.quarter_annulus(1.0, 2.0), 3, (40, 36), "mass", "full"),
+            (pkg.twisted_cube_standin(), 3, (28, 29, 27), "poisson", "surrogate"),
+            (pkg.sin_map_standin(), 3, (30, 30), "biharmonic", "surrogate"),
+            (pkg.quarter_annulus(1.0, 2.0), 2, (50, 44), "poisson", "surrogate")]
+
+    def run(job):
+        geo, p, spans, form, path = job
+        disc = pkg.make_discretization(geo, p, spans)
+        if path == "full":
+            return pkg.assemble(pkg.FormKind(form), disc).mat
+        return pkg.build_surrogate_matrix(pkg.FormKind(form), disc, pkg.ConstantSampling(8))[0].mat
+
+    seq = [run(j) for j in jobs]
+    with ThreadPoolExecutor(max_workers=len(jobs)) as ex:
+        par = list(ex.map(run, jobs * 2))
+    for k, m in enumerate(par):
+        s = seq[k % len(jobs)]
+        assert np.array_equal(m.indptr, s.indptr) and np.array_equal(m.indices, s.indices)
+        assert np.array_equal(m.data.view(np.int64), s.data.view(np.int64))
