@@ -419,6 +419,11 @@ int compute_D(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* t
     gp.nbx = (gp.Gp[0] + gp.BX - 1) / gp.BX;
     gp.nby = (gp.Gp[1] + gp.BY - 1) / gp.BY;
     const int64_t nblk_all = (int64_t)gp.nbx * gp.nby * gp.Gp[2];
+    // 3D: several z-planes per block (the x/y tables and spans are loaded once), enough blocks for
+    // every SM several times over
+    gp.ZB = 1;
+    if (n == 3)
+        while (gp.ZB < 8 && (int64_t)gp.nbx * gp.nby * ((gp.Gp[2] + 2 * gp.ZB - 1) / (2 * gp.ZB)) >= 8 * 148) gp.ZB *= 2;
     // function-range bounds per block
     auto gbound = [&](int d, int B) {
         int mx = 1;
@@ -491,7 +496,7 @@ int compute_D(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* t
     void* kfn = get_geom_kernel(n, dp.pr.form, dp.rational);
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     void* args[] = {&gp};
-    const int64_t nb = nblk_all;
+    const int64_t nb = (int64_t)gp.nbx * gp.nby * ((gp.Gp[2] + gp.ZB - 1) / gp.ZB);
     c.kbegin("geom_D");
     cudaError_t e = cudaLaunchKernel(kfn, dim3((unsigned)nb), dim3(256), args, smem, c.stream);
     c.kend();

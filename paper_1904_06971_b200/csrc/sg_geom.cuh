@@ -353,6 +353,7 @@ struct GeomParams {
     int GN0, GN1, WN0, WN1;  // smem bounds of function ranges
     int off_G0, off_G1, off_gs0, off_gs1, off_B0, off_B1, off_ws0, off_ws1, off_Hz, off_Hy, off_Wz, off_Wy, off_misc;
     int U;
+    int ZB;                  // z-planes per block (3D): the x/y tables are loaded once per block
     int Dys;                 // y stride of D (Gp1 rounded up to even: 16-byte rows for TMA)
     double* D;               // [Gp2][U][Gp0][Dys]
 };
@@ -369,9 +370,16 @@ __global__ void __launch_bounds__(256) geom_D_kernel(const GeomParams prm) {
     const int g = prm.g, pg = prm.pg, p = prm.p;
     const int NB = (NU + 1) * (p + 1), NBG = (NUG + 1) * (pg + 1);
     const int NBp = NB | 1, NBGp = NBG | 1;  // odd per-point strides: per-lane y tables conflict free
-    const int blk = prm.blocks ? prm.blocks[blockIdx.x] : (int)blockIdx.x;
-    if (prm.blockmask && !prm.blockmask[blk]) return;
-    const int bx = blk % prm.nbx, by = (blk / prm.nbx) % prm.nby, z = blk / (prm.nbx * prm.nby);
+    // block = (bx, by, z-batch of ZB planes); a plane whose (bx, by, z) block is not marked in a
+    // restricted plan is skipped
+    const int blk = (int)blockIdx.x;
+    const int bx = blk % prm.nbx, by = (blk / prm.nbx) % prm.nby, zb = blk / (prm.nbx * prm.nby);
+    const int z0 = zb * prm.ZB, z1 = min(prm.Gp[2], z0 + prm.ZB);
+    if (prm.blockmask) {
+        bool any = false;
+        for (int z = z0; z < z1; ++z) any = any || prm.blockmask[bx + prm.nbx * (by + prm.nby * z)];
+        if (!any) return;
+    }
     const int x0 = bx * prm.BX, y0 = by * prm.BY;
     const int X = min(prm.BX, prm.Gp[0] - x0);
     const int Y = NDIM >= 2 ? min(prm.BY, prm.Gp[1] - y0) : 1;
@@ -412,6 +420,9 @@ __global__ void __launch_bounds__(256) geom_D_kernel(const GeomParams prm) {
             for (int y = tid; y < Y; y += nt) ws1[y] = (y0 + y) / g + p;
         }
     }
+    for (int z = z0; z < z1; ++z) {
+    if (prm.blockmask && !prm.blockmask[bx + prm.nbx * (by + prm.nby * z)]) continue;  // uniform over the block
+    __syncthreads();  // the previous plane's Hz / Hx / z tables are no longer read
     int sz = 0, szw = 0;
     if constexpr (NDIM == 3) {
         for (int k = tid; k < NBG; k += nt) G2p[k] = prm.G[2][(long long)z * NBG + k];
@@ -458,6 +469,7 @@ __global__ void __launch_bounds__(256) geom_D_kernel(const GeomParams prm) {
         for (int u = 0; u < U; ++u)
             prm.D[((plane + u) * prm.Gp[0] + x0 + x) * (long long)prm.Dys + y0 + y] = Dp[u];
     }
+    }  // z planes of the block
 }
 
 }  // namespace sg
