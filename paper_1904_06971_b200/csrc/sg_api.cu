@@ -528,7 +528,14 @@ static int encode_dmap(CUtensorMap* map, const double* D, int Dys, const int Gp[
     return 0;
 }
 
-static bool plan_mma(DevProblem& dp, Plan& pl) {
+static int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return (v && *v) ? atoi(v) : dflt;
+}
+// tile depth in z (rows) for restricted plans (quadrature rows, rows=); whole-matrix plans choose theirs
+constexpr int kT2Restricted = 24;
+
+static bool plan_mma(DevProblem& dp, Plan& pl, int t2) {
     const int n = dp.n, P = dp.p, g = dp.g;
     if (P > 4 || g != P + 1 || getenv("SG_NO_MMA")) return false;
     int nthreads = 0;
@@ -542,16 +549,36 @@ static bool plan_mma(DevProblem& dp, Plan& pl) {
     pl.nthreads = nthreads;
     pl.T[0] = M.T0;
     pl.T[1] = M.T1;
-    pl.T[2] = n == 3 ? kMmaT2 : 1;
+    // z depth of a tile: deeper tiles recompute fewer halo planes per owned plane (the p element
+    // layers below a tile are streamed again by the tile below); restricted plans (surrogate
+    // quadrature rows, rows=) touch few planes per tile and prefer shallower tiles
+    if (n == 3) {
+        if (t2 <= 0) t2 = env_int("SG_T2_FULL", 0);
+        if (t2 <= 0) {
+            // whole-matrix plans: the fewest, deepest z tiles (<= kMmaT2 rows, equal depths) that still
+            // give every SM several tiles (config 5: two tiles of 66 rows, 48.4 -> 41.5 ms for Poisson)
+            int sms = 148, dev = 0;
+            cudaGetDevice(&dev);  // the calling Call has selected its device
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            const int64_t xy = (int64_t)((dp.m[0] + M.T0 - 1) / M.T0) * ((dp.m[1] + M.T1 - 1) / M.T1);
+            int nz = (dp.m[2] + kMmaT2 - 1) / kMmaT2;
+            while (xy * nz < 8LL * sms && nz < dp.m[2]) ++nz;
+            t2 = (dp.m[2] + nz - 1) / nz;
+        }
+        pl.T[2] = std::min(kMmaT2, std::max(1, t2));
+    } else {
+        pl.T[2] = 1;
+    }
     for (int d = 0; d < 3; ++d) pl.tgrid[d] = (dp.m[d] + pl.T[d] - 1) / pl.T[d];
     pl.smem = M.total * sizeof(double);
     pl.ntiles = (int64_t)pl.tgrid[0] * pl.tgrid[1] * pl.tgrid[2];
     return true;
 }
 
-int plan_assembly(DevProblem& dp, Plan& pl) {
+int plan_assembly(DevProblem& dp, Plan& pl, bool restricted) {
+    const int t2 = restricted ? env_int("SG_T2_RESTR", kT2Restricted) : 0;
     pl.mma = false;
-    if (plan_mma(dp, pl)) return 0;
+    if (plan_mma(dp, pl, t2)) return 0;
     pl.kfn = get_kernel(dp.n, dp.pr.form, dp.p, dp.rational, &pl.kmax);
     if (!pl.kfn) return fail(-2, "no kernel instantiated for n=%d p=%d form=%d", dp.n, dp.p, dp.pr.form);
     pl.nthreads = 512;
@@ -681,7 +708,7 @@ int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>
 int launch_assembly(Call& c, DevProblem& dp, const uint8_t* d_rowmask, const int64_t* d_rowstart, const int64_t* h_rows,
                     int64_t nrows, int64_t slab_lo, int64_t slab_hi, int* d_indices, double* d_data) {
     Plan pl;
-    int rc = plan_assembly(dp, pl);
+    int rc = plan_assembly(dp, pl, h_rows != nullptr);
     if (rc) return rc;
     const bool full_slab = (slab_lo <= 0 && slab_hi >= dp.N);
     if (!h_rows && full_slab) return run_assembly(c, dp, pl, nullptr, d_rowmask, d_rowstart, slab_lo, slab_hi, d_indices, d_data, nullptr);

@@ -81,7 +81,7 @@ struct Plan {
 };
 
 int prepare_problem(Call& c, const sg_problem* pr, DevProblem& dp);
-int plan_assembly(DevProblem& dp, Plan& pl);
+int plan_assembly(DevProblem& dp, Plan& pl, bool restricted = false);
 void tile_box(const Plan& pl, const DevProblem& dp, int64_t t, int64_t lo[3], int64_t hi[3]);
 int64_t tile_of_row(const Plan& pl, const DevProblem& dp, int64_t r);
 int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* tiles, const uint8_t* d_rowmask,

@@ -1177,7 +1177,7 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
 
     // ---- K4: quadrature rows (the slab's quad rows + halo neighbours + every lattice row)
     Plan pl;
-    rc = plan_assembly(dp, pl);
+    rc = plan_assembly(dp, pl, true);
     if (rc) return rc;
     const int64_t halo = (int64_t)p * (1 + dp.m[0] + (int64_t)dp.m[0] * dp.m[1]);
     const int64_t qlo = std::max<int64_t>(0, slab_lo - halo), qhi = std::min<int64_t>(N, slab_hi + halo);

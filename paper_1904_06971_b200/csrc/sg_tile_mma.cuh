@@ -163,7 +163,10 @@ __host__ __device__ constexpr int mma_minb(int ndim, int P, int form, bool rat) 
 }
 
 // ---- compile-time tile geometry (shared by host planning and the kernel)
-constexpr int kMmaT2 = 16;  // rows per CTA in z (3D)
+#ifndef SG_MMA_T2
+#define SG_MMA_T2 72
+#endif
+constexpr int kMmaT2 = SG_MMA_T2;  // max rows per CTA in z (3D); the plan picks the depth T2 <= kMmaT2 per call
 
 struct MmaGeom {
     int NC1, NCP, T0, T1, G, W, MT, KS, KS3, XW, XWp, YW, NTY, DY, TY, NCOMBO, NMT, CH, NCH, TC, U, NG1, NG2, NU1, NB, NK1, NK2;
