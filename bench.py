@@ -180,14 +180,16 @@ def run_ours(args):
         res.free()
         return nnz, nrows, nl, kt, cs, n_irows
 
+    # the clock sampler (an nvidia-smi process polling every 100 ms) starts before the warm-up: its
+    # start-up (NVML initialisation) stalled the first timed step by ~15 ms when started right before it
+    clocks = Clocks(local)
+    clocks.start()
     for _ in range(args.warmup):
         for f, path in jobs:
             one(f, path)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    clocks = Clocks(local)
-    clocks.start()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
