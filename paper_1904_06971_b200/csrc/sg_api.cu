@@ -368,7 +368,10 @@ static int choose_layout(const DevProblem& dp, int kmax, int nthreads, Layout& o
 static void* get_geom_kernel(int n, int form, bool rat) { return kernel_ptr(n, form, rat, 2, 1, nullptr); }
 
 struct GeomMark {
-    int n, P, g, T[3], tg[3], S[3], BX, BY, nbx, nby;
+    int n, P, g, T[3], tg[3], S[3], BX, BY, nbx, nby, z0;
+    int m[3];
+    const uint8_t* rowmask;  // restricted plans: rows the tiles own (nullptr: every row of the slab)
+    int64_t slab_lo, slab_hi;
 };
 // geometry blocks needed by a tile list: the element window [lo - P, lo + T - 1] of every tile
 __global__ void geom_mark_kernel(GeomMark m, const int* __restrict__ tiles, int64_t ntiles, uint8_t* __restrict__ mask) {
@@ -377,9 +380,30 @@ __global__ void geom_mark_kernel(GeomMark m, const int* __restrict__ tiles, int6
     const int t = tiles[i];
     const int tc[3] = {t % m.tg[0], (t / m.tg[0]) % m.tg[1], t / (m.tg[0] * m.tg[1])};
     int64_t plo[3] = {0, 0, 0}, phi[3] = {0, 0, 0};
+    int64_t rlo[3], rhi[3];  // the tile's row box
+    for (int d = 0; d < 3; ++d) {
+        rlo[d] = (d == 2 ? m.z0 : 0) + (int64_t)tc[d] * m.T[d];
+        rhi[d] = min((int64_t)m.m[d] - 1, rlo[d] + m.T[d] - 1);
+    }
+    if (m.n == 3) {
+        // slowest direction: only the rows the tile owns (the kernel streams just their layers; a
+        // tile kept for a few sampled rows needs a few planes of D, not its whole depth)
+        int64_t zlo = INT64_MAX, zhi = -1;
+        for (int64_t i2 = rlo[2]; i2 <= rhi[2]; ++i2)
+            for (int64_t i1 = rlo[1]; i1 <= rhi[1]; ++i1)
+                for (int64_t i0 = rlo[0]; i0 <= rhi[0]; ++i0) {
+                    const int64_t row = i0 + (int64_t)m.m[0] * (i1 + (int64_t)m.m[1] * i2);
+                    if (row >= m.slab_lo && row < m.slab_hi && (!m.rowmask || m.rowmask[row])) {
+                        zlo = min(zlo, i2);
+                        zhi = max(zhi, i2);
+                    }
+                }
+        if (zhi < 0) return;
+        rlo[2] = zlo;
+        rhi[2] = zhi;
+    }
     for (int d = 0; d < m.n; ++d) {
-        const int64_t lo = (int64_t)tc[d] * m.T[d];
-        const int64_t e0 = max((int64_t)0, lo - m.P), e1 = min((int64_t)m.S[d] - 1, lo + m.T[d] - 1);
+        const int64_t e0 = max((int64_t)0, rlo[d] - m.P), e1 = min((int64_t)m.S[d] - 1, rhi[d]);
         plo[d] = e0 * m.g;
         phi[d] = (e1 + 1) * m.g - 1;
     }
@@ -388,7 +412,8 @@ __global__ void geom_mark_kernel(GeomMark m, const int* __restrict__ tiles, int6
             for (int64_t bx = plo[0] / m.BX; bx <= phi[0] / m.BX; ++bx) mask[bx + m.nbx * (by + m.nby * z)] = 1;
 }
 
-int compute_D(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* tiles) {
+int compute_D(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* tiles, const uint8_t* d_rowmask,
+              int64_t slab_lo, int64_t slab_hi) {
     const int n = dp.n, g = dp.g, P = dp.p, pg = dp.pr.geo_p;
     const Tables TT = make_tables(n, dp.pr.form, dp.rational);
     const int U = TT.MS * (TT.MS + 1) / 2;
@@ -484,6 +509,11 @@ int compute_D(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* t
             gm.tg[d] = pl.tgrid[d];
             gm.S[d] = dp.S[d];
         }
+        gm.z0 = pl.z0;
+        for (int d = 0; d < 3; ++d) gm.m[d] = dp.m[d];
+        gm.rowmask = d_rowmask;
+        gm.slab_lo = slab_lo;
+        gm.slab_hi = slab_hi;
         gm.BX = gp.BX;
         gm.BY = gp.BY;
         gm.nbx = gp.nbx;
@@ -535,7 +565,7 @@ static int env_int(const char* name, int dflt) {
 // tile depth in z (rows) for restricted plans (quadrature rows, rows=); whole-matrix plans choose theirs
 constexpr int kT2Restricted = 24;
 
-static bool plan_mma(DevProblem& dp, Plan& pl, int t2) {
+static bool plan_mma(DevProblem& dp, Plan& pl, int t2, int z0) {
     const int n = dp.n, P = dp.p, g = dp.g;
     if (P > 4 || g != P + 1 || getenv("SG_NO_MMA")) return false;
     int nthreads = 0;
@@ -561,24 +591,28 @@ static bool plan_mma(DevProblem& dp, Plan& pl, int t2) {
             cudaGetDevice(&dev);  // the calling Call has selected its device
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
             const int64_t xy = (int64_t)((dp.m[0] + M.T0 - 1) / M.T0) * ((dp.m[1] + M.T1 - 1) / M.T1);
-            int nz = (dp.m[2] + kMmaT2 - 1) / kMmaT2;
-            while (xy * nz < 8LL * sms && nz < dp.m[2]) ++nz;
-            t2 = (dp.m[2] + nz - 1) / nz;
+            const int nzr = dp.m[2] - z0;  // planes from the grid origin
+            int nz = (nzr + kMmaT2 - 1) / kMmaT2;
+            while (xy * nz < 8LL * sms && nz < nzr) ++nz;
+            t2 = (nzr + nz - 1) / nz;
         }
         pl.T[2] = std::min(kMmaT2, std::max(1, t2));
+        pl.z0 = z0;
     } else {
         pl.T[2] = 1;
+        pl.z0 = 0;
     }
-    for (int d = 0; d < 3; ++d) pl.tgrid[d] = (dp.m[d] + pl.T[d] - 1) / pl.T[d];
+    for (int d = 0; d < 3; ++d) pl.tgrid[d] = (dp.m[d] - (d == 2 ? pl.z0 : 0) + pl.T[d] - 1) / pl.T[d];
     pl.smem = M.total * sizeof(double);
     pl.ntiles = (int64_t)pl.tgrid[0] * pl.tgrid[1] * pl.tgrid[2];
     return true;
 }
 
-int plan_assembly(DevProblem& dp, Plan& pl, bool restricted) {
-    const int t2 = restricted ? env_int("SG_T2_RESTR", kT2Restricted) : 0;
+int plan_assembly(DevProblem& dp, Plan& pl, bool restricted, int t2, int z0) {
+    if (t2 <= 0 && restricted) t2 = env_int("SG_T2_RESTR", kT2Restricted);
     pl.mma = false;
-    if (plan_mma(dp, pl, t2)) return 0;
+    pl.z0 = 0;
+    if (plan_mma(dp, pl, t2, z0)) return 0;
     pl.kfn = get_kernel(dp.n, dp.pr.form, dp.p, dp.rational, &pl.kmax);
     if (!pl.kfn) return fail(-2, "no kernel instantiated for n=%d p=%d form=%d", dp.n, dp.p, dp.pr.form);
     pl.nthreads = 512;
@@ -599,21 +633,21 @@ int plan_assembly(DevProblem& dp, Plan& pl, bool restricted) {
 void tile_box(const Plan& pl, const DevProblem& dp, int64_t t, int64_t lo[3], int64_t hi[3]) {
     int64_t tc[3] = {t % pl.tgrid[0], (t / pl.tgrid[0]) % pl.tgrid[1], t / ((int64_t)pl.tgrid[0] * pl.tgrid[1])};
     for (int d = 0; d < 3; ++d) {
-        lo[d] = tc[d] * pl.T[d];
+        lo[d] = (d == 2 ? pl.z0 : 0) + tc[d] * pl.T[d];
         hi[d] = std::min<int64_t>(lo[d] + pl.T[d], dp.m[d]) - 1;
     }
 }
 
 int64_t tile_of_row(const Plan& pl, const DevProblem& dp, int64_t r) {
     const int64_t i0 = r % dp.m[0], i1 = (r / dp.m[0]) % dp.m[1], i2 = r / ((int64_t)dp.m[0] * dp.m[1]);
-    return (i0 / pl.T[0]) + pl.tgrid[0] * ((i1 / pl.T[1]) + (int64_t)pl.tgrid[1] * (i2 / pl.T[2]));
+    return (i0 / pl.T[0]) + pl.tgrid[0] * ((i1 / pl.T[1]) + (int64_t)pl.tgrid[1] * ((i2 - pl.z0) / pl.T[2]));
 }
 
 int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* tiles, const uint8_t* d_rowmask,
                  const int64_t* d_rowstart, int64_t slab_lo, int64_t slab_hi, int* d_indices, double* d_data,
                  unsigned long long* d_zeros) {
     if (tiles && tiles->empty()) return 0;
-    int rc = compute_D(c, dp, pl, tiles);
+    int rc = compute_D(c, dp, pl, tiles, d_rowmask, slab_lo, slab_hi);
     if (rc) return rc;
     if (pl.mma) {
         MmaParams mp;
@@ -643,6 +677,7 @@ int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>
         mp.indices = d_indices;
         mp.data = d_data;
         mp.zeros = d_zeros;
+        mp.z0 = pl.z0;
         if (!c.dmma) {
             c.dmma = (unsigned long long*)c.alloc(sizeof(unsigned long long), true);
             if (c.dmma) cudaMemsetAsync(c.dmma, 0, sizeof(unsigned long long), c.stream);
@@ -708,9 +743,19 @@ int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>
 int launch_assembly(Call& c, DevProblem& dp, const uint8_t* d_rowmask, const int64_t* d_rowstart, const int64_t* h_rows,
                     int64_t nrows, int64_t slab_lo, int64_t slab_hi, int* d_indices, double* d_data) {
     Plan pl;
-    int rc = plan_assembly(dp, pl, h_rows != nullptr);
-    if (rc) return rc;
     const bool full_slab = (slab_lo <= 0 && slab_hi >= dp.N);
+    int t2 = 0, z0 = 0;
+    if (!h_rows && !full_slab && dp.n == 3) {
+        // row slab (multi-GPU): the tile grid starts at the slab's first plane and its z tiles split
+        // the slab's planes evenly, so no tile straddles a slab edge (one halo per slab)
+        const int64_t pl01 = (int64_t)dp.m[0] * dp.m[1];
+        z0 = (int)(std::max<int64_t>(0, slab_lo) / pl01);
+        const int planes = (int)((std::min<int64_t>(dp.N, slab_hi) - 1) / pl01) - z0 + 1;
+        const int nz = (planes + kMmaT2 - 1) / kMmaT2;
+        t2 = (planes + nz - 1) / nz;
+    }
+    int rc = plan_assembly(dp, pl, h_rows != nullptr, t2, z0);
+    if (rc) return rc;
     if (!h_rows && full_slab) return run_assembly(c, dp, pl, nullptr, d_rowmask, d_rowstart, slab_lo, slab_hi, d_indices, d_data, nullptr);
     std::vector<uint8_t> mark(pl.ntiles, 0);
     if (h_rows) {
@@ -1168,8 +1213,10 @@ int sg_result_free(sg_result* r) {
     cudaSetDevice(r->dev);
     cudaDeviceSynchronize();
     if (r->indptr) cudaFreeAsync(r->indptr, 0);
-    if (r->indices) cudaFreeAsync(r->indices, 0);
-    if (r->data) cudaFreeAsync(r->data, 0);
+    if (r->own_indices) cudaFreeAsync(r->own_indices, 0);
+    else if (r->indices) cudaFreeAsync(r->indices, 0);
+    if (r->own_data) cudaFreeAsync(r->own_data, 0);
+    else if (r->data) cudaFreeAsync(r->data, 0);
     cudaStreamSynchronize(0);
     delete r;
     return 0;

@@ -19,6 +19,8 @@ struct sg_result {
     double* data = nullptr;     // device
     int64_t tiles = 0;
     void* stream_hint = nullptr;
+    void* own_indices = nullptr;  // allocations to free when indices / data point inside a larger buffer
+    void* own_data = nullptr;
 };
 
 namespace sg {
@@ -76,12 +78,13 @@ struct Plan {
     void* kfn = nullptr;
     int kmax = 1, nthreads = 512;
     int T[3], tgrid[3], ypad, off[6];
+    int z0 = 0;                  // z origin of the tile grid (row slabs start their tiles at their first plane)
     size_t smem = 0;
     int64_t ntiles = 0;
 };
 
 int prepare_problem(Call& c, const sg_problem* pr, DevProblem& dp);
-int plan_assembly(DevProblem& dp, Plan& pl, bool restricted = false);
+int plan_assembly(DevProblem& dp, Plan& pl, bool restricted = false, int t2 = 0, int z0 = 0);
 void tile_box(const Plan& pl, const DevProblem& dp, int64_t t, int64_t lo[3], int64_t hi[3]);
 int64_t tile_of_row(const Plan& pl, const DevProblem& dp, int64_t r);
 int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* tiles, const uint8_t* d_rowmask,

@@ -43,6 +43,8 @@ struct SurrParams {
     int TB[3], tg[3];
     int cmax[3];  // max coefficient rows per direction touched by a (shifted) tile
     int64_t slab_lo, slab_hi;
+    int64_t qlo, qhi;  // rows whose quadrature values this call needs (the slab and its p-plane halo)
+    int tile0;         // first interpolation tile of the launch (row slabs launch their z range only)
 };
 
 __device__ __forceinline__ bool row_interp(const SurrParams& s, int j0, int j1, int j2) {
@@ -56,7 +58,12 @@ __global__ void classify_kernel(SurrParams s, int64_t N, uint8_t* quadmask) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
     const int i0 = (int)(i % s.m[0]), i1 = (int)((i / s.m[0]) % s.m[1]), i2 = (int)(i / ((int64_t)s.m[0] * s.m[1]));
-    quadmask[i] = row_interp(s, i0, i1, i2) ? 0 : 1;
+    // quadrature rows of this call: the slab's and its halo's (transposed entries of interpolated rows)
+    // and every fully sampled row (the interpolation samples), whatever the slab
+    const bool quad = !row_interp(s, i0, i1, i2);
+    bool need = i >= s.qlo && i < s.qhi;
+    if (!need) need = s.smp[0][i0] && (s.n < 2 || s.smp[1][i1]) && (s.n < 3 || s.smp[2][i2]);
+    quadmask[i] = quad && need ? 1 : 0;
 }
 
 // S[o][lat colex] = A[row(lat), o]  (bit-exact gather; lattice rows have the full P pattern)
@@ -113,7 +120,7 @@ __global__ void __launch_bounds__(512, 2) interp_tiles_kernel(SurrParams s) {
     double* red = sm + (size_t)nw * scr;                 // [nw][NR] partial row sums
     double* dgv = red + (size_t)nw * NR;                 // [NR] pre-reset diagonal value
     int* rcnt = reinterpret_cast<int*>(dgv + NR);        // [nw][NR][3]: off-diag interp, interp, zeros
-    const int t = blockIdx.x;
+    const int t = blockIdx.x + s.tile0;
     const int tc0 = t % s.tg[0], tc1 = (t / s.tg[0]) % s.tg[1], tc2 = t / (s.tg[0] * s.tg[1]);
     const int org0 = tc0 * TB0, org1 = tc1 * TB1, org2 = tc2 * TB2;
     const int q0 = s.qd[0], q1 = s.qd[1], q2 = s.qd[2];
@@ -364,7 +371,7 @@ __global__ void __launch_bounds__(512, 2) interp_fix_kernel(SurrParams s) {
     const int L0 = TB0 + 2 * p, L1 = TB1 + 2 * p, L2 = NDIM == 3 ? TB2 + 2 * p : 1;
     uint8_t* mk1 = mk0 + L0;
     uint8_t* mk2 = mk1 + L1;
-    const int t = blockIdx.x;
+    const int t = blockIdx.x + s.tile0;
     const int tc0 = t % s.tg[0], tc1 = (t / s.tg[0]) % s.tg[1], tc2 = t / (s.tg[0] * s.tg[1]);
     const int org[3] = {tc0 * TB0, tc1 * TB1, NDIM == 3 ? tc2 * TB2 : 0};
     const int TBd[3] = {TB0, TB1, TB2};
@@ -689,7 +696,7 @@ __global__ void __launch_bounds__(256, 2) interp_rows3_kernel(SurrParams s) {
     constexpr int L0 = TB0 + 2 * p, L1 = TB1 + 2 * p, L2 = TB2 + 2 * p;
     uint8_t* mk1 = mk0 + L0;
     uint8_t* mk2 = mk1 + L1;
-    const int t = blockIdx.x;
+    const int t = blockIdx.x + s.tile0;
     const int tc0 = t % s.tg[0], tc1 = (t / s.tg[0]) % s.tg[1], tc2 = t / (s.tg[0] * s.tg[1]);
     const int org[3] = {tc0 * TB0, tc1 * TB1, tc2 * TB2};
     const int TBd[3] = {TB0, TB1, TB2};
@@ -1109,6 +1116,12 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
     s.mode = sp->mode;
     s.slab_lo = slab_lo;
     s.slab_hi = slab_hi;
+    {
+        const int64_t halo0 = (int64_t)p * (1 + dp.m[0] + (int64_t)dp.m[0] * dp.m[1]);
+        s.qlo = std::max<int64_t>(0, slab_lo - halo0);
+        s.qhi = std::min<int64_t>(N, slab_hi + halo0);
+    }
+    s.tile0 = 0;
     // per-direction masks (surrogate.py:509-531)
     std::vector<std::vector<uint8_t>> inb(3), smp(3);
     int64_t nlat_tot = 1;
@@ -1179,8 +1192,7 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
     Plan pl;
     rc = plan_assembly(dp, pl, true);
     if (rc) return rc;
-    const int64_t halo = (int64_t)p * (1 + dp.m[0] + (int64_t)dp.m[0] * dp.m[1]);
-    const int64_t qlo = std::max<int64_t>(0, slab_lo - halo), qhi = std::min<int64_t>(N, slab_hi + halo);
+    const int64_t qlo = s.qlo, qhi = s.qhi;
     std::vector<int> tiles;
     // per direction and tile coordinate: every index in the box / some index sampled (the tile
     // grid is a tensor product, so a tile's classes are ANDs of three per-direction flags)
@@ -1339,12 +1351,27 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
         }
         smem = sizeof(double) * ((size_t)nw * scr + (size_t)nw * NR + NR) + sizeof(int) * ((size_t)nw * NR * 3 + 2) + tabs + 64;
     }
-    const int ntiles = s.tg[0] * s.tg[1] * s.tg[2];
+    int ntiles = s.tg[0] * s.tg[1] * s.tg[2];
+    if (slab_lo > 0 || slab_hi < N) {
+        // row slab: only the tiles whose slowest-direction range meets the slab's planes (tiles are
+        // ordered with the slowest direction outermost)
+        const int64_t plane = n == 3 ? (int64_t)dp.m[0] * dp.m[1] : (n == 2 ? dp.m[0] : 1);
+        const int zs = (int)(slab_lo / plane), ze = (int)((slab_hi - 1) / plane);
+        const int d = n - 1, TBs = s.TB[d];
+        const int c0 = std::max(0, (zs - s.blo[d]) / TBs), c1 = std::min(s.tg[d] - 1, std::max(0, ze - s.blo[d]) / TBs);
+        const int per = n == 3 ? s.tg[0] * s.tg[1] : (n == 2 ? s.tg[0] : 1);
+        if (ze < s.blo[d] || zs > s.blo[d] + s.bn[d] - 1) {
+            ntiles = 0;  // the slab holds no box plane: no interpolated rows
+        } else {
+            s.tile0 = c0 * per;
+            ntiles = (c1 - c0 + 1) * per;
+        }
+    }
     if (smem > 227 * 1024) return fail(-2, "surrogate tile does not fit shared memory (%zu B)", smem);
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     void* args[] = {&s};
     c.kbegin(rows3 ? "interp_rows3" : "interp_tiles");
-    cudaError_t e = cudaLaunchKernel(kfn, dim3(ntiles), dim3(nthr), args, smem, c.stream);
+    cudaError_t e = ntiles > 0 ? cudaLaunchKernel(kfn, dim3(ntiles), dim3(nthr), args, smem, c.stream) : cudaSuccess;
     c.kend();
     if (e != cudaSuccess) return fail(-3, "interp launch failed: %s", cudaGetErrorString(e));
     if (rows3) {
@@ -1383,15 +1410,14 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
             r->indices = indices;
             r->data = data;
         } else {
-            // row slab: the full-size work arrays are temporaries; the slab portion is the result
-            r->indices = (int*)c.alloc(sizeof(int) * std::max<int64_t>(r->nnz, 1), false);
-            r->data = (double*)c.alloc(sizeof(double) * std::max<int64_t>(r->nnz, 1), false);
-            if (!r->indices || !r->data) {
-                delete r;
-                return fail(-4, "device allocation failed");
-            }
-            cudaMemcpyAsync(r->indices, indices + nnz_lo, sizeof(int) * r->nnz, cudaMemcpyDeviceToDevice, c.stream);
-            cudaMemcpyAsync(r->data, data + nnz_lo, sizeof(double) * r->nnz, cudaMemcpyDeviceToDevice, c.stream);
+            // row slab: the result is the slab's range of the work arrays (no copy); the whole
+            // allocations are freed with the result
+            c.release(indices);
+            c.release(data);
+            r->own_indices = indices;
+            r->own_data = data;
+            r->indices = indices + nnz_lo;
+            r->data = data + nnz_lo;
         }
         cudaMemcpyAsync(r->indptr, rowstart + slab_lo, sizeof(int64_t) * (r->nrows + 1), cudaMemcpyDeviceToDevice, c.stream);
         if (nnz_lo) {

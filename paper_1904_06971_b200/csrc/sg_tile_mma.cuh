@@ -250,6 +250,9 @@ __host__ __device__ constexpr TileChoice mma_tile(int ndim, int P, int form, boo
             if (mma_geom(2, P, form, rat, t, t).total <= cap) return {t, t};
         return {1, 1};
     }
+#if defined(SG_FORCE_FORM) && defined(SG_FORCE_T0) && defined(SG_FORCE_T1)
+    if (form == SG_FORCE_FORM && mma_geom(3, P, form, rat, SG_FORCE_T0, SG_FORCE_T1).total <= cap) return {SG_FORCE_T0, SG_FORCE_T1};
+#endif
     if (form == 1 && mma_minb(3, P, form, rat) > 1 && mma_geom(3, P, form, rat, SG_MASS_T0, SG_MASS_T1).total <= cap / mma_minb(3, P, form, rat))
         return {SG_MASS_T0, SG_MASS_T1};
 #if defined(SG_POIS_T0) && defined(SG_POIS_T1)
@@ -410,6 +413,7 @@ struct MmaParams {
     int tma;                     // 1: TMA double-buffered D windows; 0: plain loads (debug / fallback)
     int Dys;
     unsigned long long* dmma;    // executed DMMA instructions (per warp, summed per launch), or nullptr
+    int z0;                      // z origin of the tile grid (rows)
 };
 
 template <int NDIM, int P, int FORM, bool RAT>
@@ -432,7 +436,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
 
     const int tile = prm.tiles ? prm.tiles[blockIdx.x] : (int)blockIdx.x;
     const int tc0 = tile % prm.tgrid[0], tc1 = (tile / prm.tgrid[0]) % prm.tgrid[1], tc2 = tile / (prm.tgrid[0] * prm.tgrid[1]);
-    const int b0 = tc0 * T0, b1 = tc1 * T1, b2 = tc2 * prm.T2;
+    const int b0 = tc0 * T0, b1 = tc1 * T1, b2 = prm.z0 + tc2 * prm.T2;
     // fixed windows: element e of direction d sits at local element (e - (b_d - P)); elements outside
     // the mesh have zero basis tables and zero D, so every index below is compile-time + lane
     const int ew0 = b0 - P, ew1 = b1 - P;
