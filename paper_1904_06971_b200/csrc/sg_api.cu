@@ -412,6 +412,11 @@ __global__ void geom_mark_kernel(GeomMark m, const int* __restrict__ tiles, int6
             for (int64_t bx = plo[0] / m.BX; bx <= phi[0] / m.BX; ++bx) mask[bx + m.nbx * (by + m.nby * z)] = 1;
 }
 
+static int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return (v && *v) ? atoi(v) : dflt;
+}
+
 int compute_D(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* tiles, const uint8_t* d_rowmask,
               int64_t slab_lo, int64_t slab_hi) {
     const int n = dp.n, g = dp.g, P = dp.p, pg = dp.pr.geo_p;
@@ -439,8 +444,11 @@ int compute_D(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* t
     gp.U = U;
     gp.Dys = n >= 2 ? ((gp.Gp[1] + 1) & ~1) : 1;
     dp.Dys = gp.Dys;
-    gp.BX = n == 1 ? 256 : 32;
-    gp.BY = n >= 2 ? 32 : 1;
+    // 32 x 32 points per block (16 x 16 for the sparse restricted plans measured slower: the per-block
+    // table set-up dominates; SG_GEOM_BXY_RESTR for experiments)
+    const int bxy = (n == 3 && tiles) ? env_int("SG_GEOM_BXY_RESTR", 32) : 32;
+    gp.BX = n == 1 ? 256 : bxy;
+    gp.BY = n >= 2 ? bxy : 1;
     gp.nbx = (gp.Gp[0] + gp.BX - 1) / gp.BX;
     gp.nby = (gp.Gp[1] + gp.BY - 1) / gp.BY;
     const int64_t nblk_all = (int64_t)gp.nbx * gp.nby * gp.Gp[2];
@@ -558,10 +566,6 @@ static int encode_dmap(CUtensorMap* map, const double* D, int Dys, const int Gp[
     return 0;
 }
 
-static int env_int(const char* name, int dflt) {
-    const char* v = getenv(name);
-    return (v && *v) ? atoi(v) : dflt;
-}
 // tile depth in z (rows) for restricted plans (quadrature rows, rows=); whole-matrix plans choose theirs
 constexpr int kT2Restricted = 24;
 
