@@ -532,7 +532,7 @@ int compute_D(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* t
         gp.blockmask = mask;
     }
     void* kfn = get_geom_kernel(n, dp.pr.form, dp.rational);
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptinMax);
     void* args[] = {&gp};
     const int64_t nb = (int64_t)gp.nbx * gp.nby * ((gp.Gp[2] + gp.ZB - 1) / gp.ZB);
     c.kbegin("geom_D");
@@ -692,7 +692,7 @@ int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>
             mp.tiles = (const int*)c.upload(tiles->data(), sizeof(int) * tiles->size());
             nb = (int64_t)tiles->size();
         }
-        cudaFuncSetAttribute(pl.kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+        cudaFuncSetAttribute(pl.kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptinMax);
         void* args[] = {&mp};
         c.kbegin("assemble_mma");
         cudaError_t e = cudaLaunchKernel(pl.kfn, dim3((unsigned)nb), dim3(pl.nthreads), args, pl.smem, c.stream);
@@ -733,7 +733,7 @@ int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>
         prm.tiles = (const int*)c.upload(tiles->data(), sizeof(int) * tiles->size());
         nblocks = (int64_t)tiles->size();
     }
-    cudaFuncSetAttribute(pl.kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    cudaFuncSetAttribute(pl.kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptinMax);
     void* args[] = {&prm};
     c.kbegin("assemble_tiles");
     cudaError_t e = cudaLaunchKernel(pl.kfn, dim3((unsigned)nblocks), dim3(pl.nthreads), args, pl.smem, c.stream);

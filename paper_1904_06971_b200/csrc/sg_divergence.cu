@@ -400,7 +400,7 @@ static int run_divergence(Call& c, DivParams& s, int64_t npts, size_t local_smem
         if constexpr (NDIM >= 2) {
             if (sf_smem <= 227 * 1024 && !getenv("SG_DIV_DIRECT")) {
                 if (sf_smem > 48 * 1024)
-                    cudaFuncSetAttribute(div_local_sf_kernel<NDIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sf_smem);
+                    cudaFuncSetAttribute(div_local_sf_kernel<NDIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptinMax);
                 c.kbegin("div_local");
                 div_local_sf_kernel<NDIM><<<(unsigned)s.nelem, 256, sf_smem, c.stream>>>(s);
                 c.kend();
@@ -408,7 +408,7 @@ static int run_divergence(Call& c, DivParams& s, int64_t npts, size_t local_smem
             }
         }
         if (local_smem > 48 * 1024)
-            cudaFuncSetAttribute(div_local_kernel<NDIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)local_smem);
+            cudaFuncSetAttribute(div_local_kernel<NDIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptinMax);
         c.kbegin("div_local");
         div_local_kernel<NDIM><<<(unsigned)s.nelem, 256, local_smem, c.stream>>>(s);
         c.kend();

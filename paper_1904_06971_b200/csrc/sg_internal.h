@@ -25,6 +25,10 @@ struct sg_result {
 
 namespace sg {
 
+// opt-in ceiling for dynamic shared memory set once per kernel function: the attribute is shared by
+// every caller of the function, so per-launch sizes would race between concurrent library calls
+constexpr int kSmemOptinMax = 227 * 1024;
+
 int fail(int code, const char* fmt, ...);
 
 // One API call: stream, stream-ordered temporaries, per-kernel event timing.

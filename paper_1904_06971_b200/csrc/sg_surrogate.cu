@@ -1368,7 +1368,7 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
         }
     }
     if (smem > 227 * 1024) return fail(-2, "surrogate tile does not fit shared memory (%zu B)", smem);
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptinMax);
     void* args[] = {&s};
     c.kbegin(rows3 ? "interp_rows3" : "interp_tiles");
     cudaError_t e = ntiles > 0 ? cudaLaunchKernel(kfn, dim3(ntiles), dim3(nthr), args, smem, c.stream) : cudaSuccess;

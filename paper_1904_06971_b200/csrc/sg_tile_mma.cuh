@@ -245,6 +245,12 @@ __host__ __device__ constexpr TileChoice mma_tile(int ndim, int P, int form, boo
     const long cap = 224 * 1024 / 8;
     if (ndim == 1) return {32, 1};
     if (ndim == 2) {
+#if defined(SG_FORCE2_FORM) && defined(SG_FORCE2_T0) && defined(SG_FORCE2_T1)
+        if (form == SG_FORCE2_FORM && mma_geom(2, P, form, rat, SG_FORCE2_T0, SG_FORCE2_T1).total <= cap) return {SG_FORCE2_T0, SG_FORCE2_T1};
+#endif
+        // 2D bi-Laplacian, p = 3: a deeper y extent (2 x 5 instead of 3 x 3) halves the x-contraction
+        // work per row (config 4: 7.04 -> 6.12 ms)
+        if (form == 2 && P == 3 && mma_geom(2, P, form, rat, 2, 5).total <= cap) return {2, 5};
         const int cand[] = {12, 10, 8, 6, 4, 3, 2, 1};
         for (int t : cand)
             if (mma_geom(2, P, form, rat, t, t).total <= cap) return {t, t};
