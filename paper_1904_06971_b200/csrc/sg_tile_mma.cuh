@@ -259,7 +259,9 @@ __host__ __device__ constexpr TileChoice mma_tile(int ndim, int P, int form, boo
 #if defined(SG_FORCE_FORM) && defined(SG_FORCE_T0) && defined(SG_FORCE_T1)
     if (form == SG_FORCE_FORM && mma_geom(3, P, form, rat, SG_FORCE_T0, SG_FORCE_T1).total <= cap) return {SG_FORCE_T0, SG_FORCE_T1};
 #endif
-    if (form == 1 && mma_minb(3, P, form, rat) > 1 && mma_geom(3, P, form, rat, SG_MASS_T0, SG_MASS_T1).total <= cap / mma_minb(3, P, form, rat))
+    // several CTAs per SM: 228 KB of shared memory per SM minus 1 KB reserved per CTA
+    if (form == 1 && mma_minb(3, P, form, rat) > 1 &&
+        mma_geom(3, P, form, rat, SG_MASS_T0, SG_MASS_T1).total <= (228L * 1024 / 8) / mma_minb(3, P, form, rat) - 128)
         return {SG_MASS_T0, SG_MASS_T1};
 #if defined(SG_POIS_T0) && defined(SG_POIS_T1)
     if (form == 0 && mma_geom(3, P, form, rat, SG_POIS_T0, SG_POIS_T1).total <= cap) return {SG_POIS_T0, SG_POIS_T1};
