@@ -1215,7 +1215,8 @@ int sg_result_checksum(const sg_result* r, double out[5]) {
 int sg_result_free(sg_result* r) {
     if (!r) return 0;
     cudaSetDevice(r->dev);
-    cudaDeviceSynchronize();
+    // no device-wide synchronisation: the calls that use a result synchronise their own streams
+    // before returning, so freeing it never waits for other threads' work on the device
     if (r->indptr) cudaFreeAsync(r->indptr, 0);
     if (r->own_indices) cudaFreeAsync(r->own_indices, 0);
     else if (r->indices) cudaFreeAsync(r->indices, 0);
