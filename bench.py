@@ -281,7 +281,7 @@ def run_ours(args):
                        "write": t["dram_bytes_write"], "source": t["source"]}
     except (OSError, ValueError, KeyError):
         traffic = None
-    roof.update({"traffic": traffic, "kernel": dom.get("kernel"), "peak_source": "measured fp64 microbenchmark"
+    roof.update({"traffic": traffic["bytes"] if traffic else None, "traffic_detail": traffic, "kernel": dom.get("kernel"), "peak_source": "measured fp64 microbenchmark"
                  if dom.get("unit") == "TFLOP/s" else hbm_src,
                  "algorithmic": "SURVEY §8d reference-algorithm flops (F_elem x elements); the kernel is sum-factorised",
                  "issued": "issued_tflops / issued_frac: the fp64 tensor-core work the kernel actually executed "
