@@ -976,15 +976,21 @@ __global__ void __launch_bounds__(256) slow_rows_kernel(SurrParams s) {
         const int64_t rb = s.rowstart[row];
         double corr = 0.0;
         int nq = 0;
+        // loads through a separate no-alias view: the gathered quadrature rows are never written here
+        // and every slot of this row is read before it is written, so the loads of later iterations
+        // may be issued ahead of earlier stores (the gathers are DRAM-latency bound)
+        const double* __restrict__ dsrc = s.data;
+        double* __restrict__ ddst = s.data;
+#pragma unroll 4
         for (int k = lane; k < P; k += 32) {
             const int q0 = k % NS, q1 = (k / NS) % NS, q2 = k / K;
             const unsigned a = (ib[0] >> q0) & (ib[1] >> q1) & (ib[2] >> q2) & 1u;
             const unsigned b = (sm[0] >> q0) & (sm[1] >> q1) & (sm[2] >> q2) & 1u;
             if (a && !b) continue;  // interpolated neighbour: the slot is final
             const int64_t col = row + (q0 - p) + (int64_t)s.m[0] * ((q1 - p) + (int64_t)s.m[1] * (q2 - p));
-            const double old = s.data[rb + k];
-            const double v = s.data[s.rowstart[col] + (P - 1 - k)];  // transposed quadrature entry A[j, i]
-            s.data[rb + k] = v;
+            const double old = dsrc[rb + k];
+            const double v = dsrc[__ldg(s.rowstart + col) + (P - 1 - k)];  // transposed quadrature entry A[j, i]
+            ddst[rb + k] = v;
             corr += v - old;
             nq++;
             n_zero += (v == 0.0) - (old == 0.0);
