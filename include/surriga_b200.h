@@ -17,7 +17,10 @@
  * Conventions: plain pointers and sizes only; every input pointer is a HOST pointer that is
  * borrowed for the duration of the call (copied to the device inside the call).  Results live
  * on the device behind an opaque handle until sg_result_free().  Every function returns 0 on
- * success and a negative status on failure; sg_last_error() gives a thread-local message.
+ * success and a negative status on failure; sg_last_error() gives a thread-local message:
+ * -1 invalid argument (the reference's ValueError), -2 unsupported configuration, -3 CUDA
+ * error, -4 allocation failure, -5 I/O error, -6 index out of bounds (the reference's
+ * IndexError, e.g. surrogate.py:673-680's positional reset after an exact-zero drop).
  * Multi-index / flat-index order is colex (first direction fastest), as in bspline.py:306-339.
  */
 #ifndef SURRIGA_B200_H

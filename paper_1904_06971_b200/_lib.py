@@ -115,6 +115,8 @@ def check(rc):
         msg = lib().sg_last_error().decode(errors="replace")
         if rc == -1:
             raise ValueError(msg)
+        if rc == -6:
+            raise IndexError(msg)
         raise NativeError(f"surriga_b200 error {rc}: {msg}")
 
 

@@ -1464,7 +1464,7 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
             cudaStreamSynchronize(c.stream);
             if (hb) {
                 sg_result_free(r);
-                return fail(-1, "index out of bounds in kernel-preserving reset after zero drop");
+                return fail(-6, "index out of bounds in kernel-preserving reset after zero drop");
             }
         }
     }

@@ -64,6 +64,9 @@ CASES = [
     ("twisted_poisson_surr_p1", "twisted_cube_p3_m12.geo", 1, (12, 12, 12), "poisson", "surrogate", {"M": 3}),
     ("twisted_mass_surr_nI0", "twisted_cube_p3_m12.geo", 2, (8, 8, 8), "mass", "surrogate", {"M": 2}),
     ("coons_quad_q5_surr", "coons_quadratic", 2, (30, 30), "poisson", "surrogate", {"M": 3, "q": 5}),
+    # coefficient 0: every entry is an exact zero, dropped by the CSR add (surrogate.py:670) -> empty pattern
+    ("annulus_poisson_surr_zero_general", "annulus", 2, (14, 13), "poisson", "surrogate",
+     {"M": 4, "mode": "general", "coefficient": 0.0}),
 ]
 
 
@@ -87,7 +90,8 @@ def run_case(case, gname, p, spans, form, kind, extra):
         mode = extra.get("mode")
         q = extra.get("q", 3)
         A, rep = build_surrogate_matrix(fk, disc, ConstantSampling(M), q=q,
-                                        mode=None if mode is None else SurrogateMode(mode))
+                                        mode=None if mode is None else SurrogateMode(mode),
+                                        coefficient=meta["coefficient"])
         meta.update(M=M, q=q, mode=mode, symmetric=A.symmetric,
                     report={k: getattr(rep, k) for k in ("N", "p", "q", "M", "H", "quad_entries", "interp_entries",
                                                          "quad_fraction", "active_elements", "flags")})
@@ -98,7 +102,10 @@ def run_case(case, gname, p, spans, form, kind, extra):
 
 
 def main():
+    only = set(sys.argv[1:])  # optional case names: regenerate just those
     for c in CASES:
+        if only and c[0] not in only:
+            continue
         nnz = run_case(*c)
         print(f"{c[0]}: nnz={nnz}", file=sys.stderr)
 

@@ -18,7 +18,8 @@ def test_gpu_surrogate_matches_reference_golden(case):
     meta, arr = load(case)
     disc = disc_from_golden(meta, arr)
     mode = None if meta["mode"] is None else pkg.SurrogateMode(meta["mode"])
-    A, rep = pkg.build_surrogate_matrix(form_of(meta), disc, pkg.ConstantSampling(meta["M"]), q=meta["q"], mode=mode)
+    A, rep = pkg.build_surrogate_matrix(form_of(meta), disc, pkg.ConstantSampling(meta["M"]), q=meta["q"], mode=mode,
+                                        coefficient=meta.get("coefficient", 1.0))
     m = A.mat
     assert m.indptr.dtype == np.int32 and m.indices.dtype == np.int32
     assert np.array_equal(m.indptr, arr["indptr"]), "indptr differs"
@@ -112,3 +113,33 @@ def test_gpu_rows3_kernel_matches_64row_kernel(p, spans, form, monkeypatch):
     assert rep.interp_entries == rep2.interp_entries and rep.quad_entries == rep2.quad_entries
     if A.symmetric:
         assert pkg.is_bitwise_symmetric(A)
+
+
+ZERO = [("annulus", 2, (14, 13), 4), ("twisted", 2, (26, 27, 25), 8)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("geom,p,spans,M", ZERO)
+def test_gpu_surrogate_exact_zero_drop(geom, p, spans, M):
+    # coefficient 0: every merged entry is an exact zero and scipy's CSR add drops it
+    # (surrogate.py:670).  GENERAL: empty pattern, report counts unchanged, as the reference gives;
+    # SKP: the positional reset (surrogate.py:673-680) then indexes an empty row -- IndexError in the
+    # reference, the oracle and here alike.
+    import paper_1904_06971_b200 as pkg
+
+    g = pkg.quarter_annulus(1.0, 2.0) if geom == "annulus" else pkg.twisted_cube_standin()
+    disc = pkg.make_discretization(g, p, spans)
+    fk = pkg.FormKind.POISSON
+    prob = O.problem_from_disc(fk, disc, coefficient=0.0)
+    A, rep = pkg.build_surrogate_matrix(fk, disc, pkg.ConstantSampling(M), mode=pkg.SurrogateMode.GENERAL,
+                                        coefficient=0.0)
+    (ip, ix, d), sym, r2 = O.surrogate(prob, M, 3, "general")
+    assert d.size == 0 and A.mat.nnz == 0 and np.array_equal(A.mat.indptr, ip)
+    assert rep.interp_entries == r2["interp_entries"] and rep.quad_entries == r2["quad_entries"]
+    with pytest.raises(IndexError):
+        O.surrogate(prob, M, 3, None)
+    with pytest.raises(IndexError):
+        pkg.build_surrogate_matrix(fk, disc, pkg.ConstantSampling(M), coefficient=0.0)
+    # the library stays usable after the failed call
+    B, _ = pkg.build_surrogate_matrix(fk, disc, pkg.ConstantSampling(M))
+    assert B.mat.nnz > 0

@@ -42,3 +42,12 @@ def test_oracle_p1_stencil_kat():
     expect = np.zeros((5, 5))
     expect[1:4, 1:4] = np.outer(k1, m1) + np.outer(m1, k1)
     assert np.max(np.abs(row - expect)) < 1e-13
+
+
+def test_oracle_skp_after_zero_drop_raises_like_reference():
+    # the reference raises IndexError (surrogate.py:673-680 indexes an emptied row) for coefficient 0
+    # in kernel-preserving mode; GENERAL mode gives the empty golden above
+    meta, arr = load("annulus_poisson_surr_zero_general")
+    prob = oracle_problem(meta, arr)
+    with pytest.raises(IndexError):
+        O.surrogate(prob, meta["M"], meta["q"], None)
