@@ -613,13 +613,15 @@ def div_elements_for_rows(mp, pp, sv, rows):
     return np.flatnonzero(mask.ravel(order="F"))
 
 
-def divergence(vel: Problem, pp: int, rows=None, chunk=1024):
+def divergence(vel: Problem, pp: int, rows=None, chunk=1024, prs_w=None):
     """Pressure/velocity divergence pairing, one CSR per component c (assembly.py:654-725).
 
     ``vel`` describes the velocity discretisation (degree pp+1 on the halved mesh, Gauss order,
     geometry); the pressure space has degree ``pp`` and half the velocity spans.  Entry (i, j) of
     component c is  sum_q w_q P_i(x_q) sum_a d_a V_j(x_q) adj(J)[a, c]  (no determinant: the
-    adjugate folds it).  Non-rational spaces (unit weights) only.
+    adjugate folds it).  Rational spaces (``vel.sol_w`` / ``prs_w`` not all equal) use the NURBS
+    basis R = w N / W and its quotient-rule gradient, as the reference's _SpaceBinding
+    (assembly.py:400-430, 689-691) binds both spaces with their own weights.
     Returns ``(indptr, indices, [data_c for c < n], populated_rows)``.
     """
     n, pv, g = vel.n, vel.p, vel.g
@@ -643,6 +645,15 @@ def divergence(vel: Problem, pp: int, rows=None, chunk=1024):
         wq = (pws[d][:, None] * wq[None, :]).ravel()
     geo = geometry_on_grid(vel, axes, 1)
     jacE = _to_elements(geo["jac"], sv, g)
+    vrat = vel.rational
+    prs_w = None if prs_w is None else np.asarray(prs_w, dtype=float)
+    prat = prs_w is not None and not bool(np.all(prs_w == prs_w[0]))
+    if vrat:
+        Wvf = field_on_grid(pv, mv, vel.sol_w[:, None], axes, 1)
+        WvE = _to_elements(Wvf[(0,) * n][..., 0], sv, g)
+        dWvE = np.stack([_to_elements(Wvf[_unit(n, a)][..., 0], sv, g) for a in range(n)], axis=-1)
+    if prat:
+        WpE = _to_elements(field_on_grid(pp, mp, prs_w[:, None], axes, 0)[(0,) * n][..., 0], sv, g)
     if rows is None:
         eids = np.arange(int(np.prod(sv)))
         rowsel = None
@@ -669,6 +680,13 @@ def divergence(vel: Problem, pp: int, rows=None, chunk=1024):
         gp = et[:, None, :] // 2 + Ip[None, :, :]           # pressure multi (E, Lp, n)
         gv = et[:, None, :] + Iv[None, :, :]                # velocity multi (E, Lv, n)
         rflat = (gp * pstr).sum(-1)
+        if prat:  # R_l = w_l N_l / W_p
+            Pw = prs_w[rflat][:, None, :] * Bp / WpE[ce][..., None] * wq[None, :, None]
+        if vrat:  # d_a R_k = (w_k d_a N_k - R_k d_a W_v) / W_v
+            wlv = vel.sol_w[(gv * np.cumprod((1,) + tuple(mv[:-1]))).sum(-1)][:, None, :]
+            Wv = WvE[ce][..., None]
+            Rv = wlv * _local_tensor(tabs_v, et, (0,) * n, pv, g) / Wv
+            dV = np.stack([(wlv * dV[..., a] - Rv * dWvE[ce][..., a][..., None]) / Wv for a in range(n)], axis=-1)
         lo, hi = div_col_range(mv, pp, gp)
         cnt = hi - lo + 1
         rel = gv[:, None, :, :] - lo[:, :, None, :]          # (E, Lp, Lv, n)
@@ -866,7 +884,7 @@ def surrogate(prob: Problem, M: int, q: int = 3, mode=None):
     return (indptr, indices, data), mode in ("symmetric", "symmetric_kernel_preserving"), rep
 
 
-def surrogate_divergence(vel: Problem, pp: int, M: int, q: int = 3):
+def surrogate_divergence(vel: Problem, pp: int, M: int, q: int = 3, prs_w=None):
     """Surrogate divergence pairing, general mode only (surrogate.py:702-819).
 
     Returns ``([(indptr, indices, data) per component], report dict)``.
@@ -880,7 +898,7 @@ def surrogate_divergence(vel: Problem, pp: int, M: int, q: int = 3):
     Np = int(np.prod(mp))
     h0 = 1.0 / (mp[0] - pp)
     if any(m <= 4 * pp for m in mp):
-        ip, ix, data, _ = divergence(vel, pp)
+        ip, ix, data, _ = divergence(vel, pp, prs_w=prs_w)
         rep = dict(N=Np, p=pp, q=q, M=M, H=M * h0, quad_entries=ix.size * n, interp_entries=0, quad_fraction=1.0,
                    active_elements=int(np.prod(sv)), flags=["surrogate=disabled"])
         return [(ip, ix, d) for d in data], rep
@@ -905,7 +923,7 @@ def surrogate_divergence(vel: Problem, pp: int, M: int, q: int = 3):
     core_flat, samp_flat = flat(core), flat(smp)
     quad_rows = np.flatnonzero(~core_flat | samp_flat)
     interp_rows = np.flatnonzero(core_flat & ~samp_flat)
-    ipq, ixq, dq, _ = divergence(vel, pp, rows=quad_rows)
+    ipq, ixq, dq, _ = divergence(vel, pp, rows=quad_rows, prs_w=prs_w)
     active = div_elements_for_rows(mp, pp, sv, quad_rows).size
     H = M * h0
     nI = interp_rows.size

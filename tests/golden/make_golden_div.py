@@ -35,6 +35,11 @@ CASES = [
     ("sdiv_unit_square_p1", "unit_square", 1, (14, 12), {"M": 3}),
     ("sdiv_twisted_p1", "twisted_cube_p3_m12.geo", 1, (9, 10, 9), {"M": 3}),
     ("sdiv_coons_quad_disabled", "coons_quadratic", 2, (7, 7), {"M": 2}),
+    # rational (NURBS) spaces: both spaces carry the annulus / rational Coons weights
+    ("div_annulus_p2", "annulus", 2, (5, 4), {}),
+    ("div_annulus_p2_rows", "annulus", 2, (6, 5), {"rows": [0, 9, 20, 41, 55]}),
+    ("div_coons_rational_p2", "coons_rational", 2, (4, 5), {}),
+    ("sdiv_annulus_p2", "annulus", 2, (20, 18), {"M": 4}),
 ]
 
 
@@ -68,7 +73,10 @@ def run_case(case, gname, pp, spans, extra):
 
 def main():
     os.makedirs(HERE, exist_ok=True)
+    only = set(sys.argv[1:])  # optional case names: regenerate just those
     for c in CASES:
+        if only and c[0] not in only:
+            continue
         print(f"{c[0]}: nnz={run_case(*c)}", file=sys.stderr)
 
 

@@ -44,7 +44,7 @@ def check_component(arr, c, ip, ix, d):
 def test_oracle_divergence_matches_reference(case):
     meta, arr = load_div(case)
     vel = vel_problem(meta, arr)
-    ip, ix, data, pop = O.divergence(vel, meta["pp"], rows=arr.get("rows"))
+    ip, ix, data, pop = O.divergence(vel, meta["pp"], rows=arr.get("rows"), prs_w=arr["prs_w"])
     if "rows" in arr:
         assert np.array_equal(pop, arr["populated_rows"])
     for c in range(meta["n"]):
@@ -54,7 +54,7 @@ def test_oracle_divergence_matches_reference(case):
 @pytest.mark.parametrize("case", [c for c in div_cases() if c.startswith("sdiv_")])
 def test_oracle_surrogate_divergence_matches_reference(case):
     meta, arr = load_div(case)
-    mats, rep = O.surrogate_divergence(vel_problem(meta, arr), meta["pp"], meta["M"], meta["q"])
+    mats, rep = O.surrogate_divergence(vel_problem(meta, arr), meta["pp"], meta["M"], meta["q"], prs_w=arr["prs_w"])
     for k, v in meta["report"].items():
         assert rep[k] == v, (k, rep[k], v)
     for c, (ip, ix, d) in enumerate(mats):
