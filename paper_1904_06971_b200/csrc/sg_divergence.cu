@@ -34,7 +34,10 @@ struct DivParams {
     const int* gspan[3];
     const double* qw[3];
     const double* hom;             // [Ng][n+1] homogeneous control points (colex)
-    double* Dg;                    // [npts][n][n]: w_q adj[a][c]
+    double* Dg;                    // [npts][na][n]: w_q adj[a][c] (rational: see div_geom_kernel)
+    int na;                        // a-terms per point: n, or n + 1 for a rational velocity space
+    const double* wv;              // velocity weights (colex, device) or nullptr (B-spline space)
+    const double* wp;              // pressure weights (colex, device) or nullptr
     const int64_t* elems;          // element ids (colex over velocity elements), ascending
     int64_t nelem;
     const int* eslot;              // element id -> slot (-1: not computed); nullptr = identity
@@ -118,11 +121,86 @@ __global__ void div_geom_kernel(DivParams s) {
     double wq = s.qw[0][x[0] % s.g];
     if (NDIM >= 2) wq *= s.qw[1][x[1] % s.g];
     if (NDIM >= 3) wq *= s.qw[2][x[2] % s.g];
-    double* out = s.Dg + t * NDIM * NDIM;
+    if (!s.wv && !s.wp) {
+        double* out = s.Dg + t * NDIM * NDIM;
+#pragma unroll
+        for (int a = 0; a < NDIM; ++a)
+#pragma unroll
+            for (int c = 0; c < NDIM; ++c) out[a * NDIM + c] = wq * adj[a][c];
+        return;
+    }
+    // NURBS spaces (assembly.py:400-430 via _SpaceBinding): R_l = w_l N_l / W_p for the pressure,
+    // d_a R_k = w_k (d_a N_k / W_v - N_k d_a W_v / W_v^2) for the velocity.  The global weights
+    // w_l w_k are applied at the gather; here the point factors: a < n carries
+    // w_q adj[a][c] / (W_p W_v) against d_a N_k, the extra term a = n carries
+    // -w_q sum_b d_b W_v adj[b][c] / (W_p W_v^2) against N_k.
+    double Wv = 1.0, dWv[NDIM], Wp = 1.0;
+#pragma unroll
+    for (int a = 0; a < NDIM; ++a) dWv[a] = 0.0;
+    int ev[3] = {0, 0, 0};
+    for (int d = 0; d < NDIM; ++d) ev[d] = x[d] / s.g;  // velocity element = first local function
+    if (s.wv) {
+        const int pv = s.pv;
+        Wv = 0.0;
+        for (int t2 = 0; t2 <= (NDIM >= 3 ? pv : 0); ++t2)
+            for (int t1 = 0; t1 <= (NDIM >= 2 ? pv : 0); ++t1)
+                for (int t0 = 0; t0 <= pv; ++t0) {
+                    const int tt[3] = {t0, t1, t2};
+                    const int64_t ci = (int64_t)(ev[0] + t0) +
+                                       (int64_t)s.mv[0] * ((NDIM >= 2 ? (int64_t)(ev[1] + t1) : 0) +
+                                                           (int64_t)s.mv[1] * (NDIM >= 3 ? (int64_t)(ev[2] + t2) : 0));
+                    const double w = s.wv[ci];
+                    double val[NDIM], der[NDIM];
+#pragma unroll
+                    for (int d = 0; d < NDIM; ++d) {
+                        const double* vt = s.V[d] + (int64_t)x[d] * 2 * (pv + 1);
+                        val[d] = vt[tt[d]];
+                        der[d] = vt[pv + 1 + tt[d]];
+                    }
+                    double b = w;
+#pragma unroll
+                    for (int d = 0; d < NDIM; ++d) b *= val[d];
+                    Wv += b;
+#pragma unroll
+                    for (int a = 0; a < NDIM; ++a) {
+                        double db = w;
+#pragma unroll
+                        for (int d = 0; d < NDIM; ++d) db *= d == a ? der[d] : val[d];
+                        dWv[a] += db;
+                    }
+                }
+    }
+    if (s.wp) {
+        const int pp = s.pp;
+        Wp = 0.0;
+        for (int t2 = 0; t2 <= (NDIM >= 3 ? pp : 0); ++t2)
+            for (int t1 = 0; t1 <= (NDIM >= 2 ? pp : 0); ++t1)
+                for (int t0 = 0; t0 <= pp; ++t0) {
+                    const int tt[3] = {t0, t1, t2};
+                    const int64_t ci = (int64_t)(ev[0] / 2 + t0) +
+                                       (int64_t)s.mp[0] * ((NDIM >= 2 ? (int64_t)(ev[1] / 2 + t1) : 0) +
+                                                           (int64_t)s.mp[1] * (NDIM >= 3 ? (int64_t)(ev[2] / 2 + t2) : 0));
+                    double b = s.wp[ci];
+#pragma unroll
+                    for (int d = 0; d < NDIM; ++d) b *= s.Pt[d][(int64_t)x[d] * (pp + 1) + tt[d]];
+                    Wp += b;
+                }
+    }
+    const double f = wq / (Wp * Wv);
+    double* out = s.Dg + t * s.na * NDIM;
 #pragma unroll
     for (int a = 0; a < NDIM; ++a)
 #pragma unroll
-        for (int c = 0; c < NDIM; ++c) out[a * NDIM + c] = wq * adj[a][c];
+        for (int c = 0; c < NDIM; ++c) out[a * NDIM + c] = f * adj[a][c];
+    if (s.na > NDIM) {
+#pragma unroll
+        for (int c = 0; c < NDIM; ++c) {
+            double g = 0.0;
+#pragma unroll
+            for (int b = 0; b < NDIM; ++b) g = fma(dWv[b], adj[b][c], g);
+            out[NDIM * NDIM + c] = -f * g / Wv;
+        }
+    }
 }
 
 // one CTA per element: loc[c][l][k] = sum_q P_l(q) sum_a dV_k^a(q) Dg(q)[a][c]
@@ -133,7 +211,8 @@ __global__ void __launch_bounds__(256) div_local_kernel(DivParams s) {
     const int Q = NDIM == 1 ? g : (NDIM == 2 ? g * g : g * g * g);
     double* Pt = sm;                                  // [d][g][pp+1]
     double* Vt = Pt + NDIM * g * (pp + 1);            // [d][g][2][pv+1]
-    double* Dq = Vt + NDIM * g * 2 * (pv + 1);        // [Q][NDIM][NDIM]
+    double* Dq = Vt + NDIM * g * 2 * (pv + 1);        // [Q][na][NDIM]
+    const int NA = s.na, NAN_ = NA * NDIM;
     const int64_t eid = s.elems[blockIdx.x];
     int e[3] = {0, 0, 0};
     e[0] = (int)(eid % s.Sv[0]);
@@ -147,13 +226,13 @@ __global__ void __launch_bounds__(256) div_local_kernel(DivParams s) {
         const int d = it / (g * 2 * (pv + 1)), r = it % (g * 2 * (pv + 1));
         Vt[it] = s.V[d][(int64_t)e[d] * g * 2 * (pv + 1) + r];
     }
-    for (int it = threadIdx.x; it < Q * NDIM * NDIM; it += blockDim.x) {
-        const int q = it / (NDIM * NDIM), u = it % (NDIM * NDIM);
+    for (int it = threadIdx.x; it < Q * NAN_; it += blockDim.x) {
+        const int q = it / NAN_, u = it % NAN_;
         const int q0 = q % g, q1 = (q / g) % g, q2 = q / (g * g);
         int64_t pt = (int64_t)e[0] * g + q0;
         if (NDIM >= 2) pt += (int64_t)s.G[0] * ((int64_t)e[1] * g + q1);
         if (NDIM >= 3) pt += (int64_t)s.G[0] * s.G[1] * ((int64_t)e[2] * g + q2);
-        Dq[it] = s.Dg[pt * NDIM * NDIM + u];
+        Dq[it] = s.Dg[pt * NAN_ + u];
     }
     __syncthreads();
     int Lp = pp + 1, Lv = pv + 1;
@@ -181,12 +260,13 @@ __global__ void __launch_bounds__(256) div_local_kernel(DivParams s) {
                 val[d] = vt[k_[d]];
                 der[d] = vt[pv + 1 + k_[d]];
             }
-            const double* Dp = Dq + q * NDIM * NDIM;
+            const double* Dp = Dq + q * NAN_;
 #pragma unroll
             for (int c = 0; c < NDIM; ++c) {
                 double t = 0.0;
 #pragma unroll
-                for (int a = 0; a < NDIM; ++a) {
+                for (int a = 0; a < NDIM + 1; ++a) {
+                    if (a == NA) break;  // a = NDIM: the rational value term (N_k against its factor)
                     double dv = 1.0;
 #pragma unroll
                     for (int d = 0; d < NDIM; ++d) dv *= (d == a) ? der[d] : val[d];
@@ -208,12 +288,12 @@ template <int NDIM>
 __global__ void __launch_bounds__(256) div_local_sf_kernel(DivParams s) {
     static_assert(NDIM == 2 || NDIM == 3, "2D / 3D");
     extern __shared__ double sm[];
-    constexpr int NAC = NDIM * NDIM;                   // (a, c) pairs
+    const int NA = s.na, NAC = NA * NDIM;              // (a, c) pairs (a = NDIM: rational value term)
     const int pp = s.pp, pv = s.pv, g = s.g;
     const int LK = (pp + 1) * (pv + 1);               // 1D (l, k) pairs
     const int Q = NDIM == 2 ? g * g : g * g * g;
     const int R = Q / g;
-    double* Dq = sm;                                   // [Q][NDIM][NDIM]
+    double* Dq = sm;                                   // [Q][na][NDIM]
     double* W = Dq + Q * NAC;                          // [d][alpha][LK][g]
     double* A1 = W + NDIM * 2 * LK * g;                // [ac][LK][R]
     double* A2 = A1 + NAC * LK * R;                    // [ac][LK][LK][g] (3D)
@@ -273,7 +353,8 @@ __global__ void __launch_bounds__(256) div_local_sf_kernel(DivParams s) {
         for (int c = 0; c < NDIM; ++c) {
             double acc = 0.0;
 #pragma unroll
-            for (int a = 0; a < NDIM; ++a) {
+            for (int a = 0; a < NDIM + 1; ++a) {
+                if (a == NA) break;
                 const int ac = a * NDIM + c;
                 double v = 0.0;
                 if constexpr (NDIM == 2) {
@@ -370,6 +451,11 @@ __global__ void div_gather_kernel(DivParams s) {
                     for (int c = 0; c < NDIM; ++c) acc[c] += lp[(int64_t)c * Lp * Lv];
                 }
         const int64_t col = (int64_t)j[0] + (int64_t)s.mv[0] * ((int64_t)j[1] + (int64_t)s.mv[1] * j[2]);
+        if (s.wv || s.wp) {  // global NURBS weights w_l w_k of the pair
+            const double wlk = (s.wp ? s.wp[r] : 1.0) * (s.wv ? s.wv[col] : 1.0);
+#pragma unroll
+            for (int c = 0; c < NDIM; ++c) acc[c] *= wlk;
+        }
 #pragma unroll
         for (int c = 0; c < NDIM; ++c) {
             s.data[c][base + t] = acc[c];
@@ -394,9 +480,9 @@ static int run_divergence(Call& c, DivParams& s, int64_t npts, size_t local_smem
         const int LK = (s.pp + 1) * (s.pv + 1);
         int Q = 1;
         for (int d = 0; d < NDIM; ++d) Q *= s.g;
-        const size_t sf_smem = sizeof(double) * ((size_t)Q * NDIM * NDIM + (size_t)NDIM * 2 * LK * s.g +
-                                                 (size_t)NDIM * NDIM * LK * (Q / s.g) +
-                                                 (NDIM == 3 ? (size_t)NDIM * NDIM * LK * LK * s.g : 0));
+        const size_t nac = (size_t)s.na * NDIM;
+        const size_t sf_smem = sizeof(double) * ((size_t)Q * nac + (size_t)NDIM * 2 * LK * s.g + nac * LK * (Q / s.g) +
+                                                 (NDIM == 3 ? nac * LK * LK * s.g : 0));
         if constexpr (NDIM >= 2) {
             if (sf_smem <= 227 * 1024 && !getenv("SG_DIV_DIRECT")) {
                 if (sf_smem > 48 * 1024)
@@ -555,7 +641,6 @@ static int div_setup(Call& c, const sg_problem* vel, const sg_problem* prs, DevP
     for (int d = 0; d < n; ++d)
         if (vel->m[d] - vel->p != 2 * (prs->m[d] - prs->p))
             return fail(-1, "velocity mesh must halve every pressure element (subgrid pair)");
-    if (vel->sol_w || prs->sol_w) return fail(-2, "rational (NURBS) Stokes spaces are not supported by the divergence kernels");
     sg_problem vp = *vel;
     vp.form = POISSON;  // velocity tables with first derivatives, geometry with first derivatives
     int rc = prepare_problem(c, &vp, dp);
@@ -600,8 +685,12 @@ static int div_setup(Call& c, const sg_problem* vel, const sg_problem* prs, DevP
         tabulate(c, kn, prs->m[d] + prs->p + 1, prs->p, qp, np_, 0, sp, tab);
         s.Pt[d] = tab;
     }
-    s.Dg = (double*)c.alloc(sizeof(double) * npts * n * n, true);
-    return s.Dg ? 0 : fail(-4, "device allocation failed");
+    // NURBS spaces: weights of both spaces on the device (K4 keeps the velocity ones in dp.sol_w)
+    s.wv = vel->sol_w ? dp.sol_w : nullptr;
+    s.wp = prs->sol_w ? (const double*)c.upload(prs->sol_w, sizeof(double) * Np) : nullptr;
+    s.na = s.wv ? n + 1 : n;
+    s.Dg = (double*)c.alloc(sizeof(double) * npts * s.na * n, true);
+    return s.Dg && (!vel->sol_w || s.wv) ? 0 : fail(-4, "device allocation failed");
 }
 
 // elements supporting the listed pressure rows (assembly.py:347-360, ratio 2) + gather row mask
@@ -682,7 +771,7 @@ static int div_rowstart(Call& c, DivParams& s, int64_t*& rowstart, int64_t& nnz)
 static size_t div_local_smem(const DivParams& s) {
     int Q = 1;
     for (int d = 0; d < s.n; ++d) Q *= s.g;
-    return sizeof(double) * ((size_t)s.n * s.g * (s.pp + 1) + (size_t)s.n * s.g * 2 * (s.pv + 1) + (size_t)Q * s.n * s.n);
+    return sizeof(double) * ((size_t)s.n * s.g * (s.pp + 1) + (size_t)s.n * s.g * 2 * (s.pv + 1) + (size_t)Q * s.na * s.n);
 }
 
 static int div_run(Call& c, DivParams& s, int64_t npts) {

@@ -71,12 +71,26 @@ def test_gpu_divergence_rows_bitwise_and_constant_field():
 
 
 @pytest.mark.gpu
-def test_gpu_divergence_rejects_rational_spaces():
+@pytest.mark.parametrize("pp,spans", [(2, (14, 11)), (3, (9, 10))])
+def test_gpu_divergence_rational_spaces(pp, spans):
+    # NURBS velocity and pressure spaces (quarter annulus): the oracle's rational restatement (pinned
+    # by the div_annulus_* goldens), partition of unity (constant velocity -> 0), rows bitwise
     import paper_1904_06971_b200 as pkg
 
-    st = pkg.stokes_subgrid_spaces(pkg.quarter_annulus(1.0, 2.0), 2, (4, 4))
-    with pytest.raises((NotImplementedError, ValueError, RuntimeError)):
-        pkg.assemble_divergence(st)
+    st = pkg.stokes_subgrid_spaces(pkg.quarter_annulus(1.0, 2.0), pp, spans)
+    assert np.ptp(st.velocity.weights.weights) > 0 and np.ptp(st.pressure.weights.weights) > 0
+    D = pkg.assemble_divergence(st)
+    vel = O.problem_from_disc("stokes_divergence", st.velocity)
+    ip, ix, data, _ = O.divergence(vel, pp, prs_w=st.pressure.weights.weights)
+    ones = np.ones(st.velocity.space.N)
+    for c, Dc in enumerate(D):
+        assert np.array_equal(Dc.mat.indptr, ip) and np.array_equal(Dc.mat.indices, ix)
+        assert O.row_scaled_error(ip, ix, data[c], Dc.mat.indptr, Dc.mat.indices, Dc.mat.data) <= TOL
+        assert np.max(np.abs(Dc.mat @ ones)) < 1e-12 * np.max(np.abs(Dc.mat.data))
+    rows = np.array([0, 7, 30, st.pressure.space.N - 1])
+    part = pkg.assemble_divergence(st, rows=rows)
+    for Df, Dp in zip(D, part):
+        assert pkg.matrices_bitwise_equal(Df, Dp, rows=rows)
 
 
 def check_zero_drop_tolerant(arr, c, A, tol=TOL):
@@ -129,3 +143,34 @@ def test_gpu_surrogate_divergence_matches_oracle_3d():
     for Dc, (ip, ix, d) in zip(D, mats):
         assert np.array_equal(Dc.mat.indptr, ip) and np.array_equal(Dc.mat.indices, ix)
         assert O.row_scaled_error(ip, ix, d, Dc.mat.indptr, Dc.mat.indices, Dc.mat.data) <= TOL
+
+
+def thick_annulus():
+    """3D NURBS domain: the quarter annulus extruded linearly in z (rational weights vary in y)."""
+    from paper_1904_06971_b200.geometry import _from_bezier
+
+    radii = np.array([1.0, 1.5, 2.0])
+    arc = np.array([[1.0, 0.0], [1.0, 1.0], [0.0, 1.0]])
+    warc = np.array([1.0, np.sqrt(2.0) / 2.0, 1.0])
+    hom = np.empty((3, 3, 3, 4))
+    for i in range(3):
+        for j in range(3):
+            for k in range(3):
+                hom[i, j, k, :2] = warc[j] * radii[i] * arc[j]
+                hom[i, j, k, 2] = warc[j] * 0.5 * k
+                hom[i, j, k, 3] = warc[j]
+    return _from_bezier(2, 3, hom, "thick_annulus")
+
+
+@pytest.mark.gpu
+def test_gpu_divergence_rational_3d():
+    import paper_1904_06971_b200 as pkg
+
+    st = pkg.stokes_subgrid_spaces(thick_annulus(), 2, (3, 4, 3))
+    assert np.ptp(st.velocity.weights.weights) > 0
+    D = pkg.assemble_divergence(st)
+    vel = O.problem_from_disc("stokes_divergence", st.velocity)
+    ip, ix, data, _ = O.divergence(vel, 2, prs_w=st.pressure.weights.weights)
+    for c, Dc in enumerate(D):
+        assert np.array_equal(Dc.mat.indptr, ip) and np.array_equal(Dc.mat.indices, ix)
+        assert O.row_scaled_error(ip, ix, data[c], Dc.mat.indptr, Dc.mat.indices, Dc.mat.data) <= TOL
