@@ -109,7 +109,7 @@ int sg_result_copy_i64(const sg_result* r, int64_t* indptr, int32_t* indices, do
    one per velocity component c (out[0..n-1]): rows = pressure functions, columns = velocity functions, entry
    sum_q w_q P_i sum_a d_a V_j adj(J)[a][c].  `rows` (sorted, unique) restricts to pressure rows as the reference's
    `rows=` (bitwise equal to the full assembly).  B-spline or NURBS spaces (sol_w of either problem);
-   no row slabs. */
+   sg_exec slab_lo/hi: pressure rows [lo, hi) only (not with `rows`). */
 int sg_assemble_divergence(const sg_problem* velocity, const sg_problem* pressure, const int64_t* rows, int64_t nrows,
                            const sg_exec* exec, sg_result** out);
 /* Surrogate divergence pairing, general mode (replaces surriga/surrogate.py:702-819 `build_surrogate_divergence`):

@@ -367,8 +367,11 @@ def stokes_subgrid_spaces(geom: GeometryMap, p_pressure: int, spans, gauss: int 
     return StokesSpaces(geom=geom, velocity=velocity, pressure=pressure)
 
 
-def assemble_divergence_device(stokes, rows=None, *, device=None, stream=None):
-    """Divergence pairing on the GPU, CSRs kept in HBM: ``([_lib.Result per component], rows)``."""
+def assemble_divergence_device(stokes, rows=None, *, device=None, stream=None, slab=None):
+    """Divergence pairing on the GPU, CSRs kept in HBM: ``([_lib.Result per component], rows)``.
+
+    ``slab=(lo, hi)``: only pressure rows [lo, hi) (one GPU's share); the results hold
+    those rows, which stitch bitwise into the full matrices (slabs.stitch)."""
     vel, prs = stokes.velocity, stokes.pressure
     n = len(vel.space.kvs)
     vpr, vkeep, _, _ = problem_arrays(FormKind.POISSON, vel)
@@ -391,7 +394,7 @@ def assemble_divergence_device(stokes, rows=None, *, device=None, stream=None):
         if rsel.size and (rsel[0] < 0 or rsel[-1] >= Np):
             raise ValueError("pressure row index out of range")
         rptr, nr = rsel.ctypes.data_as(_lib._i64), rsel.size
-    ex = _exec(device, stream, None)
+    ex = _exec(device, stream, slab)
     hs = (C.c_void_p * 3)()
     _lib.check(_lib.lib().sg_assemble_divergence(C.byref(vpr), C.byref(ppr), rptr, nr, C.byref(ex), hs))
     del vkeep, pkeep

@@ -823,7 +823,8 @@ extern "C" int sg_assemble_divergence(const sg_problem* vel, const sg_problem* p
     if (!out) return fail(-1, "null output handles");
     if (!vel || !prs) return fail(-1, "null problem");
     for (int k = 0; k < 3 && k < vel->n; ++k) out[k] = nullptr;
-    if (ex && (ex->slab_lo != 0 || ex->slab_hi != 0)) return fail(-2, "row slabs are not supported for the divergence pairing");
+    const bool slab = ex && (ex->slab_lo != 0 || ex->slab_hi != 0);
+    if (slab && rows) return fail(-1, "rows= cannot be combined with a row slab");
     Call c(ex);
     DevProblem dp;
     DivParams s;
@@ -831,20 +832,58 @@ extern "C" int sg_assemble_divergence(const sg_problem* vel, const sg_problem* p
     int rc = div_setup(c, vel, prs, dp, s, npts, Ev);
     if (rc) return rc;
     std::vector<int64_t> elist;
-    if ((rc = div_elements(c, s, rows, nrows, Ev, elist))) return rc;
-    s.countmask = s.rowmask;  // restricted rows: only those rows are present
+    int64_t lo = 0, hi = s.Np;
+    if (slab) {
+        // a contiguous block of pressure rows per GPU; the velocity element layers under it
+        // (halo included) are recomputed, no exchange.  Element superset: every element whose slowest
+        // index lies in the window of the slab's first / last slowest-direction plane.
+        lo = ex->slab_lo;
+        hi = ex->slab_hi;
+        if (lo < 0 || hi > s.Np || lo >= hi) return fail(-1, "row slab [%lld, %lld) outside [0, %lld)", (long long)lo, (long long)hi, (long long)s.Np);
+        const int ls = s.n - 1;
+        int64_t pstride = 1, estride = 1;
+        for (int d = 0; d < ls; ++d) {
+            pstride *= s.mp[d];
+            estride *= s.Sv[d];
+        }
+        const int ilo = (int)(lo / pstride), ihi = (int)((hi - 1) / pstride);
+        const int64_t elo = 2 * std::max(0, ilo - s.pp), ehi = std::min<int64_t>(2 * std::min(s.Sp[ls] - 1, ihi) + 1, s.Sv[ls] - 1);
+        for (int64_t e = elo * estride; e < (ehi + 1) * estride; ++e) elist.push_back(e);
+        std::vector<int> slot(Ev, -1);
+        for (size_t k = 0; k < elist.size(); ++k) slot[elist[k]] = (int)k;
+        s.eslot = (const int*)c.upload(slot.data(), sizeof(int) * Ev);
+        uint8_t* rowmask = (uint8_t*)c.alloc(s.Np + 1, true);
+        cudaMemsetAsync(rowmask, 0, s.Np + 1, c.stream);
+        cudaMemsetAsync(rowmask + lo, 1, hi - lo, c.stream);
+        s.rowmask = rowmask;
+        s.nelem = (int64_t)elist.size();
+        s.elems = (const int64_t*)c.upload(elist.data(), sizeof(int64_t) * elist.size());
+        int64_t Lp = 1, Lv = 1;
+        for (int d = 0; d < s.n; ++d) {
+            Lp *= s.pp + 1;
+            Lv *= s.pv + 1;
+        }
+        s.eloc = (double*)c.alloc(std::max<size_t>((size_t)s.nelem * s.n * Lp * Lv * sizeof(double), 8), true);
+        if (!s.eloc || !s.eslot || !s.elems) return fail(-4, "device allocation failed");
+    } else if ((rc = div_elements(c, s, rows, nrows, Ev, elist))) {
+        return rc;
+    }
+    s.countmask = s.rowmask;  // restricted rows / slab: only those rows are present
     int64_t* rowstart = nullptr;
     int64_t nnz = 0;
     div_rowstart(c, s, rowstart, nnz);
     const int n = s.n;
     sg_result* res[3] = {nullptr, nullptr, nullptr};
     for (int k = 0; k < n; ++k) {
-        res[k] = new_result(c, s.Np, nnz, true);
+        res[k] = new_result(c, hi - lo, nnz, true);
         if (!res[k]->indptr || !res[k]->indices || !res[k]->data) {
             for (int q = 0; q <= k; ++q) sg_result_free(res[q]);
             return fail(-4, "device allocation failed (nnz=%lld)", (long long)nnz);
         }
-        cudaMemcpyAsync(res[k]->indptr, rowstart, sizeof(int64_t) * (s.Np + 1), cudaMemcpyDeviceToDevice, c.stream);
+        res[k]->nrows_global = s.Np;
+        res[k]->row_lo = lo;
+        // rows before the slab hold no entries, so rowstart[lo] = 0: the slab's indptr is a plain slice
+        cudaMemcpyAsync(res[k]->indptr, rowstart + lo, sizeof(int64_t) * (hi - lo + 1), cudaMemcpyDeviceToDevice, c.stream);
         s.indices[k] = res[k]->indices;
         s.data[k] = res[k]->data;
     }

@@ -174,3 +174,30 @@ def test_gpu_divergence_rational_3d():
     for c, Dc in enumerate(D):
         assert np.array_equal(Dc.mat.indptr, ip) and np.array_equal(Dc.mat.indices, ix)
         assert O.row_scaled_error(ip, ix, data[c], Dc.mat.indptr, Dc.mat.indices, Dc.mat.data) <= TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("geo,pp,spans", [("coons_quadratic", 2, (9, 8)), ("annulus", 2, (7, 9)), ("twisted", 1, (4, 5, 6))])
+def test_gpu_divergence_row_slabs_stitch_bitwise(geo, pp, spans):
+    # SURVEY §8e for the mixed pairing: per-GPU pressure-row slabs (velocity halo recomputed, no
+    # exchange) reproduce every component bit for bit
+    import paper_1904_06971_b200 as pkg
+    from paper_1904_06971_b200.assembly import assemble_divergence_device
+    from paper_1904_06971_b200.slabs import plane_slabs, stitch
+
+    g = {"coons_quadratic": lambda: pkg.builtin_domain("coons_quadratic"), "annulus": lambda: pkg.quarter_annulus(1.0, 2.0),
+         "twisted": pkg.twisted_cube_standin}[geo]()
+    st = pkg.stokes_subgrid_spaces(g, pp, spans)
+    full = pkg.assemble_divergence(st)
+    ms = tuple(kv.m for kv in st.pressure.space.kvs)
+    for world in (2, 3):
+        parts = [[] for _ in full]
+        for lo, hi in plane_slabs(ms, world):
+            res, _ = assemble_divergence_device(st, slab=(lo, hi))
+            for c, r in enumerate(res):
+                parts[c].append(r.to_host())
+                r.free()
+        for c, Dc in enumerate(full):
+            ip, ix, d = stitch(parts[c])
+            assert np.array_equal(ip, Dc.mat.indptr) and np.array_equal(ix, Dc.mat.indices)
+            assert np.array_equal(d.view(np.int64), Dc.mat.data.view(np.int64))
