@@ -1432,38 +1432,41 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
             c.kend();
         }
     } else {
-        if (slab_lo != 0 || slab_hi != N) {
-            sg_result_free(r);
-            return fail(-2, "exact-zero drop combined with row slabs is not supported");
-        }
-        int64_t* cnt = (int64_t*)c.alloc(sizeof(int64_t) * (N + 1), true);
+        // exact zeros present (surrogate.py:670, scipy's CSR add drops them): compact the slab's rows
+        const int64_t nr = slab_hi - slab_lo;
+        int64_t* cnt = (int64_t*)c.alloc(sizeof(int64_t) * (nr + 1), true);
         c.kbegin("nz_count");
-        nz_count_kernel<<<nblk(N + 1, 256), 256, 0, c.stream>>>(rowstart, data, 0, N, cnt);
+        nz_count_kernel<<<nblk(nr + 1, 256), 256, 0, c.stream>>>(rowstart, data, slab_lo, slab_hi, cnt);
         c.kend();
         size_t tb = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, r->indptr, N + 1, c.stream);
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, r->indptr, nr + 1, c.stream);
         void* tmp = c.alloc(tb, true);
-        cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, r->indptr, N + 1, c.stream);
+        cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, r->indptr, nr + 1, c.stream);
         int64_t nnz_new = 0;
-        cudaMemcpyAsync(&nnz_new, r->indptr + N, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream);
+        cudaMemcpyAsync(&nnz_new, r->indptr + nr, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream);
         cudaStreamSynchronize(c.stream);
         r->nnz = nnz_new;
         r->indices = (int*)c.alloc(sizeof(int) * std::max<int64_t>(nnz_new, 1), false);
         r->data = (double*)c.alloc(sizeof(double) * std::max<int64_t>(nnz_new, 1), false);
         c.kbegin("compact");
-        compact_kernel<<<nblk(N, 256), 256, 0, c.stream>>>(rowstart, data, indices, 0, N, r->indptr, r->data, r->indices);
+        compact_kernel<<<nblk(nr, 256), 256, 0, c.stream>>>(rowstart, data, indices, slab_lo, slab_hi, r->indptr, r->data, r->indices);
         c.kend();
         if (s.mode == SG_SYMMETRIC_KERNEL_PRESERVING) {
-            double* nv = (double*)c.alloc(sizeof(double) * N, true);
+            // surrogate.py:673-680 is positional on the global CSR: a reset row's window of P entries may
+            // run into the following rows.  Inside a slab those rows are local; past the slab's end they
+            // belong to the next slab (refused), past the matrix's end it is the reference's IndexError.
+            double* nv = (double*)c.alloc(sizeof(double) * std::max<int64_t>(nr, 1), true);
             int* bad = (int*)c.alloc(sizeof(int), true);
             cudaMemsetAsync(bad, 0, sizeof(int), c.stream);
-            skp_positional_kernel<<<nblk(N, 256), 256, 0, c.stream>>>(reset, r->indptr, 0, N, P, center, nnz_new, r->data, nv, bad);
-            skp_positional_apply<<<nblk(N, 256), 256, 0, c.stream>>>(reset, r->indptr, 0, N, center, nv, r->data);
+            skp_positional_kernel<<<nblk(nr, 256), 256, 0, c.stream>>>(reset, r->indptr, slab_lo, slab_hi, P, center, nnz_new, r->data, nv, bad);
+            skp_positional_apply<<<nblk(nr, 256), 256, 0, c.stream>>>(reset, r->indptr, slab_lo, slab_hi, center, nv, r->data);
             int hb = 0;
             cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c.stream);
             cudaStreamSynchronize(c.stream);
             if (hb) {
                 sg_result_free(r);
+                if (slab_hi != N)
+                    return fail(-2, "kernel-preserving reset window crosses the row slab end after an exact-zero drop");
                 return fail(-6, "index out of bounds in kernel-preserving reset after zero drop");
             }
         }

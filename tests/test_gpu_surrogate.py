@@ -143,3 +143,34 @@ def test_gpu_surrogate_exact_zero_drop(geom, p, spans, M):
     # the library stays usable after the failed call
     B, _ = pkg.build_surrogate_matrix(fk, disc, pkg.ConstantSampling(M))
     assert B.mat.nnz > 0
+
+
+@pytest.mark.gpu
+def test_gpu_surrogate_exact_zero_drop_row_slabs():
+    # the zero-drop compaction per row slab: GENERAL slabs stitch to the full result;
+    # SKP's positional reset (surrogate.py:673-680) past a slab's end is refused, past the matrix's
+    # end it is the reference's IndexError
+    import paper_1904_06971_b200 as pkg
+    from paper_1904_06971_b200._lib import NativeError
+    from paper_1904_06971_b200.slabs import plane_slabs, stitch
+    from paper_1904_06971_b200.surrogate import surrogate_device
+
+    disc = pkg.make_discretization(pkg.twisted_cube_standin(), 2, (26, 27, 25))
+    fk = pkg.FormKind.POISSON
+    full, st, _ = surrogate_device(fk, disc, 8, 3, "general", coefficient=0.0)
+    fip, fix, fd = full.to_host()
+    full.free()
+    assert st.n_zero_dropped > 0 and fd.size == 0
+    ms = tuple(kv.m for kv in disc.space.kvs)
+    parts = []
+    slabs = plane_slabs(ms, 3)
+    for lo, hi in slabs:
+        res, _, _ = surrogate_device(fk, disc, 8, 3, "general", slab=(lo, hi), coefficient=0.0)
+        parts.append(res.to_host())
+        res.free()
+    ip, ix, d = stitch(parts)
+    assert np.array_equal(ip, fip) and ix.size == 0 and d.size == 0
+    with pytest.raises(NativeError):
+        surrogate_device(fk, disc, 8, 3, "symmetric_kernel_preserving", slab=slabs[0], coefficient=0.0)
+    with pytest.raises(IndexError):
+        surrogate_device(fk, disc, 8, 3, "symmetric_kernel_preserving", slab=slabs[-1], coefficient=0.0)
