@@ -116,7 +116,8 @@ int sg_assemble_divergence(const sg_problem* velocity, const sg_problem* pressur
    `params` as for sg_surrogate over the pressure space (lattice, per-direction degree, averaged knots, inverse
    collocation matrices, in-box midpoints); `shifts` the P mixed offsets [-2pp, pp+2]^n (colex, n ints each);
    `quad_rows` the host-classified quadrature rows (not in the one-index-shrunk box, or on the lattice).  Quadrature
-   rows by quadrature, the others interpolated per offset; exact zeros dropped per component. */
+   rows by quadrature, the others interpolated per offset; exact zeros dropped per component.  sg_exec slab_lo/hi:
+   pressure rows [lo, hi) only (the slab's quadrature rows and every lattice row are assembled). */
 int sg_surrogate_divergence(const sg_problem* velocity, const sg_problem* pressure, const sg_surrogate_params* params,
                             const int32_t* shifts, const int64_t* quad_rows, int64_t nquad, const sg_exec* exec,
                             sg_result** out, sg_surrogate_stats* stats);

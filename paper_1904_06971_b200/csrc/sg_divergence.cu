@@ -543,15 +543,16 @@ struct DivInterp {
     int* indices[3];
     double* data[3];
     int64_t Np;
+    int64_t row_lo, row_hi;  // rows interpolated by this call (row slab)
     unsigned long long* counters;  // 0 interp rows, 1 zeros
 };
 
 // one warp per interpolated pressure row, lanes on offsets: the row's P columns 2 i + shift(o)
 template <int NDIM>
 __global__ void div_interp_kernel(DivInterp s) {
-    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t r = s.row_lo + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
-    if (r >= s.Np) return;
+    if (r >= s.row_hi) return;
     int i[3] = {0, 0, 0};
     int64_t rem = r;
     bool core = true, samp = true;
@@ -901,7 +902,7 @@ extern "C" int sg_surrogate_divergence(const sg_problem* vel, const sg_problem* 
     if (!out || !vel || !prs || !sp || !shifts) return fail(-1, "null argument");
     for (int k = 0; k < 3 && k < vel->n; ++k) out[k] = nullptr;
     if (sp->mode != SG_GENERAL) return fail(-1, "the divergence pairing only supports the general mode");
-    if (ex && (ex->slab_lo != 0 || ex->slab_hi != 0)) return fail(-2, "row slabs are not supported for the divergence pairing");
+    const bool slab = ex && (ex->slab_lo != 0 || ex->slab_hi != 0);
     Call c(ex);
     DevProblem dp;
     DivParams s;
@@ -909,9 +910,40 @@ extern "C" int sg_surrogate_divergence(const sg_problem* vel, const sg_problem* 
     int rc = div_setup(c, vel, prs, dp, s, npts, Ev);
     if (rc) return rc;
     const int n = s.n, pp = s.pp;
-    // quadrature rows by quadrature (elements supporting them); every row present in the pattern
+    int64_t lo = 0, hi = s.Np;
+    if (slab) {
+        lo = ex->slab_lo;
+        hi = ex->slab_hi;
+        if (lo < 0 || hi > s.Np || lo >= hi) return fail(-1, "row slab [%lld, %lld) outside [0, %lld)", (long long)lo, (long long)hi, (long long)s.Np);
+    }
+    // lattice rows (colex) -- sampled rows, assembled by every slab
+    int64_t nlat = 1;
+    for (int d = 0; d < n; ++d) nlat *= sp->nlat[d];
+    std::vector<int64_t> latrows(nlat);
+    for (int64_t t = 0; t < nlat; ++t) {
+        int64_t rem = t, row = 0, str = 1;
+        for (int d = 0; d < n; ++d) {
+            const int a = (int)(rem % sp->nlat[d]);
+            rem /= sp->nlat[d];
+            row += sp->lat_idx[d][a] * str;
+            str *= s.mp[d];
+        }
+        latrows[t] = row;
+    }
+    // quadrature rows by quadrature (elements supporting them); every row present in the pattern.
+    // Row slab: the slab's quadrature rows plus every lattice row (the samples of the
+    // coefficient solve), so each slab interpolates exactly as the whole-matrix call does
+    std::vector<int64_t> qsel;
+    if (slab) {
+        std::vector<int64_t> ls(latrows);
+        std::sort(ls.begin(), ls.end());
+        for (int64_t k = 0; k < nquad; ++k) {
+            const int64_t q = quad_rows[k];
+            if ((q >= lo && q < hi) || std::binary_search(ls.begin(), ls.end(), q)) qsel.push_back(q);
+        }
+    }
     std::vector<int64_t> elist;
-    if ((rc = div_elements(c, s, quad_rows, nquad, Ev, elist))) return rc;
+    if ((rc = div_elements(c, s, slab ? qsel.data() : quad_rows, slab ? (int64_t)qsel.size() : nquad, Ev, elist))) return rc;
     s.countmask = nullptr;
     int64_t* rowstart = nullptr;
     int64_t nnz = 0;
@@ -929,25 +961,14 @@ extern "C" int sg_surrogate_divergence(const sg_problem* vel, const sg_problem* 
     // samples S[o][lattice colex] from the quadrature rows (surrogate.py:336-379), per component
     int P = 1;
     for (int d = 0; d < n; ++d) P *= 3 * pp + 3;
-    int64_t nlat = 1;
-    for (int d = 0; d < n; ++d) nlat *= sp->nlat[d];
-    std::vector<int64_t> latrows(nlat);
-    for (int64_t t = 0; t < nlat; ++t) {
-        int64_t rem = t, row = 0, str = 1;
-        for (int d = 0; d < n; ++d) {
-            const int a = (int)(rem % sp->nlat[d]);
-            rem /= sp->nlat[d];
-            row += sp->lat_idx[d][a] * str;
-            str *= s.mp[d];
-        }
-        latrows[t] = row;
-    }
     const int64_t* dlat = (const int64_t*)c.upload(latrows.data(), sizeof(int64_t) * nlat);
     DivInterp I{};
     I.n = n;
     I.P = P;
     I.pp = pp;
     I.Np = s.Np;
+    I.row_lo = lo;
+    I.row_hi = hi;
     I.rowstart = rowstart;
     for (int d = 0; d < 3; ++d) {
         I.mp[d] = s.mp[d];
@@ -1012,7 +1033,7 @@ extern "C" int sg_surrogate_divergence(const sg_problem* vel, const sg_problem* 
     cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * 2, c.stream);
     I.counters = counters;
     c.kbegin("div_interp");
-    const unsigned nb = (unsigned)((s.Np * 32 + 255) / 256);
+    const unsigned nb = (unsigned)(((hi - lo) * 32 + 255) / 256);
     if (n == 1) div_interp_kernel<1><<<nb, 256, 0, c.stream>>>(I);
     if (n == 2) div_interp_kernel<2><<<nb, 256, 0, c.stream>>>(I);
     if (n == 3) div_interp_kernel<3><<<nb, 256, 0, c.stream>>>(I);
@@ -1023,22 +1044,34 @@ extern "C" int sg_surrogate_divergence(const sg_problem* vel, const sg_problem* 
     // merge: exact zeros dropped (scipy CSR add, surrogate.py:810), per component
     sg_result* res[3] = {nullptr, nullptr, nullptr};
     int64_t dropped = 0;
+    // slab: rows [lo, hi) of the work CSR (rowstart + lo keeps absolute offsets into the work arrays)
+    const int64_t nr = hi - lo;
+    int64_t slab_nnz = nnz;
+    if (slab) {
+        int64_t b[2] = {0, 0};
+        cudaMemcpyAsync(&b[0], rowstart + lo, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream);
+        cudaMemcpyAsync(&b[1], rowstart + hi, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream);
+        cudaStreamSynchronize(c.stream);
+        slab_nnz = b[1] - b[0];
+    }
     for (int k = 0; k < n; ++k) {
-        int64_t* cnt = (int64_t*)c.alloc(sizeof(int64_t) * (s.Np + 1), true);
+        int64_t* cnt = (int64_t*)c.alloc(sizeof(int64_t) * (nr + 1), true);
         c.kbegin("div_nz_count");
-        div_nz_count_kernel<<<(unsigned)((s.Np + 256) / 256), 256, 0, c.stream>>>(rowstart, wdat[k], s.Np, cnt);
+        div_nz_count_kernel<<<(unsigned)((nr + 256) / 256), 256, 0, c.stream>>>(rowstart + lo, wdat[k], nr, cnt);
         c.kend();
-        sg_result* r = new_result(c, s.Np, 0, false);
+        sg_result* r = new_result(c, nr, 0, false);
+        r->nrows_global = s.Np;
+        r->row_lo = lo;
         size_t tb = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, r->indptr, s.Np + 1, c.stream);
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, r->indptr, nr + 1, c.stream);
         void* tmp = c.alloc(tb, true);
-        cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, r->indptr, s.Np + 1, c.stream);
+        cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, r->indptr, nr + 1, c.stream);
         int64_t nz = 0;
-        cudaMemcpyAsync(&nz, r->indptr + s.Np, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream);
+        cudaMemcpyAsync(&nz, r->indptr + nr, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream);
         cudaStreamSynchronize(c.stream);
         r->nnz = nz;
-        dropped += nnz - nz;
-        if (nz == nnz) {
+        dropped += slab_nnz - nz;
+        if (!slab && nz == nnz) {
             c.release(wind[k]);
             c.release(wdat[k]);
             r->indices = wind[k];
@@ -1047,8 +1080,8 @@ extern "C" int sg_surrogate_divergence(const sg_problem* vel, const sg_problem* 
             r->indices = (int*)c.alloc(sizeof(int) * std::max<int64_t>(nz, 1), false);
             r->data = (double*)c.alloc(sizeof(double) * std::max<int64_t>(nz, 1), false);
             c.kbegin("div_compact");
-            div_compact_kernel<<<(unsigned)((s.Np + 255) / 256), 256, 0, c.stream>>>(rowstart, wdat[k], wind[k], s.Np, r->indptr,
-                                                                                     r->data, r->indices);
+            div_compact_kernel<<<(unsigned)((nr + 255) / 256), 256, 0, c.stream>>>(rowstart + lo, wdat[k], wind[k], nr, r->indptr,
+                                                                                   r->data, r->indices);
             c.kend();
         }
         res[k] = r;

@@ -572,29 +572,7 @@ def build_surrogate_divergence(stokes, strategy=None, q: int = 3, mode=None):
         return ([SparseMatrix(mat=Dc.mat, symmetric=False) for Dc in Dq],
                 AssemblyReport(N=Np, p=pp, q=q, M=M, H=lattice.H, quad_entries=nnz, interp_entries=0,
                                quad_fraction=1.0, active_elements=active, assembly_seconds=dt, flags=[]))
-    # device call
-    vpr, vkeep, _, _ = problem_arrays(FormKind.POISSON, vel)
-    pkeep = _AKeep()
-    ppr = _lib.SgProblem()
-    ppr.n = n
-    ppr.p = pp
-    ppr.g = int(prs.gauss)
-    for d, kv in enumerate(prs.space.kvs):
-        ppr.m[d] = int(kv.m)
-        ppr.knots[d] = pkeep.ptr(make_open_uniform_knots(pp, int(kv.m)).knots)
-    pw = np.asarray(prs.weights.weights, dtype=float)
-    ppr.sol_w = None if bool(np.all(pw == pw[0])) else pkeep.ptr(pw)
-    spp, fkeep, lowered = _fit_params(prs, lattice, tilde, q, "general", M)
-    offs = build_offsets(pp, n, mixed=True)
-    shifts = np.ascontiguousarray(offs.shifts, dtype=np.int32)
-    qr = np.ascontiguousarray(quad_rows, dtype=np.int64)
-    hs = (C.c_void_p * 3)()
-    st = _lib.SgSurrogateStats()
-    ex = _exec(None, None, None)
-    _lib.check(_lib.lib().sg_surrogate_divergence(C.byref(vpr), C.byref(ppr), C.byref(spp),
-                                                  shifts.ctypes.data_as(C.POINTER(C.c_int32)),
-                                                  qr.ctypes.data_as(_lib._i64), qr.size, C.byref(ex), hs, C.byref(st)))
-    del vkeep, pkeep, fkeep
+    hs, st, lowered = _surrogate_divergence_call(stokes, lattice, tilde, q, M, quad_rows)
     Nv = int(np.prod([kv.m for kv in vel.space.kvs]))
     out = []
     quad_entries = 0
@@ -621,3 +599,62 @@ def _div_pattern_rows_nnz(mp, mv, pp, rows) -> int:
     lo = np.maximum(2 * multi - 2 * pp, 0)
     hi = np.minimum(2 * multi + pp + 2, np.asarray(mv) - 1)
     return int(np.prod(hi - lo + 1, axis=1).sum())
+
+
+def _surrogate_divergence_call(stokes, lattice, tilde, q, M, quad_rows, slab=None):
+    """The native surrogate divergence call: ``(handles[n], stats, lowered)``."""
+    prs, vel = stokes.pressure, stokes.velocity
+    n = stokes.n
+    pp = int(prs.space.kvs[0].p)
+    vpr, vkeep, _, _ = problem_arrays(FormKind.POISSON, vel)
+    pkeep = _AKeep()
+    ppr = _lib.SgProblem()
+    ppr.n = n
+    ppr.p = pp
+    ppr.g = int(prs.gauss)
+    for d, kv in enumerate(prs.space.kvs):
+        ppr.m[d] = int(kv.m)
+        ppr.knots[d] = pkeep.ptr(make_open_uniform_knots(pp, int(kv.m)).knots)
+    pw = np.asarray(prs.weights.weights, dtype=float)
+    ppr.sol_w = None if bool(np.all(pw == pw[0])) else pkeep.ptr(pw)
+    spp, fkeep, lowered = _fit_params(prs, lattice, tilde, q, "general", M)
+    offs = build_offsets(pp, n, mixed=True)
+    shifts = np.ascontiguousarray(offs.shifts, dtype=np.int32)
+    qr = np.ascontiguousarray(quad_rows, dtype=np.int64)
+    hs = (C.c_void_p * 3)()
+    st = _lib.SgSurrogateStats()
+    ex = _exec(None, None, slab)
+    _lib.check(_lib.lib().sg_surrogate_divergence(C.byref(vpr), C.byref(ppr), C.byref(spp),
+                                                  shifts.ctypes.data_as(C.POINTER(C.c_int32)),
+                                                  qr.ctypes.data_as(_lib._i64), qr.size, C.byref(ex), hs, C.byref(st)))
+    del vkeep, pkeep, fkeep
+    return hs, st, lowered
+
+
+def surrogate_divergence_device(stokes, strategy=None, q: int = 3, *, slab=None):
+    """Device-resident surrogate divergence pairing (general mode), optionally on a pressure-row slab
+    ``(lo, hi)`` (one GPU's share: the slab's quadrature rows plus every lattice row are
+    assembled, only the slab's rows interpolated): ``[_lib.Result per component]``.  Needs an active
+    surrogate (a non-empty pressure box with interpolated rows)."""
+    if strategy is None:
+        strategy = ConstantSampling(1)
+    prs = stokes.pressure
+    n = stokes.n
+    pp = int(prs.space.kvs[0].p)
+    mp = tuple(int(kv.m) for kv in prs.space.kvs)
+    tilde = tilde_domain(pp, mp)
+    if tilde.is_empty:
+        raise ValueError("the surrogate is disabled for this mesh (empty pressure box)")
+    M = mesh_dependent_M(strategy, 1.0 / (mp[0] - pp), pp, q)
+    lattice = build_sampling_lattice(prs.space.kvs, M, tilde)
+    _, smp = _masks(tilde, lattice)
+    core = []
+    for d in range(n):
+        lo, hi = tilde.index_range(d)
+        a = np.zeros(mp[d], dtype=bool)
+        if lo + 1 <= hi - 1:
+            a[lo + 1:hi] = True
+        core.append(a)
+    quad_rows = np.flatnonzero(~_flat(core) | _flat(smp))
+    hs, _, _ = _surrogate_divergence_call(stokes, lattice, tilde, q, M, quad_rows, slab)
+    return [_lib.Result(hs[c]) for c in range(n)]
