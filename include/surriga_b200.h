@@ -98,6 +98,26 @@ int sg_assemble(const sg_problem* prob, const int64_t* rows, int64_t nrows, cons
 int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* sp, const sg_exec* ex, sg_result** out,
                  sg_surrogate_stats* stats);
 
+/* Surrogate assembly on a row slab in two phases, for several devices sharing one matrix (SURVEY
+ * §8e): every device assembles only its slab's quadrature rows (and their p-plane halo), so the
+ * samples of the lattice rows outside its slab come from the devices that own them.
+ *   sg_surrogate_begin : the slab's quadrature rows (K4) and the samples of the lattice rows inside
+ *       [slab_lo, slab_hi), written into the state's device table *samples = S[o][lattice colex]
+ *       (P * *nlat doubles, P = (2p+1)^n; the other lattice columns are zero).  Returns after the
+ *       table is complete on the device.
+ *   [the caller fills the other lattice columns on the device, e.g. an all-gather of every slab's
+ *    own columns over NCCL, and synchronises]
+ *   sg_surrogate_finish : collocation solves, interpolation, merge, SKP diagonal; `params` must be
+ *       the same as for begin.  Frees the state (also on error).
+ * sg_surrogate() on a slab is begin + a row-restricted assembly of the other lattice rows + finish.
+ * Results are bitwise those of the whole-matrix call, whatever the slabs. */
+typedef struct sg_surrogate_state sg_surrogate_state;
+int sg_surrogate_begin(const sg_problem* prob, const sg_surrogate_params* params, const sg_exec* exec,
+                       sg_surrogate_state** state, double** samples, int64_t* nlat);
+int sg_surrogate_finish(sg_surrogate_state* state, const sg_surrogate_params* params, sg_result** out,
+                        sg_surrogate_stats* stats);
+int sg_surrogate_state_free(sg_surrogate_state* state);
+
 /* Result inspection / transfer. */
 int sg_result_sizes(const sg_result* r, int64_t* nrows, int64_t* nnz);
 /* Copy CSR to host: indptr int32[nrows+1] (or int64 if *_i64 variant), indices int32[nnz], data f64[nnz]. */

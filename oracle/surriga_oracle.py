@@ -434,14 +434,22 @@ def element_matrices(prob: Problem, eids):
         if nu >= 2:
             d2B = d2N
 
+    # the (q, derivative) contraction of every element matrix runs as one batched matmul
+    # (E, L, Q*k) @ (E, Q*k, L): same sums as the reference's einsums, BLAS speed
+    def _gram(X, Y):
+        E_, Q_, L_ = X.shape[:3]
+        Xf = np.ascontiguousarray(np.moveaxis(X, 2, 1)).reshape(E_, L_, -1)
+        Yf = np.ascontiguousarray(np.moveaxis(Y, 2, 1)).reshape(E_, L_, -1)
+        return Xf @ np.swapaxes(Yf, 1, 2)
+
     if form in ("poisson", "stokes_velocity"):
         K = np.einsum("eqab,eqcb->eqac", A, A) / detE[..., None, None]
         K = K * prob.coefficient
         Kw = K * wq[None, :, None, None]
-        loc = np.einsum("eqla,eqab,eqkb->elk", dB, Kw, dB)
+        loc = _gram(np.einsum("eqla,eqab->eqlb", dB, Kw), dB)
     elif form == "mass":
         s = detE * wq[None, :]
-        loc = np.einsum("eql,eq,eqk->elk", B, s, B)
+        loc = _gram((B * s[..., None])[..., None], B[..., None])
     elif form == "biharmonic":
         hessE = _to_elements(geo["hess"], sub_spans, g)[sub_eids]
         C = np.einsum("eqac,eqbc->eqab", A, A) / (detE ** 2)[..., None, None]
@@ -449,7 +457,7 @@ def element_matrices(prob: Problem, eids):
         T = d2B - np.einsum("eqlc,eqcab->eqlab", pg, hessE)
         lap = np.einsum("eqlab,eqab->eql", T, C)
         s = detE * wq[None, :]
-        loc = np.einsum("eql,eq,eqk->elk", lap, s, lap)
+        loc = _gram((lap * s[..., None])[..., None], lap[..., None])
     else:
         raise ValueError(f"unsupported square form {form}")
     # upper triangle mirrored (assembly.py:524-528)
@@ -882,6 +890,194 @@ def surrogate(prob: Problem, M: int, q: int = 3, mode=None):
     rep = dict(N=N, p=p, q=q, M=M, H=H, quad_entries=quad_entries, interp_entries=n_interp,
                quad_fraction=quad_entries / (quad_entries + n_interp), active_elements=int(active), flags=flags)
     return (indptr, indices, data), mode in ("symmetric", "symmetric_kernel_preserving"), rep
+
+
+# ---------------------------------------------------------------------------
+# sampled-row surrogate: selected rows of the surrogate matrix at sizes where the whole
+# matrix is out of reach of a CPU oracle (config 5: 741M nnz)
+# ---------------------------------------------------------------------------
+
+def _assemble_rows_local(prob: Problem, rows):
+    """Full-quadrature rows ``rows`` (sorted, unique) as (cnt, cols, vals), without any O(N) array.
+
+    Same element sums as ``assemble(prob, rows=rows)`` (assembly.py:579-651): every element
+    supporting a row contributes its local row, in ascending element order.
+    """
+    n, p, ms = prob.n, prob.p, prob.ms
+    spans = np.asarray(prob.spans)
+    rows = np.asarray(rows, dtype=np.int64)
+    strides = np.cumprod((1,) + tuple(ms[:-1]))
+    multi = np.stack(np.unravel_index(rows, ms, order="F"), axis=-1)
+    lo, hi = row_col_range(ms, p, multi)
+    cnt = np.prod(hi - lo + 1, axis=1)
+    start = np.zeros(rows.size + 1, np.int64)
+    np.cumsum(cnt, out=start[1:])
+    L = (p + 1) ** n
+    Il = np.stack(np.unravel_index(np.arange(L), (p + 1,) * n, order="F"), axis=-1)
+    em = multi[:, None, :] - Il[None, :, :]
+    ok = np.all((em >= 0) & (em < spans), axis=-1)
+    eids = np.unique((em[ok] * np.cumprod((1,) + tuple(spans[:-1]))).sum(-1))
+    vals = np.zeros(start[-1])
+    loc, et = element_matrices(prob, eids)
+    gm = et[:, None, :] + Il[None, :, :]                       # (E, L, n)
+    grow = (gm * strides).sum(-1)                               # (E, L) global row of local l
+    k = np.searchsorted(rows, grow)
+    k = np.minimum(k, rows.size - 1)
+    hit = rows[k] == grow                                       # local row l of element e is requested
+    ee, ll = np.nonzero(hit)
+    rr = k[ee, ll]
+    # position of column gm[e, kc] inside row rr's segment
+    rel = gm[ee][:, :, :] - lo[rr][:, None, :]                  # (H, L, n)
+    cs = np.concatenate([np.ones((rr.size, 1), np.int64), np.cumprod((hi - lo + 1)[rr][:, :-1], -1)], -1)
+    pos = start[rr][:, None] + (rel * cs[:, None, :]).sum(-1)
+    vals += np.bincount(pos.ravel(), weights=loc[ee, ll].ravel(), minlength=vals.size)
+    cols = []
+    offs = offsets(p, n)
+    for r in range(rows.size):
+        jm = multi[r] + offs
+        inside = np.all((jm >= 0) & (jm < np.asarray(ms)), axis=-1)
+        cols.append((jm[inside] * strides).sum(-1))
+    return cnt, (np.concatenate(cols) if cols else np.zeros(0, np.int64)), vals
+
+
+def assemble_rows_grouped(prob: Problem, rows, lines_per_group=8):
+    """``_assemble_rows_local`` over spatially local groups of rows (rows sharing their slower
+    indices up to blocks of ``lines_per_group``), so the geometry of each batch stays on a small
+    sub-grid.  Returns a dict row -> (cols, vals)."""
+    rows = np.unique(np.asarray(rows, dtype=np.int64))
+    ms = prob.ms
+    multi = np.stack(np.unravel_index(rows, ms, order="F"), axis=-1)
+    key = multi[:, 1:] // lines_per_group if prob.n > 1 else np.zeros((rows.size, 1), np.int64)
+    out = {}
+    _, inv = np.unique(key, axis=0, return_inverse=True)
+    for gidx in np.unique(inv):
+        grp = rows[inv.ravel() == gidx]
+        cnt, cols, vals = _assemble_rows_local(prob, grp)
+        s = 0
+        for r, c in zip(grp, cnt):
+            out[int(r)] = (cols[s:s + c], vals[s:s + c])
+            s += c
+    return out
+
+
+def surrogate_rows(prob: Problem, M: int, q: int = 3, mode=None, rows=None):
+    """Rows ``rows`` of ``surrogate(prob, M, q, mode)`` without building the whole matrix.
+
+    Follows surrogate.py:538-691 for the requested rows only: the lattice rows and the
+    quadrature neighbours of the requested interpolated rows are assembled by quadrature
+    (``assemble_rows_grouped``), the stencil interpolant is fitted exactly as in ``surrogate``
+    (same collocation solves), evaluated only at the box points the rows need, and the placement
+    (quadrature transposes / canonical / symmetric copies, surrogate.py:611-667) and the
+    kernel-preserving diagonal reset (surrogate.py:673-680) are applied per row.  Exact-zero drop
+    (surrogate.py:670) is not modelled: a requested row that would drop a zero raises.
+
+    Returns ``(rows, cnt, cols, vals)`` (rows sorted) and the row classes ``{"interp": mask}``.
+    """
+    from scipy.linalg import solve
+
+    n, p, ms = prob.n, prob.p, prob.ms
+    mode = DEFAULT_MODE[prob.form] if mode is None else mode
+    rows = np.unique(np.asarray(rows, dtype=np.int64))
+    if any(m <= 4 * p for m in ms):
+        got = assemble_rows_grouped(prob, rows)
+        cnt = np.array([got[int(r)][0].size for r in rows])
+        return (rows, cnt, np.concatenate([got[int(r)][0] for r in rows]),
+                np.concatenate([got[int(r)][1] for r in rows])), {"interp": np.zeros(rows.size, bool)}
+    lat = [lattice_indices(p, m, M) for m in ms]
+    inb, smp = [], []
+    for d, m in enumerate(ms):
+        lo, hi = box_range(p, m)
+        a = np.zeros(m, bool)
+        a[lo:hi + 1] = True
+        s = np.zeros(m, bool)
+        s[lat[d]] = True
+        inb.append(a)
+        smp.append(s)
+
+    def is_interp(mult):
+        jin = np.ones(mult.shape[0], bool)
+        jsm = np.ones(mult.shape[0], bool)
+        for d in range(n):
+            jin &= inb[d][mult[:, d]]
+            jsm &= smp[d][mult[:, d]]
+        return jin & ~jsm
+
+    offs = offsets(p, n)
+    P = offs.shape[0]
+    center = (P - 1) // 2
+    strides = np.cumprod((1,) + tuple(ms[:-1]))
+    multi = np.stack(np.unravel_index(rows, ms, order="F"), axis=-1)
+    interp = is_interp(multi)
+    Im = multi[interp]
+    # quadrature rows needed: every lattice row (the samples), the requested quadrature rows and the
+    # quadrature neighbours of the requested interpolated rows (their transposed entries)
+    lat_grid = np.stack([g.ravel(order="F") for g in np.meshgrid(*lat, indexing="ij")], -1)
+    lat_rows = lat_grid @ strides
+    need = [lat_rows, rows[~interp]]
+    jm_all = Im[:, None, :] + offs[None, :, :]                  # (nI, P, n)
+    jint_all = is_interp(jm_all.reshape(-1, n)).reshape(Im.shape[0], P)
+    need.append((jm_all[~jint_all] * strides).sum(-1))
+    qv = assemble_rows_grouped(prob, np.concatenate(need))
+
+    S = np.stack([qv[int(r)][1] for r in lat_rows])             # (nlat, P): lattice rows are full
+    assert S.shape[1] == P
+    lat_shape = tuple(x.size for x in lat)
+    coef = S.T.reshape((P,) + lat_shape, order="F")
+    qd, kn = [], []
+    for d in range(n):
+        sites = midpoints(p, ms[d], lat[d])
+        qq = min(q, sites.size - 1)
+        qd.append(qq)
+        kn.append(averaging_knots(sites, qq) if qq >= 1 else None)
+        if qq >= 1:
+            C = collocation_matrix(kn[d], qq, sites)
+            moved = np.moveaxis(coef, 1 + d, 0)
+            sol = solve(C, moved.reshape(sites.size, -1))
+            coef = np.moveaxis(sol.reshape(moved.shape), 0, 1 + d)
+    Ed = []
+    for d in range(n):
+        lo, hi = box_range(p, ms[d])
+        pts = midpoints(p, ms[d], np.arange(lo, hi + 1))
+        Ed.append(np.ones((pts.size, 1)) if kn[d] is None else collocation_matrix(kn[d], qd[d], pts))
+
+    def V(o, bm):
+        """Interpolant of offset o at box multi-indices bm (k, n): directions contracted in order."""
+        t = np.broadcast_to(coef[o], (bm.shape[0],) + coef.shape[1:])
+        for d in range(n):
+            t = np.einsum("kr,kr...->k...", Ed[d][bm[:, d]], t)
+        return t
+
+    out_cnt, out_cols, out_vals = [], [], []
+    ii = 0
+    for r, mlt, isi in zip(rows, multi, interp):
+        if not isi:
+            c, v = qv[int(r)]
+            out_cnt.append(c.size)
+            out_cols.append(c)
+            out_vals.append(v)
+            continue
+        jm = jm_all[ii]
+        jint = jint_all[ii]
+        ii += 1
+        vals = np.empty(P)
+        for o in np.flatnonzero(~jint):
+            vals[o] = qv[int(jm[o] @ strides)][1][P - 1 - o]
+        bi = (mlt - 2 * p)[None, :]
+        for o in np.flatnonzero(jint):
+            if mode == "general" or o >= center:
+                vals[o] = V(o, bi)[0]
+            else:
+                vals[o] = V(P - 1 - o, (jm[o] - 2 * p)[None, :])[0]
+        if np.any(vals == 0.0):
+            raise ValueError(f"row {r}: exact zero (the merge would drop it); not modelled here")
+        offd = int(jint.sum()) - int(jint[center])
+        if mode == "symmetric_kernel_preserving" and offd > 0:
+            vals[center] = vals[center] - vals.sum()
+        out_cnt.append(P)
+        out_cols.append((jm * strides).sum(-1))
+        out_vals.append(vals)
+    return (rows, np.array(out_cnt, np.int64), np.concatenate(out_cols), np.concatenate(out_vals)), \
+        {"interp": interp}
 
 
 def surrogate_divergence(vel: Problem, pp: int, M: int, q: int = 3, prs_w=None):

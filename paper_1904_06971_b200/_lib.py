@@ -72,6 +72,11 @@ def lib():
         L.sg_assemble.argtypes = [C.POINTER(SgProblem), _i64, C.c_int64, C.POINTER(SgExec), C.POINTER(C.c_void_p)]
         L.sg_surrogate.argtypes = [C.POINTER(SgProblem), C.POINTER(SgSurrogateParams), C.POINTER(SgExec),
                                    C.POINTER(C.c_void_p), C.POINTER(SgSurrogateStats)]
+        L.sg_surrogate_begin.argtypes = [C.POINTER(SgProblem), C.POINTER(SgSurrogateParams), C.POINTER(SgExec),
+                                         C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), _i64]
+        L.sg_surrogate_finish.argtypes = [C.c_void_p, C.POINTER(SgSurrogateParams), C.POINTER(C.c_void_p),
+                                          C.POINTER(SgSurrogateStats)]
+        L.sg_surrogate_state_free.argtypes = [C.c_void_p]
         L.sg_result_sizes.argtypes = [C.c_void_p, _i64, _i64]
         L.sg_result_copy.argtypes = [C.c_void_p, _i32, _i32, _d]
         L.sg_result_copy_i64.argtypes = [C.c_void_p, _i64, _i32, _d]
@@ -102,7 +107,7 @@ def lib():
     return _lib
 
 
-SYMBOLS = ("sg_assemble", "sg_surrogate", "sg_result_sizes", "sg_result_copy", "sg_result_copy_i64",
+SYMBOLS = ("sg_assemble", "sg_surrogate", "sg_surrogate_begin", "sg_surrogate_finish", "sg_surrogate_state_free", "sg_result_sizes", "sg_result_copy", "sg_result_copy_i64",
            "sg_result_device_ptrs", "sg_result_checksum", "sg_result_free", "sg_last_timing",
            "sg_last_kernel_times", "sg_last_error", "sg_version", "sg_max_degree", "sg_host_staging_init",
            "sg_assemble_divergence", "sg_surrogate_divergence", "sg_host_register", "sg_host_unregister",

@@ -98,6 +98,15 @@ void Call::release(void* p) {
         if (t == p) t = nullptr;
 }
 
+void Call::free_temp(void* p) {
+    if (!p) return;
+    for (auto& t : temps)
+        if (t == p) {
+            t = nullptr;
+            cudaFreeAsync(p, stream);
+        }
+}
+
 void* Call::upload(const void* host, size_t bytes) {
     void* d = alloc(bytes, true);
     if (d && host && bytes) cudaMemcpyAsync(d, host, bytes, cudaMemcpyHostToDevice, stream);
@@ -204,6 +213,55 @@ __global__ void scatter_mask_kernel(const int64_t* __restrict__ rows, int64_t n,
     if (i < n) mask[rows[i]] = 1;
 }
 
+
+int64_t nnz_before_row(const DevProblem& dp, int64_t r) {
+    if (r >= dp.N) {
+        int64_t tot = 1;
+        for (int d = 0; d < 3; ++d) tot *= pre1d(dp.m[d], dp.m[d], dp.p);
+        return tot;
+    }
+    const int64_t i0 = r % dp.m[0], i1 = (r / dp.m[0]) % dp.m[1], i2 = r / ((int64_t)dp.m[0] * dp.m[1]);
+    const int64_t t0 = pre1d(dp.m[0], dp.m[0], dp.p), t1 = pre1d(dp.m[1], dp.m[1], dp.p);
+    return pre1d(i2, dp.m[2], dp.p) * t1 * t0 +
+           cnt1d(i2, dp.m[2], dp.p) * (pre1d(i1, dp.m[1], dp.p) * t0 + cnt1d(i1, dp.m[1], dp.p) * pre1d(i0, dp.m[0], dp.p));
+}
+
+int assemble_rows_compact(Call& c, DevProblem& dp, const std::vector<int64_t>& rows, int64_t** d_rowstart, int** d_ind,
+                          double** d_dat) {
+    // the rows= path of sg_assemble into call temporaries: rowstart over all N rows (zero-length
+    // rows outside `rows`), entries of the listed rows only
+    const int64_t N = dp.N;
+    Dims D;
+    for (int d = 0; d < 3; ++d) D.m[d] = dp.m[d];
+    D.p = dp.p;
+    int64_t* rowstart = (int64_t*)c.alloc(sizeof(int64_t) * (N + 1), true);
+    uint8_t* mask = (uint8_t*)c.alloc(N + 1, true);
+    int64_t* counts = (int64_t*)c.alloc(sizeof(int64_t) * (N + 1), true);
+    if (!rowstart || !mask || !counts) return fail(-4, "device allocation failed");
+    cudaMemsetAsync(mask, 0, N + 1, c.stream);
+    int64_t nnz = 0;
+    for (int64_t r : rows) {
+        const int64_t i0 = r % dp.m[0], i1 = (r / dp.m[0]) % dp.m[1], i2 = r / ((int64_t)dp.m[0] * dp.m[1]);
+        nnz += cnt1d(i0, dp.m[0], dp.p) * cnt1d(i1, dp.m[1], dp.p) * cnt1d(i2, dp.m[2], dp.p);
+    }
+    if (!rows.empty()) {
+        int64_t* drows = (int64_t*)c.upload(rows.data(), sizeof(int64_t) * rows.size());
+        scatter_mask_kernel<<<(unsigned)((rows.size() + 255) / 256), 256, 0, c.stream>>>(drows, (int64_t)rows.size(), mask);
+    }
+    row_counts_kernel<<<(unsigned)((N + 1 + 255) / 256), 256, 0, c.stream>>>(D, N, mask, counts);
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, rowstart, N + 1, c.stream);
+    void* tmp = c.alloc(tmp_bytes, true);
+    cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, rowstart, N + 1, c.stream);
+    int* ind = (int*)c.alloc(sizeof(int) * std::max<int64_t>(nnz, 1), true);
+    double* dat = (double*)c.alloc(sizeof(double) * std::max<int64_t>(nnz, 1), true);
+    if (!ind || !dat) return fail(-4, "device allocation failed");
+    *d_rowstart = rowstart;
+    *d_ind = ind;
+    *d_dat = dat;
+    if (rows.empty()) return 0;
+    return launch_assembly(c, dp, mask, rowstart, rows.data(), (int64_t)rows.size(), 0, N, ind, dat);
+}
 
 void launch_indptr_full(Call& c, const DevProblem& dp, int64_t base, int64_t* rowstart) {
     Dims D;
@@ -700,6 +758,8 @@ int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>
         if (e != cudaSuccess)
             return fail(-3, "assembly (mma) launch failed: %s (smem %zu B, %lld tiles)", cudaGetErrorString(e), pl.smem, (long long)nb);
         dp.last_tiles = nb;
+        c.free_temp(dp.D);  // stream ordered: released once the kernel is done with it
+        dp.D = nullptr;
         return 0;
     }
     AsmParams prm;
@@ -741,6 +801,8 @@ int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>
     if (e != cudaSuccess)
         return fail(-3, "assembly launch failed: %s (smem %zu B, %lld tiles)", cudaGetErrorString(e), pl.smem, (long long)nblocks);
     dp.last_tiles = nblocks;
+    c.free_temp(dp.D);
+    dp.D = nullptr;
     return 0;
 }
 

@@ -49,6 +49,7 @@ struct Call {
     ~Call();
     void* alloc(size_t bytes, bool temp);
     void release(void* p);  // hand a temporary over to a result (no free at call end)
+    void free_temp(void* p);  // free a temporary early (stream ordered)
     void* upload(const void* host, size_t bytes);
     void kbegin(const char* name);
     void kend();
@@ -95,6 +96,11 @@ int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>
                  const int64_t* d_rowstart, int64_t slab_lo, int64_t slab_hi, int* d_indices, double* d_data,
                  unsigned long long* d_zeros);
 void launch_indptr_full(Call& c, const DevProblem& dp, int64_t base, int64_t* rowstart);
+// entries before row r of the full basis-overlap pattern (closed form, host)
+int64_t nnz_before_row(const DevProblem& dp, int64_t r);
+// rows= assembly of sorted unique `rows` into call temporaries (rowstart over all N rows)
+int assemble_rows_compact(Call& c, DevProblem& dp, const std::vector<int64_t>& rows, int64_t** d_rowstart, int** d_ind,
+                          double** d_dat);
 int launch_assembly(Call& c, DevProblem& dp, const uint8_t* d_rowmask, const int64_t* d_rowstart, const int64_t* h_rows,
                     int64_t nrows, int64_t slab_lo, int64_t slab_hi, int* d_indices, double* d_data);
 int tabulate(Call& c, const double* d_knots, int nk, int p, const double* d_pts, int npts, int nu, int* d_span,

@@ -58,22 +58,25 @@ __global__ void classify_kernel(SurrParams s, int64_t N, uint8_t* quadmask) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
     const int i0 = (int)(i % s.m[0]), i1 = (int)((i / s.m[0]) % s.m[1]), i2 = (int)(i / ((int64_t)s.m[0] * s.m[1]));
-    // quadrature rows of this call: the slab's and its halo's (transposed entries of interpolated rows)
-    // and every fully sampled row (the interpolation samples), whatever the slab
+    // quadrature rows of this call: the slab's and its halo's (transposed entries of interpolated rows);
+    // lattice rows outside them come from a separate row-restricted assembly or another rank
     const bool quad = !row_interp(s, i0, i1, i2);
-    bool need = i >= s.qlo && i < s.qhi;
-    if (!need) need = s.smp[0][i0] && (s.n < 2 || s.smp[1][i1]) && (s.n < 3 || s.smp[2][i2]);
+    const bool need = i >= s.qlo && i < s.qhi;
     quadmask[i] = quad && need ? 1 : 0;
 }
 
-// S[o][lat colex] = A[row(lat), o]  (bit-exact gather; lattice rows have the full P pattern)
+// S[o][lat colex] = A[row(lat), o] for the lattice rows in [lo, hi) (bit-exact gather; lattice rows
+// have the full P pattern); the other columns of S are left untouched
 __global__ void gather_samples_kernel(const int64_t* __restrict__ rowstart, const double* __restrict__ data,
-                                      const int64_t* __restrict__ latrows, int64_t nlat, int P, double* __restrict__ S) {
+                                      const int64_t* __restrict__ latrows, int64_t nlat, int P, int64_t lo, int64_t hi,
+                                      double* __restrict__ S) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= nlat * P) return;
     const int64_t t = k / P;
     const int o = (int)(k % P);
-    S[(int64_t)o * nlat + t] = data[rowstart[latrows[t]] + o];
+    const int64_t r = latrows[t];
+    if (r < lo || r >= hi) return;
+    S[(int64_t)o * nlat + t] = data[rowstart[r] + o];
 }
 
 // out[..., s, ...] = sum_t Cinv[s][t] in[..., t, ...] along one direction (stride = inner block)
@@ -1093,12 +1096,39 @@ static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / 
 
 using namespace sg;
 
-extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* sp, const sg_exec* ex, sg_result** out,
-                            sg_surrogate_stats* stats) {
-    if (!out || !sp) return fail(-1, "null argument");
-    *out = nullptr;
-    Call c(ex);
+
+// ==========================================================================================
+// Surrogate call in two phases (strategy B for row slabs):
+//   begin  : masks, analytic pattern, quadrature rows of the slab and its p-plane halo (K4) into
+//            work arrays sized for exactly those rows, samples of the lattice rows inside the slab;
+//   [the caller fills the other lattice rows' samples: another rank's all-gather, or the
+//    single-call path's row-restricted assembly of the foreign lattice rows]
+//   finish : collocation solves (K6), interpolation (K7), merge / zero drop, SKP diagonal.
+// ==========================================================================================
+struct sg_surrogate_state {
+    Call c;
     DevProblem dp;
+    SurrParams s;
+    int n = 0, p = 0, P = 0, center = 0;
+    int64_t N = 0, slab_lo = 0, slab_hi = 0, nnz_lo = 0, nnz_hi = 0, nnz_all = 0, nnz_qlo = 0, nnz_qhi = 0;
+    int64_t nlat_tot = 1;
+    std::vector<int64_t> latrows;
+    int64_t* dlat = nullptr;
+    int64_t* rowstart = nullptr;
+    int* indices = nullptr;  // allocation: entries of rows [qlo, qhi)
+    double* data = nullptr;
+    uint8_t* reset = nullptr;
+    double* newdiag = nullptr;
+    unsigned long long* counters = nullptr;
+    double* bufA = nullptr;
+    double* bufB = nullptr;
+    int64_t cpad = 0;
+    explicit sg_surrogate_state(const sg_exec* ex) : c(ex) {}
+};
+
+static int surr_begin(sg_surrogate_state& S, const sg_problem* prob, const sg_surrogate_params* sp, const sg_exec* ex) {
+    Call& c = S.c;
+    DevProblem& dp = S.dp;
     int rc = prepare_problem(c, prob, dp);
     if (rc) return rc;
     const int n = dp.n, p = dp.p;
@@ -1113,7 +1143,14 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
         slab_hi = std::min<int64_t>(N, ex->slab_hi);
         if (slab_lo >= slab_hi) return fail(-1, "empty row slab");
     }
-    SurrParams s;
+    S.n = n;
+    S.p = p;
+    S.P = P;
+    S.center = center;
+    S.N = N;
+    S.slab_lo = slab_lo;
+    S.slab_hi = slab_hi;
+    SurrParams& s = S.s;
     memset(&s, 0, sizeof(s));
     s.n = n;
     s.p = p;
@@ -1130,7 +1167,6 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
     s.tile0 = 0;
     // per-direction masks (surrogate.py:509-531)
     std::vector<std::vector<uint8_t>> inb(3), smp(3);
-    int64_t nlat_tot = 1;
     for (int d = 0; d < 3; ++d) {
         s.m[d] = dp.m[d];
         if (d < n) {
@@ -1141,7 +1177,11 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
             smp[d].assign(dp.m[d], 0);
             for (int k = s.blo[d]; k < s.blo[d] + s.bn[d]; ++k) inb[d][k] = 1;
             s.nl[d] = sp->nlat[d];
-            for (int k = 0; k < sp->nlat[d]; ++k) smp[d][sp->lat_idx[d][k]] = 1;
+            for (int k = 0; k < sp->nlat[d]; ++k) {
+                const int64_t li = sp->lat_idx[d][k];
+                if (li < s.blo[d] || li >= s.blo[d] + s.bn[d]) return fail(-1, "lattice index outside the box");
+                smp[d][li] = 1;
+            }
             s.qd[d] = sp->qd[d];
         } else {
             s.blo[d] = 0;
@@ -1151,7 +1191,7 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
             s.nl[d] = 1;
             s.qd[d] = 0;
         }
-        nlat_tot *= s.nl[d];
+        S.nlat_tot *= s.nl[d];
         s.inb[d] = (const uint8_t*)c.upload(inb[d].data(), inb[d].size());
         s.smp[d] = (const uint8_t*)c.upload(smp[d].data(), smp[d].size());
     }
@@ -1166,39 +1206,41 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
     }
     s.shifts = (const int*)c.upload(shifts.data(), sizeof(int) * shifts.size());
 
-    // result arrays: full pattern
-    int64_t* rowstart = (int64_t*)c.alloc(sizeof(int64_t) * (N + 1), true);
-    launch_indptr_full(c, dp, 0, rowstart);
-    int64_t nnz_all = 1;
-    for (int d = 0; d < 3; ++d) nnz_all *= pre1d(dp.m[d], dp.m[d], p);
-    int64_t nnz_lo = 0, nnz_hi = 0;
-    cudaMemcpyAsync(&nnz_lo, rowstart + slab_lo, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream);
-    cudaMemcpyAsync(&nnz_hi, rowstart + slab_hi, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream);
-    int* indices = (int*)c.alloc(sizeof(int) * nnz_all, true);
-    double* data = (double*)c.alloc(sizeof(double) * nnz_all, true);
+    // analytic pattern; work arrays hold the entries of rows [qlo, qhi) only (the slab, its halo):
+    // kernels index them with global row starts through base pointers shifted by nnz(qlo)
+    S.rowstart = (int64_t*)c.alloc(sizeof(int64_t) * (N + 1), true);
+    launch_indptr_full(c, dp, 0, S.rowstart);
+    S.nnz_all = nnz_before_row(dp, N);
+    S.nnz_lo = nnz_before_row(dp, slab_lo);
+    S.nnz_hi = nnz_before_row(dp, slab_hi);
+    S.nnz_qlo = nnz_before_row(dp, s.qlo);
+    S.nnz_qhi = nnz_before_row(dp, s.qhi);
+    const int64_t nwork = std::max<int64_t>(S.nnz_qhi - S.nnz_qlo, 1);
+    S.indices = (int*)c.alloc(sizeof(int) * nwork, true);
+    S.data = (double*)c.alloc(sizeof(double) * nwork, true);
     uint8_t* quadmask = (uint8_t*)c.alloc(N, true);
-    unsigned long long* counters = (unsigned long long*)c.alloc(8 * sizeof(unsigned long long), true);
-    cudaMemsetAsync(counters, 0, 8 * sizeof(unsigned long long), c.stream);
-    double* newdiag = (double*)c.alloc(sizeof(double) * N, true);
-    uint8_t* reset = (uint8_t*)c.alloc(N, true);
-    cudaMemsetAsync(reset, 0, N, c.stream);
-    if (!indices || !data || !newdiag) return fail(-4, "device allocation failed");
-    s.rowstart = rowstart;
-    s.indices = indices;
-    s.data = data;
-    s.newdiag = newdiag;
-    s.reset = reset;
-    s.counters = counters;
+    S.counters = (unsigned long long*)c.alloc(8 * sizeof(unsigned long long), true);
+    S.newdiag = (double*)c.alloc(sizeof(double) * N, true);
+    S.reset = (uint8_t*)c.alloc(N, true);
+    if (!S.rowstart || !S.indices || !S.data || !quadmask || !S.counters || !S.newdiag || !S.reset)
+        return fail(-4, "device allocation failed (%lld work entries)", (long long)nwork);
+    cudaMemsetAsync(S.counters, 0, 8 * sizeof(unsigned long long), c.stream);
+    cudaMemsetAsync(S.reset, 0, N, c.stream);
+    s.rowstart = S.rowstart;
+    s.indices = S.indices - S.nnz_qlo;
+    s.data = S.data - S.nnz_qlo;
+    s.newdiag = S.newdiag;
+    s.reset = S.reset;
+    s.counters = S.counters;
     s.slow = nullptr;
     c.kbegin("classify");
     classify_kernel<<<nblk(N, 256), 256, 0, c.stream>>>(s, N, quadmask);
     c.kend();
 
-    // ---- K4: quadrature rows (the slab's quad rows + halo neighbours + every lattice row)
+    // ---- K4: the quadrature rows of [qlo, qhi) (the slab's own, the halo's transposed entries)
     Plan pl;
     rc = plan_assembly(dp, pl, true);
     if (rc) return rc;
-    const int64_t qlo = s.qlo, qhi = s.qhi;
     std::vector<int> tiles;
     // per direction and tile coordinate: every index in the box / some index sampled (the tile
     // grid is a tensor product, so a tile's classes are ANDs of three per-direction flags)
@@ -1219,44 +1261,80 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
         int64_t lo[3], hi[3];
         tile_box(pl, dp, t, lo, hi);
         const int64_t tc[3] = {t % pl.tgrid[0], (t / pl.tgrid[0]) % pl.tgrid[1], t / ((int64_t)pl.tgrid[0] * pl.tgrid[1])};
-        bool all_in = true, any_samp_all = true, any_lat = true;
+        bool all_in = true, any_samp_all = true;
         for (int d = 0; d < n; ++d) {
             all_in = all_in && fin[d][tc[d]];
             any_samp_all = any_samp_all && fsm[d][tc[d]];
-            any_lat = any_lat && fsm[d][tc[d]];
         }
         const bool has_quad = !all_in || any_samp_all;
         if (!has_quad) continue;
         const int64_t flo = lo[0] + dp.m[0] * (lo[1] + (int64_t)dp.m[1] * lo[2]);
         const int64_t fhi = hi[0] + dp.m[0] * (hi[1] + (int64_t)dp.m[1] * hi[2]);
-        if ((fhi >= qlo && flo < qhi) || any_lat) tiles.push_back((int)t);
+        if (fhi >= s.qlo && flo < s.qhi) tiles.push_back((int)t);
     }
-    rc = run_assembly(c, dp, pl, &tiles, quadmask, rowstart, 0, N, indices, data, counters + 4);
+    rc = run_assembly(c, dp, pl, &tiles, quadmask, S.rowstart, s.qlo, s.qhi, s.indices, s.data, S.counters + 4);
     if (rc) return rc;
 
-    // ---- K6: samples -> spline coefficients
-    std::vector<int64_t> latrows(nlat_tot);
-    for (int64_t t = 0; t < nlat_tot; ++t) {
+    // ---- lattice rows (colex over the lattice) and the sample table S[o][lattice colex]
+    S.latrows.resize(S.nlat_tot);
+    for (int64_t t = 0; t < S.nlat_tot; ++t) {
         int64_t r = t, idx[3] = {0, 0, 0};
         for (int d = 0; d < n; ++d) {
             idx[d] = sp->lat_idx[d][r % s.nl[d]];
             r /= s.nl[d];
         }
-        latrows[t] = idx[0] + dp.m[0] * (idx[1] + (int64_t)dp.m[1] * idx[2]);
+        S.latrows[t] = idx[0] + dp.m[0] * (idx[1] + (int64_t)dp.m[1] * idx[2]);
     }
-    int64_t* dlat = (int64_t*)c.upload(latrows.data(), sizeof(int64_t) * nlat_tot);
+    S.dlat = (int64_t*)c.upload(S.latrows.data(), sizeof(int64_t) * S.nlat_tot);
     // a zeroed tail of one lattice plane + row behind the coefficients: the row-staged K7 kernel
     // reads whole 5-wide windows without clamping (the taps past the last site have weight 0)
-    const int64_t cpad = (int64_t)s.nl[0] * s.nl[1] + s.nl[0] + 16;
-    double* bufA = (double*)c.alloc(sizeof(double) * (P * nlat_tot + cpad), true);
-    double* bufB = (double*)c.alloc(sizeof(double) * (P * nlat_tot + cpad), true);
-    cudaMemsetAsync(bufA + P * nlat_tot, 0, sizeof(double) * cpad, c.stream);
-    cudaMemsetAsync(bufB + P * nlat_tot, 0, sizeof(double) * cpad, c.stream);
+    S.cpad = (int64_t)s.nl[0] * s.nl[1] + s.nl[0] + 16;
+    S.bufA = (double*)c.alloc(sizeof(double) * (P * S.nlat_tot + S.cpad), true);
+    S.bufB = (double*)c.alloc(sizeof(double) * (P * S.nlat_tot + S.cpad), true);
+    if (!S.bufA || !S.bufB) return fail(-4, "device allocation failed");
+    cudaMemsetAsync(S.bufA, 0, sizeof(double) * (P * S.nlat_tot + S.cpad), c.stream);
+    cudaMemsetAsync(S.bufB + P * S.nlat_tot, 0, sizeof(double) * S.cpad, c.stream);
     c.kbegin("gather_samples");
-    gather_samples_kernel<<<nblk(nlat_tot * P, 256), 256, 0, c.stream>>>(rowstart, data, dlat, nlat_tot, P, bufA);
+    gather_samples_kernel<<<nblk(S.nlat_tot * P, 256), 256, 0, c.stream>>>(S.rowstart, s.data, S.dlat, S.nlat_tot, P, slab_lo,
+                                                                           slab_hi, S.bufA);
     c.kend();
-    double* cur = bufA;
-    double* nxt = bufB;
+    return 0;
+}
+
+// single-call path: the lattice rows outside the slab by a row-restricted assembly (bitwise the
+// same rows, assembly.py:613-622), gathered into the sample table
+static int surr_foreign_samples(sg_surrogate_state& S) {
+    Call& c = S.c;
+    std::vector<int64_t> rows;
+    for (int64_t r : S.latrows)
+        if (r < S.slab_lo || r >= S.slab_hi) rows.push_back(r);
+    if (rows.empty()) return 0;
+    std::sort(rows.begin(), rows.end());
+    int64_t* rs = nullptr;
+    int* ind = nullptr;
+    double* dat = nullptr;
+    int rc = assemble_rows_compact(c, S.dp, rows, &rs, &ind, &dat);
+    if (rc) return rc;
+    c.kbegin("gather_samples");
+    gather_samples_kernel<<<nblk(S.nlat_tot * S.P, 256), 256, 0, c.stream>>>(rs, dat, S.dlat, S.nlat_tot, S.P, 0, S.slab_lo,
+                                                                             S.bufA);
+    gather_samples_kernel<<<nblk(S.nlat_tot * S.P, 256), 256, 0, c.stream>>>(rs, dat, S.dlat, S.nlat_tot, S.P, S.slab_hi, S.N,
+                                                                             S.bufA);
+    c.kend();
+    c.free_temp(ind);
+    c.free_temp(dat);
+    return 0;
+}
+
+static int surr_finish(sg_surrogate_state& S, const sg_surrogate_params* sp, sg_result** out, sg_surrogate_stats* stats) {
+    Call& c = S.c;
+    DevProblem& dp = S.dp;
+    SurrParams& s = S.s;
+    const int n = S.n, p = S.p, P = S.P, center = S.center;
+    const int64_t N = S.N, slab_lo = S.slab_lo, slab_hi = S.slab_hi, nlat_tot = S.nlat_tot;
+    // ---- K6: samples -> spline coefficients
+    double* cur = S.bufA;
+    double* nxt = S.bufB;
     int64_t inner = 1;
     for (int d = 0; d < n; ++d) {
         const int len = s.nl[d];
@@ -1270,6 +1348,7 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
         }
         inner *= len;
     }
+    // the zeroed tail behind the coefficients (bufA's was cleared in begin, bufB's too)
     s.coef = cur;
 
     // ---- evaluation tables at the in-box midpoints (Cox-de Boor on the averaged knots)
@@ -1297,24 +1376,22 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
         s.TB[d] = rows3 ? (d == 0 ? rows3::TB0 : (d == 1 ? rows3::TB1 : rows3::TB2)) : TBdef[n - 1][d];
         s.tg[d] = (s.bn[d] + s.TB[d] - 1) / s.TB[d];
     }
-    {
-        for (int d = 0; d < 3; ++d) {
-            if (d >= n || s.qd[d] < 1) {
-                s.cmax[d] = 1;
-                continue;
-            }
-            std::vector<double> kn(sp->interp_knots[d], sp->interp_knots[d] + s.nl[d] + s.qd[d] + 1);
-            std::vector<int> spn(s.bn[d]);
-            for (int k = 0; k < s.bn[d]; ++k) spn[k] = find_span(kn.data(), (int)kn.size(), s.qd[d], sp->box_pts[d][k]);
-            int cm = 1;
-            for (int org = 0; org < s.bn[d]; org += s.TB[d])
-                for (int sh = -p; sh <= p; ++sh) {
-                    const int a = std::min(std::max(org + sh, 0), s.bn[d] - 1);
-                    const int b = std::min(std::max(org + s.TB[d] - 1 + sh, 0), s.bn[d] - 1);
-                    cm = std::max(cm, spn[b] - spn[a] + s.qd[d] + 1);
-                }
-            s.cmax[d] = cm;
+    for (int d = 0; d < 3; ++d) {
+        if (d >= n || s.qd[d] < 1) {
+            s.cmax[d] = 1;
+            continue;
         }
+        std::vector<double> kn(sp->interp_knots[d], sp->interp_knots[d] + s.nl[d] + s.qd[d] + 1);
+        std::vector<int> spn(s.bn[d]);
+        for (int k = 0; k < s.bn[d]; ++k) spn[k] = find_span(kn.data(), (int)kn.size(), s.qd[d], sp->box_pts[d][k]);
+        int cm = 1;
+        for (int org = 0; org < s.bn[d]; org += s.TB[d])
+            for (int sh = -p; sh <= p; ++sh) {
+                const int a = std::min(std::max(org + sh, 0), s.bn[d] - 1);
+                const int b = std::min(std::max(org + s.TB[d] - 1 + sh, 0), s.bn[d] - 1);
+                cm = std::max(cm, spn[b] - spn[a] + s.qd[d] + 1);
+            }
+        s.cmax[d] = cm;
     }
     // ---- K7
     const int nthreads = 512;
@@ -1391,7 +1468,7 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
 
     // ---- merge: zero check
     unsigned long long hc[8];
-    cudaMemcpyAsync(hc, counters, sizeof(hc), cudaMemcpyDeviceToHost, c.stream);
+    cudaMemcpyAsync(hc, S.counters, sizeof(hc), cudaMemcpyDeviceToHost, c.stream);
     cudaStreamSynchronize(c.stream);
     e = cudaGetLastError();
     if (e != cudaSuccess) return fail(-3, "CUDA error in surrogate: %s", cudaGetErrorString(e));
@@ -1405,30 +1482,29 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
     if (zeros == 0) {
         if (s.mode == SG_SYMMETRIC_KERNEL_PRESERVING) {
             c.kbegin("skp_apply");
-            skp_apply_kernel<<<nblk(slab_hi - slab_lo, 256), 256, 0, c.stream>>>(reset, newdiag, rowstart, center, slab_lo, slab_hi, data);
+            skp_apply_kernel<<<nblk(slab_hi - slab_lo, 256), 256, 0, c.stream>>>(S.reset, S.newdiag, S.rowstart, center, slab_lo,
+                                                                                slab_hi, s.data);
             c.kend();
         }
-        r->nnz = nnz_hi - nnz_lo;
-        if (nnz_lo == 0 && nnz_hi == nnz_all) {
-            // whole matrix: the work arrays become the result (no copy)
-            c.release(indices);
-            c.release(data);
-            r->indices = indices;
-            r->data = data;
+        r->nnz = S.nnz_hi - S.nnz_lo;
+        c.release(S.indices);
+        c.release(S.data);
+        if (S.nnz_qlo == S.nnz_lo && S.nnz_qhi == S.nnz_hi) {
+            // the work arrays are exactly the result's rows (whole matrix): no copy
+            r->indices = S.indices;
+            r->data = S.data;
         } else {
-            // row slab: the result is the slab's range of the work arrays (no copy); the whole
-            // allocations are freed with the result
-            c.release(indices);
-            c.release(data);
-            r->own_indices = indices;
-            r->own_data = data;
-            r->indices = indices + nnz_lo;
-            r->data = data + nnz_lo;
+            // row slab: the result is the slab's range of the work arrays (sized for the slab and its
+            // p-plane halo only); the allocations are freed with the result
+            r->own_indices = S.indices;
+            r->own_data = S.data;
+            r->indices = S.indices + (S.nnz_lo - S.nnz_qlo);
+            r->data = S.data + (S.nnz_lo - S.nnz_qlo);
         }
-        cudaMemcpyAsync(r->indptr, rowstart + slab_lo, sizeof(int64_t) * (r->nrows + 1), cudaMemcpyDeviceToDevice, c.stream);
-        if (nnz_lo) {
+        cudaMemcpyAsync(r->indptr, S.rowstart + slab_lo, sizeof(int64_t) * (r->nrows + 1), cudaMemcpyDeviceToDevice, c.stream);
+        if (S.nnz_lo) {
             c.kbegin("rebase");
-            rebase_kernel<<<nblk(r->nrows + 1, 256), 256, 0, c.stream>>>(r->indptr, r->nrows + 1, nnz_lo);
+            rebase_kernel<<<nblk(r->nrows + 1, 256), 256, 0, c.stream>>>(r->indptr, r->nrows + 1, S.nnz_lo);
             c.kend();
         }
     } else {
@@ -1436,7 +1512,7 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
         const int64_t nr = slab_hi - slab_lo;
         int64_t* cnt = (int64_t*)c.alloc(sizeof(int64_t) * (nr + 1), true);
         c.kbegin("nz_count");
-        nz_count_kernel<<<nblk(nr + 1, 256), 256, 0, c.stream>>>(rowstart, data, slab_lo, slab_hi, cnt);
+        nz_count_kernel<<<nblk(nr + 1, 256), 256, 0, c.stream>>>(S.rowstart, s.data, slab_lo, slab_hi, cnt);
         c.kend();
         size_t tb = 0;
         cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, r->indptr, nr + 1, c.stream);
@@ -1449,7 +1525,8 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
         r->indices = (int*)c.alloc(sizeof(int) * std::max<int64_t>(nnz_new, 1), false);
         r->data = (double*)c.alloc(sizeof(double) * std::max<int64_t>(nnz_new, 1), false);
         c.kbegin("compact");
-        compact_kernel<<<nblk(nr, 256), 256, 0, c.stream>>>(rowstart, data, indices, slab_lo, slab_hi, r->indptr, r->data, r->indices);
+        compact_kernel<<<nblk(nr, 256), 256, 0, c.stream>>>(S.rowstart, s.data, s.indices, slab_lo, slab_hi, r->indptr, r->data,
+                                                           r->indices);
         c.kend();
         if (s.mode == SG_SYMMETRIC_KERNEL_PRESERVING) {
             // surrogate.py:673-680 is positional on the global CSR: a reset row's window of P entries may
@@ -1458,8 +1535,9 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
             double* nv = (double*)c.alloc(sizeof(double) * std::max<int64_t>(nr, 1), true);
             int* bad = (int*)c.alloc(sizeof(int), true);
             cudaMemsetAsync(bad, 0, sizeof(int), c.stream);
-            skp_positional_kernel<<<nblk(nr, 256), 256, 0, c.stream>>>(reset, r->indptr, slab_lo, slab_hi, P, center, nnz_new, r->data, nv, bad);
-            skp_positional_apply<<<nblk(nr, 256), 256, 0, c.stream>>>(reset, r->indptr, slab_lo, slab_hi, center, nv, r->data);
+            skp_positional_kernel<<<nblk(nr, 256), 256, 0, c.stream>>>(S.reset, r->indptr, slab_lo, slab_hi, P, center, nnz_new,
+                                                                       r->data, nv, bad);
+            skp_positional_apply<<<nblk(nr, 256), 256, 0, c.stream>>>(S.reset, r->indptr, slab_lo, slab_hi, center, nv, r->data);
             int hb = 0;
             cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c.stream);
             cudaStreamSynchronize(c.stream);
@@ -1471,7 +1549,7 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
             }
         }
     }
-    rc = c.finish();
+    int rc = c.finish();
     if (rc) {
         sg_result_free(r);
         return rc;
@@ -1491,5 +1569,53 @@ extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* s
         stats->n_quad_rows = N - (int64_t)hc[3];
     }
     *out = r;
+    return 0;
+}
+
+extern "C" int sg_surrogate(const sg_problem* prob, const sg_surrogate_params* sp, const sg_exec* ex, sg_result** out,
+                            sg_surrogate_stats* stats) {
+    if (!out || !sp) return fail(-1, "null argument");
+    *out = nullptr;
+    sg_surrogate_state S(ex);
+    int rc = surr_begin(S, prob, sp, ex);
+    if (rc) return rc;
+    rc = surr_foreign_samples(S);
+    if (rc) return rc;
+    return surr_finish(S, sp, out, stats);
+}
+
+extern "C" int sg_surrogate_begin(const sg_problem* prob, const sg_surrogate_params* sp, const sg_exec* ex,
+                                  sg_surrogate_state** state, double** samples, int64_t* nlat) {
+    if (!state || !sp) return fail(-1, "null argument");
+    *state = nullptr;
+    sg_surrogate_state* S = new sg_surrogate_state(ex);
+    int rc = surr_begin(*S, prob, sp, ex);
+    if (rc) {
+        delete S;
+        return rc;
+    }
+    cudaStreamSynchronize(S->c.stream);  // the slab's samples are in the table when this returns
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        delete S;
+        return fail(-3, "CUDA error in surrogate begin: %s", cudaGetErrorString(e));
+    }
+    if (samples) *samples = S->bufA;
+    if (nlat) *nlat = S->nlat_tot;
+    *state = S;
+    return 0;
+}
+
+extern "C" int sg_surrogate_finish(sg_surrogate_state* state, const sg_surrogate_params* sp, sg_result** out,
+                                   sg_surrogate_stats* stats) {
+    if (!state || !sp || !out) return fail(-1, "null argument");
+    *out = nullptr;
+    const int rc = surr_finish(*state, sp, out, stats);
+    delete state;
+    return rc;
+}
+
+extern "C" int sg_surrogate_state_free(sg_surrogate_state* state) {
+    delete state;
     return 0;
 }

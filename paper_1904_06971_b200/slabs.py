@@ -12,7 +12,7 @@ from __future__ import annotations
 import numpy as np
 
 __all__ = ["plane_slabs", "weighted_plane_slabs", "surrogate_plane_cost", "job_slabs", "csr_checksum", "stitch",
-           "allreduce_checksum"]
+           "allreduce_checksum", "lattice_owners", "exchange_samples"]
 
 # Relative device cost per row of the surrogate's parts (measured on one B200 at config 5, p=3,
 # DESIGN.md §8): quadrature row (K4 on the quadrature tiles), interpolated row (K7), any row (K3
@@ -115,3 +115,58 @@ def allreduce_checksum(cs, dist=None):
     t = torch.tensor(np.asarray(cs, dtype=np.float64), device=dev)
     dist.all_reduce(t)
     return t.cpu().numpy()
+
+
+def lattice_owners(ms, lattice_indices, slabs) -> np.ndarray:
+    """Rank owning each lattice row (lattice colex order, direction 0 fastest): the slab holding it."""
+    ms = tuple(int(m) for m in ms)
+    grids = np.meshgrid(*[np.asarray(ix, dtype=np.int64) for ix in lattice_indices], indexing="ij")
+    strides = np.cumprod((1,) + ms[:-1])
+    rows = sum(g.ravel(order="F") * s for g, s in zip(grids, strides))
+    lo = np.array([a for a, _ in slabs], dtype=np.int64)
+    owner = np.searchsorted(lo, rows, side="right") - 1
+    hi = np.array([b for _, b in slabs], dtype=np.int64)
+    assert np.all(rows < hi[owner]), "slabs do not cover every lattice row"
+    return owner
+
+
+def exchange_samples(owner, dist, device=None):
+    """``exchange`` callback of ``surrogate_device`` for strategy B: every rank wrote
+    the samples of its own lattice rows into its device table; one all-gather of the owned columns
+    (<= 2 MB at config 5) completes every rank's table.  NCCL moves device buffers over NVLink; a
+    gloo group (CPU tests) goes through host copies."""
+    owner = np.asarray(owner)
+
+    def run(ptr, P, nlat):
+        import torch
+
+        rank = dist.get_rank()
+        world = dist.get_world_size()
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        table = _device_view(ptr, (P, nlat), dev)
+        cols = [np.flatnonzero(owner == k) for k in range(world)]
+        width = max(1, max(c.size for c in cols))
+        comm_dev = dev if dist.get_backend() == "nccl" else torch.device("cpu")
+        mine = torch.zeros((P, width), dtype=torch.float64, device=dev)
+        if cols[rank].size:
+            mine[:, :cols[rank].size] = table[:, torch.as_tensor(cols[rank], device=dev)]
+        mine = mine.to(comm_dev)
+        parts = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(parts, mine)
+        for k in range(world):
+            if k != rank and cols[k].size:
+                table[:, torch.as_tensor(cols[k], device=dev)] = parts[k][:, :cols[k].size].to(dev)
+        torch.cuda.synchronize(dev)
+
+    return run
+
+
+def _device_view(ptr, shape, dev):
+    """A torch view of a float64 device array owned by the library (``__cuda_array_interface__``)."""
+    import torch
+
+    class _Arr:
+        __cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f8", "data": (int(ptr), False), "version": 3,
+                                    "strides": None}
+
+    return torch.as_tensor(_Arr(), device=dev)

@@ -363,8 +363,14 @@ def _fit_params_build(disc, lattice: SamplingLattice, tilde: TildeDomain, q: int
 
 
 def surrogate_device(form, disc, M: int, q: int, mode_name: str, coefficient=1.0, *, device=None, stream=None,
-                     slab=None, lattice=None, tilde=None):
-    """Run the native surrogate; returns (Result, stats, lowered)."""
+                     slab=None, lattice=None, tilde=None, exchange=None):
+    """Run the native surrogate; returns (Result, stats, lowered).
+
+    ``exchange`` (row slabs on several devices): a callable ``exchange(ptr, P, nlat)``
+    that completes the device sample table ``S[o][lattice colex]`` at ``ptr`` (float64, P x nlat)
+    with the lattice rows of the other slabs (``slabs.exchange_samples``: an all-gather over the
+    process group) and synchronises.  Without it, a slab call assembles the other slabs' lattice
+    rows itself (row-restricted quadrature, bitwise the same rows)."""
     pr, keep, fname, N = problem_arrays(form, disc, coefficient)
     space = disc.space
     if tilde is None:
@@ -375,7 +381,22 @@ def surrogate_device(form, disc, M: int, q: int, mode_name: str, coefficient=1.0
     ex = _exec(device, stream, slab)
     h = C.c_void_p()
     st = _lib.SgSurrogateStats()
-    _lib.check(_lib.lib().sg_surrogate(C.byref(pr), C.byref(spp), C.byref(ex), C.byref(h), C.byref(st)))
+    L = _lib.lib()
+    if exchange is None:
+        _lib.check(L.sg_surrogate(C.byref(pr), C.byref(spp), C.byref(ex), C.byref(h), C.byref(st)))
+    else:
+        state = C.c_void_p()
+        table = C.c_void_p()
+        nlat = C.c_int64()
+        _lib.check(L.sg_surrogate_begin(C.byref(pr), C.byref(spp), C.byref(ex), C.byref(state), C.byref(table),
+                                        C.byref(nlat)))
+        try:
+            P = (2 * int(space.kvs[0].p) + 1) ** space.n
+            exchange(int(table.value), P, int(nlat.value))
+        except BaseException:
+            L.sg_surrogate_state_free(state)
+            raise
+        _lib.check(L.sg_surrogate_finish(state, C.byref(spp), C.byref(h), C.byref(st)))
     del keep, keep2
     return _lib.Result(h.value), st, lowered
 
