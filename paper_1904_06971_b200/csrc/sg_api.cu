@@ -45,7 +45,22 @@ int fail(int code, const char* fmt, ...) {
     return code;
 }
 
+// Small host inputs (knots, Gauss points, masks, tables) are staged through a per-thread pinned arena,
+// so their copies are truly asynchronous: a pageable cudaMemcpyAsync blocks the host until the stream
+// reaches it, which serialised host planning behind every kernel already queued (~0.5 ms of device
+// idle per call at config 5).  The arena is rewound when the last live Call of the thread has been
+// destroyed (every Call synchronises its stream before it dies, so no staged copy is pending).
+struct PinnedArena {
+    char* base = nullptr;
+    size_t cap = 0, off = 0;
+    int users = 0;
+    bool tried = false;
+};
+static thread_local PinnedArena g_arena;
+constexpr size_t kArenaBytes = 64u << 20;
+
 Call::Call(const sg_exec* ex) {
+    g_arena.users++;
     dev = ex ? ex->device : 0;
     cudaSetDevice(dev);
     if (ex && ex->stream) {
@@ -67,6 +82,7 @@ Call::Call(const sg_exec* ex) {
     cudaEventCreate(&ev0);
     cudaEventCreate(&ev1);
     cudaEventRecord(ev0, stream);
+    t_host0 = std::chrono::steady_clock::now();
     launches = 0;
 }
 
@@ -79,10 +95,9 @@ Call::~Call() {
     }
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
-    if (own_stream) {
-        cudaStreamSynchronize(stream);
-        cudaStreamDestroy(stream);
-    }
+    cudaStreamSynchronize(stream);  // staged uploads are complete (no-op when the call already synchronised)
+    if (own_stream) cudaStreamDestroy(stream);
+    if (--g_arena.users == 0) g_arena.off = 0;
 }
 
 void* Call::alloc(size_t bytes, bool temp) {
@@ -109,18 +124,37 @@ void Call::free_temp(void* p) {
 
 void* Call::upload(const void* host, size_t bytes) {
     void* d = alloc(bytes, true);
-    if (d && host && bytes) cudaMemcpyAsync(d, host, bytes, cudaMemcpyHostToDevice, stream);
+    if (!d || !host || !bytes) return d;
+    if (!g_arena.tried) {
+        g_arena.tried = true;
+        if (cudaMallocHost((void**)&g_arena.base, kArenaBytes) == cudaSuccess) g_arena.cap = kArenaBytes;
+        else g_arena.base = nullptr;
+    }
+    const size_t need = (bytes + 255) & ~size_t(255);
+    if (g_arena.base && g_arena.off + need <= g_arena.cap) {
+        char* h = g_arena.base + g_arena.off;
+        memcpy(h, host, bytes);
+        g_arena.off += need;
+        cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, stream);
+    } else {
+        cudaMemcpyAsync(d, host, bytes, cudaMemcpyHostToDevice, stream);
+    }
     return d;
 }
 
 void Call::kbegin(const char* name) {
     KEv k;
     k.name = name;
+    k.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
     cudaEventCreate(&k.a);
     cudaEventCreate(&k.b);
     cudaEventRecord(k.a, stream);
     kev.push_back(k);
     launches++;
+}
+void Call::hmark(const char* what) {
+    static const bool on = getenv("SG_TRACE") != nullptr;
+    if (on) hmarks.push_back({what, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count()});
 }
 void Call::kend() { cudaEventRecord(kev.back().b, stream); }
 
@@ -144,6 +178,17 @@ void Call::record_timing() {
         cudaEventElapsedTime(&t, k.a, k.b);
         g_ktimes.push_back({k.name, (double)t});
     }
+    if (getenv("SG_TRACE")) {
+        // device timeline of the call (start offset / duration) next to the host time of each launch
+        fprintf(stderr, "[sg trace] call total %.3f ms\n", ms);
+        for (auto& k : kev) {
+            float t0 = 0.f, t1 = 0.f;
+            cudaEventElapsedTime(&t0, ev0, k.a);
+            cudaEventElapsedTime(&t1, k.a, k.b);
+            fprintf(stderr, "[sg trace]   %-18s dev start %8.3f dur %7.3f  host launch %8.3f\n", k.name.c_str(), t0, t1, k.host_ms);
+        }
+        for (auto& h : hmarks) fprintf(stderr, "[sg trace]   host mark %-24s %8.3f\n", h.first, h.second);
+    }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -158,6 +203,31 @@ __global__ void tabulate_kernel(const double* __restrict__ knots, int nk, int p,
     if (span_out) span_out[i] = span;
     const int w = (nu + 1) * (p + 1);
     for (int k = 0; k < w; ++k) tab_out[(long long)i * w + k] = ders[k];
+}
+
+// several tabulations in one launch (blockIdx.y = job): the per-direction solution and geometry
+// tables of a call are tiny, so their launch overhead dominated the call's prologue
+struct TabJob {
+    const double* knots;
+    const double* pts;
+    int* span;
+    double* tab;
+    int nk, p, npts, nu;
+};
+struct TabJobs {
+    TabJob j[6];
+    int n;
+};
+
+__global__ void tabulate_multi_kernel(TabJobs jobs) {
+    const TabJob& J = jobs.j[blockIdx.y];
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= J.npts) return;
+    double ders[(SG_MAX_PG + 1) * 3];
+    const int span = basis_ders(J.knots, J.nk, J.p, J.pts[i], J.nu, ders);
+    if (J.span) J.span[i] = span;
+    const int w = (J.nu + 1) * (J.p + 1);
+    for (int k = 0; k < w; ++k) J.tab[(long long)i * w + k] = ders[k];
 }
 
 int tabulate(Call& c, const double* d_knots, int nk, int p, const double* d_pts, int npts, int nu, int* d_span,
@@ -306,25 +376,32 @@ int prepare_problem(Call& c, const sg_problem* pr, DevProblem& dp) {
         dp.Ng *= dp.mg[d];
     }
     dp.rational = pr->sol_w != nullptr;
-    // uploads
+    // uploads; the 2n tables (solution and geometry bases per direction) in one launch
+    TabJobs jobs;
+    jobs.n = 0;
+    int maxpts = 0;
     for (int d = 0; d < pr->n; ++d) {
         const int npts = dp.S[d] * dp.g;
+        maxpts = std::max(maxpts, npts);
         double* kn = (double*)c.upload(pr->knots[d], sizeof(double) * (dp.m[d] + dp.p + 1));
         double* qp = (double*)c.upload(pr->qpts[d], sizeof(double) * npts);
         dp.qw[d] = (double*)c.upload(pr->qwts[d], sizeof(double) * dp.g);
         dp.B[d] = (double*)c.alloc(sizeof(double) * npts * (dp.nu + 1) * (dp.p + 1), true);
         dp.bspan[d] = (int*)c.alloc(sizeof(int) * npts, true);
-        tabulate(c, kn, dp.m[d] + dp.p + 1, dp.p, qp, npts, dp.nu, dp.bspan[d], dp.B[d]);
+        jobs.j[jobs.n++] = TabJob{kn, qp, dp.bspan[d], dp.B[d], dp.m[d] + dp.p + 1, dp.p, npts, dp.nu};
         double* gk = (double*)c.upload(pr->geo_knots[d], sizeof(double) * (dp.mg[d] + pr->geo_p + 1));
         dp.G[d] = (double*)c.alloc(sizeof(double) * npts * (dp.nug + 1) * (pr->geo_p + 1), true);
         dp.gspan[d] = (int*)c.alloc(sizeof(int) * npts, true);
-        tabulate(c, gk, dp.mg[d] + pr->geo_p + 1, pr->geo_p, qp, npts, dp.nug, dp.gspan[d], dp.G[d]);
+        jobs.j[jobs.n++] = TabJob{gk, qp, dp.gspan[d], dp.G[d], dp.mg[d] + pr->geo_p + 1, pr->geo_p, npts, dp.nug};
         // host copies of geometry spans for the smem bound
         std::vector<double> hk(pr->geo_knots[d], pr->geo_knots[d] + dp.mg[d] + pr->geo_p + 1);
         dp.hgspan[d].resize(npts);
         for (int i = 0; i < npts; ++i)
             dp.hgspan[d][i] = find_span(hk.data(), (int)hk.size(), pr->geo_p, pr->qpts[d][i]);
     }
+    c.kbegin("tabulate");
+    tabulate_multi_kernel<<<dim3((maxpts + 127) / 128, jobs.n), 128, 0, c.stream>>>(jobs);
+    c.kend();
     for (int d = pr->n; d < 3; ++d) {
         dp.qw[d] = nullptr;
         dp.B[d] = nullptr;
@@ -557,7 +634,9 @@ int compute_D(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* t
     const size_t smem = o * sizeof(double);
     if (smem > kSmemCap) return fail(-2, "geometry block does not fit shared memory (%zu B)", smem);
     const size_t npts = (size_t)gp.Gp[0] * gp.Dys * gp.Gp[2];
+    c.hmark("compute_D:layout");
     gp.D = (double*)c.alloc(sizeof(double) * npts * U, true);
+    c.hmark("compute_D:alloc");
     if (!gp.D) return fail(-4, "device allocation of the D tensor failed (%zu MB)", sizeof(double) * npts * U >> 20);
     dp.D = gp.D;
     if (tiles) {
@@ -709,7 +788,9 @@ int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>
                  const int64_t* d_rowstart, int64_t slab_lo, int64_t slab_hi, int* d_indices, double* d_data,
                  unsigned long long* d_zeros) {
     if (tiles && tiles->empty()) return 0;
+    c.hmark("run_assembly:start");
     int rc = compute_D(c, dp, pl, tiles, d_rowmask, slab_lo, slab_hi);
+    c.hmark("run_assembly:D launched");
     if (rc) return rc;
     if (pl.mma) {
         MmaParams mp;
@@ -752,6 +833,7 @@ int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>
         }
         cudaFuncSetAttribute(pl.kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptinMax);
         void* args[] = {&mp};
+        c.hmark("run_assembly:pre-launch");
         c.kbegin("assemble_mma");
         cudaError_t e = cudaLaunchKernel(pl.kfn, dim3((unsigned)nb), dim3(pl.nthreads), args, pl.smem, c.stream);
         c.kend();
@@ -820,9 +902,22 @@ int launch_assembly(Call& c, DevProblem& dp, const uint8_t* d_rowmask, const int
         const int nz = (planes + kMmaT2 - 1) / kMmaT2;
         t2 = (planes + nz - 1) / nz;
     }
+    c.hmark("launch_assembly:start");
     int rc = plan_assembly(dp, pl, h_rows != nullptr, t2, z0);
+    c.hmark("launch_assembly:planned");
     if (rc) return rc;
     if (!h_rows && full_slab) return run_assembly(c, dp, pl, nullptr, d_rowmask, d_rowstart, slab_lo, slab_hi, d_indices, d_data, nullptr);
+    const int64_t pl01 = (int64_t)dp.m[0] * dp.m[1];
+    if (!h_rows && dp.n == 3 && slab_lo % pl01 == 0 && (slab_hi % pl01 == 0 || slab_hi >= dp.N)) {
+        // plane-aligned slab on a grid starting at its first plane: the tiles of the z-tile rows
+        // covering the slab's planes, a contiguous index range (no per-tile test)
+        const int64_t ze = (std::min<int64_t>(dp.N, slab_hi) - 1) / pl01;
+        const int64_t nzt = std::min<int64_t>(pl.tgrid[2], (ze - pl.z0) / pl.T[2] + 1);
+        std::vector<int> tiles((size_t)(nzt * pl.tgrid[0] * pl.tgrid[1]));
+        for (size_t t = 0; t < tiles.size(); ++t) tiles[t] = (int)t;
+        c.hmark("launch_assembly:tiles");
+        return run_assembly(c, dp, pl, &tiles, d_rowmask, d_rowstart, slab_lo, slab_hi, d_indices, d_data, nullptr);
+    }
     std::vector<uint8_t> mark(pl.ntiles, 0);
     if (h_rows) {
         for (int64_t k = 0; k < nrows; ++k)
@@ -839,6 +934,7 @@ int launch_assembly(Call& c, DevProblem& dp, const uint8_t* d_rowmask, const int
     std::vector<int> tiles;
     for (int64_t t = 0; t < pl.ntiles; ++t)
         if (mark[t]) tiles.push_back((int)t);
+    c.hmark("launch_assembly:tiles");
     return run_assembly(c, dp, pl, &tiles, d_rowmask, d_rowstart, slab_lo, slab_hi, d_indices, d_data, nullptr);
 }
 
@@ -980,11 +1076,18 @@ int sg_assemble(const sg_problem* prob, const int64_t* rows, int64_t nrows, cons
         cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, rowstart, N + 1, c.stream);
         c.kend();
     }
-    // nnz of this result
+    // nnz of this result: closed form (whole pattern) or the listed rows' counts -- no round trip
     int64_t nnz_lo = 0, nnz_hi = 0;
-    cudaMemcpyAsync(&nnz_lo, rowstart + slab_lo, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream);
-    cudaMemcpyAsync(&nnz_hi, rowstart + slab_hi, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream);
-    cudaStreamSynchronize(c.stream);
+    if (!rows) {
+        nnz_hi = nnz_before_row(dp, slab_hi) - nnz_before_row(dp, slab_lo);  // rowstart is already rebased
+    } else {
+        for (int64_t k = 0; k < nrows; ++k) {
+            const int64_t rr = rows[k];
+            if (rr < slab_lo || rr >= slab_hi) continue;
+            const int64_t i0 = rr % dp.m[0], i1 = (rr / dp.m[0]) % dp.m[1], i2 = rr / ((int64_t)dp.m[0] * dp.m[1]);
+            nnz_hi += cnt1d(i0, dp.m[0], dp.p) * cnt1d(i1, dp.m[1], dp.p) * cnt1d(i2, dp.m[2], dp.p);
+        }
+    }
     r->nnz = nnz_hi - nnz_lo;
     // result arrays (owned by the handle)
     r->indptr = (int64_t*)c.alloc(sizeof(int64_t) * (r->nrows + 1), false);
@@ -1247,6 +1350,7 @@ int sg_result_copy(const sg_result* r, int32_t* indptr, int32_t* indices, double
 
 int sg_result_device_ptrs(const sg_result* r, void** indptr_i64, void** indices_i32, void** data_f64) {
     if (!r) return fail(-1, "null result");
+    const_cast<sg_result*>(r)->exported = true;
     if (indptr_i64) *indptr_i64 = r->indptr;
     if (indices_i32) *indices_i32 = r->indices;
     if (data_f64) *data_f64 = r->data;
@@ -1277,8 +1381,11 @@ int sg_result_checksum(const sg_result* r, double out[5]) {
 int sg_result_free(sg_result* r) {
     if (!r) return 0;
     cudaSetDevice(r->dev);
-    // no device-wide synchronisation: the calls that use a result synchronise their own streams
-    // before returning, so freeing it never waits for other threads' work on the device
+    // the library's own calls on a result synchronise their streams before returning, so a result
+    // whose device pointers were never handed out is freed without waiting for other threads' work;
+    // once sg_result_device_ptrs exported them, a consumer may still read them on any stream: wait
+    // for the whole device before the memory can be reused
+    if (r->exported) cudaDeviceSynchronize();
     if (r->indptr) cudaFreeAsync(r->indptr, 0);
     if (r->own_indices) cudaFreeAsync(r->own_indices, 0);
     else if (r->indices) cudaFreeAsync(r->indices, 0);

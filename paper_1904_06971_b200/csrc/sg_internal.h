@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <chrono>
 #include <string>
 #include <vector>
 
@@ -21,6 +22,7 @@ struct sg_result {
     void* stream_hint = nullptr;
     void* own_indices = nullptr;  // allocations to free when indices / data point inside a larger buffer
     void* own_data = nullptr;
+    bool exported = false;  // device pointers handed out (sg_result_device_ptrs): free waits for the device
 };
 
 namespace sg {
@@ -41,7 +43,11 @@ struct Call {
     struct KEv {
         std::string name;
         cudaEvent_t a, b;
+        double host_ms = 0.0;  // host time of the launch since the call started (SG_TRACE)
     };
+    std::chrono::steady_clock::time_point t_host0;
+    std::vector<std::pair<const char*, double>> hmarks;  // host-only timeline marks (SG_TRACE)
+    void hmark(const char* what);
     std::vector<KEv> kev;
     int launches = 0;
     unsigned long long* dmma = nullptr;  // device counter of executed DMMA instructions (K4)

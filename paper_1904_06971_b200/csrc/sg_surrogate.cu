@@ -1236,10 +1236,22 @@ static int surr_begin(sg_surrogate_state& S, const sg_problem* prob, const sg_su
     c.kbegin("classify");
     classify_kernel<<<nblk(N, 256), 256, 0, c.stream>>>(s, N, quadmask);
     c.kend();
+    c.hmark("surr_begin:classified");
 
-    // ---- K4: the quadrature rows of [qlo, qhi) (the slab's own, the halo's transposed entries)
+    // ---- K4: the quadrature rows of [qlo, qhi) (the slab's own, the halo's transposed entries).
+    // A row slab starts its tile grid at its first plane and splits its planes into equal-depth z
+    // tiles, so no tile streams element layers of planes outside [qlo, qhi)
     Plan pl;
-    rc = plan_assembly(dp, pl, true);
+    int t2 = 0, z0 = 0;
+    if (n == 3 && (s.qlo > 0 || s.qhi < N)) {
+        const int64_t pl01 = (int64_t)dp.m[0] * dp.m[1];
+        z0 = (int)(s.qlo / pl01);
+        const int planes = (int)((s.qhi - 1) / pl01) - z0 + 1;
+        const int nz = (planes + 23) / 24;
+        t2 = (planes + nz - 1) / nz;
+    }
+    rc = plan_assembly(dp, pl, true, t2, z0);
+    c.hmark("surr_begin:planned");
     if (rc) return rc;
     std::vector<int> tiles;
     // per direction and tile coordinate: every index in the box / some index sampled (the tile
@@ -1250,28 +1262,39 @@ static int surr_begin(sg_surrogate_state& S, const sg_problem* prob, const sg_su
         fsm[d].assign(pl.tgrid[d], d < n ? 0 : 1);
         if (d >= n) continue;
         for (int tc = 0; tc < pl.tgrid[d]; ++tc) {
-            const int64_t lo = (int64_t)tc * pl.T[d], hi = std::min<int64_t>(lo + pl.T[d], dp.m[d]) - 1;
+            const int64_t lo = (d == 2 ? pl.z0 : 0) + (int64_t)tc * pl.T[d], hi = std::min<int64_t>(lo + pl.T[d], dp.m[d]) - 1;
             for (int64_t k = lo; k <= hi; ++k) {
                 fin[d][tc] = fin[d][tc] && inb[d][k];
                 fsm[d][tc] = fsm[d][tc] || smp[d][k];
             }
         }
     }
-    for (int64_t t = 0; t < pl.ntiles; ++t) {
-        int64_t lo[3], hi[3];
-        tile_box(pl, dp, t, lo, hi);
-        const int64_t tc[3] = {t % pl.tgrid[0], (t / pl.tgrid[0]) % pl.tgrid[1], t / ((int64_t)pl.tgrid[0] * pl.tgrid[1])};
-        bool all_in = true, any_samp_all = true;
-        for (int d = 0; d < n; ++d) {
-            all_in = all_in && fin[d][tc[d]];
-            any_samp_all = any_samp_all && fsm[d][tc[d]];
-        }
-        const bool has_quad = !all_in || any_samp_all;
-        if (!has_quad) continue;
-        const int64_t flo = lo[0] + dp.m[0] * (lo[1] + (int64_t)dp.m[1] * lo[2]);
-        const int64_t fhi = hi[0] + dp.m[0] * (hi[1] + (int64_t)dp.m[1] * hi[2]);
-        if (fhi >= s.qlo && flo < s.qhi) tiles.push_back((int)t);
+    {
+        // tiles with a quadrature row whose slowest-direction range meets the planes of [qlo, qhi)
+        // (tile classes are ANDs of per-direction flags; tiles are ordered z-slowest)
+        const int64_t plane = n == 3 ? (int64_t)dp.m[0] * dp.m[1] : (n == 2 ? dp.m[0] : 1);
+        const int ds = n - 1;
+        const int64_t zlo = s.qlo / plane, zhi = (s.qhi - 1) / plane;
+        const int64_t org = ds == 2 ? pl.z0 : 0;
+        const int tz0 = (int)std::max<int64_t>(0, (zlo - org) / pl.T[ds]);
+        const int tz1 = (int)std::min<int64_t>(pl.tgrid[ds] - 1, (zhi - org) / pl.T[ds]);
+        int tsz[3] = {pl.tgrid[0], pl.tgrid[1], pl.tgrid[2]};
+        int lo3[3] = {0, 0, 0};
+        lo3[ds] = tz0;
+        tsz[ds] = tz1 + 1;
+        for (int c2 = lo3[2]; c2 < tsz[2]; ++c2)
+            for (int c1 = lo3[1]; c1 < tsz[1]; ++c1)
+                for (int c0 = lo3[0]; c0 < tsz[0]; ++c0) {
+                    const int tc[3] = {c0, c1, c2};
+                    bool all_in = true, any_samp_all = true;
+                    for (int d = 0; d < n; ++d) {
+                        all_in = all_in && fin[d][tc[d]];
+                        any_samp_all = any_samp_all && fsm[d][tc[d]];
+                    }
+                    if (!all_in || any_samp_all) tiles.push_back(c0 + pl.tgrid[0] * (c1 + pl.tgrid[1] * c2));
+                }
     }
+    c.hmark("surr_begin:tiles");
     rc = run_assembly(c, dp, pl, &tiles, quadmask, S.rowstart, s.qlo, s.qhi, s.indices, s.data, S.counters + 4);
     if (rc) return rc;
 

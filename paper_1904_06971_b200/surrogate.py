@@ -287,6 +287,29 @@ def _flat(masks) -> np.ndarray:
     return acc
 
 
+def _active_element_count(ms, p, tilde: TildeDomain, lattice: SamplingLattice) -> int:
+    """Number of elements supporting a quadrature row, ``_elements_for_rows(quad_rows).size``
+    (surrogate.py:590, assembly.py:347-360), without the O(N) row mask.
+
+    Element e supports the rows e..e+p per direction, so it touches no quadrature row iff every
+    such row is interpolated: the row box [e, e+p]^n lies inside the tilde box and holds no fully
+    sampled row, i.e. not every direction has a lattice index in [e_d, e_d+p].  Both conditions
+    factor per direction: inactive = prod_d A_d - prod_d B_d with A_d = #{e_d : [e_d, e_d+p] in the
+    box} and B_d = #{those e_d whose window also holds a lattice index}."""
+    A = B = 1
+    for d, m in enumerate(ms):
+        lo, hi = tilde.index_range(d)
+        e = np.arange(m - p)
+        inside = (e >= lo) & (e + p <= hi)
+        lat = np.asarray(lattice.indices[d], dtype=np.int64)
+        first = np.searchsorted(lat, e, side="left")
+        has = (first < lat.size) & (lat[np.minimum(first, lat.size - 1)] <= e + p)
+        A *= int(inside.sum())
+        B *= int((inside & has).sum())
+    total = int(np.prod([m - p for m in ms]))
+    return total - (A - B)
+
+
 def _pattern_nnz(ms, p) -> int:
     tot = 1
     for m in ms:
@@ -428,11 +451,10 @@ def build_surrogate_matrix(form, disc, strategy=None, q: int = 3, mode=None, coe
                                  quad_fraction=1.0, active_elements=int(np.prod(spans)), assembly_seconds=dt,
                                  flags=["surrogate=disabled"])
     lattice = build_sampling_lattice(space.kvs, M, tilde)
-    inb, smp = _masks(tilde, lattice)
-    in_flat, samp_flat = _flat(inb), _flat(smp)
-    quad_rows = np.flatnonzero(~in_flat | samp_flat)
-    nI = N - quad_rows.size
-    active = _elements_for_rows(ms, p, quad_rows).size
+    # interpolated rows = box minus the lattice's tensor product: counted per direction
+    nI = int(np.prod([tilde.index_range(d)[1] - tilde.index_range(d)[0] + 1 for d in range(n)])) - \
+        int(np.prod([len(ix) for ix in lattice.indices]))
+    active = _active_element_count(ms, p, tilde, lattice)
     if nI == 0:
         A = assemble(form, disc, coefficient=coefficient)  # every row is a quadrature row
         dt = time.perf_counter() - t0
@@ -517,10 +539,9 @@ def surrogate_plan(disc, strategy=None, q: int = 3) -> SurrogatePlan:
         lb *= _band_pairs(lat, box, p)
         ll *= _band_pairs(lat, lat, p)
     interp_entries = bb - bl - lb + ll
-    inb, smp = _masks(tilde, lattice)
-    quad_rows = np.flatnonzero(~_flat(inb) | _flat(smp))
-    active = _elements_for_rows(ms, p, quad_rows).size
-    return SurrogatePlan(N=N, M=M, H=lattice.H, quad_rows=quad_rows.size, interp_rows=N - quad_rows.size,
+    n_interp = int(np.prod([tilde.index_count(d) for d in range(n)])) - int(np.prod([len(ix) for ix in lattice.indices]))
+    active = _active_element_count(ms, p, tilde, lattice)
+    return SurrogatePlan(N=N, M=M, H=lattice.H, quad_rows=N - n_interp, interp_rows=n_interp,
                          quad_entries=int(total_entries - interp_entries), interp_entries=int(interp_entries),
                          active_elements=int(active), total_elements=total,
                          gauss_points_surrogate=int(active) * g ** n, gauss_points_full=total * g ** n)

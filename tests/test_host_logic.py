@@ -117,3 +117,22 @@ def test_argument_validation_messages():
         pkg.build_surrogate_matrix(pkg.FormKind.STOKES_DIVERGENCE, disc)
     with pytest.raises(ValueError):
         pkg.make_discretization(pkg.unit_square(), 2, (4, 4), gauss=0)
+
+
+@pytest.mark.parametrize("p,spans,M", [(2, (24, 24), 5), (3, (30, 29, 31), 4), (1, (12, 12, 12), 3), (3, (40,), 7),
+                                       (2, (9, 10), 2), (3, (128, 128, 128), 16)])
+def test_active_element_count_matches_row_dilation(p, spans, M):
+    # the closed-form count of elements supporting a quadrature row equals the O(N) row-mask
+    # dilation (_elements_for_rows of the quadrature rows, surrogate.py:590)
+    from paper_1904_06971_b200.assembly import _elements_for_rows
+    from paper_1904_06971_b200.spaces import make_tensor_space
+    from paper_1904_06971_b200.surrogate import (_active_element_count, _flat, _masks, build_sampling_lattice,
+                                                 tilde_domain)
+
+    space = make_tensor_space(p, [s + p for s in spans])
+    ms = tuple(kv.m for kv in space.kvs)
+    tilde = tilde_domain(p, ms)
+    lat = build_sampling_lattice(space.kvs, M, tilde)
+    inb, smp = _masks(tilde, lat)
+    quad = np.flatnonzero(~_flat(inb) | _flat(smp))
+    assert _active_element_count(ms, p, tilde, lat) == _elements_for_rows(ms, p, quad).size
