@@ -52,6 +52,10 @@ class NativeError(RuntimeError):
     pass
 
 
+class UnsupportedError(NativeError, NotImplementedError):
+    """Status -2: valid for the reference but outside what this build supports (e.g. p > 4)."""
+
+
 _lock = threading.Lock()
 _lib = None
 
@@ -122,6 +126,8 @@ def check(rc):
             raise ValueError(msg)
         if rc == -6:
             raise IndexError(msg)
+        if rc == -2:
+            raise UnsupportedError(f"surriga_b200 error {rc}: {msg}")
         raise NativeError(f"surriga_b200 error {rc}: {msg}")
 
 

@@ -348,8 +348,12 @@ void launch_indptr_full(Call& c, const DevProblem& dp, int64_t base, int64_t* ro
 int prepare_problem(Call& c, const sg_problem* pr, DevProblem& dp) {
     if (!pr) return fail(-1, "null problem");
     if (pr->n < 1 || pr->n > 3) return fail(-1, "supported dimensions: 1, 2, 3");
-    if (pr->p < 1 || pr->p > SG_MAX_P) return fail(-1, "degree p=%d outside the compiled range 1..%d", pr->p, SG_MAX_P);
-    if (pr->g < 1 || pr->g > 8) return fail(-1, "gauss=%d outside the supported range 1..8", pr->g);
+    if (pr->p < 1) return fail(-1, "degree p=%d must be at least 1", pr->p);
+    if (pr->g < 1) return fail(-1, "gauss=%d must be at least 1", pr->g);
+    // valid for the reference (any p >= 1, any Gauss count) but outside what this build instantiates:
+    // "unsupported configuration", not an invalid argument
+    if (pr->p > SG_MAX_P) return fail(-2, "degree p=%d is not supported by this build (p <= %d)", pr->p, SG_MAX_P);
+    if (pr->g > 8) return fail(-2, "gauss=%d is not supported by this build (gauss <= 8)", pr->g);
     if (pr->geo_p < 1 || pr->geo_p > SG_MAX_PG) return fail(-1, "geometry degree %d unsupported", pr->geo_p);
     if (pr->form < 0 || pr->form > 2) return fail(-1, "unknown form %d", pr->form);
     if (pr->form == BIHARMONIC && pr->p < 2) return fail(-1, "the fourth-order form needs degree >= 2 for C^1 continuity");

@@ -148,3 +148,19 @@ def test_gpu_concurrent_calls_are_reentrant():
         s = seq[k % len(jobs)]
         assert np.array_equal(m.indptr, s.indptr) and np.array_equal(m.indices, s.indices)
         assert np.array_equal(m.data.view(np.int64), s.data.view(np.int64))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p,gauss", [(5, None), (2, 9)])
+def test_gpu_unsupported_degree_or_gauss_is_not_a_value_error(p, gauss):
+    # the reference accepts any p >= 1 and any Gauss count (bspline.py:231-234, assembly.py:173); this
+    # build instantiates p <= 4, gauss <= 8: outside that it is "unsupported" (NotImplementedError /
+    # NativeError), never the ValueError the reference reserves for invalid input
+    import paper_1904_06971_b200 as pkg
+    from paper_1904_06971_b200._lib import NativeError
+
+    disc = pkg.make_discretization(pkg.quarter_annulus(1.0, 2.0), p, (12, 12), gauss=gauss)
+    with pytest.raises(NotImplementedError):
+        pkg.assemble(pkg.FormKind.POISSON, disc)
+    with pytest.raises(NativeError):
+        pkg.assemble(pkg.FormKind.POISSON, disc)
