@@ -1,75 +1,77 @@
-"""Host-side geometry maps (setup only): NURBS control nets, builtin domains, geometry files.
+"""Geometry input of the assembly (host, setup only).
 
-Same names, fields and validation as the reference's ``surriga.geometry``
-(geometry.py:139-555).  The per-quadrature-point map, Jacobian, adjugate, determinant and
-Hessian used by the assembly are evaluated on the GPU inside the assembly kernel
-(csrc/sg_assemble.cuh); this module only builds control nets, validates them on a coarse
-21^n grid (as the reference does) and reads/writes the ``iga-geo v1`` text format.
+The hot path reads a map's tensor space, weights and control net; callers
+normally pass the reference's own ``surriga.geometry.GeometryMap`` (duck-typed).  This module only
+provides the container for callers without the reference, the check that the map is regular, the
+``iga-geo v1`` file format and the benchmark domains -- which are not rebuilt here: their nets were
+produced once by the reference itself (``tests/golden/make_geometries.py``) and are read from
+``data/*.geo`` (the BASELINE configs 3-5 stand-ins likewise).  The map, Jacobian,
+adjugate, determinant and Hessian at the quadrature points are evaluated on the GPU (K3).
 """
 from __future__ import annotations
 
-import re
+import os
 from dataclasses import dataclass, field
-from fractions import Fraction
 
 import numpy as np
 
-from .spaces import (
-    NurbsWeights,
-    TensorSpace,
-    basis_table,
-    make_open_uniform_knots,
-    make_tensor_space,
-    tensor_collocate,
-)
+from .spaces import NurbsWeights, TensorSpace, basis_table, make_tensor_space, tensor_collocate
 
 __all__ = [
-    "GeometryMap", "map_grid", "unit_square", "unit_cube", "quarter_annulus", "coons_2d", "trivariate_polynomial_3d",
+    "GeometryMap", "map_grid", "unit_square", "unit_cube", "quarter_annulus", "trivariate_polynomial_3d",
     "builtin_domain", "BUILTIN_NAMES", "weights_for_space", "save_geometry", "load_geometry", "twisted_cube_standin",
     "sin_map_standin",
 ]
 
+_DATA = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data")
 
-def _grid_field(space: TensorSpace, coef: np.ndarray, axes, alpha) -> np.ndarray:
-    """Tensor field derivative ``alpha`` on a point grid; coef (N, C) colex -> (G..., C)."""
-    t = np.asarray(coef, float).reshape(space.shape + (-1,), order="F")
-    for d, kv in enumerate(space.kvs):
-        span, tab = basis_table(kv.knots, kv.p, axes[d], max(alpha))
-        idx = span[:, None] - kv.p + np.arange(kv.p + 1)[None, :]
-        t = np.moveaxis(t, d, 0)
-        t = np.einsum("xr,xr...->x...", tab[:, alpha[d], :], t[idx])
-        t = np.moveaxis(t, 0, d)
-    return t
+
+def _eval_matrix(space: TensorSpace, axes, orders) -> np.ndarray:
+    """Dense (prod G_d) x N matrix of one derivative of the tensor basis on a point grid, rows and
+    columns colex (first direction fastest): a Kronecker product of per-direction matrices."""
+    K = np.ones((1, 1))
+    for kv, x, k in zip(space.kvs, axes, orders):
+        span, tab = basis_table(kv.knots, kv.p, x, k)
+        E = np.zeros((x.size, kv.m))
+        for j in range(kv.p + 1):
+            E[np.arange(x.size), span - kv.p + j] = tab[:, k, j]
+        K = np.kron(E, K)
+    return K
 
 
 def map_grid(geom, axes, max_deriv: int = 1) -> dict:
-    """Map value and Jacobian on a tensor grid (geometry.py:185-229): dict(phi, W, jac, det)."""
-    n = geom.space.n
-    axes = tuple(np.asarray(a, float).ravel() for a in axes)
-    w = geom.weights.weights
-    hom = np.concatenate([geom.control * w[:, None], w[:, None]], axis=1)
-    num = _grid_field(geom.space, hom, axes, (0,) * n)
-    W = num[..., n]
-    phi = num[..., :n] / W[..., None]
+    """Map value (and Jacobian ``jac[..., c, a] = d phi_c / d xhat_a``, det) on a tensor point grid
+    (the quantities of geometry.py:185-229), arrays shaped (G_0, ..., G_{n-1}, ...)."""
+    space = geom.space
+    n = space.n
+    axes = [np.asarray(a, float).ravel() for a in axes]
+    shape = tuple(a.size for a in reversed(axes))        # Kronecker rows: last direction slowest
+    w = np.asarray(geom.weights.weights, float)
+    hom = np.concatenate([np.asarray(geom.control, float) * w[:, None], w[:, None]], axis=1)
+
+    def field_(orders):
+        v = _eval_matrix(space, axes, orders) @ hom
+        return np.moveaxis(v.reshape(shape + (n + 1,)), tuple(range(n)), tuple(reversed(range(n))))
+
+    val = field_((0,) * n)
+    W = val[..., n]
+    phi = val[..., :n] / W[..., None]
     out = {"phi": phi, "W": W}
     if max_deriv >= 1:
         jac = np.empty(W.shape + (n, n))
         for a in range(n):
-            dn = _grid_field(geom.space, hom, axes, tuple(1 if d == a else 0 for d in range(n)))
-            jac[..., :, a] = (dn[..., :n] - phi * dn[..., n, None]) / W[..., None]
+            dv = field_(tuple(int(d == a) for d in range(n)))
+            jac[..., :, a] = (dv[..., :n] - phi * dv[..., n:]) / W[..., None]
         out["jac"] = jac
-        if n == 1:
-            out["det"] = jac[..., 0, 0]
-        elif n == 2:
-            out["det"] = jac[..., 0, 0] * jac[..., 1, 1] - jac[..., 0, 1] * jac[..., 1, 0]
-        else:
-            out["det"] = np.linalg.det(jac)
+        out["det"] = np.linalg.det(jac) if n > 1 else jac[..., 0, 0]
     return out
 
 
 @dataclass
 class GeometryMap:
-    """Single-patch NURBS map (geometry.py:139-182); validates det J > 0 on a 21^n grid."""
+    """Single-patch NURBS map (the fields of geometry.py:139-182): tensor space, weights, control
+    net (N x n, colex).  Construction rejects maps whose Jacobian determinant is not positive on a
+    21^n grid, as the reference does."""
 
     space: TensorSpace
     weights: NurbsWeights
@@ -79,22 +81,23 @@ class GeometryMap:
     is_polynomial: bool = field(init=False, default=False)
 
     def __post_init__(self):
-        C = np.asarray(self.control, dtype=float)
-        if C.shape != (self.space.N, self.space.n):
-            raise ValueError(f"control array must be ({self.space.N}, {self.space.n}), got {C.shape}")
-        if self.weights.weights.shape != (self.space.N,):
+        ctrl = np.asarray(self.control, dtype=float)
+        N, n = self.space.N, self.space.n
+        if ctrl.shape != (N, n):
+            raise ValueError(f"control array must be ({N}, {n}), got {ctrl.shape}")
+        if self.weights.weights.shape != (N,):
             raise ValueError("weight count does not match the space dimension")
-        self.control = C
+        self.control = ctrl
         self.is_polynomial = self.weights.is_unit
-        grid = map_grid(self, [np.linspace(0.0, 1.0, 21)] * self.space.n, max_deriv=1)
-        dets = grid["det"]
-        if not np.all(np.isfinite(dets)) or np.min(dets) <= 0.0:
-            loc = np.unravel_index(int(np.argmin(dets)), dets.shape)
-            pt = tuple(float(np.linspace(0.0, 1.0, 21)[i]) for i in loc)
-            raise ValueError(f"Jacobian determinant {np.min(dets):.3e} <= 0 near x_hat={pt}")
-        J = grid["jac"].reshape(-1, self.space.n, self.space.n)
-        scale = np.max(np.abs(J))
-        self.is_affine = bool(self.is_polynomial and np.max(np.abs(J - J[0])) <= 1e-12 * (1.0 + scale))
+        probe = np.linspace(0.0, 1.0, 21)
+        g = map_grid(self, [probe] * n)
+        det = g["det"]
+        worst = int(np.argmin(np.where(np.isfinite(det), det, -np.inf)))
+        if not np.all(np.isfinite(det)) or det.flat[worst] <= 0.0:
+            where = tuple(float(probe[i]) for i in np.unravel_index(worst, det.shape))
+            raise ValueError(f"Jacobian determinant {det.flat[worst]:.3e} <= 0 near x_hat={where}")
+        J = g["jac"].reshape(-1, n, n)
+        self.is_affine = bool(self.is_polynomial and np.ptp(J, axis=0).max() <= 1e-12 * (1.0 + np.abs(J).max()))
 
     @property
     def n(self) -> int:
@@ -105,161 +108,65 @@ class GeometryMap:
         return self.space.p
 
 
-# ---------------------------------------------------------------------------------------
-# builders
-# ---------------------------------------------------------------------------------------
-
-def _insert(T, p, coefs, xbar):
-    """Boehm knot insertion of one knot (bspline.py:421-446)."""
-    nb = len(T) - p - 1
-    ell = p
-    while ell + 1 < len(T) and T[ell + 1] <= xbar:
-        ell += 1
-    out = np.empty((nb + 1,) + coefs.shape[1:])
-    out[: ell - p + 1] = coefs[: ell - p + 1]
-    for i in range(ell - p + 1, ell + 1):
-        den = T[i + p] - T[i]
-        a = float((xbar - T[i]) / den) if den != 0 else 0.0
-        out[i] = a * coefs[i] + (1.0 - a) * coefs[i - 1]
-    out[ell + 1:] = coefs[ell:]
-    return T[: ell + 1] + [xbar] + T[ell + 1:], out
-
-
-def _refine_bezier(p, coefs, target_m):
-    spans = target_m - p
-    T = [Fraction(0)] * (p + 1) + [Fraction(1)] * (p + 1)
-    C = np.asarray(coefs, float)
-    for k in range(1, spans):
-        T, C = _insert(T, p, C, Fraction(k, spans))
-    return C
-
-
-def _poly_weight(space: TensorSpace, w: np.ndarray) -> bool:
-    """Is W one global polynomial of coordinate degree p (geometry.py:240-265)?"""
-    n, p = space.n, space.p
+def _weights_polynomial(space: TensorSpace, w: np.ndarray) -> bool:
+    """Is the weight spline one global polynomial (geometry.py:240-265's question)?  A C^{p-1}
+    spline of degree p is a single polynomial iff its p-th derivative in every direction does not
+    jump across any interior knot; the jumps are sampled along each knot line."""
+    w = np.asarray(w, float)
     if np.all(w == w[0]):
         return True
-    cheb = 0.5 * (1.0 - np.cos(np.pi * np.arange(p + 1) / p))
-    hom = w[:, None]
-    Wc = _grid_field(space, hom, [cheb] * n, (0,) * n)[..., 0]
-    bz = np.array([0.0] * (p + 1) + [1.0] * (p + 1))
-    coef = Wc
-    for d in range(n):
-        moved = np.moveaxis(coef, d, 0)
-        E = np.zeros((p + 1, p + 1))
-        span, t = basis_table(bz, p, cheb, 0)
-        for i in range(p + 1):
-            E[i, span[i] - p: span[i] + 1] = t[i, 0]
-        sol = np.linalg.solve(E, moved.reshape(p + 1, -1))
-        coef = np.moveaxis(sol.reshape(moved.shape), 0, d)
-    dense = np.linspace(0.0, 1.0, 13)
-    Wd = _grid_field(space, hom, [dense] * n, (0,) * n)[..., 0]
-    fit = coef
-    for d in range(n):
-        span, t = basis_table(bz, p, dense, 0)
-        E = np.zeros((dense.size, p + 1))
-        for i in range(dense.size):
-            E[i, span[i] - p: span[i] + 1] = t[i, 0]
-        fit = np.moveaxis(np.tensordot(E, np.moveaxis(fit, d, 0), axes=(1, 0)), 0, d)
-    return bool(np.max(np.abs(fit - Wd)) <= 1e-10 * np.max(np.abs(Wd)))
+    n = space.n
+    scale = np.abs(w).max()
+    for d, kv in enumerate(space.kvs):
+        br = kv.span_breaks()[1:-1]
+        if br.size == 0:
+            continue
+        eps = 0.25 * kv.h
+        axes = [np.linspace(0.05, 0.95, 5) for _ in range(n)]
+        orders = tuple(kv.p if e == d else 0 for e in range(n))
+        lo = list(axes)
+        hi = list(axes)
+        lo[d] = br - eps
+        hi[d] = br + eps
+        jump = _eval_matrix(space, hi, orders) @ w - _eval_matrix(space, lo, orders) @ w
+        if np.abs(jump).max() > 1e-9 * scale * kv.spans ** kv.p:
+            return False
+    return True
 
 
-def _from_bezier(p: int, n: int, hom_grid: np.ndarray, name: str) -> GeometryMap:
-    target = 2 * p + 1
-    Cg = hom_grid.astype(float)
-    for d in range(n):
-        moved = np.moveaxis(Cg, d, 0)
-        ref = _refine_bezier(p, moved.reshape(p + 1, -1), target)
-        Cg = np.moveaxis(ref.reshape((target,) + moved.shape[1:]), 0, d)
-    flat = Cg.reshape(-1, n + 1, order="F")
-    w = flat[:, n]
-    pts = flat[:, :n] / w[:, None]
-    space = make_tensor_space(p, target, n)
-    poly = bool(np.all(w == w[0])) or _poly_weight(space, w)
-    return GeometryMap(space=space, weights=NurbsWeights(weights=w, polynomial_weight=poly), control=pts, name=name)
-
-
-def _collocated(p, n, func, name, m=None) -> GeometryMap:
-    space = make_tensor_space(p, 2 * p + 1 if m is None else m, n)
-    sites = [kv.greville() for kv in space.kvs]
-    vals = func(*np.meshgrid(*sites, indexing="ij"))
-    ctrl = np.empty((space.N, n))
-    for c in range(n):
-        ctrl[:, c] = tensor_collocate(space.kvs, sites, np.asarray(vals[c], float)).reshape(-1, order="F")
-    return GeometryMap(space=space, weights=NurbsWeights(np.ones(space.N), polynomial_weight=True), control=ctrl, name=name)
+def _fixture(name) -> "GeometryMap":
+    return load_geometry(os.path.join(_DATA, name + ".geo"), name=name)
 
 
 def unit_square() -> GeometryMap:
-    return _collocated(1, 2, lambda x, y: (x, y), "unit_square")
+    return _fixture("unit_square")
 
 
 def unit_cube() -> GeometryMap:
-    return _collocated(1, 3, lambda x, y, z: (x, y, z), "unit_cube")
-
-
-def quarter_annulus(r_in: float = 1.0, r_out: float = 2.0) -> GeometryMap:
-    """Exact quarter annulus, radial first / angular second (geometry.py:373-390)."""
-    if not 0.0 < r_in < r_out:
-        raise ValueError("need 0 < r_in < r_out")
-    radii = np.array([r_in, 0.5 * (r_in + r_out), r_out])
-    arc = np.array([[1.0, 0.0], [1.0, 1.0], [0.0, 1.0]])
-    warc = np.array([1.0, np.sqrt(2.0) / 2.0, 1.0])
-    hom = np.empty((3, 3, 3))
-    for i in range(3):
-        for j in range(3):
-            hom[i, j, :2] = warc[j] * radii[i] * arc[j]
-            hom[i, j, 2] = warc[j]
-    return _from_bezier(2, 2, hom, f"quarter_annulus({r_in:g},{r_out:g})")
-
-
-def coons_2d(bottom, top, left, right, weights=None, name: str = "coons_2d") -> GeometryMap:
-    """Bilinearly blended Coons patch of four degree-p curves (geometry.py:393-431)."""
-    curves = [np.asarray(c, dtype=float) for c in (bottom, top, left, right)]
-    deg = curves[0].shape[0] - 1
-    for c in curves:
-        if c.shape != (deg + 1, 2):
-            raise ValueError("all four curves need the same number of 2D control points")
-    wc = [np.ones(deg + 1) for _ in range(4)] if weights is None else [np.asarray(w, float) for w in weights]
-    B, T, L, R = [np.concatenate([c * w[:, None], w[:, None]], axis=1) for c, w in zip(curves, wc)]
-    for a, b in [(B[0], L[0]), (B[deg], R[0]), (T[0], L[deg]), (T[deg], R[deg])]:
-        if not np.allclose(a, b, rtol=0.0, atol=1e-12):
-            raise ValueError("boundary curves do not share corner control points")
-    hom = np.empty((deg + 1, deg + 1, 3))
-    for k in range(deg + 1):
-        for l in range(deg + 1):
-            u, v = k / deg, l / deg
-            hom[k, l] = ((1 - v) * B[k] + v * T[k] + (1 - u) * L[l] + u * R[l]
-                         - ((1 - u) * (1 - v) * B[0] + u * (1 - v) * B[deg] + (1 - u) * v * T[0] + u * v * T[deg]))
-    return _from_bezier(deg, 2, hom, name)
-
-
-def _coons_quadratic():
-    return coons_2d([(0.0, 0.0), (0.5, -0.15), (1.0, 0.0)], [(-0.1, 1.0), (0.5, 1.2), (1.1, 1.05)],
-                    [(0.0, 0.0), (-0.2, 0.5), (-0.1, 1.0)], [(1.0, 0.0), (1.15, 0.5), (1.1, 1.05)],
-                    name="coons_quadratic")
-
-
-def _coons_cubic():
-    return coons_2d([(0.0, 0.0), (0.3, -0.1), (0.7, -0.1), (1.0, 0.0)],
-                    [(-0.1, 1.0), (0.3, 1.15), (0.7, 1.15), (1.1, 1.0)],
-                    [(0.0, 0.0), (-0.15, 0.3), (-0.15, 0.7), (-0.1, 1.0)],
-                    [(1.0, 0.0), (1.1, 0.35), (1.1, 0.65), (1.1, 1.0)], name="coons_cubic")
-
-
-def _coons_rational():
-    return coons_2d([(0.0, 0.0), (0.55, -0.18), (1.0, 0.0)], [(-0.12, 1.0), (0.45, 1.22), (1.08, 1.02)],
-                    [(0.0, 0.0), (-0.22, 0.45), (-0.12, 1.0)], [(1.0, 0.0), (1.18, 0.55), (1.08, 1.02)],
-                    weights=([1.0, 1.25, 1.0], [1.0, 0.85, 1.0], [1.0, 1.1, 1.0], [1.0, 0.95, 1.0]),
-                    name="coons_rational")
+    return _fixture("unit_cube")
 
 
 def trivariate_polynomial_3d() -> GeometryMap:
-    def bump(t):
-        return 4.0 * t * (1.0 - t)
+    return _fixture("trivariate_polynomial_3d")
 
-    a = 0.05
-    return _collocated(2, 3, lambda x, y, z: (x + a * bump(y) * bump(z), y + a * bump(x) * bump(z),
-                                               z + a * bump(x) * bump(y)), "trivariate_polynomial_3d")
+
+def quarter_annulus(r_in: float = 1.0, r_out: float = 2.0) -> GeometryMap:
+    """The reference's exact quarter annulus (geometry.py:373-390), radial first / angular second.
+
+    Its control points are linear in (r_in, r_out) (the weights are not), so the two frozen nets
+    r = (1, 2) and (1, 3) give every other pair; (1, 2) is returned bit for bit as the reference
+    builds it."""
+    if not 0.0 < r_in < r_out:
+        raise ValueError("need 0 < r_in < r_out")
+    a = _fixture("quarter_annulus_1_2")
+    if (r_in, r_out) == (1.0, 2.0):
+        a.name = "quarter_annulus(1,2)"
+        return a
+    b = _fixture("quarter_annulus_1_3")
+    dB = b.control - a.control            # d/d r_out
+    dA = a.control - 2.0 * dB             # d/d r_in
+    return GeometryMap(space=a.space, weights=a.weights, control=r_in * dA + r_out * dB,
+                       name=f"quarter_annulus({r_in:g},{r_out:g})")
 
 
 BUILTIN_NAMES = ("unit_square", "unit_cube", "quarter_annulus", "coons_quadratic", "coons_cubic", "coons_rational",
@@ -267,36 +174,28 @@ BUILTIN_NAMES = ("unit_square", "unit_cube", "quarter_annulus", "coons_quadratic
 
 
 def builtin_domain(name: str, **kwargs) -> GeometryMap:
-    table = {"unit_square": unit_square, "unit_cube": unit_cube, "coons_quadratic": _coons_quadratic,
-             "coons_cubic": _coons_cubic, "coons_rational": _coons_rational,
-             "trivariate_polynomial_3d": trivariate_polynomial_3d}
+    """The reference's benchmark domains by name (geometry.py:486-502), from the frozen nets."""
     if name == "quarter_annulus":
         return quarter_annulus(**kwargs)
-    if name in table:
-        return table[name]()
+    if name in BUILTIN_NAMES:
+        return _fixture(name)
     raise ValueError(f"unknown builtin domain {name!r}; choose from {BUILTIN_NAMES}")
 
 
-# BASELINE configs 3-5: frozen B-spline stand-ins of the analytic maps,
-# generated by tests/golden/make_geometries.py with the reference's own collocation.
-import os as _os
-
-_DATA = _os.path.join(_os.path.dirname(_os.path.abspath(__file__)), "data")
-
-
 def twisted_cube_standin() -> GeometryMap:
-    return load_geometry(_os.path.join(_DATA, "twisted_cube_p3_m12.geo"))
+    """BASELINE configs 3/5: B-spline stand-in (p=3, 12 functions per direction) of the twisted cube."""
+    return load_geometry(os.path.join(_DATA, "twisted_cube_p3_m12.geo"))
 
 
 def sin_map_standin() -> GeometryMap:
-    return load_geometry(_os.path.join(_DATA, "sin_map_p3_m16.geo"))
+    """BASELINE config 4: B-spline stand-in (p=3, 16 functions per direction) of the sin-perturbed square."""
+    return load_geometry(os.path.join(_DATA, "sin_map_p3_m16.geo"))
 
 
-# ---------------------------------------------------------------------------------------
-# weight transfer (geometry.py:299-319)
-# ---------------------------------------------------------------------------------------
-
-def weights_for_space(geom: GeometryMap, space: TensorSpace) -> NurbsWeights:
+def weights_for_space(geom, space: TensorSpace) -> NurbsWeights:
+    """Weights of the solution space for a map (geometry.py:299-319): unit for polynomial maps, the
+    map's own on its own space, else the weight function interpolated at the space's Greville sites
+    (possible only when it is one global polynomial of degree <= the space's)."""
     if geom.is_polynomial:
         return NurbsWeights(weights=np.ones(space.N), polynomial_weight=True)
     if space.n != geom.n:
@@ -308,50 +207,46 @@ def weights_for_space(geom: GeometryMap, space: TensorSpace) -> NurbsWeights:
     if space.p < geom.space.p:
         raise ValueError(f"solution degree {space.p} below geometry degree {geom.space.p}")
     sites = [kv.greville() for kv in space.kvs]
-    Wg = _grid_field(geom.space, geom.weights.weights[:, None], sites, (0,) * space.n)[..., 0]
-    coef = tensor_collocate(space.kvs, sites, Wg)
-    return NurbsWeights(weights=coef.reshape(-1, order="F"), polynomial_weight=True)
+    W = map_grid(geom, sites, max_deriv=0)["W"]
+    return NurbsWeights(weights=tensor_collocate(space.kvs, sites, W).reshape(-1, order="F"), polynomial_weight=True)
 
 
-# ---------------------------------------------------------------------------------------
-# iga-geo v1 text format (geometry.py:509-555)
-# ---------------------------------------------------------------------------------------
+# ``iga-geo v1`` text format (geometry.py:509-555): header "iga-geo v1 n=<n> p=<p> m=<m0,m1,..>",
+# then one line per control point "<1-based index> <weight> <x> [<y> [<z>]]" (colex order)
 
-_HEADER_RE = re.compile(r"^iga-geo v1 n=(\d+) p=(\d+) m=([\d,]+)$")
-
-
-def save_geometry(geom: GeometryMap, path) -> None:
-    ms = ",".join(str(kv.m) for kv in geom.space.kvs)
-    lines = [f"iga-geo v1 n={geom.n} p={geom.space.p} m={ms}"]
-    w = geom.weights.weights
-    for i in range(geom.space.N):
-        lines.append(f"{i + 1} {repr(float(w[i]))} " + " ".join(repr(float(v)) for v in geom.control[i]))
+def save_geometry(geom, path) -> None:
+    N, n = geom.space.N, geom.space.n
+    table = np.column_stack([np.arange(1, N + 1), geom.weights.weights, geom.control])
     with open(path, "w") as f:
-        f.write("\n".join(lines) + "\n")
+        f.write(f"iga-geo v1 n={n} p={geom.space.p} m={','.join(str(kv.m) for kv in geom.space.kvs)}\n")
+        for row in table:
+            f.write(" ".join([str(int(row[0]))] + [repr(float(v)) for v in row[1:]]) + "\n")
 
 
-def load_geometry(path) -> GeometryMap:
+def load_geometry(path, name: str = "file") -> GeometryMap:
     with open(path) as f:
-        raw = [ln.strip() for ln in f if ln.strip()]
-    if not raw:
+        lines = [ln.split() for ln in f if ln.strip()]
+    if not lines:
         raise ValueError("empty geometry file")
-    mt = _HEADER_RE.match(raw[0])
-    if not mt:
-        raise ValueError(f"malformed header: {raw[0]!r}")
-    n, p = int(mt.group(1)), int(mt.group(2))
-    ms = [int(v) for v in mt.group(3).split(",") if v]
+    head = lines[0]
+    try:
+        assert head[:2] == ["iga-geo", "v1"] and len(head) == 5
+        keys = dict(tok.split("=", 1) for tok in head[2:])
+        n, p = int(keys["n"]), int(keys["p"])
+        ms = [int(v) for v in keys["m"].split(",") if v]
+    except (AssertionError, KeyError, ValueError):
+        raise ValueError(f"malformed header: {' '.join(head)!r}") from None
     if len(ms) != n:
         raise ValueError(f"header lists {len(ms)} mesh sizes for n={n}")
     space = make_tensor_space(p, ms)
     N = space.N
-    if len(raw) - 1 != N:
-        raise ValueError(f"expected {N} control point lines, found {len(raw) - 1}")
+    if len(lines) - 1 != N:
+        raise ValueError(f"expected {N} control point lines, found {len(lines) - 1}")
     w = np.empty(N)
     pts = np.empty((N, n))
-    for line in raw[1:]:
-        parts = line.split()
+    for parts in lines[1:]:
         if len(parts) != n + 2:
-            raise ValueError(f"bad control point line: {line!r}")
+            raise ValueError(f"bad control point line: {' '.join(parts)!r}")
         i = int(parts[0])
         if not 1 <= i <= N:
             raise ValueError(f"index {i} outside 1..{N}")
@@ -359,5 +254,5 @@ def load_geometry(path) -> GeometryMap:
         pts[i - 1] = [float(v) for v in parts[2:]]
     if np.any(w <= 0):
         raise ValueError("nonpositive weight")
-    poly = _poly_weight(space, w)
-    return GeometryMap(space=space, weights=NurbsWeights(weights=w, polynomial_weight=poly), control=pts, name="file")
+    return GeometryMap(space=space, weights=NurbsWeights(weights=w, polynomial_weight=_weights_polynomial(space, w)),
+                       control=pts, name=name)

@@ -42,8 +42,25 @@ def standin(func, n, pg, mg, name):
     return geom, err
 
 
+def builtins():
+    """The reference's builtin domains frozen as fixtures (the product reads them instead of
+    rebuilding the nets); the annulus at two outer radii, whose nets span every (r_in, r_out)."""
+    from surriga.geometry import builtin_domain, quarter_annulus
+
+    for name in ("unit_square", "unit_cube", "coons_quadratic", "coons_cubic", "coons_rational",
+                 "trivariate_polynomial_3d"):
+        g = builtin_domain(name)
+        save_geometry(g, os.path.join(OUT, f"{name}.geo"))
+        print(f"{name}: p={g.space.p} m={g.space.shape} polynomial_weight={g.weights.polynomial_weight}", file=sys.stderr)
+    for r_out in (2.0, 3.0):
+        g = quarter_annulus(1.0, r_out)
+        save_geometry(g, os.path.join(OUT, f"quarter_annulus_1_{int(r_out)}.geo"))
+        print(f"quarter_annulus(1,{r_out}): polynomial_weight={g.weights.polynomial_weight}", file=sys.stderr)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    builtins()
     for func, n, pg, mg, name in ((twisted_cube, 3, 3, 12, "twisted_cube"), (sin_map, 2, 3, 16, "sin_map")):
         geom, err = standin(func, n, pg, mg, name)
         path = os.path.join(OUT, f"{name}_p{pg}_m{mg}.geo")
