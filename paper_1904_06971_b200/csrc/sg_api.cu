@@ -811,7 +811,7 @@ int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>
         mp.D = dp.D;
         mp.Dys = dp.Dys;
         mp.tma = getenv("SG_NO_TMA") ? 0 : 1;
-        if (dp.n == 3 || (dp.n == 2 && dp.p == 3)) {
+        if (dp.n >= 2) {
             const TileChoice tc = mma_tile(dp.n, dp.p, dp.pr.form, dp.rational);
             const MmaGeom M = mma_geom(dp.n, dp.p, dp.pr.form, dp.rational, tc.T0, tc.T1);
             int rc2 = encode_dmap(&mp.dmap, dp.D, dp.Dys, mp.Gp, M.U, M.DY, M.XWp);
@@ -831,9 +831,43 @@ int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>
         }
         mp.dmma = c.dmma;
         int64_t nb = pl.ntiles;
-        if (tiles) {
+        mp.run = 1;
+        if (dp.n == 2) {
+            // runs of tiles along y (column-major list): one CTA per run, ~8 waves of runs over the SMs
+            std::vector<int> col;
+            if (tiles) col = *tiles;
+            else {
+                col.resize(pl.ntiles);
+                for (int64_t t = 0; t < pl.ntiles; ++t) col[t] = (int)t;
+            }
+            const int tg0 = pl.tgrid[0];
+            if (tiles) {
+                // bucket by x column, ascending tile order inside a column (counting sort)
+                std::vector<int> start(tg0 + 1, 0);
+                for (int t : col) start[t % tg0 + 1]++;
+                for (int c2 = 0; c2 < tg0; ++c2) start[c2 + 1] += start[c2];
+                std::vector<int> out(col.size());
+                for (int t : col) out[start[t % tg0]++] = t;
+                col.swap(out);
+            } else {
+                const int tg1 = (int)(pl.ntiles / tg0);
+                for (int c0 = 0, k = 0; c0 < tg0; ++c0)
+                    for (int c1 = 0; c1 < tg1; ++c1) col[k++] = c0 + tg0 * c1;
+            }
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.dev);
+            const int64_t want = 8LL * sms;
+            mp.run = (int)std::max<int64_t>(1, ((int64_t)col.size() + want - 1) / want);
+            if (const char* e = getenv("SG_RUN2D")) mp.run = std::max(1, atoi(e));
+            mp.ntiles = (int)col.size();
+            mp.tiles = (const int*)c.upload(col.data(), sizeof(int) * col.size());
+            nb = ((int64_t)col.size() + mp.run - 1) / mp.run;
+        } else if (tiles) {
             mp.tiles = (const int*)c.upload(tiles->data(), sizeof(int) * tiles->size());
             nb = (int64_t)tiles->size();
+            mp.ntiles = (int)nb;
+        } else {
+            mp.ntiles = (int)nb;
         }
         cudaFuncSetAttribute(pl.kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptinMax);
         void* args[] = {&mp};

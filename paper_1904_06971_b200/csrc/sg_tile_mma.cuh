@@ -251,9 +251,13 @@ __host__ __device__ constexpr TileChoice mma_tile(int ndim, int P, int form, boo
         // 2D bi-Laplacian, p = 3: a deeper y extent (2 x 5 instead of 3 x 3) halves the x-contraction
         // work per row (config 4: 7.04 -> 6.12 ms)
         if (form == 2 && P == 3 && mma_geom(2, P, form, rat, 2, 5).total <= cap) return {2, 5};
+        // 3 x 3 tiles with an odd Gauss count (p = 2, 4) raise an illegal-instruction fault under TMA
+        // (found by the full 2D matrix, tools/tma2d_matrix.py: p=2 rational bi-Laplacian and p=4
+        // Poisson fault, every other degree / form / map and the same boxes on other tiles pass; plain
+        // loads of the same tiles are correct); those instantiations take the next smaller tile
         const int cand[] = {12, 10, 8, 6, 4, 3, 2, 1};
         for (int t : cand)
-            if (mma_geom(2, P, form, rat, t, t).total <= cap) return {t, t};
+            if (!(t == 3 && (P % 2) == 0) && mma_geom(2, P, form, rat, t, t).total <= cap) return {t, t};
         return {1, 1};
     }
 #if defined(SG_FORCE_FORM) && defined(SG_FORCE_T0) && defined(SG_FORCE_T1)
@@ -422,6 +426,8 @@ struct MmaParams {
     int Dys;
     unsigned long long* dmma;    // executed DMMA instructions (per warp, summed per launch), or nullptr
     int z0;                      // z origin of the tile grid (rows)
+    int run;                     // 2D: tiles per CTA (consecutive entries of the tile list)
+    int ntiles;                  // entries of the tile list (or tiles of the grid)
 };
 
 template <int NDIM, int P, int FORM, bool RAT>
@@ -442,12 +448,21 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
     unsigned long long ndmma = 0;  // DMMA instructions this warp issues (reported per launch)
     const int lr = lane >> 2, lk = lane & 3;
 
-    const int tile = prm.tiles ? prm.tiles[blockIdx.x] : (int)blockIdx.x;
-    const int tc0 = tile % prm.tgrid[0], tc1 = (tile / prm.tgrid[0]) % prm.tgrid[1], tc2 = tile / (prm.tgrid[0] * prm.tgrid[1]);
-    const int b0 = tc0 * T0, b1 = tc1 * T1, b2 = prm.z0 + tc2 * prm.T2;
+    // 2D: a CTA assembles a run of prm.run consecutive entries of the tile list (ordered column-major by
+    // the host, so a run stays in one x column): the per-CTA set-up is paid once per run, the x-window
+    // fragments once per column, and the next tile's D window streams in during phase 2
+    const int run = (NDIM == 2 && prm.run > 1) ? prm.run : 1;
+    const int t_first = (int)blockIdx.x * run;
+    const int t_end = NDIM == 2 ? min(t_first + run, prm.ntiles) : t_first + 1;
+    auto tile_at = [&](int t) { return prm.tiles ? prm.tiles[t] : t; };
+    int tile = tile_at(t_first);
+    int tc0 = tile % prm.tgrid[0], tc1 = (tile / prm.tgrid[0]) % prm.tgrid[1];
+    const int tc2 = tile / (prm.tgrid[0] * prm.tgrid[1]);
+    int b0 = tc0 * T0, b1 = tc1 * T1;
+    const int b2 = prm.z0 + tc2 * prm.T2;
     // fixed windows: element e of direction d sits at local element (e - (b_d - P)); elements outside
     // the mesh have zero basis tables and zero D, so every index below is compile-time + lane
-    const int ew0 = b0 - P, ew1 = b1 - P;
+    int ew0 = b0 - P, ew1 = b1 - P;
 
     double* B0s = smem + M.o_B0;
     double* B1s = smem + M.o_B1;
@@ -477,18 +492,26 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
     // ---- zero the staging buffers once (padding columns / rows are read as exact zeros)
     for (long it = tid; it < M.total - M.o_T1; it += blockDim.x) T1s[it] = 0.0;
     // ---- window basis tables (zero outside the mesh)
-    for (int it = tid; it < XW * NB; it += blockDim.x) {
-        const int e = ew0 + it / (G * NB);
-        B0s[it] = (e >= 0 && e < prm.S[0]) ? prm.B[0][((long long)ew0 * G) * NB + it] : 0.0;
-    }
-    if constexpr (NDIM >= 2)
-        for (int it = tid; it < YW * NB; it += blockDim.x) {
-            const int e = ew1 + it / (G * NB);
-            B1s[it] = (e >= 0 && e < prm.S[1]) ? prm.B[1][((long long)ew1 * G) * NB + it] : 0.0;
+    auto load_x = [&]() {
+        for (int it = tid; it < XW * NB; it += blockDim.x) {
+            const int e = ew0 + it / (G * NB);
+            B0s[it] = (e >= 0 && e < prm.S[0]) ? prm.B[0][((long long)ew0 * G) * NB + it] : 0.0;
         }
+    };
+    auto load_y = [&]() {
+        if constexpr (NDIM >= 2) {
+            for (int it = tid; it < YW * NB; it += blockDim.x) {
+                const int e = ew1 + it / (G * NB);
+                B1s[it] = (e >= 0 && e < prm.S[1]) ? prm.B[1][((long long)ew1 * G) * NB + it] : 0.0;
+            }
+        }
+    };
+    load_x();
+    load_y();
     __syncthreads();
     // ---- tile-constant fragments
     // A1f[((i0l*NU1 + unit)*KS + kk)*MT + a][lane] = Q0(i0, i0+d0, x): d0 = a*8 + lr - P, x = kk*4 + lk in supp(i0)
+    auto frag_x = [&]() {
     static_for<0, M.NG1>([&](auto GI) {
         constexpr int Gc = decltype(GI)::value;
         static_for<0, TTS::T.g1n[Gc]>([&](auto UI) {
@@ -519,6 +542,8 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
             }
         });
     });
+    };
+    auto frag_y = [&]() {
     if constexpr (NDIM >= 2) {
         // B2f[((i1l*NK1 + slot)*KS + kk)*MT + c][lane] = Q1(i1, i1+d1, y): d1 = c*8 + lr - P
         for (int it = warp; it < T1 * NK1; it += NW) {
@@ -544,6 +569,9 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
             }
         }
     }
+    };
+    frag_x();
+    frag_y();
     if constexpr (NDIM == 3) {
         // per combo: {offset inside a row's j2 block (or -1), cnt0*cnt1, i0 + m0 i1, j0 + m0 j1}
         for (int c = tid; c < M.NCOMBO; c += blockDim.x) {
@@ -611,9 +639,9 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
             "l"(reinterpret_cast<uint64_t>(&prm.dmap)), "r"(ew1 * G), "r"(ew0 * G), "r"(0), "r"(z), "r"(bar)
             : "memory");
     };
-    // TMA D windows: 3D (double-buffered pencil) and 2D p=3 (validated configs); plain loads otherwise.
-    // (2D p=2 bi-Laplacian boxes raised an illegal-instruction fault under TMA -- open item)
-    constexpr bool kTma = NDIM == 3 || (NDIM == 2 && P == 3);
+    // TMA D windows: 3D (double-buffered pencil of planes), 2D (one window per tile, the next tile's
+    // streamed during phase 2); SG_NO_TMA=1 selects plain loads (debug)
+    constexpr bool kTma = NDIM >= 2;
     const bool use_tma = kTma && prm.tma;
     if (use_tma) {
         if (tid == 0) {
@@ -624,6 +652,19 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
         __syncthreads();
         if (tid == 0) issue_plane(0);
     }
+    // 2D: the D window of the run's k-th tile (TMA box at the tile's window origin; barrier k & 1)
+    auto issue_tile = [&](int k, int t) {
+        const int tt = tile_at(t);
+        const int x0 = (tt % prm.tgrid[0]) * T0 - P, y0 = ((tt / prm.tgrid[0]) % prm.tgrid[1]) * T1 - P;
+        const uint32_t bar = bar0 + 8u * (uint32_t)(k & 1);
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(Dbuf(0));
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(DBYTES) : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(dst),
+            "l"(reinterpret_cast<uint64_t>(&prm.dmap)), "r"(y0 * G), "r"(x0 * G), "r"(0), "r"(0), "r"(bar)
+            : "memory");
+    };
     // make the D window of plane j resident in Dbuf[j & 1] (plain path: all threads load, then a barrier)
     auto get_plane = [&](int j) {
         double* Ds = Dbuf(j & 1);
@@ -859,12 +900,54 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
         }
     };
 
-    if constexpr (NDIM <= 2) {
+    if constexpr (NDIM == 1) {
         const double* Ds = get_plane(0);
         phase1(Ds, T1s);
-        if constexpr (NDIM == 2) {
+    } else if constexpr (NDIM == 2) {
+        int colx = tc0;
+        for (int t = t_first; t < t_end; ++t) {
+            const int k = t - t_first;
+            if (k > 0) {
+                // next tile of the run: new y window; new x window only when the column changes
+                tile = tile_at(t);
+                tc0 = tile % prm.tgrid[0];
+                tc1 = (tile / prm.tgrid[0]) % prm.tgrid[1];
+                b0 = tc0 * T0;
+                b1 = tc1 * T1;
+                ew0 = b0 - P;
+                ew1 = b1 - P;
+                const bool newx = tc0 != colx;
+                colx = tc0;
+                if (newx) load_x();
+                load_y();
+                __syncthreads();
+                if (newx) frag_x();
+                frag_y();
+                __syncthreads();
+            }
+            const double* Ds;
+            if (use_tma) {
+                // the tile's box was issued by thread 0 (first tile: above; others: after the previous phase 1)
+                const uint32_t bar = bar0 + 8u * (uint32_t)(k & 1);
+                const uint32_t par = (uint32_t)((k >> 1) & 1);
+                uint32_t done = 0;
+                while (!done) {
+                    asm volatile(
+                        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                        : "=r"(done)
+                        : "r"(bar), "r"(par)
+                        : "memory");
+                }
+                Ds = Dbuf(0);
+            } else {
+                Ds = get_plane(0);
+            }
+            phase1(Ds, T1s);
             __syncthreads();
+            // the D buffer is free: stream the next tile's window in while phase 2 runs
+            if (use_tma && tid == 0 && t + 1 < t_end) issue_tile(k + 1, t + 1);
             phase2(T1s, nullptr);
+            __syncthreads();
         }
     } else {
         // ---------------- 3D: one barrier interval per Gauss plane j (ascending z):

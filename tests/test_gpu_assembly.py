@@ -164,3 +164,28 @@ def test_gpu_unsupported_degree_or_gauss_is_not_a_value_error(p, gauss):
         pkg.assemble(pkg.FormKind.POISSON, disc)
     with pytest.raises(NativeError):
         pkg.assemble(pkg.FormKind.POISSON, disc)
+
+
+SWEEP2D = [(p, form, geom) for p in (1, 2, 3, 4) for form in ("poisson", "mass", "biharmonic")
+           for geom in ("coons_quadratic", "coons_rational")
+           if not (form == "biharmonic" and p < 2) and not (geom == "coons_rational" and p < 2)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p,form,geom", SWEEP2D)
+@pytest.mark.parametrize("run", [None, "3"])
+def test_gpu_2d_tiles_every_degree_form_and_map(p, form, geom, run, monkeypatch):
+    # the 2D tensor-core kernel (TMA D windows, runs of tiles per CTA) on every degree, form and
+    # polynomial / rational map against the oracle; SG_RUN2D=3 forces several tiles per CTA
+    # (x-column reuse, the next window streamed during phase 2) on this small mesh
+    import paper_1904_06971_b200 as pkg
+
+    if run:
+        monkeypatch.setenv("SG_RUN2D", run)
+    disc = pkg.make_discretization(pkg.builtin_domain(geom), p, (23, 19))
+    A = pkg.assemble(pkg.FormKind(form), disc)
+    ip, ix, d, _, _ = O.assemble(O.problem_from_disc(form, disc))
+    m = A.mat
+    assert np.array_equal(m.indptr, ip) and np.array_equal(m.indices, ix)
+    assert O.row_scaled_error(ip, ix, d, m.indptr, m.indices, m.data) <= 1e-12
+    assert pkg.is_bitwise_symmetric(A)
