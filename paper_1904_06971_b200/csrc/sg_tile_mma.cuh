@@ -446,6 +446,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     unsigned long long ndmma = 0;  // DMMA instructions this warp issues (reported per launch)
+    unsigned nzero = 0;            // exact zeros this thread wrote to the CSR (3D; summed per launch)
     const int lr = lane >> 2, lk = lane & 3;
 
     // 2D: a CTA assembles a run of prm.run consecutive entries of the tile list (ordered column-major by
@@ -585,7 +586,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
                 c01 = cnt0 * cnt1;
             }
             cmb[4 * c + 0] = off;
-            cmb[4 * c + 1] = c01;
+            cmb[4 * c + 1] = c01 | ((c / (W * W)) << 16);  // cnt0*cnt1 | tile row of the combo << 16
             cmb[4 * c + 2] = i0 + prm.m[0] * i1;
             cmb[4 * c + 3] = j0 + prm.m[0] * j1;
         }
@@ -1021,34 +1022,51 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
                     // accumulate the layer into O[(i2 mod G)*G + (j2 mod G)][combo] (the entries live at this
                     // layer have i2, j2 in [e2, e2+P]: distinct residues); the first layer of an entry
                     // overwrites, its last layer writes the CSR (once, no read-modify-write in HBM)
-                    const int64_t* rb = reinterpret_cast<const int64_t*>(smem + M.o_rb);
+                    // Per (c, h) the lane's z offset d2 is fixed, so everything that depends only on it and
+                    // on the item (validity, first / last layer of the entry, O slot, CSR column offset) is
+                    // hoisted out of the m-tile loop: first layer iff e2 == 0 or max(r2, rj2) == P, last
+                    // iff e2 == S2-1 or min(r2, rj2) == 0 (the entry's layers are [max(i2,j2)-P, min(i2,j2)]).
+                    const int64_t* rb = reinterpret_cast<const int64_t*>(smem + M.o_rb) + (i2 - b2);
                     const int i2m = i2 % G;
+                    const int jlo2 = max(0, i2 - P);
+                    bool ok[MT][2], fst[MT][2], lst[MT][2];
+                    int soff[MT][2], dj[MT][2], jcol[MT][2];
+#pragma unroll
+                    for (int c = 0; c < MT; ++c)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int d2 = c * 8 + 2 * lk + h - P;
+                            const int rj2 = r2 + d2;
+                            ok[c][h] = d2 <= P && rj2 >= 0 && rj2 <= P;
+                            fst[c][h] = e2 == 0 || max(r2, rj2) == P;
+                            lst[c][h] = e2 == prm.S[2] - 1 || min(r2, rj2) == 0;
+                            soff[c][h] = (i2m * G + (i2m + d2 + G) % G) * M.NCP;
+                            dj[c][h] = i2 + d2 - jlo2;
+                            jcol[c][h] = m01 * (i2 + d2);
+                        }
 #pragma unroll
                     for (int mm = 0; mm < CH; ++mm) {
                         const int combo = (ch * CH + mm) * 8 + lr;
                         if (combo >= M.NCOMBO) continue;
                         const int4 cb = reinterpret_cast<const int4*>(cmb)[combo];
-                        const int64_t rowb = rb[(combo / (W * W)) * kMmaT2 + (i2 - b2)];
+                        const int64_t rowb = rb[(cb.y >> 16) * kMmaT2];
+                        const int cnt01 = cb.y & 0xffff;
+                        double* Oc = Os + combo;
 #pragma unroll
                         for (int c = 0; c < MT; ++c)
 #pragma unroll
                             for (int h = 0; h < 2; ++h) {
-                                const int d2 = c * 8 + 2 * lk + h - P;
-                                const int rj2 = r2 + d2;
-                                if (d2 > P || rj2 < 0 || rj2 > P) continue;
-                                const int j2 = e2 + rj2;
-                                const int first = max(0, max(i2, j2) - P);
-                                const int last = min(min(i2, j2), prm.S[2] - 1);
-                                double* slot = Os + (i2m * G + j2 % G) * M.NCP + combo;
+                                if (!ok[c][h]) continue;
+                                double* slot = Oc + soff[c][h];
                                 double v = accS[mm][c][h];
-                                if (e2 != first) v = *slot + v;
-                                if (e2 != last) {
+                                if (!fst[c][h]) v = *slot + v;
+                                if (!lst[c][h]) {
                                     *slot = v;
                                 } else if (cb.x >= 0 && rowb >= 0) {
-                                    const int64_t pos = rowb + cb.x + (int64_t)cb.y * (j2 - max(0, i2 - P));
-                                    const int col = cb.w + m01 * j2;
+                                    const int64_t pos = rowb + cb.x + (int64_t)cnt01 * dj[c][h];
+                                    const int col = cb.w + jcol[c][h];
                                     if constexpr (RAT) v = v * (prm.sol_w[(int64_t)cb.z + (int64_t)m01 * i2] * prm.sol_w[col]);
-                                    if (prm.zeros && v == 0.0) atomicAdd(prm.zeros, 1ull);
+                                    nzero += v == 0.0 ? 1u : 0u;
                                     prm.data[pos] = v;
                                     prm.indices[pos] = col;
                                 }
@@ -1087,6 +1105,10 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
         }
     }
     if (prm.dmma && lane == 0 && ndmma) atomicAdd(prm.dmma, ndmma);  // all lanes of a warp run the same items
+    if constexpr (NDIM == 3) {
+        for (int o = 16; o > 0; o >>= 1) nzero += __shfl_xor_sync(0xffffffffu, nzero, o);
+        if (prm.zeros && lane == 0 && nzero) atomicAdd(prm.zeros, (unsigned long long)nzero);
+    }
 }
 
 }  // namespace sg
