@@ -825,6 +825,7 @@ int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>
         mp.data = d_data;
         mp.zeros = d_zeros;
         mp.z0 = pl.z0;
+        mp.dbg = env_int("SG_K4_DBG", 0);
         if (!c.dmma) {
             c.dmma = (unsigned long long*)c.alloc(sizeof(unsigned long long), true);
             if (c.dmma) cudaMemsetAsync(c.dmma, 0, sizeof(unsigned long long), c.stream);

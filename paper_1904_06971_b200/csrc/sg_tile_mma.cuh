@@ -122,7 +122,10 @@ __host__ __device__ constexpr int pad8_4(int v) {  // smallest w >= v with w % 8
 }
 
 #ifndef SG_CH_MASS
-#define SG_CH_MASS 4
+#define SG_CH_MASS 1
+#endif
+#ifndef SG_CH_POIS
+#define SG_CH_POIS 1
 #endif
 #ifndef SG_P12_EPI
 #define SG_P12_EPI 0
@@ -162,6 +165,30 @@ __host__ __device__ constexpr int mma_minb(int ndim, int P, int form, bool rat) 
     return ndim == 3 && form == 1 ? SG_MASS_MINB : 1;
 }
 
+// ---- warp specialisation of the 3D pipeline (Poisson / Stokes velocity): warps [0, NW - NB) run
+// phases 1-2 plane by plane (group A), warps [NW - NB, NW) run phase 3 layer by layer (group B); the
+// groups hand T2 planes over through mbarriers instead of one CTA barrier per plane, so the phase-3
+// burst of every G-th plane no longer stalls phases 1-2 (and B's barrier waits overlap A's work)
+#ifndef SG_SPEC_NB
+#define SG_SPEC_NB 4
+#endif
+__host__ __device__ constexpr bool mma_spec(int ndim, int form) {
+#ifdef SG_NO_SPEC
+    return false;
+#else
+    return ndim == 3 && form == 0;
+#endif
+}
+__host__ __device__ constexpr int mma_spec_nb(int ndim, int form) { return mma_spec(ndim, form) ? SG_SPEC_NB : 0; }
+// T2 ring: G + 1 planes (phase 3 of a layer while phase 2 writes the next plane); + 1 under
+// specialisation (group A may run two planes ahead of the layer group B is consuming)
+// phase 3 contracts a row plane i2 over the whole z support of its rows (layers i2-P .. i2, (P+1) G
+// planes): the ring holds those planes plus the one phase 2 writes meanwhile; under specialisation one
+// more layer, so group A can run a layer ahead of group B
+__host__ __device__ constexpr int mma_ns(int ndim, int P, int form) {
+    return (P + 1) * (P + 1) + 1 + (mma_spec(ndim, form) ? P + 1 : 0);
+}
+
 // ---- compile-time tile geometry (shared by host planning and the kernel)
 #ifndef SG_MMA_T2
 #define SG_MMA_T2 72
@@ -183,7 +210,7 @@ __host__ __device__ constexpr MmaGeom mma_geom(int ndim, int P, int form, bool r
     m.W = 2 * P + 1;
     m.MT = (m.W + 7) / 8;
     m.KS = ((P + 1) * m.G + 3) / 4;
-    m.KS3 = (m.G + 3) / 4;
+    m.KS3 = ((P + 1) * m.G + 3) / 4;  // phase 3: the whole z support of a row (P+1 layers)
     m.XW = (T0 + P) * m.G;
     m.XWp = (m.XW + 3) & ~3;  // TMA: box bytes DY*XWp*8 stay a multiple of 128
     m.YW = ndim >= 2 ? (m.T1 + P) * m.G : 1;
@@ -199,7 +226,7 @@ __host__ __device__ constexpr MmaGeom mma_geom(int ndim, int P, int form, bool r
     m.TY = pad8_4(m.NTY * 8 > m.YW + 4 ? m.NTY * 8 : m.YW + 4);
     m.NCOMBO = T0 * m.T1 * m.W * m.W;
     m.NMT = (m.NCOMBO + 7) / 8;
-    m.CH = form == 1 ? SG_CH_MASS : 4;  // mass: finer phase-3 items (its epilogue, not DMMA, dominates)
+    m.CH = form == 1 ? SG_CH_MASS : SG_CH_POIS;  // m-tiles per phase-3 item
     m.NCH = (m.NMT + m.CH - 1) / m.CH;
     m.TC = pad8_4(m.NCH * m.CH * 8);
     m.NCP = pad8_4(m.NCH * m.CH * 8);
@@ -216,7 +243,7 @@ __host__ __device__ constexpr MmaGeom mma_geom(int ndim, int P, int form, bool r
     m.o_B2 = o;
     m.o_A1 = o; o += (long)T0 * m.NU1 * m.KS * m.MT * 32;                      // phase-1 A fragments
     m.o_B2f = o; o += ndim >= 2 ? (long)m.T1 * m.NK1 * m.KS * m.MT * 32 : 0;     // phase-2 B fragments
-    m.o_B3f = o; o += ndim == 3 ? 2L * (P + 1) * m.NK2 * m.KS3 * m.MT * 32 : 0;  // phase-3 B fragments (2 layers)
+    m.o_B3f = o; o += ndim == 3 ? 2L * m.NK2 * m.KS3 * m.MT * 32 : 0;         // phase-3 B fragments (2 row planes)
     o = (o + 1) & ~1L;
     m.o_cmb = o; o += ndim == 3 ? (long)m.NCOMBO * 2 + 2 : 0;                  // per-combo {off, cnt01, row01, col01}
     {
@@ -228,14 +255,14 @@ __host__ __device__ constexpr MmaGeom mma_geom(int ndim, int P, int form, bool r
     }
     m.o_rb = o; o += ndim == 3 ? (long)T0 * m.T1 * kMmaT2 + 1 : 0;                // CSR start of every tile row (int64, -1: not owned)
     m.o_tab = o; o += (m.NTAB + 1) / 2;                                        // item schedule + unit tables (int)
-    m.o_bar = o; o += 2;                                                       // two mbarriers (TMA)
+    m.o_bar = o; o += 4;                                                       // 2 TMA mbarriers + 2 hand-over counters
     o = align16(o);
     m.o_D = o; o += align16((long)m.U * m.XWp * m.DY);                          // D window, double buffered (TMA)
     m.o_D2 = ndim == 3 ? o : m.o_D;                                           // 2D/1D: one plane per tile
     o += ndim == 3 ? align16((long)m.U * m.XWp * m.DY) : 0;
     m.o_T1 = o; o += ndim >= 2 ? (ndim == 3 ? 2L : 1L) * m.NG1 * T0 * m.MT * 8 * m.TY : 0;  // 3D: 2 planes
-    m.o_T2 = o; o += ndim == 3 ? (long)(m.G + 1) * m.NG2 * m.TC : 0;            // ring of G+1 planes
-    m.o_O = o; o += ndim == 3 ? (long)(P + 1) * (P + 1) * m.NCP : 0;            // live (i2, j2) partial sums
+    m.o_T2 = o; o += ndim == 3 ? (long)mma_ns(ndim, P, form) * m.NG2 * m.TC : 0;  // ring of T2 planes
+    m.o_O = o;                                                                  // (no live partial sums: one z chain per entry)
     m.total = o;
     return m;
 }
@@ -308,21 +335,23 @@ __host__ __device__ constexpr MmaTab mma_tab(int ndim, int P, int form, bool rat
     MmaTab S{};
     const int n1 = M.NG1 * M.T0 * M.NC1;
     const int n2 = ndim >= 2 ? T.NG2 * M.T1 * M.T0 : 0;
-    const int n3 = ndim == 3 ? (P + 1) * M.NCH : 0;
+    const int n3 = ndim == 3 ? M.NCH : 0;  // phase-3 items of a row plane: chunks of CH m-tiles
     int w1[512] = {}, w2[512] = {}, w3[512] = {};
     long load[64] = {};
     int cost[1024] = {};
     int kind[1024] = {}, idx[1024] = {};
     bool done[1024] = {};
     int n = 0;
+    const int NBs = mma_spec_nb(ndim, form);
+    int wlo = 0, whi = NW;  // warps the next lpt() pass may use
     auto lpt = [&]() {
         for (int it = 0; it < n; ++it) {
             int best = -1;
             for (int k = 0; k < n; ++k)
                 if (!done[k] && (best < 0 || cost[k] > cost[best])) best = k;
             done[best] = true;
-            int w = 0;
-            for (int v = 1; v < NW; ++v)
+            int w = wlo;
+            for (int v = wlo + 1; v < whi; ++v)
                 if (load[v] < load[w]) w = v;
             load[w] += cost[best];
             if (kind[best] == 1) w1[idx[best]] = w;
@@ -343,7 +372,12 @@ __host__ __device__ constexpr MmaTab mma_tab(int ndim, int P, int form, bool rat
         cost[n] = g2_blocks(T, k / (M.T1 * M.T0)) * M.KS * M.MT * M.MT + 2 + SG_P12_EPI * M.MT * M.MT;
         kind[n] = 2; idx[n] = k; done[n] = false; ++n;
     }
+    if (NBs) whi = NW - NBs;
     lpt();
+    if (NBs) {
+        wlo = NW - NBs;
+        whi = NW;
+    }
     const int fb = T.NF + f_npairs(T);
     for (int k = 0; k < n3; ++k) {
         cost[n] = fb * M.KS3 * M.CH * M.MT + 2 + SG_P3_EPI * M.CH;  // + epilogue (live-sum update / CSR write)
@@ -427,6 +461,7 @@ struct MmaParams {
     unsigned long long* dmma;    // executed DMMA instructions (per warp, summed per launch), or nullptr
     int z0;                      // z origin of the tile grid (rows)
     int run;                     // 2D: tiles per CTA (consecutive entries of the tile list)
+    int dbg;                     // timing experiments only (SG_K4_DBG): 1 skip phase 3, 2 skip its epilogue
     int ntiles;                  // entries of the tile list (or tiles of the grid)
 };
 
@@ -685,7 +720,9 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
             const long long gx0 = (long long)ew0 * G, gy0 = (long long)ew1 * G;
             const long long z = (long long)elo2 * G + j;
             const long long G1 = NDIM >= 2 ? prm.Gp[1] : 1;
-            for (int it = tid; it < M.U * XWp * DY; it += blockDim.x) {
+            // (under warp specialisation only group A loads planes)
+            const int nld = mma_spec_nb(NDIM, FORM) > 0 ? (NW - mma_spec_nb(NDIM, FORM)) * 32 : (int)blockDim.x;
+            for (int it = tid; it < M.U * XWp * DY; it += nld) {
                 const int y = it % DY, r = it / DY;
                 const int u = r / XWp, x = r % XWp;
                 const long long gx = gx0 + x, gy = gy0 + y;
@@ -694,7 +731,11 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
                     v = prm.D[((z * M.U + u) * G0 + gx) * (long long)prm.Dys + gy];
                 Ds[r * DY + y] = v;
             }
-            __syncthreads();
+            if constexpr (mma_spec_nb(NDIM, FORM) > 0) {
+                asm volatile("bar.sync 1, %0;\n" ::"r"((NW - mma_spec_nb(NDIM, FORM)) * 32) : "memory");
+            } else {
+                __syncthreads();
+            }
         }
         return Ds;
     };
@@ -956,152 +997,198 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
         //   | phase 1(plane j) | phase 2(plane j-1) | phase-3 fragments of the layer starting at j
         // T1 is double buffered by plane parity, T2 is a ring of G+1 plane slots, the phase-3
         // fragments are double buffered by layer parity.
-        constexpr int NS = G + 1;
-        constexpr int B3SZ = (P + 1) * NK2 * KS3 * MT * 32;
+        constexpr int NS = mma_ns(NDIM, P, FORM);
+        constexpr int B3SZ = NK2 * KS3 * MT * 32;
         constexpr int CH = M.CH;
+        constexpr int KZ = (P + 1) * G;  // z points of a row's support
         const int m01 = prm.m[0] * prm.m[1];
-        double* Os = smem + M.o_O;
-        for (int j = 0; j <= nplanes + 1; ++j) {
-            const double* Ds = j < nplanes ? get_plane(j) : nullptr;
-            // ---- phase 3 (z) of layer L3: items (row offset r2, chunk of CH m-tiles) -> O
-            if (j >= G + 1 && (j - 1) % G == 0) {
-                const int L3 = (j - 1) / G - 1;
-                const int e2 = elo2 + L3;
-                const double* B3b = B3f + (L3 & 1) * B3SZ;
-                const int qe = tab[TAB::S.o_off3 + warp + 1];
-                for (int q = tab[TAB::S.o_off3 + warp]; q < qe; ++q) {
-                    const int k = tab[TAB::S.o_it3 + q];
-                    const int r2 = k % (P + 1), ch = k / (P + 1);
-                    const int i2 = e2 + r2;
-                    if (i2 < b2 || i2 >= b2 + prm.T2 || i2 >= prm.m[2]) continue;
-                    auto block = [&](int ga, int kd, double (&acc)[CH][MT][2]) {
-                        const double* bfp = B3b + ((r2 * NK2 + kd) * KS3) * MT * 32 + lane;
+        const int* zrng = reinterpret_cast<const int*>(smem + M.o_rb + T0 * T1 * kMmaT2);
+        const int zr0 = zrng[0], zr1 = zrng[1];
+        const int nlayers = nplanes / G;
+        // row planes elo2 .. elo2 + nsteps - 1; the rows above the last streamed layer (ehi2) have all
+        // their layers streamed by then and follow it
+        const int nsteps = nlayers + max(0, zr1 - ehi2);
+        // ---- phase 3 (z) of row plane i2 = elo2 + L: every entry is one DMMA chain over the z points of
+        // its row's support (layers i2-P .. i2 ascending; the column basis vanishes outside the shared
+        // layers, so those terms add exact zeros), written straight to the CSR.  Items: chunks of CH m-tiles.
+        auto phase3 = [&](const int L) {
+            if (prm.dbg & 1) return;
+            const int i2 = elo2 + L;
+            if (i2 < zr0 || i2 > zr1) return;
+            const double* B3b = B3f + (L & 1) * B3SZ;
+            // T2 slot of this lane's z point s = kk*4 + lk: plane (i2 - P + s/G - elo2)*G + s%G of the stream
+            int zslot[KS3];
 #pragma unroll
-                        for (int kk = 0; kk < KS3; ++kk) {
-                            double bfs[MT];
+            for (int kk = 0; kk < KS3; ++kk) {
+                const int sz = kk * 4 + lk < KZ ? kk * 4 + lk : 0;
+                const int rel = (i2 - P + sz / G - elo2) * G + sz % G;
+                zslot[kk] = ((rel % NS) + NS) % NS;  // planes before the stream: zero fragments, any slot
+            }
+            const int64_t* rb = reinterpret_cast<const int64_t*>(smem + M.o_rb) + (i2 - b2);
+            const int jlo2 = max(0, i2 - P);
+            const int qe = tab[TAB::S.o_off3 + warp + 1];
+            for (int q = tab[TAB::S.o_off3 + warp]; q < qe; ++q) {
+                const int ch = tab[TAB::S.o_it3 + q];
+                auto block = [&](int ga, int kd, double (&acc)[CH][MT][2]) {
+                    const double* bfp = B3b + (kd * KS3) * MT * 32 + lane;
+                    const double* t2b = T2s + ga * TC + ch * CH * 8 + lr;
 #pragma unroll
-                            for (int c = 0; c < MT; ++c) bfs[c] = bfp[(kk * MT + c) * 32];
-                            const int s = kk * 4 + lk;
-                            const int slot = (L3 * G + (s < G ? s : 0)) % NS;
-                            const double* t2 = T2s + (slot * M.NG2 + ga) * TC + ch * CH * 8 + lr;
+                    for (int kk = 0; kk < KS3; ++kk) {
+                        double bfs[MT];
 #pragma unroll
-                            for (int mm = 0; mm < CH; ++mm) {
-                                const double av = t2[mm * 8];
+                        for (int c = 0; c < MT; ++c) bfs[c] = bfp[(kk * MT + c) * 32];
+                        const double* t2 = t2b + (long)zslot[kk] * M.NG2 * TC;
 #pragma unroll
-                                for (int c = 0; c < MT; ++c) dmma(acc[mm][c][0], acc[mm][c][1], av, bfs[c]);
-                            }
-                        }
-                    };
-                    double accS[CH][MT][2];
+                        for (int mm = 0; mm < CH; ++mm) {
+                            const double av = t2[mm * 8];
 #pragma unroll
-                    for (int mm = 0; mm < CH; ++mm)
-#pragma unroll
-                        for (int c = 0; c < MT; ++c) accS[mm][c][0] = accS[mm][c][1] = 0.0;
-                    ndmma += (unsigned long long)(TTS::T.NF + f_npairs(TTS::T)) * KS3 * CH * MT;  // compile-time per item
-                    for (int u = 0; u < TTS::T.NF; ++u) {
-                        const int d = tab[TAB::S.o_u3 + u];
-                        const int ga = d & 255, kd = (d >> 16) & 15;
-                        if (!(d >> 24)) {
-                            block(ga, kd, accS);
-                        } else {
-                            double tA[CH][MT][2], tB[CH][MT][2];
-#pragma unroll
-                            for (int mm = 0; mm < CH; ++mm)
-#pragma unroll
-                                for (int c = 0; c < MT; ++c) tA[mm][c][0] = tA[mm][c][1] = tB[mm][c][0] = tB[mm][c][1] = 0.0;
-                            block(ga, kd, tA);
-                            block((d >> 8) & 255, (d >> 20) & 15, tB);
-#pragma unroll
-                            for (int mm = 0; mm < CH; ++mm)
-#pragma unroll
-                                for (int c = 0; c < MT; ++c)
-#pragma unroll
-                                    for (int h = 0; h < 2; ++h) accS[mm][c][h] = __dadd_rn(accS[mm][c][h], __dadd_rn(tA[mm][c][h], tB[mm][c][h]));
+                            for (int c = 0; c < MT; ++c) dmma(acc[mm][c][0], acc[mm][c][1], av, bfs[c]);
                         }
                     }
-                    // accumulate the layer into O[(i2 mod G)*G + (j2 mod G)][combo] (the entries live at this
-                    // layer have i2, j2 in [e2, e2+P]: distinct residues); the first layer of an entry
-                    // overwrites, its last layer writes the CSR (once, no read-modify-write in HBM)
-                    // Per (c, h) the lane's z offset d2 is fixed, so everything that depends only on it and
-                    // on the item (validity, first / last layer of the entry, O slot, CSR column offset) is
-                    // hoisted out of the m-tile loop: first layer iff e2 == 0 or max(r2, rj2) == P, last
-                    // iff e2 == S2-1 or min(r2, rj2) == 0 (the entry's layers are [max(i2,j2)-P, min(i2,j2)]).
-                    const int64_t* rb = reinterpret_cast<const int64_t*>(smem + M.o_rb) + (i2 - b2);
-                    const int i2m = i2 % G;
-                    const int jlo2 = max(0, i2 - P);
-                    bool ok[MT][2], fst[MT][2], lst[MT][2];
-                    int soff[MT][2], dj[MT][2], jcol[MT][2];
+                };
+                double accS[CH][MT][2];
+#pragma unroll
+                for (int mm = 0; mm < CH; ++mm)
+#pragma unroll
+                    for (int c = 0; c < MT; ++c) accS[mm][c][0] = accS[mm][c][1] = 0.0;
+                ndmma += (unsigned long long)(TTS::T.NF + f_npairs(TTS::T)) * KS3 * CH * MT;  // compile-time per item
+                for (int u = 0; u < TTS::T.NF; ++u) {
+                    const int d = tab[TAB::S.o_u3 + u];
+                    const int ga = d & 255, kd = (d >> 16) & 15;
+                    if (!(d >> 24)) {
+                        block(ga, kd, accS);
+                    } else {
+                        double tA[CH][MT][2], tB[CH][MT][2];
+#pragma unroll
+                        for (int mm = 0; mm < CH; ++mm)
+#pragma unroll
+                            for (int c = 0; c < MT; ++c) tA[mm][c][0] = tA[mm][c][1] = tB[mm][c][0] = tB[mm][c][1] = 0.0;
+                        block(ga, kd, tA);
+                        block((d >> 8) & 255, (d >> 20) & 15, tB);
+#pragma unroll
+                        for (int mm = 0; mm < CH; ++mm)
+#pragma unroll
+                            for (int c = 0; c < MT; ++c)
+#pragma unroll
+                                for (int h = 0; h < 2; ++h) accS[mm][c][h] = __dadd_rn(accS[mm][c][h], __dadd_rn(tA[mm][c][h], tB[mm][c][h]));
+                    }
+                }
+                if (prm.dbg & 2) {
+                    nzero += accS[0][0][0] == 0.0 ? 1u : 0u;
+                    continue;
+                }
+                // final entries: row (combo's (i0, i1), i2), column (j0, j1, j2 = i2 + d2)
+#pragma unroll
+                for (int mm = 0; mm < CH; ++mm) {
+                    const int combo = (ch * CH + mm) * 8 + lr;
+                    if (combo >= M.NCOMBO) continue;
+                    const int4 cb = reinterpret_cast<const int4*>(cmb)[combo];
+                    const int64_t rowb = rb[(cb.y >> 16) * kMmaT2];
+                    if (cb.x < 0 || rowb < 0) continue;
+                    const int cnt01 = cb.y & 0xffff;
 #pragma unroll
                     for (int c = 0; c < MT; ++c)
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
                             const int d2 = c * 8 + 2 * lk + h - P;
-                            const int rj2 = r2 + d2;
-                            ok[c][h] = d2 <= P && rj2 >= 0 && rj2 <= P;
-                            fst[c][h] = e2 == 0 || max(r2, rj2) == P;
-                            lst[c][h] = e2 == prm.S[2] - 1 || min(r2, rj2) == 0;
-                            soff[c][h] = (i2m * G + (i2m + d2 + G) % G) * M.NCP;
-                            dj[c][h] = i2 + d2 - jlo2;
-                            jcol[c][h] = m01 * (i2 + d2);
+                            const int j2 = i2 + d2;
+                            if (d2 > P || j2 < 0 || j2 >= prm.m[2]) continue;
+                            double v = accS[mm][c][h];
+                            const int64_t pos = rowb + cb.x + (int64_t)cnt01 * (j2 - jlo2);
+                            const int col = cb.w + m01 * j2;
+                            if constexpr (RAT) v = v * (prm.sol_w[(int64_t)cb.z + (int64_t)m01 * i2] * prm.sol_w[col]);
+                            nzero += v == 0.0 ? 1u : 0u;
+                            prm.data[pos] = v;
+                            prm.indices[pos] = col;
                         }
-#pragma unroll
-                    for (int mm = 0; mm < CH; ++mm) {
-                        const int combo = (ch * CH + mm) * 8 + lr;
-                        if (combo >= M.NCOMBO) continue;
-                        const int4 cb = reinterpret_cast<const int4*>(cmb)[combo];
-                        const int64_t rowb = rb[(cb.y >> 16) * kMmaT2];
-                        const int cnt01 = cb.y & 0xffff;
-                        double* Oc = Os + combo;
-#pragma unroll
-                        for (int c = 0; c < MT; ++c)
-#pragma unroll
-                            for (int h = 0; h < 2; ++h) {
-                                if (!ok[c][h]) continue;
-                                double* slot = Oc + soff[c][h];
-                                double v = accS[mm][c][h];
-                                if (!fst[c][h]) v = *slot + v;
-                                if (!lst[c][h]) {
-                                    *slot = v;
-                                } else if (cb.x >= 0 && rowb >= 0) {
-                                    const int64_t pos = rowb + cb.x + (int64_t)cnt01 * dj[c][h];
-                                    const int col = cb.w + jcol[c][h];
-                                    if constexpr (RAT) v = v * (prm.sol_w[(int64_t)cb.z + (int64_t)m01 * i2] * prm.sol_w[col]);
-                                    nzero += v == 0.0 ? 1u : 0u;
-                                    prm.data[pos] = v;
-                                    prm.indices[pos] = col;
-                                }
-                            }
+                }
+            }
+        };
+        // ---- phase-3 B fragments of row plane i2 = elo2 + L (warps w0 .. w0+nw-1):
+        // B3f[L&1][(slot*KS3 + kk)*MT + c][lane] = B^a2_{i2}(z_s) B^b2_{i2+d2}(z_s), s = kk*4 + lk, d2 = c*8 + lr - P
+        auto build_b3 = [&](const int L, const int w0, const int nw) {
+            const int i2 = elo2 + L;
+            double* B3b = B3f + (L & 1) * B3SZ;
+            for (int slot = warp - w0; slot < NK2; slot += nw) {
+                int kind = 0;
+                static_for<0, NK2>([&](auto SI) { if (slot == decltype(SI)::value) kind = kind_of_slot2(TTS::T, decltype(SI)::value); });
+                const int a2 = kind % 3, bb2 = kind / 3;
+                for (int kk = 0; kk < KS3; ++kk) {
+                    const int sz = kk * 4 + lk;
+                    const int e = i2 - P + sz / G, r = P - sz / G;
+                    for (int c = 0; c < MT; ++c) {
+                        const int d2 = c * 8 + lr - P;
+                        const int rj = r + d2;
+                        double v = 0.0;
+                        if (sz < KZ && d2 <= P && rj >= 0 && rj <= P && e >= 0 && e < prm.S[2]) {
+                            const double* bz = prm.B[2] + ((long long)e * G + sz % G) * NB;
+                            v = __dmul_rn(bz[a2 * (P + 1) + r], bz[bb2 * (P + 1) + rj]);
+                        }
+                        B3b[((slot * KS3 + kk) * MT + c) * 32 + lane] = v;
                     }
                 }
             }
-            if (j < nplanes) phase1(Ds, T1s + (j & 1) * T1SZ);
-            if (j >= 1 && j <= nplanes) phase2(T1s + ((j - 1) & 1) * T1SZ, T2s + (long)((j - 1) % NS) * M.NG2 * TC);
-            // ---- phase-3 B fragments of the layer starting at plane j: B3f[L&1][((r2*NK2 + slot)*KS3 + kk)*MT + c][lane]
-            if (j < nplanes && j % G == 0) {
-                const int L = j / G, e2 = elo2 + L;
-                double* B3b = B3f + (L & 1) * B3SZ;
-                const double* bz0 = prm.B[2] + (long long)e2 * G * NB;
-                for (int it = warp; it < (P + 1) * NK2; it += NW) {
-                    const int r2 = it % (P + 1), slot = it / (P + 1);
-                    int kind = 0;
-                    static_for<0, NK2>([&](auto SI) { if (slot == decltype(SI)::value) kind = kind_of_slot2(TTS::T, decltype(SI)::value); });
-                    const int a2 = kind % 3, bb2 = kind / 3;
-                    for (int kk = 0; kk < KS3; ++kk) {
-                        const int s = kk * 4 + lk;
-                        for (int c = 0; c < MT; ++c) {
-                            const int d2 = c * 8 + lr - P;
-                            const int rj2 = r2 + d2;
-                            double v = 0.0;
-                            if (s < G && d2 <= P && rj2 >= 0 && rj2 <= P) {
-                                const double* bz = bz0 + s * NB;
-                                v = __dmul_rn(bz[a2 * (P + 1) + r2], bz[bb2 * (P + 1) + rj2]);
-                            }
-                            B3b[(((r2 * NK2 + slot) * KS3 + kk) * MT + c) * 32 + lane] = v;
-                        }
-                    }
-                }
+        };
+        constexpr int NBW = mma_spec_nb(NDIM, FORM);
+        if constexpr (NBW > 0) {
+            // ---- warp-specialised pipeline: group A (phases 1-2, planes) / group B (phase 3, row planes),
+            // handing over through two monotonic counters: ready = layers whose planes are in T2,
+            // done = row planes finished (a T2 plane of layer l is free once row plane l + P is done)
+            constexpr int NAW = NW - NBW;
+            volatile int* cnt = reinterpret_cast<volatile int*>(smem + M.o_bar + 2);  // [0] ready, [1] done
+            if (tid == 0) {
+                cnt[0] = 0;
+                cnt[1] = 0;
             }
             __syncthreads();
+            auto wait_ge = [&](int which, int v) {
+                for (long it = 0; cnt[which] < v; ++it) {
+                    __nanosleep(64);
+                    if (it > (1L << 26)) __trap();  // a lost hand-over aborts the launch instead of hanging the GPU
+                }
+                __threadfence_block();
+            };
+            if (warp < NAW) {
+                for (int j = 0; j <= nplanes; ++j) {
+                    const double* Ds = j < nplanes ? get_plane(j) : nullptr;
+                    if (j < nplanes) phase1(Ds, T1s + (j & 1) * T1SZ);
+                    if (j >= 1) phase2(T1s + ((j - 1) & 1) * T1SZ, T2s + (long)((j - 1) % NS) * M.NG2 * TC);
+                    // before the next interval's phase 2 writes plane j over plane j - NS: the last row
+                    // plane reading that plane's layer must be done
+                    if (tid == 0 && j < nplanes && j >= NS) wait_ge(1, (j - NS) / G + P + 1);
+                    asm volatile("bar.sync 1, %0;\n" ::"r"(NAW * 32) : "memory");
+                    if (tid == 0 && j >= 1 && j % G == 0) {
+                        __threadfence_block();
+                        cnt[0] = j / G;
+                    }
+                }
+            } else {
+                const int tb0 = NAW * 32;
+                if (nsteps > 0) build_b3(0, NAW, NBW);
+                for (int L = 0; L < nsteps; ++L) {
+                    if (tid == tb0) wait_ge(0, min(L, nlayers - 1) + 1);
+                    asm volatile("bar.sync 2, %0;\n" ::"r"(NBW * 32) : "memory");
+                    phase3(L);
+                    if (L + 1 < nsteps) build_b3(L + 1, NAW, NBW);
+                    asm volatile("bar.sync 2, %0;\n" ::"r"(NBW * 32) : "memory");
+                    if (tid == tb0) {
+                        __threadfence_block();
+                        cnt[1] = L + 1;
+                    }
+                }
+            }
+        } else {
+            // one barrier interval per Gauss plane j: phase 3 (row plane whose last layer completed one
+            // interval earlier) | phase 1 (plane j) | phase 2 (plane j-1) | fragments of the next row plane
+            const int jend = max(nplanes, (nsteps + 1) * G) + 1;
+            for (int j = 0; j <= jend; ++j) {
+                const double* Ds = j < nplanes ? get_plane(j) : nullptr;
+                if (j >= G + 1 && (j - 1) % G == 0 && (j - 1) / G - 1 < nsteps) phase3((j - 1) / G - 1);
+                if (j < nplanes) phase1(Ds, T1s + (j & 1) * T1SZ);
+                if (j >= 1 && j <= nplanes) phase2(T1s + ((j - 1) & 1) * T1SZ, T2s + (long)((j - 1) % NS) * M.NG2 * TC);
+                if (j % G == 0 && j / G < nsteps) build_b3(j / G, 0, NW);
+                __syncthreads();
+            }
         }
     }
     if (prm.dmma && lane == 0 && ndmma) atomicAdd(prm.dmma, ndmma);  // all lanes of a warp run the same items
