@@ -146,20 +146,19 @@ def test_gpu_surrogate_divergence_matches_oracle_3d():
 
 
 def thick_annulus():
-    """3D NURBS domain: the quarter annulus extruded linearly in z (rational weights vary in y)."""
-    from paper_1904_06971_b200.geometry import _from_bezier
+    """3D NURBS domain: the quarter annulus (the reference's net, data/quarter_annulus_1_2.geo)
+    extruded linearly in z over [0, 1] with degree 2 (rational weights vary in y, not in z)."""
+    import paper_1904_06971_b200 as pkg
+    from paper_1904_06971_b200.geometry import GeometryMap
+    from paper_1904_06971_b200.spaces import NurbsWeights, make_tensor_space
 
-    radii = np.array([1.0, 1.5, 2.0])
-    arc = np.array([[1.0, 0.0], [1.0, 1.0], [0.0, 1.0]])
-    warc = np.array([1.0, np.sqrt(2.0) / 2.0, 1.0])
-    hom = np.empty((3, 3, 3, 4))
-    for i in range(3):
-        for j in range(3):
-            for k in range(3):
-                hom[i, j, k, :2] = warc[j] * radii[i] * arc[j]
-                hom[i, j, k, 2] = warc[j] * 0.5 * k
-                hom[i, j, k, 3] = warc[j]
-    return _from_bezier(2, 3, hom, "thick_annulus")
+    a = pkg.quarter_annulus(1.0, 2.0)
+    space = make_tensor_space(2, tuple(a.space.shape) + (5,))
+    zg = space.kvs[2].greville()
+    n2 = a.space.N
+    w = np.tile(a.weights.weights, zg.size)
+    ctrl = np.column_stack([np.tile(a.control, (zg.size, 1)), np.repeat(zg, n2)])
+    return GeometryMap(space=space, weights=NurbsWeights(w, polynomial_weight=True), control=ctrl, name="thick_annulus")
 
 
 @pytest.mark.gpu
