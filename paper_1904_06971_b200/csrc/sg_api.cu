@@ -9,6 +9,7 @@
 #include <atomic>
 #include <condition_variable>
 #include <deque>
+#include <functional>
 #include <mutex>
 #include <cstdarg>
 #include <cstdio>
@@ -1165,6 +1166,11 @@ int sg_assemble(const sg_problem* prob, const int64_t* rows, int64_t nrows, cons
     }
     c.record_timing();
     r->tiles = dp.last_tiles;
+    if (!rows) {
+        r->analytic = true;
+        r->p = dp.p;
+        for (int d = 0; d < 3; ++d) r->m[d] = dp.m[d];
+    }
     *out = r;
     return 0;
 }
@@ -1188,7 +1194,7 @@ struct CopyPool {
     std::vector<std::thread> th;
     std::mutex mu;
     std::condition_variable cv, done_cv;
-    struct Task { char* dst; const char* src; size_t len; std::atomic<int>* left; };
+    struct Task { char* dst; const char* src; size_t len; std::atomic<int>* left; std::function<void()> fn; };
     std::deque<Task> q;
     bool stop = false;
     explicit CopyPool(int n) {
@@ -1203,7 +1209,8 @@ struct CopyPool {
                         tk = q.front();
                         q.pop_front();
                     }
-                    memcpy(tk.dst, tk.src, tk.len);
+                    if (tk.fn) tk.fn();
+                    else memcpy(tk.dst, tk.src, tk.len);
                     if (tk.left->fetch_sub(1) == 1) {
                         std::lock_guard<std::mutex> lk(mu);
                         done_cv.notify_all();
@@ -1228,6 +1235,14 @@ struct CopyPool {
                 const size_t lo = (size_t)p * piece, len = std::min(piece, n - lo);
                 q.push_back({dst + lo, src + lo, len, left});
             }
+        }
+        cv.notify_all();
+    }
+    void run(std::vector<std::function<void()>>& fns, std::atomic<int>* left) {
+        left->store((int)fns.size());
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            for (auto& f : fns) q.push_back({nullptr, nullptr, 0, left, f});
         }
         cv.notify_all();
     }
@@ -1368,10 +1383,53 @@ int sg_result_copy_i64(const sg_result* r, int64_t* indptr, int32_t* indices, do
     // every call that creates a result synchronises its stream before returning the handle, so no
     // device-wide synchronisation here: a copy can overlap the next assembly on the same device
     int rc = 0;
-    if (indptr && (rc = d2h(indptr, r->indptr, sizeof(int64_t) * (r->nrows + 1), r->dev))) return rc;
+    std::vector<int64_t> ipv;
+    int64_t* ip = indptr;
+    if (!ip && indices && r->analytic) {
+        ipv.resize(r->nrows + 1);
+        ip = ipv.data();
+    }
+    if (ip && (rc = d2h(ip, r->indptr, sizeof(int64_t) * (r->nrows + 1), r->dev))) return rc;
     if (r->nnz > 0) {
-        if (indices && (rc = d2h(indices, r->indices, sizeof(int32_t) * r->nnz, r->dev))) return rc;
-        if (data && (rc = d2h(data, r->data, sizeof(double) * r->nnz, r->dev))) return rc;
+        if (indices && r->analytic && !getenv("SG_COPY_INDICES")) {
+            // closed-form columns on the host pool, concurrent with the values' D2H
+            std::atomic<int> left(0);
+            std::vector<std::function<void()>> fns;
+            const int nt = 64;  // small tasks: staging copies of a concurrent pageable D2H interleave in the queue
+            int64_t r0 = 0;
+            for (int t = 0; t < nt && r0 < r->nrows; ++t) {
+                int64_t r1 = r->nrows;
+                if (t + 1 < nt) {  // balance by entries
+                    const int64_t target = ip[0] + (ip[r->nrows] - ip[0]) * (t + 1) / nt;
+                    r1 = std::max<int64_t>(r0, (int64_t)(std::upper_bound(ip, ip + r->nrows + 1, target) - ip) - 1);
+                }
+                fns.push_back([r, ip, indices, r0, r1] {
+                    const int64_t m0 = r->m[0], m1 = r->m[1], m2 = r->m[2], m01 = m0 * m1;
+                    const int p = r->p;
+                    for (int64_t k = r0; k < r1; ++k) {
+                        const int64_t row = r->row_lo + k;
+                        const int64_t i0 = row % m0, i1 = (row / m0) % m1, i2 = row / m01;
+                        const int64_t a0 = std::max<int64_t>(0, i0 - p), b0 = std::min<int64_t>(m0 - 1, i0 + p);
+                        const int64_t a1 = std::max<int64_t>(0, i1 - p), b1 = std::min<int64_t>(m1 - 1, i1 + p);
+                        const int64_t a2 = std::max<int64_t>(0, i2 - p), b2 = std::min<int64_t>(m2 - 1, i2 + p);
+                        int32_t* o = indices + (ip[k] - ip[0]);
+                        for (int64_t j2 = a2; j2 <= b2; ++j2)
+                            for (int64_t j1 = a1; j1 <= b1; ++j1) {
+                                const int32_t base = (int32_t)(m01 * j2 + m0 * j1);
+                                for (int64_t j0 = a0; j0 <= b0; ++j0) *o++ = base + (int32_t)j0;
+                            }
+                    }
+                });
+                r0 = r1;
+            }
+            copy_pool().run(fns, &left);
+            if (data) rc = d2h(data, r->data, sizeof(double) * r->nnz, r->dev);
+            copy_pool().wait(&left);
+            if (rc) return rc;
+        } else {
+            if (indices && (rc = d2h(indices, r->indices, sizeof(int32_t) * r->nnz, r->dev))) return rc;
+            if (data && (rc = d2h(data, r->data, sizeof(double) * r->nnz, r->dev))) return rc;
+        }
     }
     return 0;
 }

@@ -23,6 +23,12 @@ struct sg_result {
     void* own_indices = nullptr;  // allocations to free when indices / data point inside a larger buffer
     void* own_data = nullptr;
     bool exported = false;  // device pointers handed out (sg_result_device_ptrs): free waits for the device
+    // the result holds full rows of the square basis-overlap pattern (no row restriction, no exact-zero
+    // drop): its column indices are a closed-form function of (m, p, row) and the host copy generates
+    // them on host threads while the values stream over PCIe instead of copying them
+    bool analytic = false;
+    int p = 0;
+    int64_t m[3] = {1, 1, 1};
 };
 
 namespace sg {

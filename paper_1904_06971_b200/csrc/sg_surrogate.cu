@@ -1524,6 +1524,9 @@ static int surr_finish(sg_surrogate_state& S, const sg_surrogate_params* sp, sg_
             r->indices = S.indices + (S.nnz_lo - S.nnz_qlo);
             r->data = S.data + (S.nnz_lo - S.nnz_qlo);
         }
+        r->analytic = true;  // no exact zero dropped: the full pattern's rows
+        r->p = p;
+        for (int d = 0; d < 3; ++d) r->m[d] = dp.m[d];
         cudaMemcpyAsync(r->indptr, S.rowstart + slab_lo, sizeof(int64_t) * (r->nrows + 1), cudaMemcpyDeviceToDevice, c.stream);
         if (S.nnz_lo) {
             c.kbegin("rebase");
