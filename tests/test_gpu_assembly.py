@@ -189,3 +189,27 @@ def test_gpu_2d_tiles_every_degree_form_and_map(p, form, geom, run, monkeypatch)
     assert np.array_equal(m.indptr, ip) and np.array_equal(m.indices, ix)
     assert O.row_scaled_error(ip, ix, d, m.indptr, m.indices, m.data) <= 1e-12
     assert pkg.is_bitwise_symmetric(A)
+
+
+@pytest.mark.gpu
+def test_gpu_host_generated_columns_equal_device_columns(monkeypatch):
+    # full-pattern results hand their column indices to the host in closed form (generated on host
+    # threads during the values' D2H); they must equal the device's own indices bit for bit
+    import paper_1904_06971_b200 as pkg
+    from paper_1904_06971_b200.surrogate import surrogate_device
+
+    disc = pkg.make_discretization(pkg.twisted_cube_standin(), 3, (21, 19, 23))
+    ms = tuple(kv.m for kv in disc.space.kvs)
+    per = ms[0] * ms[1]
+    calls = [lambda: pkg.assemble_device(pkg.FormKind.POISSON, disc)[0],
+             lambda: pkg.assemble_device(pkg.FormKind.MASS, disc, slab=(5 * per, 17 * per))[0],
+             lambda: surrogate_device(pkg.FormKind.POISSON, disc, 4, 3, "symmetric_kernel_preserving")[0],
+             lambda: surrogate_device(pkg.FormKind.MASS, disc, 4, 3, "symmetric", slab=(7 * per, 20 * per))[0]]
+    for make in calls:
+        res = make()
+        ip, ix, d = res.to_host()
+        monkeypatch.setenv("SG_COPY_INDICES", "1")
+        ip2, ix2, d2 = res.to_host()
+        monkeypatch.delenv("SG_COPY_INDICES")
+        res.free()
+        assert np.array_equal(ip, ip2) and np.array_equal(ix, ix2) and np.array_equal(d.view(np.int64), d2.view(np.int64))
