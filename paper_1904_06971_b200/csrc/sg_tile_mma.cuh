@@ -54,6 +54,14 @@ __host__ __device__ constexpr int f_pairidx(const Tables& T, int f) {
     return c;
 }
 __host__ __device__ constexpr int imax(int a, int b) { return a > b ? a : b; }
+// 3D with single-unit level-1 groups (Poisson, mass): a phase-1 item covers two groups, two
+// independent DMMA chains interleaved (fewer, fatter items: the interval's warps each take one)
+__host__ __device__ constexpr bool p1_pair(const Tables& T, int ndim) {
+    if (ndim != 3 || T.NG1 < 2) return false;
+    for (int g = 0; g < T.NG1; ++g)
+        if (T.g1n[g] != 1) return false;
+    return true;
+}
 // prefix count of phase-1 units before group g (fragment slot base)
 __host__ __device__ constexpr int g1_unit_base(const Tables& T, int g) {
     int c = 0;
@@ -333,7 +341,8 @@ __host__ __device__ constexpr MmaTab mma_tab(int ndim, int P, int form, bool rat
     const MmaGeom M = mma_geom(ndim, P, form, rat, tc.T0, tc.T1);
     const int NW = mma_warps(ndim, P, form, rat);
     MmaTab S{};
-    const int n1 = M.NG1 * M.T0 * M.NC1;
+    const bool pr1 = false;  // p1_pair(T, ndim): paired phase-1 items measured no faster (config 5: 33.1 vs 32.7 ms)
+    const int n1 = (pr1 ? (M.NG1 + 1) / 2 : M.NG1) * M.T0 * M.NC1;
     const int n2 = ndim >= 2 ? T.NG2 * M.T1 * M.T0 : 0;
     const int n3 = ndim == 3 ? M.NCH : 0;  // phase-3 items of a row plane: chunks of CH m-tiles
     int w1[512] = {}, w2[512] = {}, w3[512] = {};
@@ -361,7 +370,9 @@ __host__ __device__ constexpr MmaTab mma_tab(int ndim, int P, int form, bool rat
         n = 0;
     };
     for (int k = 0; k < n1; ++k) {
-        cost[n] = T.g1n[k / (M.T0 * M.NC1)] * M.KS * M.MT * (M.NTY / M.NC1) + 2 + SG_P12_EPI * M.MT * (M.NTY / M.NC1);
+        const int gk = k / (M.T0 * M.NC1);
+        const int nun = pr1 ? (2 * gk + 1 < M.NG1 ? 2 : 1) : T.g1n[gk];
+        cost[n] = nun * M.KS * M.MT * (M.NTY / M.NC1) + 2 + SG_P12_EPI * M.MT * (M.NTY / M.NC1);
         kind[n] = 1; idx[n] = k; done[n] = false; ++n;
     }
     if (ndim != 3) {  // 2D: phase 2 after its own barrier
@@ -461,7 +472,7 @@ struct MmaParams {
     unsigned long long* dmma;    // executed DMMA instructions (per warp, summed per launch), or nullptr
     int z0;                      // z origin of the tile grid (rows)
     int run;                     // 2D: tiles per CTA (consecutive entries of the tile list)
-    int dbg;                     // timing experiments only (SG_K4_DBG): 1 skip phase 3, 2 skip its epilogue
+    int dbg;                     // timing experiments only (SG_K4_DBG): skip 1 phase 3, 2 its epilogue, 4 phase 1, 8 phase 2
     int ntiles;                  // entries of the tile list (or tiles of the grid)
 };
 
@@ -746,6 +757,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
 
     // ---------------- phase 1 (x): items (group, row i0l) -> T1[Gc][i0l][d0][y]
     auto phase1 = [&](const double* Ds, double* T1b) {
+        if (prm.dbg & 4) return;
         const int qe = tab[TAB::S.o_off1 + warp + 1];
         for (int q = tab[TAB::S.o_off1 + warp]; q < qe; ++q) {
             const int k = tab[TAB::S.o_it1 + q];
@@ -817,6 +829,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
     // Chains: non-pair units into accS in unit order, then each symmetric pair (A, B chains) folded
     // in as accS + (A + B) in order -- the mirror of the transposed entry's evaluation.
     auto phase2 = [&](const double* T1b, double* T2b) {
+        if (prm.dbg & 8) return;
         if constexpr (NDIM >= 2) {
             const int qe = tab[TAB::S.o_off2 + warp + 1];
             for (int q = tab[TAB::S.o_off2 + warp]; q < qe; ++q) {
