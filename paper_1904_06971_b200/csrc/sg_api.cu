@@ -1403,23 +1403,7 @@ int sg_result_copy_i64(const sg_result* r, int64_t* indptr, int32_t* indices, do
                     const int64_t target = ip[0] + (ip[r->nrows] - ip[0]) * (t + 1) / nt;
                     r1 = std::max<int64_t>(r0, (int64_t)(std::upper_bound(ip, ip + r->nrows + 1, target) - ip) - 1);
                 }
-                fns.push_back([r, ip, indices, r0, r1] {
-                    const int64_t m0 = r->m[0], m1 = r->m[1], m2 = r->m[2], m01 = m0 * m1;
-                    const int p = r->p;
-                    for (int64_t k = r0; k < r1; ++k) {
-                        const int64_t row = r->row_lo + k;
-                        const int64_t i0 = row % m0, i1 = (row / m0) % m1, i2 = row / m01;
-                        const int64_t a0 = std::max<int64_t>(0, i0 - p), b0 = std::min<int64_t>(m0 - 1, i0 + p);
-                        const int64_t a1 = std::max<int64_t>(0, i1 - p), b1 = std::min<int64_t>(m1 - 1, i1 + p);
-                        const int64_t a2 = std::max<int64_t>(0, i2 - p), b2 = std::min<int64_t>(m2 - 1, i2 + p);
-                        int32_t* o = indices + (ip[k] - ip[0]);
-                        for (int64_t j2 = a2; j2 <= b2; ++j2)
-                            for (int64_t j1 = a1; j1 <= b1; ++j1) {
-                                const int32_t base = (int32_t)(m01 * j2 + m0 * j1);
-                                for (int64_t j0 = a0; j0 <= b0; ++j0) *o++ = base + (int32_t)j0;
-                            }
-                    }
-                });
+                fns.push_back([r, ip, indices, r0, r1] { gen_columns(r0, r1, r->row_lo, r->m, r->p, indices + (ip[r0] - ip[0])); });
                 r0 = r1;
             }
             copy_pool().run(fns, &left);

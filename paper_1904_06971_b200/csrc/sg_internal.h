@@ -120,4 +120,14 @@ int tabulate(Call& c, const double* d_knots, int nk, int p, const double* d_pts,
 
 __global__ void rebase_kernel(int64_t* a, int64_t n, int64_t sub);
 
+// host: closed-form columns of full-pattern rows [r0, r1) of a result starting at global row row_lo
+// (sg_hostcols.cpp; AVX2 + non-temporal stores when the CPU has them)
+void gen_columns_avx2(int64_t r0, int64_t r1, int64_t row_lo, const int64_t* m, int p, int32_t* out);
+void gen_columns_base(int64_t r0, int64_t r1, int64_t row_lo, const int64_t* m, int p, int32_t* out);
+inline void gen_columns(int64_t r0, int64_t r1, int64_t row_lo, const int64_t* m, int p, int32_t* out) {
+    static const bool avx2 = __builtin_cpu_supports("avx2");
+    if (avx2) gen_columns_avx2(r0, r1, row_lo, m, p, out);
+    else gen_columns_base(r0, r1, row_lo, m, p, out);
+}
+
 }  // namespace sg
