@@ -669,11 +669,18 @@ constexpr int TB0 = 4, TB1 = 4, TB2 = 8, NR = TB0 * TB1 * TB2, CW = 5, MAXSH = 9
 constexpr int AS = 6;             // scratch A row stride (doubles): [(t2, t1)][AS] holding b0 = 0..3
 constexpr int BS = 6;             // scratch B row stride: [(t2, b1)][BS] holding b0 = 0..3
 constexpr int WS = 6;             // lane-specific weight rows [d][sh][b][WS] (5 taps + pad)
-constexpr int SCR = 25 * AS + 20 * BS + 2;  // per-warp scratch (doubles)
+constexpr int SCR_SIMT = 25 * AS + 20 * BS + 2;
+// tensor-core passes (MMA = true): x out / y in Ax[t1 (8)][SX] holding (t2, b0) = 4 t2 + b0; y out /
+// z in Bz[t2 (8)][SZ] holding (b1, b0) = 4 b1 + b0 (row strides chosen so the B-fragment loads of a
+// half warp hit distinct banks); rows 5..7 and the padding columns stay zero (finite operands of the
+// zero-weight taps)
+constexpr int SX = 28, SZ = 20;
+constexpr int SCR_MMA = 8 * SX + 8 * SZ;
+constexpr int SCR = SCR_SIMT > SCR_MMA ? SCR_SIMT : SCR_MMA;  // per-warp scratch (doubles)
 // stage row of tile point (b0, b1, b2): rho = (b1 + 4 b2) + 32 b0 (the z-pass lane is b1 + 4 b2)
 }  // namespace rows3
 
-template <int NS>
+template <int NS, bool MMA>
 __global__ void __launch_bounds__(256, 2) interp_rows3_kernel(SurrParams s) {
     using namespace rows3;
     extern __shared__ double sm[];
@@ -776,6 +783,55 @@ __global__ void __launch_bounds__(256, 2) interp_rows3_kernel(SurrParams s) {
         rfast[r] = (all0 & all1 & all2 & 1) && !(any0 & any1 & any2 & 1);
     }
     __syncthreads();
+    const int kb = (warp * K) / NWARP, ke = ((warp + 1) * K) / NWARP;  // this warp's run of offsets in every chunk
+    unsigned n_int = 0, n_zero = 0;
+    // write phase: warp owns rows [RPW*warp, RPW*warp + RPW); lane < RPW keeps row RPW*warp+lane's sums
+    const int rsl = RPW * warp + (lane < RPW ? lane : 0);
+    double rsum = 0.0, dg = 0.0;
+    auto write_chunk = [&](const int c) {
+        // ---- write the warp's row segments of the chunk: entries flattened over (row, k) so the
+        //      lanes stay busy; consecutive lanes write consecutive CSR slots of a row.  The trip
+        //      count is a compile-time constant, so unrolled iterations issue their shared loads
+        //      together (the loop was bound by shared-load latency)
+        constexpr int NE = RPW * K, NIT = (NE + 31) / 32;
+#pragma unroll 5
+        for (int it = 0; it < NIT; ++it) {
+            const int e = it * 32 + lane;
+            if (e < NE) {
+                const int rl = e / K, k = e - rl * K;
+                const int r = RPW * warp + rl;
+                const int rb = rbr[r];
+                const int o = c * K + k;
+                const int col = rowid[r] + shl[o];
+                const double v = stage[r * K + k];
+                if (rb >= 0) {
+                    n_int++;  // provisional for slow rows (corrected by slow_rows_kernel)
+                    n_zero += v == 0.0;
+                    tdata[rb + o] = v;
+                    tidx[rb + o] = col;
+                }
+            }
+        }
+        __syncwarp();
+        // ---- SKP row sums of the warp's rows (lane = row; ascending offsets in four interleaved
+        //      partial sums, joined in a fixed order)
+        if (lane < RPW && rbS[rsl] >= 0) {
+            const double* sr = stage + (size_t)rsl * K;
+            double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0;
+#pragma unroll
+            for (int k = 0; k + 3 < K; k += 4) {
+                q0 += sr[k];
+                q1 += sr[k + 1];
+                q2 += sr[k + 2];
+                q3 += sr[k + 3];
+            }
+#pragma unroll
+            for (int k = K & ~3; k < K; ++k) q0 += sr[k];
+            rsum += (q0 + q1) + (q2 + q3);
+            if (c == p) dg = sr[(K - 1) / 2];
+        }
+    };
+    if constexpr (!MMA) {
     // window row of this lane (lanes 0..24): t1 = lane % 5, t2 = lane / 5
     const int wt1 = lane % 5, wt2 = lane / 5;
     const int nl0 = s.nl[0], nl01 = s.nl[0] * s.nl[1], nl012 = nl01 * s.nl[2];
@@ -790,19 +846,13 @@ __global__ void __launch_bounds__(256, 2) interp_rows3_kernel(SurrParams s) {
             for (int r = 0; r < CW; ++r) w[r] = __ldg(cf + r);
         }
     };
-    // this warp's run of offsets in every chunk
-    const int kb = (warp * K) / NWARP, ke = ((warp + 1) * K) / NWARP;
     double wpre[CW] = {0, 0, 0, 0, 0};
     if (kb < ke) fetch(kb, wpre);
-    unsigned n_int = 0, n_zero = 0;
     const int yb1 = lane % 4, yt2 = lane / 4;  // y pass lane (lanes 0..19)
     const int zb1 = lane % 4, zb2 = lane / 4;  // z pass lane
     // the lane's y and z tap rows, reloaded only when the evaluation shift changes (z: per chunk)
     double wyr[CW], wzr[CW];
     int cur1 = -1, cur2 = -1;
-    // write phase: warp owns rows [RPW*warp, RPW*warp + RPW); lane < RPW keeps row RPW*warp+lane's sums
-    const int rsl = RPW * warp + (lane < RPW ? lane : 0);
-    double rsum = 0.0, dg = 0.0;
     for (int c = 0; c < NS; ++c) {
         // ---- compute the chunk's values into the stage
         for (int k = kb; k < ke; ++k) {
@@ -879,48 +929,138 @@ __global__ void __launch_bounds__(256, 2) interp_rows3_kernel(SurrParams s) {
             __syncwarp();
         }
         __syncthreads();
-        // ---- write the warp's row segments of the chunk: entries flattened over (row, k) so the
-        //      lanes stay busy; consecutive lanes write consecutive CSR slots of a row.  The trip
-        //      count is a compile-time constant, so unrolled iterations issue their shared loads
-        //      together (the loop was bound by shared-load latency)
-        constexpr int NE = RPW * K, NIT = (NE + 31) / 32;
-#pragma unroll 5
-        for (int it = 0; it < NIT; ++it) {
-            const int e = it * 32 + lane;
-            if (e < NE) {
-                const int rl = e / K, k = e - rl * K;
-                const int r = RPW * warp + rl;
-                const int rb = rbr[r];
-                const int o = c * K + k;
-                const int col = rowid[r] + shl[o];
-                const double v = stage[r * K + k];
-                if (rb >= 0) {
-                    n_int++;  // provisional for slow rows (corrected by slow_rows_kernel)
-                    n_zero += v == 0.0;
-                    tdata[rb + o] = v;
-                    tidx[rb + o] = col;
+        write_chunk(c);
+        __syncthreads();
+    }
+    } else {
+    // ---- tensor-core passes: per offset three m8n8k4 DMMA contractions (x: M = b0, K = t0,
+    //      N = (t1, t2); y: M = b1, K = t1, N = (t2, b0); z: M = b2, K = t2, N = (b1, b0)), taps
+    //      padded to K = 8 with zero weights: each value is the same ascending FMA chain as the
+    //      SIMT passes (a DMMA's K is a sequential FMA chain), so the results are bitwise the same
+    const int lr = lane >> 2, lk = lane & 3;
+    const int nl0 = s.nl[0], nl01 = s.nl[0] * s.nl[1], nl012 = nl01 * s.nl[2];
+    double* Ax = Aw;                 // [t1][SX]
+    double* Bz = Aw + 8 * SX;        // [t2][SZ]
+    for (int it = lane; it < SCR_MMA; it += 32) Aw[it] = 0.0;
+    __syncwarp();
+    // B-fragment element offsets of the x pass inside a coefficient window (k-step kt, n-tile j):
+    // t0 = 4 kt + lk (clamped into the window: its weight is zero beyond tap 4), n = 8 j + lr -> (t1, t2)
+    int xoff[2][4];
+#pragma unroll
+    for (int kt = 0; kt < 2; ++kt)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int t0 = min(4 * kt + lk, 4), n = min(8 * j + lr, 24);
+            xoff[kt][j] = (n / 5) * nl01 + (n % 5) * nl0 + t0;
+        }
+    auto fetch = [&](int o, double (&b)[2][4]) {
+        const int oi = oinf[o];
+        const int op = oi & 0xffff, a0 = (oi >> 16) & 15, a1 = (oi >> 20) & 15, a2 = oi >> 24;
+        const double* cf = s.coef + (op * nl012 + LO[2 * MAXSH + a2] * nl01 + LO[MAXSH + a1] * nl0 + LO[a0]);
+#pragma unroll
+        for (int kt = 0; kt < 2; ++kt)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[kt][j] = __ldg(cf + xoff[kt][j]);
+    };
+    // A fragments of the three directions for an evaluation shift: w[d][b = lr][t = 4 kt + lk]
+    auto wfrag = [&](int d, int sh, double (&a)[2]) {
+#pragma unroll
+        for (int kt = 0; kt < 2; ++kt) {
+            const int t = 4 * kt + lk;
+            a[kt] = (t < CW && lr < 8) ? W5[((d * MAXSH + sh) * CW + t) * 8 + lr] : 0.0;
+        }
+    };
+    double bpre[2][4];
+    if (kb < ke) fetch(kb, bpre);
+    double wy[2], wz[2];
+    int cur1 = -1, cur2 = -1;
+    for (int c = 0; c < NS; ++c) {
+        for (int k = kb; k < ke; ++k) {
+            const int o = c * K + k;
+            const int oi = oinf[o];
+            const int sh0 = (oi >> 16) & 15, sh1 = (oi >> 20) & 15, sh2 = oi >> 24;  // shift + p
+            double bx[2][4];
+#pragma unroll
+            for (int kt = 0; kt < 2; ++kt)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) bx[kt][j] = bpre[kt][j];
+            {
+                const int on = (k + 1 < ke) ? o + 1 : ((c + 1 < NS) ? (c + 1) * K + kb : -1);
+                if (on >= 0) fetch(on, bpre);
+            }
+            double wx[2];
+            wfrag(0, sh0, wx);
+            if (sh1 != cur1) {
+                wfrag(1, sh1, wy);
+                cur1 = sh1;
+            }
+            if (sh2 != cur2) {
+                wfrag(2, sh2, wz);
+                cur2 = sh2;
+            }
+            // x pass -> Ax[t1][4 t2 + b0]
+            {
+                double acc[4][2];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+                for (int kt = 0; kt < 2; ++kt)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) dmma(acc[j][0], acc[j][1], wx[kt], bx[kt][j]);
+                if (lr < TB0) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int n = 8 * j + 2 * lk + h;
+                            if (n < 25) Ax[(n % 5) * SX + 4 * (n / 5) + lr] = acc[j][h];
+                        }
                 }
             }
-        }
-        __syncwarp();
-        // ---- SKP row sums of the warp's rows (lane = row; ascending offsets in four interleaved
-        //      partial sums, joined in a fixed order)
-        if (lane < RPW && rbS[rsl] >= 0) {
-            const double* sr = stage + (size_t)rsl * K;
-            double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0;
+            __syncwarp();
+            // y pass -> Bz[t2][4 b1 + b0]
+            {
+                double acc[3][2];
 #pragma unroll
-            for (int k = 0; k + 3 < K; k += 4) {
-                q0 += sr[k];
-                q1 += sr[k + 1];
-                q2 += sr[k + 2];
-                q3 += sr[k + 3];
+                for (int j = 0; j < 3; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+                for (int kt = 0; kt < 2; ++kt)
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) dmma(acc[j][0], acc[j][1], wy[kt], Ax[(4 * kt + lk) * SX + 8 * j + lr]);
+                if (lr < TB1) {
+#pragma unroll
+                    for (int j = 0; j < 3; ++j)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int n = 8 * j + 2 * lk + h;  // 4 t2 + b0
+                            if (n < 20) Bz[(n / 4) * SZ + 4 * lr + (n % 4)] = acc[j][h];
+                        }
+                }
             }
+            __syncwarp();
+            // z pass -> stage rows (b1 + 4 b2) + 32 b0
+            {
+                double acc[2][2];
 #pragma unroll
-            for (int k = K & ~3; k < K; ++k) q0 += sr[k];
-            rsum += (q0 + q1) + (q2 + q3);
-            if (c == p) dg = sr[(K - 1) / 2];
+                for (int j = 0; j < 2; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+                for (int kt = 0; kt < 2; ++kt)
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) dmma(acc[j][0], acc[j][1], wz[kt], Bz[(4 * kt + lk) * SZ + 8 * j + lr]);
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int n = 8 * j + 2 * lk + h, b1 = n / 4, b0 = n % 4;
+                        stage[((b1 + 4 * lr) + 32 * b0) * K + k] = acc[j][h];
+                    }
+            }
+            __syncwarp();
         }
         __syncthreads();
+        write_chunk(c);
+        __syncthreads();
+    }
     }
     // ---- SKP diagonal values and counters
     unsigned n_reset = 0, n_rows = 0;
@@ -1438,8 +1578,13 @@ static int surr_finish(sg_surrogate_state& S, const sg_surrogate_params* sp, sg_
         s.slow = (int*)c.alloc(sizeof(int) * N, true);
         if (!s.slow) return fail(-4, "device allocation failed");
         for (int d = 0; d < n; ++d) s.cmax[d] = 5;
-        kfn = p == 1 ? (void*)interp_rows3_kernel<3>
-                     : (p == 2 ? (void*)interp_rows3_kernel<5> : (p == 3 ? (void*)interp_rows3_kernel<7> : (void*)interp_rows3_kernel<9>));
+        // tensor-core passes by default; SG_INTERP_SIMT=1 selects the SIMT passes (same values bitwise)
+        if (getenv("SG_INTERP_SIMT"))
+            kfn = p == 1 ? (void*)interp_rows3_kernel<3, false>
+                         : (p == 2 ? (void*)interp_rows3_kernel<5, false> : (p == 3 ? (void*)interp_rows3_kernel<7, false> : (void*)interp_rows3_kernel<9, false>));
+        else
+            kfn = p == 1 ? (void*)interp_rows3_kernel<3, true>
+                         : (p == 2 ? (void*)interp_rows3_kernel<5, true> : (p == 3 ? (void*)interp_rows3_kernel<7, true> : (void*)interp_rows3_kernel<9, true>));
         smem = interp_rows3_smem(p);
         nthr = rows3::NWARP * 32;
     } else if (fixq && n >= 2 && p <= 4) {

@@ -27,11 +27,6 @@
 
 namespace sg {
 
-__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                 : "+d"(c0), "+d"(c1)
-                 : "d"(a), "d"(b));
-}
 
 __host__ __device__ constexpr int g2_npairs(const Tables& T, int g) {
     int c = 0;
