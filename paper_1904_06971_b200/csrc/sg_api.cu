@@ -51,6 +51,8 @@ int fail(int code, const char* fmt, ...) {
 // reaches it, which serialised host planning behind every kernel already queued (~0.5 ms of device
 // idle per call at config 5).  The arena is rewound when the last live Call of the thread has been
 // destroyed (every Call synchronises its stream before it dies, so no staged copy is pending).
+static void pool_memcpy(void* dst, const void* src, size_t n);  // parallel host memcpy (copy pool)
+
 struct PinnedArena {
     char* base = nullptr;
     size_t cap = 0, off = 0;
@@ -141,6 +143,41 @@ void* Call::upload(const void* host, size_t bytes) {
         cudaMemcpyAsync(d, host, bytes, cudaMemcpyHostToDevice, stream);
     }
     return d;
+}
+
+std::vector<void*> Call::upload_batch(const std::vector<std::pair<const void*, size_t>>& items) {
+    // one device allocation, one pinned staging block, one copy: per-upload API overhead (allocation,
+    // memcpy call, copy launch) was ~5-10 us each; large items are packed by the host copy pool
+    std::vector<void*> out(items.size(), nullptr);
+    size_t total = 0;
+    std::vector<size_t> off(items.size());
+    for (size_t k = 0; k < items.size(); ++k) {
+        off[k] = total;
+        total += (std::max<size_t>(items[k].second, 8) + 255) & ~size_t(255);
+    }
+    if (!g_arena.tried) {
+        g_arena.tried = true;
+        if (cudaMallocHost((void**)&g_arena.base, kArenaBytes) == cudaSuccess) g_arena.cap = kArenaBytes;
+        else g_arena.base = nullptr;
+    }
+    if (!g_arena.base || g_arena.off + total > g_arena.cap) {
+        for (size_t k = 0; k < items.size(); ++k) out[k] = upload(items[k].first, items[k].second);
+        return out;
+    }
+    char* d = (char*)alloc(total, true);
+    if (!d) return out;
+    char* h = g_arena.base + g_arena.off;
+    g_arena.off += total;
+    std::vector<std::pair<size_t, size_t>> big;
+    for (size_t k = 0; k < items.size(); ++k) {
+        out[k] = d + off[k];
+        if (!items[k].first || !items[k].second) continue;
+        if (items[k].second >= (256u << 10)) big.push_back({k, items[k].second});
+        else memcpy(h + off[k], items[k].first, items[k].second);
+    }
+    for (auto& b : big) pool_memcpy(h + off[b.first], items[b.first].first, b.second);
+    cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, stream);
+    return out;
 }
 
 void Call::kbegin(const char* name) {
@@ -385,16 +422,32 @@ int prepare_problem(Call& c, const sg_problem* pr, DevProblem& dp) {
     TabJobs jobs;
     jobs.n = 0;
     int maxpts = 0;
+    // every host input of the problem in one staged copy
+    std::vector<std::pair<const void*, size_t>> ups;
+    for (int d = 0; d < pr->n; ++d) {
+        const int npts = dp.S[d] * dp.g;
+        ups.push_back({pr->knots[d], sizeof(double) * (dp.m[d] + dp.p + 1)});
+        ups.push_back({pr->qpts[d], sizeof(double) * npts});
+        ups.push_back({pr->qwts[d], sizeof(double) * dp.g});
+        ups.push_back({pr->geo_knots[d], sizeof(double) * (dp.mg[d] + pr->geo_p + 1)});
+    }
+    ups.push_back({pr->geo_hom, sizeof(double) * dp.Ng * (pr->n + 1)});
+    if (dp.rational) ups.push_back({pr->sol_w, sizeof(double) * dp.N});
+    const std::vector<void*> dv = c.upload_batch(ups);
+    for (void* v : dv)
+        if (!v) return fail(-4, "device allocation failed");
+    dp.hom = (double*)dv[4 * pr->n];
+    dp.sol_w = dp.rational ? (double*)dv[4 * pr->n + 1] : nullptr;
     for (int d = 0; d < pr->n; ++d) {
         const int npts = dp.S[d] * dp.g;
         maxpts = std::max(maxpts, npts);
-        double* kn = (double*)c.upload(pr->knots[d], sizeof(double) * (dp.m[d] + dp.p + 1));
-        double* qp = (double*)c.upload(pr->qpts[d], sizeof(double) * npts);
-        dp.qw[d] = (double*)c.upload(pr->qwts[d], sizeof(double) * dp.g);
+        double* kn = (double*)dv[4 * d];
+        double* qp = (double*)dv[4 * d + 1];
+        dp.qw[d] = (double*)dv[4 * d + 2];
         dp.B[d] = (double*)c.alloc(sizeof(double) * npts * (dp.nu + 1) * (dp.p + 1), true);
         dp.bspan[d] = (int*)c.alloc(sizeof(int) * npts, true);
         jobs.j[jobs.n++] = TabJob{kn, qp, dp.bspan[d], dp.B[d], dp.m[d] + dp.p + 1, dp.p, npts, dp.nu};
-        double* gk = (double*)c.upload(pr->geo_knots[d], sizeof(double) * (dp.mg[d] + pr->geo_p + 1));
+        double* gk = (double*)dv[4 * d + 3];
         dp.G[d] = (double*)c.alloc(sizeof(double) * npts * (dp.nug + 1) * (pr->geo_p + 1), true);
         dp.gspan[d] = (int*)c.alloc(sizeof(int) * npts, true);
         jobs.j[jobs.n++] = TabJob{gk, qp, dp.gspan[d], dp.G[d], dp.mg[d] + pr->geo_p + 1, pr->geo_p, npts, dp.nug};
@@ -414,8 +467,6 @@ int prepare_problem(Call& c, const sg_problem* pr, DevProblem& dp) {
         dp.gspan[d] = nullptr;
         dp.hgspan[d].assign(1, 0);
     }
-    dp.hom = (double*)c.upload(pr->geo_hom, sizeof(double) * dp.Ng * (pr->n + 1));
-    dp.sol_w = dp.rational ? (double*)c.upload(pr->sol_w, sizeof(double) * dp.N) : nullptr;
     return 0;
 }
 
@@ -1254,6 +1305,11 @@ struct CopyPool {
 static CopyPool& copy_pool() {
     static CopyPool pool((int)std::max(2u, std::min(16u, std::thread::hardware_concurrency())));
     return pool;
+}
+static void pool_memcpy(void* dst, const void* src, size_t n) {
+    std::atomic<int> left(0);
+    copy_pool().submit((char*)dst, (const char*)src, n, &left, std::max<size_t>(64u << 10, (n + 7) / 8));
+    copy_pool().wait(&left);
 }
 
 constexpr int kRingMax = 16;

@@ -5,6 +5,7 @@
 
 #include <chrono>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/surriga_b200.h"
@@ -63,6 +64,8 @@ struct Call {
     void release(void* p);  // hand a temporary over to a result (no free at call end)
     void free_temp(void* p);  // free a temporary early (stream ordered)
     void* upload(const void* host, size_t bytes);
+    // several host inputs in one device allocation and one staged copy (device pointers in order)
+    std::vector<void*> upload_batch(const std::vector<std::pair<const void*, size_t>>& items);
     void kbegin(const char* name);
     void kend();
     int finish();
