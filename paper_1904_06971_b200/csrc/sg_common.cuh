@@ -15,7 +15,9 @@ namespace sg {
 // one fp64 tensor-core MMA (m8n8k4, row.col): {c0, c1} += A(lane) x B(lane); bitwise a sequential FMA
 // chain over its K (profiles/fp64_peak.txt)
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+    // not volatile: the MMA's only effects are its outputs, so the compiler may schedule the shared
+    // loads of later operands ahead of it (hides the LDS latency of the operand chains)
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c0), "+d"(c1)
                  : "d"(a), "d"(b));
 }

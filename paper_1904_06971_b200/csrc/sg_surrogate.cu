@@ -1263,6 +1263,9 @@ struct sg_surrogate_state {
     double* bufA = nullptr;
     double* bufB = nullptr;
     int64_t cpad = 0;
+    const double* d_ci[3] = {nullptr, nullptr, nullptr};  // inverse collocation matrices (device)
+    const double* d_kn[3] = {nullptr, nullptr, nullptr};  // averaged knots
+    const double* d_bp[3] = {nullptr, nullptr, nullptr};  // in-box midpoints
     explicit sg_surrogate_state(const sg_exec* ex) : c(ex) {}
 };
 
@@ -1332,8 +1335,6 @@ static int surr_begin(sg_surrogate_state& S, const sg_problem* prob, const sg_su
             s.qd[d] = 0;
         }
         S.nlat_tot *= s.nl[d];
-        s.inb[d] = (const uint8_t*)c.upload(inb[d].data(), inb[d].size());
-        s.smp[d] = (const uint8_t*)c.upload(smp[d].data(), smp[d].size());
     }
     // offsets [-p,p]^n colex (surrogate.py:103-122)
     std::vector<int> shifts(P * 3, 0);
@@ -1344,7 +1345,47 @@ static int surr_begin(sg_surrogate_state& S, const sg_problem* prob, const sg_su
             r /= 2 * p + 1;
         }
     }
-    s.shifts = (const int*)c.upload(shifts.data(), sizeof(int) * shifts.size());
+    // lattice rows (colex over the lattice)
+    S.latrows.resize(S.nlat_tot);
+    for (int64_t t = 0; t < S.nlat_tot; ++t) {
+        int64_t r = t, idx[3] = {0, 0, 0};
+        for (int d = 0; d < n; ++d) {
+            idx[d] = sp->lat_idx[d][r % s.nl[d]];
+            r /= s.nl[d];
+        }
+        S.latrows[t] = idx[0] + dp.m[0] * (idx[1] + (int64_t)dp.m[1] * idx[2]);
+    }
+    // every host input of the call in one staged copy: masks, offsets, lattice rows, and the fit's
+    // per-direction tables (used by finish)
+    {
+        std::vector<std::pair<const void*, size_t>> ups;
+        for (int d = 0; d < 3; ++d) {
+            ups.push_back({inb[d].data(), inb[d].size()});
+            ups.push_back({smp[d].data(), smp[d].size()});
+        }
+        ups.push_back({shifts.data(), sizeof(int) * shifts.size()});
+        ups.push_back({S.latrows.data(), sizeof(int64_t) * S.nlat_tot});
+        for (int d = 0; d < n; ++d) {
+            const bool fit = s.qd[d] >= 1;
+            ups.push_back({fit ? sp->colloc_inv[d] : nullptr, fit ? sizeof(double) * s.nl[d] * s.nl[d] : 8});
+            ups.push_back({fit ? sp->interp_knots[d] : nullptr, fit ? sizeof(double) * (s.nl[d] + s.qd[d] + 1) : 8});
+            ups.push_back({fit ? sp->box_pts[d] : nullptr, fit ? sizeof(double) * s.bn[d] : 8});
+        }
+        const std::vector<void*> dv = c.upload_batch(ups);
+        for (void* v : dv)
+            if (!v) return fail(-4, "device allocation failed");
+        for (int d = 0; d < 3; ++d) {
+            s.inb[d] = (const uint8_t*)dv[2 * d];
+            s.smp[d] = (const uint8_t*)dv[2 * d + 1];
+        }
+        s.shifts = (const int*)dv[6];
+        S.dlat = (int64_t*)dv[7];
+        for (int d = 0; d < n; ++d) {
+            S.d_ci[d] = (const double*)dv[8 + 3 * d];
+            S.d_kn[d] = (const double*)dv[9 + 3 * d];
+            S.d_bp[d] = (const double*)dv[10 + 3 * d];
+        }
+    }
 
     // analytic pattern; work arrays hold the entries of rows [qlo, qhi) only (the slab, its halo):
     // kernels index them with global row starts through base pointers shifted by nnz(qlo)
@@ -1438,17 +1479,7 @@ static int surr_begin(sg_surrogate_state& S, const sg_problem* prob, const sg_su
     rc = run_assembly(c, dp, pl, &tiles, quadmask, S.rowstart, s.qlo, s.qhi, s.indices, s.data, S.counters + 4);
     if (rc) return rc;
 
-    // ---- lattice rows (colex over the lattice) and the sample table S[o][lattice colex]
-    S.latrows.resize(S.nlat_tot);
-    for (int64_t t = 0; t < S.nlat_tot; ++t) {
-        int64_t r = t, idx[3] = {0, 0, 0};
-        for (int d = 0; d < n; ++d) {
-            idx[d] = sp->lat_idx[d][r % s.nl[d]];
-            r /= s.nl[d];
-        }
-        S.latrows[t] = idx[0] + dp.m[0] * (idx[1] + (int64_t)dp.m[1] * idx[2]);
-    }
-    S.dlat = (int64_t*)c.upload(S.latrows.data(), sizeof(int64_t) * S.nlat_tot);
+    // ---- the sample table S[o][lattice colex]
     // a zeroed tail of one lattice plane + row behind the coefficients: the row-staged K7 kernel
     // reads whole 5-wide windows without clamping (the taps past the last site have weight 0)
     S.cpad = (int64_t)s.nl[0] * s.nl[1] + s.nl[0] + 16;
@@ -1503,7 +1534,7 @@ static int surr_finish(sg_surrogate_state& S, const sg_surrogate_params* sp, sg_
         const int len = s.nl[d];
         const int64_t outer = (int64_t)P * nlat_tot / (len * inner);
         if (s.qd[d] >= 1) {
-            double* ci = (double*)c.upload(sp->colloc_inv[d], sizeof(double) * len * len);
+            const double* ci = S.d_ci[d];
             c.kbegin("coef_solve");
             apply_dir_kernel<<<nblk(P * nlat_tot, 256), 256, 0, c.stream>>>(cur, nxt, ci, outer, len, inner);
             c.kend();
@@ -1520,8 +1551,8 @@ static int surr_finish(sg_surrogate_state& S, const sg_surrogate_params* sp, sg_
         double* et = (double*)c.alloc(sizeof(double) * s.bn[d] * (s.qd[d] + 1), true);
         if (d < n && s.qd[d] >= 1) {
             const int nk = s.nl[d] + s.qd[d] + 1;
-            double* kn = (double*)c.upload(sp->interp_knots[d], sizeof(double) * nk);
-            double* bp = (double*)c.upload(sp->box_pts[d], sizeof(double) * s.bn[d]);
+            const double* kn = S.d_kn[d];
+            const double* bp = S.d_bp[d];
             tabulate(c, kn, nk, s.qd[d], bp, s.bn[d], 0, esp, et);
         } else {
             c.kbegin("const_table");
