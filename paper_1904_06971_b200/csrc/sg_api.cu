@@ -245,12 +245,27 @@ __global__ void tabulate_kernel(const double* __restrict__ knots, int nk, int p,
 
 // several tabulations in one launch (blockIdx.y = job): the per-direction solution and geometry
 // tables of a call are tiny, so their launch overhead dominated the call's prologue
+// Are the knots uniform and every element's Gauss points the same affine image of one reference set
+// (to 1e-13 of the span width)?  Only then do interior elements share their basis values.
+static bool uniform_points(const double* kn, int p, int S, const double* x, int g) {
+    const double h = (kn[p + S] - kn[p]) / S;
+    if (!(h > 0.0)) return false;
+    const double tol = 1e-13 * h;
+    for (int e = 0; e <= S; ++e)
+        if (std::fabs(kn[p + e] - (kn[p] + e * h)) > tol) return false;
+    for (int e = 0; e < S; ++e)
+        for (int q = 0; q < g; ++q)
+            if (std::fabs((x[e * g + q] - kn[p + e]) - (x[q] - kn[p])) > tol) return false;
+    return true;
+}
+
 struct TabJob {
     const double* knots;
     const double* pts;
     int* span;
     double* tab;
     int nk, p, npts, nu;
+    int g, canon;  // canon: points of interior elements take the first interior element's values
 };
 struct TabJobs {
     TabJob j[6];
@@ -262,7 +277,14 @@ __global__ void tabulate_multi_kernel(TabJobs jobs) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= J.npts) return;
     double ders[(SG_MAX_PG + 1) * 3];
-    const int span = basis_ders(J.knots, J.nk, J.p, J.pts[i], J.nu, ders);
+    // uniform open knots: on an interior element (every nonzero function interior, e in [p, S-1-p])
+    // the basis values at the q-th Gauss point are the same numbers on every such element; they are
+    // taken from element p, so all interior elements carry bitwise identical tables (and tiles whose
+    // windows are interior share their fragments, sg_tile_mma.cuh 2D runs)
+    const int S = J.npts / J.g, e = i / J.g;
+    const bool canon = J.canon && e > J.p && e <= S - 1 - J.p;
+    int span = basis_ders(J.knots, J.nk, J.p, J.pts[canon ? J.p * J.g + i % J.g : i], J.nu, ders);
+    if (canon) span += e - J.p;
     if (J.span) J.span[i] = span;
     const int w = (J.nu + 1) * (J.p + 1);
     for (int k = 0; k < w; ++k) J.tab[(long long)i * w + k] = ders[k];
@@ -446,11 +468,12 @@ int prepare_problem(Call& c, const sg_problem* pr, DevProblem& dp) {
         dp.qw[d] = (double*)dv[4 * d + 2];
         dp.B[d] = (double*)c.alloc(sizeof(double) * npts * (dp.nu + 1) * (dp.p + 1), true);
         dp.bspan[d] = (int*)c.alloc(sizeof(int) * npts, true);
-        jobs.j[jobs.n++] = TabJob{kn, qp, dp.bspan[d], dp.B[d], dp.m[d] + dp.p + 1, dp.p, npts, dp.nu};
+        jobs.j[jobs.n++] = TabJob{kn, qp, dp.bspan[d], dp.B[d], dp.m[d] + dp.p + 1, dp.p, npts, dp.nu, dp.g,
+                                  uniform_points(pr->knots[d], dp.p, dp.S[d], pr->qpts[d], dp.g) ? 1 : 0};
         double* gk = (double*)dv[4 * d + 3];
         dp.G[d] = (double*)c.alloc(sizeof(double) * npts * (dp.nug + 1) * (pr->geo_p + 1), true);
         dp.gspan[d] = (int*)c.alloc(sizeof(int) * npts, true);
-        jobs.j[jobs.n++] = TabJob{gk, qp, dp.gspan[d], dp.G[d], dp.mg[d] + pr->geo_p + 1, pr->geo_p, npts, dp.nug};
+        jobs.j[jobs.n++] = TabJob{gk, qp, dp.gspan[d], dp.G[d], dp.mg[d] + pr->geo_p + 1, pr->geo_p, npts, dp.nug, dp.g, 0};
         // host copies of geometry spans for the smem bound
         std::vector<double> hk(pr->geo_knots[d], pr->geo_knots[d] + dp.mg[d] + pr->geo_p + 1);
         dp.hgspan[d].resize(npts);

@@ -955,6 +955,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
         phase1(Ds, T1s);
     } else if constexpr (NDIM == 2) {
         int colx = tc0;
+        int ew0_prev = ew0, ew1_prev = ew1;  // windows whose fragments are in shared memory
         for (int t = t_first; t < t_end; ++t) {
             const int k = t - t_first;
             if (k > 0) {
@@ -966,14 +967,24 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
                 b1 = tc1 * T1;
                 ew0 = b0 - P;
                 ew1 = b1 - P;
-                const bool newx = tc0 != colx;
+                // windows made of interior elements carry identical tables (K2 canonicalises them),
+                // so their fragments are reused as they are
+                auto interior = [&](int ew, int nel, int S) { return ew > P && ew + nel - 1 <= S - 1 - P; };
+                const bool xin = interior(ew0, T0 + P, prm.S[0]) && interior(ew0_prev, T0 + P, prm.S[0]);
+                const bool yin = interior(ew1, T1 + P, prm.S[1]) && interior(ew1_prev, T1 + P, prm.S[1]);
+                const bool newx = tc0 != colx && !xin;
+                const bool newy = !yin;
                 colx = tc0;
-                if (newx) load_x();
-                load_y();
-                __syncthreads();
-                if (newx) frag_x();
-                frag_y();
-                __syncthreads();
+                ew0_prev = ew0;
+                ew1_prev = ew1;
+                if (newx || newy) {
+                    if (newx) load_x();
+                    if (newy) load_y();
+                    __syncthreads();
+                    if (newx) frag_x();
+                    if (newy) frag_y();
+                    __syncthreads();
+                }
             }
             const double* Ds;
             if (use_tma) {
