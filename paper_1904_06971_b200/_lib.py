@@ -313,10 +313,13 @@ def last_dmma_count():
     return c.value
 
 
-def last_kernel_times():
+def last_kernel_times(copies: bool = False):
+    """(name, device ms) of each kernel of the last call; ``copies`` adds the timed host->device
+    staging copies ("h2d_*")."""
     names = C.create_string_buffer(4096)
     ms = (C.c_double * 64)()
     cnt = C.c_int32()
     lib().sg_last_kernel_times(names, 4096, ms, 64, C.byref(cnt))
     nm = names.value.decode().split(",") if cnt.value else []
-    return list(zip(nm, [ms[i] for i in range(min(cnt.value, 64))]))
+    out = list(zip(nm, [ms[i] for i in range(min(cnt.value, 64))]))
+    return out if copies else [(n, t) for n, t in out if not n.startswith("h2d_")]

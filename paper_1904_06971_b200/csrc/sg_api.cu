@@ -4,6 +4,7 @@
 #include <cub/cub.cuh>
 
 #include <sys/mman.h>
+#include <sched.h>
 
 #include <algorithm>
 #include <atomic>
@@ -52,6 +53,8 @@ int fail(int code, const char* fmt, ...) {
 // idle per call at config 5).  The arena is rewound when the last live Call of the thread has been
 // destroyed (every Call synchronises its stream before it dies, so no staged copy is pending).
 static void pool_memcpy(void* dst, const void* src, size_t n);  // parallel host memcpy (copy pool)
+static void copy_pool_run(std::vector<std::function<void()>>& fns, std::atomic<int>* left);
+static void copy_pool_wait(std::atomic<int>* left);
 
 struct PinnedArena {
     char* base = nullptr;
@@ -90,6 +93,7 @@ Call::Call(const sg_exec* ex) {
 }
 
 Call::~Call() {
+    flush_uploads();  // the pool must be done with the staging arena before it is reused
     for (void* p : temps)
         if (p) cudaFreeAsync(p, stream);
     for (auto& k : kev) {
@@ -136,7 +140,7 @@ void* Call::upload(const void* host, size_t bytes) {
     const size_t need = (bytes + 255) & ~size_t(255);
     if (g_arena.base && g_arena.off + need <= g_arena.cap) {
         char* h = g_arena.base + g_arena.off;
-        memcpy(h, host, bytes);
+        stream_copy(h, host, bytes);
         g_arena.off += need;
         cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, stream);
     } else {
@@ -145,9 +149,10 @@ void* Call::upload(const void* host, size_t bytes) {
     return d;
 }
 
-std::vector<void*> Call::upload_batch(const std::vector<std::pair<const void*, size_t>>& items) {
+std::vector<void*> Call::upload_batch(const std::vector<std::pair<const void*, size_t>>& items, bool defer) {
     // one device allocation, one pinned staging block, one copy: per-upload API overhead (allocation,
     // memcpy call, copy launch) was ~5-10 us each; large items are packed by the host copy pool
+    hmark("upload_batch:start");
     std::vector<void*> out(items.size(), nullptr);
     size_t total = 0;
     std::vector<size_t> off(items.size());
@@ -168,19 +173,69 @@ std::vector<void*> Call::upload_batch(const std::vector<std::pair<const void*, s
     if (!d) return out;
     char* h = g_arena.base + g_arena.off;
     g_arena.off += total;
-    std::vector<std::pair<size_t, size_t>> big;
+    std::vector<size_t> big;
     for (size_t k = 0; k < items.size(); ++k) {
         out[k] = d + off[k];
         if (!items[k].first || !items[k].second) continue;
-        if (items[k].second >= (256u << 10)) big.push_back({k, items[k].second});
-        else memcpy(h + off[k], items[k].first, items[k].second);
+        if (items[k].second >= (256u << 10)) big.push_back(k);
+        else stream_copy(h + off[k], items[k].first, items[k].second);
     }
-    for (auto& b : big) pool_memcpy(h + off[b.first], items[b.first].first, b.second);
+    if (defer && !big.empty()) {
+        // small items now (the runs between large ones), large ones packed in the background
+        flush_uploads();
+        std::vector<std::function<void()>> fns;
+        for (size_t k : big) {
+            const size_t n = items[k].second, piece = std::max<size_t>(512u << 10, (n + 3) / 4);
+            for (size_t lo = 0; lo < n; lo += piece) {
+                const size_t len = std::min(piece, n - lo);
+                char* dst = h + off[k] + lo;
+                const char* src = (const char*)items[k].first + lo;
+                fns.push_back([=] { stream_copy(dst, src, len); });
+            }
+            pending.push_back({d + off[k], h + off[k], n});
+        }
+        pending_left = new std::atomic<int>(0);
+        copy_pool_run(fns, pending_left);
+        kbegin("h2d_inputs", false);
+        size_t lo = 0;
+        for (size_t k : big) {
+            if (off[k] > lo) cudaMemcpyAsync(d + lo, h + lo, off[k] - lo, cudaMemcpyHostToDevice, stream);
+            lo = off[k] + ((items[k].second + 255) & ~size_t(255));
+        }
+        if (total > lo) cudaMemcpyAsync(d + lo, h + lo, total - lo, cudaMemcpyHostToDevice, stream);
+        kend();
+        hmark("upload_batch:small issued");
+        return out;
+    }
+    for (size_t k : big) pool_memcpy(h + off[k], items[k].first, items[k].second);
+    hmark("upload_batch:packed");
+    kbegin("h2d_inputs", false);
     cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, stream);
+    kend();
     return out;
 }
 
-void Call::kbegin(const char* name) {
+void Call::flush_uploads() {
+    if (!pending_left) return;
+    hmark("flush_uploads:enter");
+    copy_pool_wait(pending_left);
+    hmark("flush_uploads:packed");
+    delete pending_left;
+    pending_left = nullptr;
+    KEv k;
+    k.name = "h2d_deferred";
+    k.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
+    cudaEventCreate(&k.a);
+    cudaEventCreate(&k.b);
+    cudaEventRecord(k.a, stream);
+    for (auto& p : pending) cudaMemcpyAsync(p.d, p.h, p.bytes, cudaMemcpyHostToDevice, stream);
+    cudaEventRecord(k.b, stream);
+    kev.push_back(k);
+    pending.clear();
+}
+
+void Call::kbegin(const char* name, bool kernel) {
+    if (pending_left && kernel && strcmp(name, "tabulate") != 0 && strcmp(name, "indptr_full") != 0) flush_uploads();
     KEv k;
     k.name = name;
     k.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
@@ -188,7 +243,7 @@ void Call::kbegin(const char* name) {
     cudaEventCreate(&k.b);
     cudaEventRecord(k.a, stream);
     kev.push_back(k);
-    launches++;
+    if (kernel) launches++;
 }
 void Call::hmark(const char* what) {
     static const bool on = getenv("SG_TRACE") != nullptr;
@@ -197,6 +252,7 @@ void Call::hmark(const char* what) {
 void Call::kend() { cudaEventRecord(kev.back().b, stream); }
 
 int Call::finish() {
+    flush_uploads();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(-3, "CUDA launch error: %s", cudaGetErrorString(e));
     cudaEventRecord(ev1, stream);
@@ -243,8 +299,6 @@ __global__ void tabulate_kernel(const double* __restrict__ knots, int nk, int p,
     for (int k = 0; k < w; ++k) tab_out[(long long)i * w + k] = ders[k];
 }
 
-// several tabulations in one launch (blockIdx.y = job): the per-direction solution and geometry
-// tables of a call are tiny, so their launch overhead dominated the call's prologue
 // Are the knots uniform and every element's Gauss points the same affine image of one reference set
 // (to 1e-13 of the span width)?  Only then do interior elements share their basis values.
 static bool uniform_points(const double* kn, int p, int S, const double* x, int g) {
@@ -259,6 +313,8 @@ static bool uniform_points(const double* kn, int p, int S, const double* x, int 
     return true;
 }
 
+// several tabulations in one launch (blockIdx.y = job): the per-direction solution and geometry
+// tables of a call are tiny, so their launch overhead dominated the call's prologue
 struct TabJob {
     const double* knots;
     const double* pts;
@@ -455,24 +511,37 @@ int prepare_problem(Call& c, const sg_problem* pr, DevProblem& dp) {
     }
     ups.push_back({pr->geo_hom, sizeof(double) * dp.Ng * (pr->n + 1)});
     if (dp.rational) ups.push_back({pr->sol_w, sizeof(double) * dp.N});
-    const std::vector<void*> dv = c.upload_batch(ups);
+    const std::vector<void*> dv = c.upload_batch(ups, true);
     for (void* v : dv)
         if (!v) return fail(-4, "device allocation failed");
     dp.hom = (double*)dv[4 * pr->n];
     dp.sol_w = dp.rational ? (double*)dv[4 * pr->n + 1] : nullptr;
+    // the 4n tables in one allocation (cudaMallocAsync is ~5 us per call on the host)
+    size_t tab_bytes = 0;
+    auto carve = [&](size_t b) { const size_t o = tab_bytes; tab_bytes += (b + 255) & ~size_t(255); return o; };
+    size_t o_tab[3][4];
+    for (int d = 0; d < pr->n; ++d) {
+        const size_t npts = (size_t)dp.S[d] * dp.g;
+        o_tab[d][0] = carve(sizeof(double) * npts * (dp.nu + 1) * (dp.p + 1));
+        o_tab[d][1] = carve(sizeof(int) * npts);
+        o_tab[d][2] = carve(sizeof(double) * npts * (dp.nug + 1) * (pr->geo_p + 1));
+        o_tab[d][3] = carve(sizeof(int) * npts);
+    }
+    char* tabs = (char*)c.alloc(tab_bytes, true);
+    if (!tabs) return fail(-4, "device allocation failed");
     for (int d = 0; d < pr->n; ++d) {
         const int npts = dp.S[d] * dp.g;
         maxpts = std::max(maxpts, npts);
         double* kn = (double*)dv[4 * d];
         double* qp = (double*)dv[4 * d + 1];
         dp.qw[d] = (double*)dv[4 * d + 2];
-        dp.B[d] = (double*)c.alloc(sizeof(double) * npts * (dp.nu + 1) * (dp.p + 1), true);
-        dp.bspan[d] = (int*)c.alloc(sizeof(int) * npts, true);
+        dp.B[d] = (double*)(tabs + o_tab[d][0]);
+        dp.bspan[d] = (int*)(tabs + o_tab[d][1]);
         jobs.j[jobs.n++] = TabJob{kn, qp, dp.bspan[d], dp.B[d], dp.m[d] + dp.p + 1, dp.p, npts, dp.nu, dp.g,
                                   uniform_points(pr->knots[d], dp.p, dp.S[d], pr->qpts[d], dp.g) ? 1 : 0};
         double* gk = (double*)dv[4 * d + 3];
-        dp.G[d] = (double*)c.alloc(sizeof(double) * npts * (dp.nug + 1) * (pr->geo_p + 1), true);
-        dp.gspan[d] = (int*)c.alloc(sizeof(int) * npts, true);
+        dp.G[d] = (double*)(tabs + o_tab[d][2]);
+        dp.gspan[d] = (int*)(tabs + o_tab[d][3]);
         jobs.j[jobs.n++] = TabJob{gk, qp, dp.gspan[d], dp.G[d], dp.mg[d] + pr->geo_p + 1, pr->geo_p, npts, dp.nug, dp.g, 0};
         // host copies of geometry spans for the smem bound
         std::vector<double> hk(pr->geo_knots[d], pr->geo_knots[d] + dp.mg[d] + pr->geo_p + 1);
@@ -480,6 +549,7 @@ int prepare_problem(Call& c, const sg_problem* pr, DevProblem& dp) {
         for (int i = 0; i < npts; ++i)
             dp.hgspan[d][i] = find_span(hk.data(), (int)hk.size(), pr->geo_p, pr->qpts[d][i]);
     }
+    c.hmark("prepare:tables allocated");
     c.kbegin("tabulate");
     tabulate_multi_kernel<<<dim3((maxpts + 127) / 128, jobs.n), 128, 0, c.stream>>>(jobs);
     c.kend();
@@ -1310,7 +1380,13 @@ struct CopyPool {
                 q.push_back({dst + lo, src + lo, len, left});
             }
         }
-        cv.notify_all();
+        wake(np);
+    }
+    void wake(int tasks) {
+        // as many workers as tasks: waking all 16 for a 4-piece copy cost more than the copy (VM hosts)
+        if (tasks >= (int)th.size()) cv.notify_all();
+        else
+            for (int t = 0; t < tasks; ++t) cv.notify_one();
     }
     void run(std::vector<std::function<void()>>& fns, std::atomic<int>* left) {
         left->store((int)fns.size());
@@ -1318,21 +1394,45 @@ struct CopyPool {
             std::lock_guard<std::mutex> lk(mu);
             for (auto& f : fns) q.push_back({nullptr, nullptr, 0, left, f});
         }
-        cv.notify_all();
+        wake((int)fns.size());
     }
-    void wait(std::atomic<int>* left) {
+    void wait(std::atomic<int>* left, bool help = false) {
+        // help: the waiting thread runs queued tasks itself (workers parked on an idle VM vCPU can take
+        // ~100 us to wake); not in the D2H ring, whose thread must stay free to issue the next chunk
         std::unique_lock<std::mutex> lk(mu);
-        done_cv.wait(lk, [&] { return left->load() == 0; });
+        while (left->load() != 0) {
+            if (help && !q.empty()) {
+                Task tk = q.front();
+                q.pop_front();
+                lk.unlock();
+                if (tk.fn) tk.fn();
+                else memcpy(tk.dst, tk.src, tk.len);
+                lk.lock();
+                if (tk.left->fetch_sub(1) == 1) done_cv.notify_all();
+                continue;
+            }
+            done_cv.wait(lk);
+        }
     }
 };
 static CopyPool& copy_pool() {
     static CopyPool pool((int)std::max(2u, std::min(16u, std::thread::hardware_concurrency())));
     return pool;
 }
+static void copy_pool_run(std::vector<std::function<void()>>& fns, std::atomic<int>* left) { copy_pool().run(fns, left); }
+static void copy_pool_wait(std::atomic<int>* left) { copy_pool().wait(left, true); }
+
 static void pool_memcpy(void* dst, const void* src, size_t n) {
+    // packs pinned staging for an upload: streaming stores (stream_copy, sg_hostcols.cpp)
+    const size_t piece = std::max<size_t>(512u << 10, (n + 3) / 4);
+    std::vector<std::function<void()>> fns;
+    for (size_t lo = 0; lo < n; lo += piece) {
+        const size_t len = std::min(piece, n - lo);
+        fns.push_back([=] { stream_copy((char*)dst + lo, (const char*)src + lo, len); });
+    }
     std::atomic<int> left(0);
-    copy_pool().submit((char*)dst, (const char*)src, n, &left, std::max<size_t>(64u << 10, (n + 7) / 8));
-    copy_pool().wait(&left);
+    copy_pool().run(fns, &left);
+    copy_pool().wait(&left, true);
 }
 
 constexpr int kRingMax = 16;

@@ -6,6 +6,7 @@
 #include <chrono>
 #include <string>
 #include <utility>
+#include <atomic>
 #include <vector>
 
 #include "../../include/surriga_b200.h"
@@ -65,8 +66,14 @@ struct Call {
     void free_temp(void* p);  // free a temporary early (stream ordered)
     void* upload(const void* host, size_t bytes);
     // several host inputs in one device allocation and one staged copy (device pointers in order)
-    std::vector<void*> upload_batch(const std::vector<std::pair<const void*, size_t>>& items);
-    void kbegin(const char* name);
+    // defer: items >= 256 KB are packed by the copy pool while the host goes on; their copies are
+    // issued by flush_uploads(), which kbegin() calls before any kernel except tabulate / indptr_full
+    std::vector<void*> upload_batch(const std::vector<std::pair<const void*, size_t>>& items, bool defer = false);
+    struct Pending { void* d; const void* h; size_t bytes; };
+    std::vector<Pending> pending;
+    std::atomic<int>* pending_left = nullptr;
+    void flush_uploads();
+    void kbegin(const char* name, bool kernel = true);  // kernel=false: a copy (timed, not counted)
     void kend();
     int finish();
     void record_timing();
@@ -125,6 +132,7 @@ __global__ void rebase_kernel(int64_t* a, int64_t n, int64_t sub);
 
 // host: closed-form columns of full-pattern rows [r0, r1) of a result starting at global row row_lo
 // (sg_hostcols.cpp; AVX2 + non-temporal stores when the CPU has them)
+void stream_copy(void* dst, const void* src, size_t n);  // non-temporal stores (staging for DMA)
 void gen_columns_avx2(int64_t r0, int64_t r1, int64_t row_lo, const int64_t* m, int p, int32_t* out);
 void gen_columns_base(int64_t r0, int64_t r1, int64_t row_lo, const int64_t* m, int p, int32_t* out);
 inline void gen_columns(int64_t r0, int64_t r1, int64_t row_lo, const int64_t* m, int p, int32_t* out) {
