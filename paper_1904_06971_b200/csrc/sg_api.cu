@@ -36,6 +36,11 @@ static thread_local double g_last_ms = 0.0;
 static thread_local int g_last_launches = 0;
 static thread_local std::vector<std::pair<std::string, double>> g_ktimes;
 static thread_local unsigned long long g_last_dmma = 0;
+#ifdef SG_K4_PROF
+constexpr int kProfN = 2 + 32 * 8;  // DMMA count, per-warp clock sums, CTA count
+#else
+constexpr int kProfN = 1;
+#endif
 
 int fail(int code, const char* fmt, ...) {
     char buf[1024];
@@ -266,6 +271,22 @@ void Call::record_timing() {
     g_last_launches = launches;
     g_last_dmma = 0;
     if (dmma) cudaMemcpy(&g_last_dmma, dmma, sizeof(g_last_dmma), cudaMemcpyDeviceToHost);
+#ifdef SG_K4_PROF
+    if (dmma) {
+        // per-warp clock64 sums of the warp-specialised K4 loop (experimental build), cycles per CTA
+        std::vector<unsigned long long> pf(kProfN);
+        cudaMemcpy(pf.data(), dmma, sizeof(unsigned long long) * kProfN, cudaMemcpyDeviceToHost);
+        const double nct = std::max(1ull, pf[1 + 32 * 8]);
+        fprintf(stderr, "[k4 prof] CTAs %.0f; per warp, kcycles per CTA: A = plane-wait p1 p2 ring-wait bar loop | B = ready-wait bar p3 b3frag bar loop\n", nct);
+        for (int w = 0; w < 32; ++w) {
+            const unsigned long long* q = pf.data() + 1 + w * 8;
+            if (!q[5]) continue;
+            fprintf(stderr, "[k4 prof] warp %2d:", w);
+            for (int k = 0; k < 6; ++k) fprintf(stderr, " %8.1f", q[k] / nct / 1e3);
+            fprintf(stderr, "\n");
+        }
+    }
+#endif
     g_ktimes.clear();
     for (auto& k : kev) {
         float t = 0.f;
@@ -972,8 +993,8 @@ int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>
         mp.z0 = pl.z0;
         mp.dbg = env_int("SG_K4_DBG", 0);
         if (!c.dmma) {
-            c.dmma = (unsigned long long*)c.alloc(sizeof(unsigned long long), true);
-            if (c.dmma) cudaMemsetAsync(c.dmma, 0, sizeof(unsigned long long), c.stream);
+            c.dmma = (unsigned long long*)c.alloc(sizeof(unsigned long long) * kProfN, true);
+            if (c.dmma) cudaMemsetAsync(c.dmma, 0, sizeof(unsigned long long) * kProfN, c.stream);
         }
         mp.dmma = c.dmma;
         int64_t nb = pl.ntiles;

@@ -130,6 +130,17 @@ __host__ __device__ constexpr int pad8_4(int v) {  // smallest w >= v with w % 8
 #ifndef SG_CH_POIS
 #define SG_CH_POIS 1
 #endif
+// unit descriptors of the phase 1-3 items as compile-time constants (static_for over the groups)
+#ifndef SG_STATIC_UNITS
+#define SG_STATIC_UNITS 1
+#endif
+// non-pair units of a phase-2 / phase-3 item in two interleaved DMMA chains (see phase2)
+#ifndef SG_P2_ILP
+#define SG_P2_ILP 0
+#endif
+#ifndef SG_P3_ILP
+#define SG_P3_ILP 0
+#endif
 #ifndef SG_P12_EPI
 #define SG_P12_EPI 0
 #endif
@@ -674,6 +685,10 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
         const int z = elo2 * G + pi;
         const uint32_t bar = bar0 + 8u * (uint32_t)(pi & 1);
         const uint32_t dst = (uint32_t)__cvta_generic_to_shared(Dbuf(pi & 1));
+        if (prm.dbg & 16) {  // timing experiment: no D traffic (the phase completes at once)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+            return;
+        }
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(DBYTES) : "memory");
         asm volatile(
@@ -763,10 +778,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
             for (int a = 0; a < MT; ++a)
 #pragma unroll
                 for (int c = 0; c < NTI; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
-            const int ue = tab[TAB::S.o_u1b + Gc + 1];
-            ndmma += (unsigned long long)(ue - tab[TAB::S.o_u1b + Gc]) * KS * NTI * MT;
-            for (int unit = tab[TAB::S.o_u1b + Gc]; unit < ue; ++unit) {
-                const int ud = tab[TAB::S.o_u1ud + unit];
+            auto unit1 = [&](const int unit, const int ud) {
                 const double* af = A1f + ((i0l * M.NU1 + unit) * KS) * MT * 32 + lane;
                 const double* dpl = Ds + (ud * XWp) * DY + lr + cc * NTI * 8;
 #pragma unroll
@@ -784,7 +796,25 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
                         for (int a = 0; a < MT; ++a) dmma(acc[a][c][0], acc[a][c][1], afr[a], bf);
                     }
                 }
-            }
+                        };
+#if SG_STATIC_UNITS
+            // the group's units and D components are compile-time constants (no table reads per unit)
+            static_for<0, M.NG1>([&](auto GI) {
+                constexpr int g = decltype(GI)::value;
+                if (Gc != g) return;
+                constexpr int ub = TAB::S.v[TAB::S.o_u1b + g], ue = TAB::S.v[TAB::S.o_u1b + g + 1];
+                ndmma += (unsigned long long)(ue - ub) * KS * NTI * MT;
+                static_for<ub, ue>([&](auto UI) {
+                    constexpr int unit = decltype(UI)::value;
+                    constexpr int ud = TAB::S.v[TAB::S.o_u1ud + unit];
+                    unit1(unit, ud);
+                });
+            });
+#else
+            const int ue = tab[TAB::S.o_u1b + Gc + 1];
+            ndmma += (unsigned long long)(ue - tab[TAB::S.o_u1b + Gc]) * KS * NTI * MT;
+            for (int unit = tab[TAB::S.o_u1b + Gc]; unit < ue; ++unit) unit1(unit, tab[TAB::S.o_u1ud + unit]);
+#endif
             if constexpr (NDIM == 1) {
                 const int i0 = b0 + i0l;
                 if (lk == 0 && i0 < prm.m[0]) {
@@ -882,8 +912,39 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
                     for (int c = 0; c < MT; ++c) accS[a][c][0] = accS[a][c][1] = 0.0;
                 const int ue = tab[TAB::S.o_u2b + Gc + 1];
                 ndmma += (unsigned long long)(ue - tab[TAB::S.o_u2b + Gc]) * KS * MT * MT;  // + one more per pair below
-                for (int u = tab[TAB::S.o_u2b + Gc]; u < ue; ++u) {
-                    const int d = tab[TAB::S.o_u2 + u];
+                [[maybe_unused]] int u = tab[TAB::S.o_u2b + Gc];
+#if SG_P2_ILP
+                {
+                    // non-pair units (listed first) in two interleaved chains, even / odd units, added at
+                    // the end: half the dependent DMMA depth.  Every unit is its own transpose, so the
+                    // transposed entry evaluates the same sums in the same order (bitwise symmetry holds)
+                    double accO[MT][MT][2];
+                    bool odd = false;
+#pragma unroll
+                    for (int a = 0; a < MT; ++a)
+#pragma unroll
+                        for (int c = 0; c < MT; ++c) accO[a][c][0] = accO[a][c][1] = 0.0;
+                    for (; u + 1 < ue; u += 2) {
+                        const int d0 = tab[TAB::S.o_u2 + u], d1 = tab[TAB::S.o_u2 + u + 1];
+                        if ((d0 >> 24) || (d1 >> 24)) break;
+                        block2(d0 & 255, (d0 >> 16) & 15, d1 & 255, (d1 >> 16) & 15, accS, accO);
+                        odd = true;
+                    }
+                    if (u < ue && !(tab[TAB::S.o_u2 + u] >> 24)) {
+                        const int d = tab[TAB::S.o_u2 + u];
+                        block(d & 255, (d >> 16) & 15, accS);
+                        ++u;
+                    }
+                    if (odd)
+#pragma unroll
+                        for (int a = 0; a < MT; ++a)
+#pragma unroll
+                            for (int c = 0; c < MT; ++c)
+#pragma unroll
+                                for (int h = 0; h < 2; ++h) accS[a][c][h] = __dadd_rn(accS[a][c][h], accO[a][c][h]);
+                }
+#endif
+                auto unit2 = [&](const int d) {
                     const int ga = d & 255, kd = (d >> 16) & 15;
                     if (!(d >> 24)) {
                         block(ga, kd, accS);
@@ -902,7 +963,20 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
 #pragma unroll
                                 for (int h = 0; h < 2; ++h) accS[a][c][h] = __dadd_rn(accS[a][c][h], __dadd_rn(tA[a][c][h], tB[a][c][h]));
                     }
-                }
+                };
+#if SG_STATIC_UNITS && !SG_P2_ILP
+                static_for<0, (NDIM >= 2 ? TTS::T.NG2 : 0)>([&](auto GI) {
+                    constexpr int g = decltype(GI)::value;
+                    if (Gc != g) return;
+                    constexpr int ub = TAB::S.v[TAB::S.o_u2b + g], ue2 = TAB::S.v[TAB::S.o_u2b + g + 1];
+                    static_for<ub, ue2>([&](auto UI) {
+                        constexpr int d = TAB::S.v[TAB::S.o_u2 + decltype(UI)::value];
+                        unit2(d);
+                    });
+                });
+#else
+                for (; u < ue; ++u) unit2(tab[TAB::S.o_u2 + u]);
+#endif
                 if constexpr (NDIM == 2) {
                     const int64_t row = (int64_t)i0 + (int64_t)prm.m[0] * i1;
                     if (!(row >= prm.slab_lo && row < prm.slab_hi && (!prm.rowmask || prm.rowmask[row]))) continue;
@@ -1065,14 +1139,69 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
                         }
                     }
                 };
+                // two units' chains interleaved (independent accumulators)
+                auto block2 = [&](int ga, int kd, int gb, int kb, double (&accA)[CH][MT][2], double (&accB)[CH][MT][2]) {
+                    const double* bfa = B3b + (kd * KS3) * MT * 32 + lane;
+                    const double* bfb = B3b + (kb * KS3) * MT * 32 + lane;
+                    const double* t2a = T2s + ga * TC + ch * CH * 8 + lr;
+                    const double* t2bb = T2s + gb * TC + ch * CH * 8 + lr;
+#pragma unroll
+                    for (int kk = 0; kk < KS3; ++kk) {
+                        double fa[MT], fb[MT];
+#pragma unroll
+                        for (int c = 0; c < MT; ++c) {
+                            fa[c] = bfa[(kk * MT + c) * 32];
+                            fb[c] = bfb[(kk * MT + c) * 32];
+                        }
+                        const long zo = (long)zslot[kk] * M.NG2 * TC;
+#pragma unroll
+                        for (int mm = 0; mm < CH; ++mm) {
+                            const double va = t2a[zo + mm * 8], vb = t2bb[zo + mm * 8];
+#pragma unroll
+                            for (int c = 0; c < MT; ++c) {
+                                dmma(accA[mm][c][0], accA[mm][c][1], va, fa[c]);
+                                dmma(accB[mm][c][0], accB[mm][c][1], vb, fb[c]);
+                            }
+                        }
+                    }
+                };
                 double accS[CH][MT][2];
 #pragma unroll
                 for (int mm = 0; mm < CH; ++mm)
 #pragma unroll
                     for (int c = 0; c < MT; ++c) accS[mm][c][0] = accS[mm][c][1] = 0.0;
                 ndmma += (unsigned long long)(TTS::T.NF + f_npairs(TTS::T)) * KS3 * CH * MT;  // compile-time per item
-                for (int u = 0; u < TTS::T.NF; ++u) {
-                    const int d = tab[TAB::S.o_u3 + u];
+                [[maybe_unused]] int u = 0;
+#if SG_P3_ILP
+                {
+                    // non-pair units in two interleaved chains (as phase 2)
+                    double accO[CH][MT][2];
+                    bool odd = false;
+#pragma unroll
+                    for (int mm = 0; mm < CH; ++mm)
+#pragma unroll
+                        for (int c = 0; c < MT; ++c) accO[mm][c][0] = accO[mm][c][1] = 0.0;
+                    for (; u + 1 < TTS::T.NF; u += 2) {
+                        const int d0 = tab[TAB::S.o_u3 + u], d1 = tab[TAB::S.o_u3 + u + 1];
+                        if ((d0 >> 24) || (d1 >> 24)) break;
+                        block2(d0 & 255, (d0 >> 16) & 15, d1 & 255, (d1 >> 16) & 15, accS, accO);
+                        odd = true;
+                    }
+                    if (u < TTS::T.NF && !(tab[TAB::S.o_u3 + u] >> 24)) {
+                        const int d = tab[TAB::S.o_u3 + u];
+                        block(d & 255, (d >> 16) & 15, accS);
+                        ++u;
+                    }
+                    if (odd)
+#pragma unroll
+                        for (int mm = 0; mm < CH; ++mm)
+#pragma unroll
+                            for (int c = 0; c < MT; ++c)
+#pragma unroll
+                                for (int h = 0; h < 2; ++h) accS[mm][c][h] = __dadd_rn(accS[mm][c][h], accO[mm][c][h]);
+                }
+#endif
+                auto unit3 = [&](const int d) {
                     const int ga = d & 255, kd = (d >> 16) & 15;
                     if (!(d >> 24)) {
                         block(ga, kd, accS);
@@ -1082,8 +1211,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
                         for (int mm = 0; mm < CH; ++mm)
 #pragma unroll
                             for (int c = 0; c < MT; ++c) tA[mm][c][0] = tA[mm][c][1] = tB[mm][c][0] = tB[mm][c][1] = 0.0;
-                        block(ga, kd, tA);
-                        block((d >> 8) & 255, (d >> 20) & 15, tB);
+                        block2(ga, kd, (d >> 8) & 255, (d >> 20) & 15, tA, tB);
 #pragma unroll
                         for (int mm = 0; mm < CH; ++mm)
 #pragma unroll
@@ -1091,7 +1219,15 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
 #pragma unroll
                                 for (int h = 0; h < 2; ++h) accS[mm][c][h] = __dadd_rn(accS[mm][c][h], __dadd_rn(tA[mm][c][h], tB[mm][c][h]));
                     }
-                }
+                };
+#if SG_STATIC_UNITS && !SG_P3_ILP
+                static_for<0, TTS::T.NF>([&](auto UI) {
+                    constexpr int d = TAB::S.v[TAB::S.o_u3 + decltype(UI)::value];
+                    unit3(d);
+                });
+#else
+                for (; u < TTS::T.NF; ++u) unit3(tab[TAB::S.o_u3 + u]);
+#endif
                 if (prm.dbg & 2) {
                     nzero += accS[0][0][0] == 0.0 ? 1u : 0u;
                     continue;
@@ -1167,35 +1303,52 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
                 }
                 __threadfence_block();
             };
+#ifdef SG_K4_PROF
+            // clock64 breakdown per warp (experimental builds only): A: plane wait, phase 1, phase 2,
+            // ring wait, barrier, loop; B: ready wait, barrier, phase 3, fragments, barrier, loop
+            unsigned long long pf[6] = {0, 0, 0, 0, 0, 0};
+#define SG_PF(k, stmt) { const long long t_ = clock64(); stmt; pf[k] += clock64() - t_; }
+#else
+#define SG_PF(k, stmt) { stmt; }
+#endif
             if (warp < NAW) {
+                SG_PF(5,
                 for (int j = 0; j <= nplanes; ++j) {
-                    const double* Ds = j < nplanes ? get_plane(j) : nullptr;
-                    if (j < nplanes) phase1(Ds, T1s + (j & 1) * T1SZ);
-                    if (j >= 1) phase2(T1s + ((j - 1) & 1) * T1SZ, T2s + (long)((j - 1) % NS) * M.NG2 * TC);
+                    const double* Ds = nullptr;
+                    SG_PF(0, Ds = j < nplanes ? get_plane(j) : nullptr);
+                    SG_PF(1, if (j < nplanes) phase1(Ds, T1s + (j & 1) * T1SZ));
+                    SG_PF(2, if (j >= 1) phase2(T1s + ((j - 1) & 1) * T1SZ, T2s + (long)((j - 1) % NS) * M.NG2 * TC));
                     // before the next interval's phase 2 writes plane j over plane j - NS: the last row
                     // plane reading that plane's layer must be done
-                    if (tid == 0 && j < nplanes && j >= NS) wait_ge(1, (j - NS) / G + P + 1);
-                    asm volatile("bar.sync 1, %0;\n" ::"r"(NAW * 32) : "memory");
+                    SG_PF(3, if (tid == 0 && j < nplanes && j >= NS) wait_ge(1, (j - NS) / G + P + 1));
+                    SG_PF(4, asm volatile("bar.sync 1, %0;\n" ::"r"(NAW * 32) : "memory"));
                     if (tid == 0 && j >= 1 && j % G == 0) {
                         __threadfence_block();
                         cnt[0] = j / G;
                     }
-                }
+                })
             } else {
                 const int tb0 = NAW * 32;
                 if (nsteps > 0) build_b3(0, NAW, NBW);
+                SG_PF(5,
                 for (int L = 0; L < nsteps; ++L) {
-                    if (tid == tb0) wait_ge(0, min(L, nlayers - 1) + 1);
-                    asm volatile("bar.sync 2, %0;\n" ::"r"(NBW * 32) : "memory");
-                    phase3(L);
-                    if (L + 1 < nsteps) build_b3(L + 1, NAW, NBW);
-                    asm volatile("bar.sync 2, %0;\n" ::"r"(NBW * 32) : "memory");
+                    SG_PF(0, if (tid == tb0) wait_ge(0, min(L, nlayers - 1) + 1));
+                    SG_PF(1, asm volatile("bar.sync 2, %0;\n" ::"r"(NBW * 32) : "memory"));
+                    SG_PF(2, phase3(L));
+                    SG_PF(3, if (L + 1 < nsteps) build_b3(L + 1, NAW, NBW));
+                    SG_PF(4, asm volatile("bar.sync 2, %0;\n" ::"r"(NBW * 32) : "memory"));
                     if (tid == tb0) {
                         __threadfence_block();
                         cnt[1] = L + 1;
                     }
-                }
+                })
             }
+#ifdef SG_K4_PROF
+            if (lane == 0 && prm.dmma)
+                for (int k = 0; k < 6; ++k) atomicAdd(prm.dmma + 1 + warp * 8 + k, pf[k]);
+            if (lane == 0 && prm.dmma && warp == 0) atomicAdd(prm.dmma + 1 + 32 * 8, 1ull);
+#endif
+#undef SG_PF
         } else {
             // one barrier interval per Gauss plane j: phase 3 (row plane whose last layer completed one
             // interval earlier) | phase 1 (plane j) | phase 2 (plane j-1) | fragments of the next row plane
