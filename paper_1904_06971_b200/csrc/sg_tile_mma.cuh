@@ -210,10 +210,19 @@ __host__ __device__ constexpr int mma_ns(int ndim, int P, int form) {
 constexpr int kMmaT2 = SG_MMA_T2;  // max rows per CTA in z (3D); the plan picks the depth T2 <= kMmaT2 per call
 
 struct MmaGeom {
-    int NC1, NCP, T0, T1, G, W, MT, KS, KS3, XW, XWp, YW, NTY, DY, TY, NCOMBO, NMT, CH, NCH, TC, U, NG1, NG2, NU1, NB, NK1, NK2;
+    int NC1, NCP, T0, T1, G, W, MT, KS, KS3, XW, XWp, YW, NTY, DY, TY, T1SW, NCOMBO, NMT, CH, NCH, TC, T2PS, U, NG1, NG2, NU1, NB, NK1, NK2;
     int NTAB;
     long o_B0, o_B1, o_B2, o_A1, o_B2f, o_B3f, o_cmb, o_rb, o_tab, o_bar, o_D, o_D2, o_T1, o_T2, o_O, total;
 };
+
+// doubles of one T1 plane (NG1 T0 MT 8 rows; see T1SW) and the offset of its row r
+__host__ __device__ constexpr long mma_t1_plane(const MmaGeom& m) {
+    const long rows = (long)m.NG1 * m.T0 * m.MT * 8;
+    return m.T1SW ? rows / 4 * (4L * m.TY + 8) : rows * m.TY;
+}
+__host__ __device__ constexpr int mma_t1_row(const MmaGeom& m, int r) {
+    return m.T1SW ? (r >> 2) * (4 * m.TY + 8) + (r & 3) * m.TY + 4 * ((r >> 1) & 1) : r * m.TY;
+}
 
 __host__ __device__ constexpr MmaGeom mma_geom(int ndim, int P, int form, bool rat, int T0, int T1) {
     const Tables T = make_tables(ndim, form, rat);
@@ -238,6 +247,18 @@ __host__ __device__ constexpr MmaGeom mma_geom(int ndim, int P, int form, bool r
 #endif
     m.DY = pad_dy(m.NTY * 8);
     m.TY = pad8_4(m.NTY * 8 > m.YW + 4 ? m.NTY * 8 : m.YW + 4);
+    // T1SW: T1 rows r placed at t1_row(r) = (r / 4) (4 TY + 8) + (r % 4) TY + 4 ((r >> 1) & 1) with
+    // TY = 8 (mod 16): rows 0..3 of a half-warp start in distinct quarter-bank groups (phase 2's
+    // A-fragment loads: 4 consecutive y per row) and rows r, r+1 of a 128-bit store wavefront in
+    // opposite halves (phase 1's row stores; 2-way with the plain TY = 4 (mod 8) rows)
+    // (used where it takes no more shared memory than the plain rows: not for config 4's 2 x 5 tiles)
+    {
+        const int need = m.NTY * 8 > (m.T1 - 1) * m.G + m.KS * 4 ? m.NTY * 8 : (m.T1 - 1) * m.G + m.KS * 4;
+        int tys = need;
+        while (tys % 16 != 8) ++tys;
+        m.T1SW = 4 * tys + 8 <= 4 * m.TY ? 1 : 0;
+        if (m.T1SW) m.TY = tys;
+    }
     m.NCOMBO = T0 * m.T1 * m.W * m.W;
     m.NMT = (m.NCOMBO + 7) / 8;
     m.CH = form == 1 ? SG_CH_MASS : SG_CH_POIS;  // m-tiles per phase-3 item
@@ -274,8 +295,12 @@ __host__ __device__ constexpr MmaGeom mma_geom(int ndim, int P, int form, bool r
     m.o_D = o; o += align16((long)m.U * m.XWp * m.DY);                          // D window, double buffered (TMA)
     m.o_D2 = ndim == 3 ? o : m.o_D;                                           // 2D/1D: one plane per tile
     o += ndim == 3 ? align16((long)m.U * m.XWp * m.DY) : 0;
-    m.o_T1 = o; o += ndim >= 2 ? (ndim == 3 ? 2L : 1L) * m.NG1 * T0 * m.MT * 8 * m.TY : 0;  // 3D: 2 planes
-    m.o_T2 = o; o += ndim == 3 ? (long)mma_ns(ndim, P, form) * m.NG2 * m.TC : 0;  // ring of T2 planes
+    m.o_T1 = o; o += ndim >= 2 ? (ndim == 3 ? 2L : 1L) * mma_t1_plane(m) : 0;  // 3D: 2 planes
+    // T2 plane stride = 8 (mod 16) doubles: phase 3's A fragments take their four k (z points) from
+    // consecutive planes, so the lk groups of a half-warp land on the two bank halves (was 4-way)
+    m.T2PS = m.NG2 * m.TC;
+    while (m.T2PS % 16 != 8) ++m.T2PS;
+    m.o_T2 = o; o += ndim == 3 ? (long)mma_ns(ndim, P, form) * m.T2PS : 0;  // ring of T2 planes
     m.o_O = o;                                                                  // (no live partial sums: one z chain per entry)
     m.total = o;
     return m;
@@ -762,7 +787,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
     };
 
     using TAB = MmaTabS<NDIM, P, FORM, RAT>;
-    constexpr long T1SZ = (long)M.NG1 * T0 * MT * 8 * TY;
+    constexpr long T1SZ = mma_t1_plane(M);
     const int* tab = reinterpret_cast<const int*>(smem + M.o_tab);
 
     // ---------------- phase 1 (x): items (group, row i0l) -> T1[Gc][i0l][d0][y]
@@ -836,12 +861,12 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
                     }
                 }
             } else {
-                double* t1 = T1b + ((Gc * T0 + i0l) * MT * 8) * TY;
+                double* t1 = T1b + mma_t1_row(M, (Gc * T0 + i0l) * MT * 8 + lr);
 #pragma unroll
                 for (int a = 0; a < MT; ++a)
 #pragma unroll
                     for (int c = 0; c < NTI; ++c) {
-                        double* dst = t1 + (a * 8 + lr) * TY + (cc * NTI + c) * 8 + 2 * lk;
+                        double* dst = t1 + a * (mma_t1_row(M, 8) - mma_t1_row(M, 0)) + (cc * NTI + c) * 8 + 2 * lk;
                         dst[0] = acc[a][c][0];
                         dst[1] = acc[a][c][1];
                     }
@@ -855,6 +880,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
     // in as accS + (A + B) in order -- the mirror of the transposed entry's evaluation.
     auto phase2 = [&](const double* T1b, double* T2b) {
         if (prm.dbg & 8) return;
+        constexpr int T1A = mma_t1_row(M, 8) - mma_t1_row(M, 0);  // T1 offset of 8 rows (one m-tile)
         if constexpr (NDIM >= 2) {
             const int qe = tab[TAB::S.o_off2 + warp + 1];
             for (int q = tab[TAB::S.o_off2 + warp]; q < qe; ++q) {
@@ -866,7 +892,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
                 auto block = [&](int ga, int kd, double (&acc)[MT][MT][2]) {
                     const double* bfp = B2f + ((i1l * NK1 + kd) * KS) * MT * 32 + lane;
                     // y of support point s of row i1 is i1l*G + s (the support is contiguous)
-                    const double* t1 = T1b + ((ga * T0 + r) * MT * 8 + lr) * TY + i1l * G + lk;
+                    const double* t1 = T1b + mma_t1_row(M, (ga * T0 + r) * MT * 8 + lr) + i1l * G + lk;
 #pragma unroll
                     for (int kk = 0; kk < KS; ++kk) {
                         double bfs[MT];
@@ -874,7 +900,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
                         for (int c = 0; c < MT; ++c) bfs[c] = bfp[(kk * MT + c) * 32];
 #pragma unroll
                         for (int a = 0; a < MT; ++a) {
-                            const double av = t1[a * 8 * TY + kk * 4];
+                            const double av = t1[a * T1A + kk * 4];
 #pragma unroll
                             for (int c = 0; c < MT; ++c) dmma(acc[a][c][0], acc[a][c][1], av, bfs[c]);
                         }
@@ -884,8 +910,8 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
                 auto block2 = [&](int ga, int kd, int gb, int kb, double (&accA)[MT][MT][2], double (&accB)[MT][MT][2]) {
                     const double* bfa = B2f + ((i1l * NK1 + kd) * KS) * MT * 32 + lane;
                     const double* bfb = B2f + ((i1l * NK1 + kb) * KS) * MT * 32 + lane;
-                    const double* ta = T1b + ((ga * T0 + r) * MT * 8 + lr) * TY + i1l * G + lk;
-                    const double* tb = T1b + ((gb * T0 + r) * MT * 8 + lr) * TY + i1l * G + lk;
+                    const double* ta = T1b + mma_t1_row(M, (ga * T0 + r) * MT * 8 + lr) + i1l * G + lk;
+                    const double* tb = T1b + mma_t1_row(M, (gb * T0 + r) * MT * 8 + lr) + i1l * G + lk;
 #pragma unroll
                     for (int kk = 0; kk < KS; ++kk) {
                         double fa[MT], fb[MT];
@@ -896,7 +922,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
                         }
 #pragma unroll
                         for (int a = 0; a < MT; ++a) {
-                            const double va = ta[a * 8 * TY + kk * 4], vb = tb[a * 8 * TY + kk * 4];
+                            const double va = ta[a * T1A + kk * 4], vb = tb[a * T1A + kk * 4];
 #pragma unroll
                             for (int c = 0; c < MT; ++c) {
                                 dmma(accA[a][c][0], accA[a][c][1], va, fa[c]);
@@ -1130,7 +1156,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
                         double bfs[MT];
 #pragma unroll
                         for (int c = 0; c < MT; ++c) bfs[c] = bfp[(kk * MT + c) * 32];
-                        const double* t2 = t2b + (long)zslot[kk] * M.NG2 * TC;
+                        const double* t2 = t2b + (long)zslot[kk] * M.T2PS;
 #pragma unroll
                         for (int mm = 0; mm < CH; ++mm) {
                             const double av = t2[mm * 8];
@@ -1153,7 +1179,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
                             fa[c] = bfa[(kk * MT + c) * 32];
                             fb[c] = bfb[(kk * MT + c) * 32];
                         }
-                        const long zo = (long)zslot[kk] * M.NG2 * TC;
+                        const long zo = (long)zslot[kk] * M.T2PS;
 #pragma unroll
                         for (int mm = 0; mm < CH; ++mm) {
                             const double va = t2a[zo + mm * 8], vb = t2bb[zo + mm * 8];
@@ -1317,7 +1343,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
                     const double* Ds = nullptr;
                     SG_PF(0, Ds = j < nplanes ? get_plane(j) : nullptr);
                     SG_PF(1, if (j < nplanes) phase1(Ds, T1s + (j & 1) * T1SZ));
-                    SG_PF(2, if (j >= 1) phase2(T1s + ((j - 1) & 1) * T1SZ, T2s + (long)((j - 1) % NS) * M.NG2 * TC));
+                    SG_PF(2, if (j >= 1) phase2(T1s + ((j - 1) & 1) * T1SZ, T2s + (long)((j - 1) % NS) * M.T2PS));
                     // before the next interval's phase 2 writes plane j over plane j - NS: the last row
                     // plane reading that plane's layer must be done
                     SG_PF(3, if (tid == 0 && j < nplanes && j >= NS) wait_ge(1, (j - NS) / G + P + 1));
@@ -1357,7 +1383,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
                 const double* Ds = j < nplanes ? get_plane(j) : nullptr;
                 if (j >= G + 1 && (j - 1) % G == 0 && (j - 1) / G - 1 < nsteps) phase3((j - 1) / G - 1);
                 if (j < nplanes) phase1(Ds, T1s + (j & 1) * T1SZ);
-                if (j >= 1 && j <= nplanes) phase2(T1s + ((j - 1) & 1) * T1SZ, T2s + (long)((j - 1) % NS) * M.NG2 * TC);
+                if (j >= 1 && j <= nplanes) phase2(T1s + ((j - 1) & 1) * T1SZ, T2s + (long)((j - 1) % NS) * M.T2PS);
                 if (j % G == 0 && j / G < nsteps) build_b3(j / G, 0, NW);
                 __syncthreads();
             }
