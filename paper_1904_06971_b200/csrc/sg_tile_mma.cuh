@@ -296,10 +296,11 @@ __host__ __device__ constexpr MmaGeom mma_geom(int ndim, int P, int form, bool r
     m.o_D2 = ndim == 3 ? o : m.o_D;                                           // 2D/1D: one plane per tile
     o += ndim == 3 ? align16((long)m.U * m.XWp * m.DY) : 0;
     m.o_T1 = o; o += ndim >= 2 ? (ndim == 3 ? 2L : 1L) * mma_t1_plane(m) : 0;  // 3D: 2 planes
-    // T2 plane stride = 8 (mod 16) doubles: phase 3's A fragments take their four k (z points) from
-    // consecutive planes, so the lk groups of a half-warp land on the two bank halves (was 4-way)
+    // T2 plane stride = 4 (mod 16) doubles: phase 3's A fragment takes its four k (z points, lane
+    // bits 0-1) from consecutive planes and four consecutive combos per k (lane bits 2-3) in a
+    // half-warp, so the four planes must start in distinct quarter-bank groups (was 4-way at 0 mod 16)
     m.T2PS = m.NG2 * m.TC;
-    while (m.T2PS % 16 != 8) ++m.T2PS;
+    while (m.T2PS % 16 != 4) ++m.T2PS;
     m.o_T2 = o; o += ndim == 3 ? (long)mma_ns(ndim, P, form) * m.T2PS : 0;  // ring of T2 planes
     m.o_O = o;                                                                  // (no live partial sums: one z chain per entry)
     m.total = o;

@@ -1,12 +1,15 @@
 """Shared-memory instructions of an ncu report ranked by excessive (bank-conflict) wavefronts:
-python tools/ncu_smem_conflicts.py <report.ncu-rep> [top]"""
+python tools/ncu_smem_conflicts.py <report.ncu-rep> [top] [kernel index]"""
 import csv
 import io
 import subprocess
 import sys
 
 out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "source", "--csv", "--print-source", "sass"], capture_output=True, text=True).stdout
-rows = list(csv.reader(io.StringIO("\n".join(out.splitlines()[1:]))))
+# one section per profiled kernel, each starting with a "Kernel Name" line; argv[3] picks one (default 0)
+secs = [s for s in out.split('"Kernel Name"') if s.strip()]
+sec = secs[int(sys.argv[3]) if len(sys.argv) > 3 else 0]
+rows = list(csv.reader(io.StringIO("\n".join(sec.splitlines()[1:]))))
 h = rows[0]
 ix = {k: i for i, k in enumerate(h)}
 data = rows[1:]
