@@ -558,8 +558,8 @@ int prepare_problem(Call& c, const sg_problem* pr, DevProblem& dp) {
         dp.qw[d] = (double*)dv[4 * d + 2];
         dp.B[d] = (double*)(tabs + o_tab[d][0]);
         dp.bspan[d] = (int*)(tabs + o_tab[d][1]);
-        jobs.j[jobs.n++] = TabJob{kn, qp, dp.bspan[d], dp.B[d], dp.m[d] + dp.p + 1, dp.p, npts, dp.nu, dp.g,
-                                  uniform_points(pr->knots[d], dp.p, dp.S[d], pr->qpts[d], dp.g) ? 1 : 0};
+        dp.canon[d] = uniform_points(pr->knots[d], dp.p, dp.S[d], pr->qpts[d], dp.g) ? 1 : 0;
+        jobs.j[jobs.n++] = TabJob{kn, qp, dp.bspan[d], dp.B[d], dp.m[d] + dp.p + 1, dp.p, npts, dp.nu, dp.g, dp.canon[d]};
         double* gk = (double*)dv[4 * d + 3];
         dp.G[d] = (double*)(tabs + o_tab[d][2]);
         dp.gspan[d] = (int*)(tabs + o_tab[d][3]);
@@ -969,6 +969,7 @@ int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>
             mp.m[d] = dp.m[d];
             mp.S[d] = dp.S[d];
             mp.B[d] = dp.B[d];
+            mp.canon[d] = d < dp.n ? dp.canon[d] : 0;
             mp.tgrid[d] = pl.tgrid[d];
             mp.Gp[d] = d < dp.n ? dp.S[d] * dp.g : 1;
         }

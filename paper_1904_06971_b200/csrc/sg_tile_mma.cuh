@@ -506,6 +506,7 @@ struct MmaParams {
     int run;                     // 2D: tiles per CTA (consecutive entries of the tile list)
     int dbg;                     // timing experiments only (SG_K4_DBG): skip 1 phase 3, 2 its epilogue, 4 phase 1, 8 phase 2
     int ntiles;                  // entries of the tile list (or tiles of the grid)
+    int canon[3];                // B[d] holds bitwise equal values on all interior elements [p, S-1-p] (K2)
 };
 
 template <int NDIM, int P, int FORM, bool RAT>
@@ -1070,9 +1071,9 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
                 ew1 = b1 - P;
                 // windows made of interior elements carry identical tables (K2 canonicalises them),
                 // so their fragments are reused as they are
-                auto interior = [&](int ew, int nel, int S) { return ew > P && ew + nel - 1 <= S - 1 - P; };
-                const bool xin = interior(ew0, T0 + P, prm.S[0]) && interior(ew0_prev, T0 + P, prm.S[0]);
-                const bool yin = interior(ew1, T1 + P, prm.S[1]) && interior(ew1_prev, T1 + P, prm.S[1]);
+                auto interior = [&](int ew, int nel, int S) { return ew >= P && ew + nel - 1 <= S - 1 - P; };
+                const bool xin = prm.canon[0] && interior(ew0, T0 + P, prm.S[0]) && interior(ew0_prev, T0 + P, prm.S[0]);
+                const bool yin = prm.canon[1] && interior(ew1, T1 + P, prm.S[1]) && interior(ew1_prev, T1 + P, prm.S[1]);
                 const bool newx = tc0 != colx && !xin;
                 const bool newy = !yin;
                 colx = tc0;
@@ -1128,6 +1129,16 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
         // row planes elo2 .. elo2 + nsteps - 1; the rows above the last streamed layer (ehi2) have all
         // their layers streamed by then and follow it
         const int nsteps = nlayers + max(0, zr1 - ehi2);
+        // phase-3 B fragments depend on the row plane only through the z tables of its layers i2-P .. i2:
+        // on canonical tables (prm.canon[2]) every row plane with all of them interior (2P <= i2 <= S-1-P)
+        // has the same fragments, so consecutive interior row planes share one buffer (no rebuild);
+        // b3par(L) = buffer of row plane L (flips at every rebuilt row plane)
+        const int b3La = prm.canon[2] ? 2 * P - elo2 : (1 << 29), b3Lb = prm.S[2] - 1 - P - elo2;
+        auto b3reuse = [&](int L) { return L >= 1 && L - 1 >= b3La && L <= b3Lb; };
+        auto b3par = [&](int L) {
+            const int lo = max(b3La + 1, 1), hi = min(L, b3Lb);
+            return (L - (hi >= lo ? hi - lo + 1 : 0)) & 1;
+        };
         // ---- phase 3 (z) of row plane i2 = elo2 + L: every entry is one DMMA chain over the z points of
         // its row's support (layers i2-P .. i2 ascending; the column basis vanishes outside the shared
         // layers, so those terms add exact zeros), written straight to the CSR.  Items: chunks of CH m-tiles.
@@ -1135,7 +1146,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
             if (prm.dbg & 1) return;
             const int i2 = elo2 + L;
             if (i2 < zr0 || i2 > zr1) return;
-            const double* B3b = B3f + (L & 1) * B3SZ;
+            const double* B3b = B3f + b3par(L) * B3SZ;
             // T2 slot of this lane's z point s = kk*4 + lk: plane (i2 - P + s/G - elo2)*G + s%G of the stream
             int zslot[KS3];
 #pragma unroll
@@ -1290,7 +1301,8 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
         // B3f[L&1][(slot*KS3 + kk)*MT + c][lane] = B^a2_{i2}(z_s) B^b2_{i2+d2}(z_s), s = kk*4 + lk, d2 = c*8 + lr - P
         auto build_b3 = [&](const int L, const int w0, const int nw) {
             const int i2 = elo2 + L;
-            double* B3b = B3f + (L & 1) * B3SZ;
+            if (b3reuse(L)) return;
+            double* B3b = B3f + b3par(L) * B3SZ;
             for (int slot = warp - w0; slot < NK2; slot += nw) {
                 int kind = 0;
                 static_for<0, NK2>([&](auto SI) { if (slot == decltype(SI)::value) kind = kind_of_slot2(TTS::T, decltype(SI)::value); });
