@@ -94,14 +94,23 @@ __device__ void field_plane_prep(const double* __restrict__ coef, int deg, const
 
 // point evaluation: out[c][code] for all multi-indices with |alpha| <= NU (code = a0+3a1+9a2).
 // 2D/3D: t = y table of this point, s = its span, H = Hx + x*hxs.  1D: t = x table, s = x span.
-template <int NDIM, int NU, int C>
-__device__ __forceinline__ void field_point(const double* __restrict__ coef, int deg, const double* t, int s,
+// DEG >= 0: the degree as a compile-time constant (the r loop unrolls and its shared-memory loads are
+// scheduled ahead of the FMAs: the runtime-degree loop issued each load right before its FMA and
+// stalled on it, geom_D ran at ~32% of the fp64 pipe); DEG < 0: runtime degree `deg`
+template <int NDIM, int NU, int C, int DEG = -1>
+__device__ __forceinline__ void field_point(const double* __restrict__ coef, int deg_rt, const double* t, int s,
                                             const double* H, int lo1, double (&out)[C][27]) {
+    if constexpr (DEG < 0 && NDIM >= 2) {
+        if (deg_rt == 2) return field_point<NDIM, NU, C, 2>(coef, 2, t, s, H, lo1, out);
+        if (deg_rt == 3) return field_point<NDIM, NU, C, 3>(coef, 3, t, s, H, lo1, out);
+    }
+    const int deg = DEG >= 0 ? DEG : deg_rt;
     constexpr int NC = NCx<NDIM, NU>::v;
 #pragma unroll
     for (int c = 0; c < C; ++c)
 #pragma unroll
         for (int k = 0; k < 27; ++k) out[c][k] = 0.0;
+#pragma unroll
     for (int r = 0; r <= deg; ++r) {
         const int i = s - deg + r;
 #pragma unroll
