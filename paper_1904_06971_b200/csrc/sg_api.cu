@@ -536,6 +536,9 @@ int prepare_problem(Call& c, const sg_problem* pr, DevProblem& dp) {
     for (void* v : dv)
         if (!v) return fail(-4, "device allocation failed");
     dp.hom = (double*)dv[4 * pr->n];
+    // unit weights: a polynomial map (the reference's GeometryMap.is_polynomial, geometry.py:167)
+    dp.geo_poly = true;
+    for (int64_t i = 0; i < dp.Ng && dp.geo_poly; ++i) dp.geo_poly = pr->geo_hom[i * (pr->n + 1) + pr->n] == 1.0;
     dp.sol_w = dp.rational ? (double*)dv[4 * pr->n + 1] : nullptr;
     // the 4n tables in one allocation (cudaMallocAsync is ~5 us per call on the host)
     size_t tab_bytes = 0;
@@ -670,7 +673,7 @@ static int choose_layout(const DevProblem& dp, int kmax, int nthreads, Layout& o
 // ------------------------------------------------------------------------------------------
 // K3 launch: per-point form tensor D on the blocks of points the selected tiles read
 // ------------------------------------------------------------------------------------------
-static void* get_geom_kernel(int n, int form, bool rat) { return kernel_ptr(n, form, rat, 2, 1, nullptr); }
+static void* get_geom_kernel(int n, int form, bool rat, bool poly) { return kernel_ptr(n, form, rat, poly ? 3 : 2, 1, nullptr); }
 
 struct GeomMark {
     int n, P, g, T[3], tg[3], S[3], BX, BY, nbx, nby, z0;
@@ -838,7 +841,7 @@ int compute_D(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* t
         c.kend();
         gp.blockmask = mask;
     }
-    void* kfn = get_geom_kernel(n, dp.pr.form, dp.rational);
+    void* kfn = get_geom_kernel(n, dp.pr.form, dp.rational, dp.geo_poly && !getenv("SG_GEO_QUOTIENT"));
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptinMax);
     void* args[] = {&gp};
     const int64_t nb = (int64_t)gp.nbx * gp.nby * ((gp.Gp[2] + gp.ZB - 1) / gp.ZB);

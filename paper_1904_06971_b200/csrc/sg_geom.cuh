@@ -32,7 +32,9 @@ __device__ __forceinline__ constexpr int k02(int a0, int a2) { return (a0 + a2) 
 template <int NDIM, int NU>
 struct NCx { static constexpr int v = NDIM == 3 ? (NU + 1) * (NU + 2) / 2 : NU + 1; };
 
-template <int NDIM, int NU, int C>
+// C components of the field are read from coefficient rows of stride CS (a polynomial geometry map
+// skips the weight column of its homogeneous net)
+template <int NDIM, int NU, int C, int CS = C>
 __device__ void field_plane_prep(const double* __restrict__ coef, int deg, const int* md, const double* t0, int ts0,
                                  const int* s0, int X, const double* tz, int sz, int lo0, int n0, int lo1, int n1,
                                  double* Hz, double* Hx, int hxs) {
@@ -50,7 +52,7 @@ __device__ void field_plane_prep(const double* __restrict__ coef, int deg, const
             for (int a = 0; a <= NU; ++a) acc[a] = 0.0;
             if (g0 < md[0] && g1 < md[1]) {
                 for (int r = 0; r <= deg; ++r) {
-                    const double v = coef[((long long)g0 + (long long)md[0] * (g1 + (long long)md[1] * (sz - deg + r))) * C + c];
+                    const double v = coef[((long long)g0 + (long long)md[0] * (g1 + (long long)md[1] * (sz - deg + r))) * CS + c];
 #pragma unroll
                     for (int a = 0; a <= NU; ++a) acc[a] = fma(tz[a * (deg + 1) + r], v, acc[a]);
                 }
@@ -81,7 +83,7 @@ __device__ void field_plane_prep(const double* __restrict__ coef, int deg, const
                     }
                 } else {
                     const int g1 = lo1 + i1;
-                    const double v = (g1 < md[1]) ? coef[((long long)(sx - deg + r) + (long long)md[0] * g1) * C + c] : 0.0;
+                    const double v = (g1 < md[1]) ? coef[((long long)(sx - deg + r) + (long long)md[0] * g1) * CS + c] : 0.0;
 #pragma unroll
                     for (int a0 = 0; a0 <= NU; ++a0) acc[a0] = fma(t0[x * ts0 + a0 * (deg + 1) + r], v, acc[a0]);
                 }
@@ -97,12 +99,12 @@ __device__ void field_plane_prep(const double* __restrict__ coef, int deg, const
 // DEG >= 0: the degree as a compile-time constant (the r loop unrolls and its shared-memory loads are
 // scheduled ahead of the FMAs: the runtime-degree loop issued each load right before its FMA and
 // stalled on it, geom_D ran at ~32% of the fp64 pipe); DEG < 0: runtime degree `deg`
-template <int NDIM, int NU, int C, int DEG = -1>
+template <int NDIM, int NU, int C, int DEG = -1, int CS = C>
 __device__ __forceinline__ void field_point(const double* __restrict__ coef, int deg_rt, const double* t, int s,
                                             const double* H, int lo1, double (&out)[C][27]) {
     if constexpr (DEG < 0 && NDIM >= 2) {
-        if (deg_rt == 2) return field_point<NDIM, NU, C, 2>(coef, 2, t, s, H, lo1, out);
-        if (deg_rt == 3) return field_point<NDIM, NU, C, 3>(coef, 3, t, s, H, lo1, out);
+        if (deg_rt == 2) return field_point<NDIM, NU, C, 2, CS>(coef, 2, t, s, H, lo1, out);
+        if (deg_rt == 3) return field_point<NDIM, NU, C, 3, CS>(coef, 3, t, s, H, lo1, out);
     }
     const int deg = DEG >= 0 ? DEG : deg_rt;
     constexpr int NC = NCx<NDIM, NU>::v;
@@ -116,7 +118,7 @@ __device__ __forceinline__ void field_point(const double* __restrict__ coef, int
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             if constexpr (NDIM == 1) {
-                const double v = coef[(long long)i * C + c];
+                const double v = coef[(long long)i * CS + c];
 #pragma unroll
                 for (int a0 = 0; a0 <= NU; ++a0) out[c][a0] = fma(t[a0 * (deg + 1) + r], v, out[c][a0]);
             } else {
@@ -148,22 +150,25 @@ __device__ __forceinline__ constexpr int ucode(int a) { return a == 0 ? 1 : (a =
 // quotient rule), :98-131 (det, adj), assembly.py:558-576 (K, C, hess), :531-548 (integrands),
 // :496-517 (rational basis).
 // ---------------------------------------------------------------------------------------------
-template <int NDIM, int FORM, bool RAT>
+// GPOLY: the geometry map is polynomial (unit weights, the reference's GeometryMap.is_polynomial,
+// geometry.py:167): W = 1 and its derivatives vanish, so the quotient rule of map_grid
+// (geometry.py:196-227) reduces to the numerators (num[NDIM] is not read)
+template <int NDIM, int FORM, bool RAT, bool GPOLY = false>
 __device__ __forceinline__ void point_D(const double (&num)[NDIM + 1][27], const double (&wf)[1][27], double wq,
                                         double coefv, double* Dout) {
     constexpr Tables TT = TermTables<NDIM, FORM, RAT>::T;
     constexpr int MS = TT.MS;
     constexpr int NUG = geo_deriv(FORM);
-    const double W = num[NDIM][0];
-    const double iW = 1.0 / W;
+    const double iW = GPOLY ? 1.0 : 1.0 / num[NDIM][0];
     double phi[NDIM], jac[NDIM][NDIM], dW[NDIM];
 #pragma unroll
-    for (int c = 0; c < NDIM; ++c) phi[c] = num[c][0] * iW;
+    for (int c = 0; c < NDIM; ++c) phi[c] = GPOLY ? num[c][0] : num[c][0] * iW;
 #pragma unroll
     for (int a = 0; a < NDIM; ++a) {
-        dW[a] = num[NDIM][ucode(a)];
+        dW[a] = GPOLY ? 0.0 : num[NDIM][ucode(a)];
 #pragma unroll
-        for (int c = 0; c < NDIM; ++c) jac[c][a] = (num[c][ucode(a)] - phi[c] * num[NDIM][ucode(a)]) * iW;
+        for (int c = 0; c < NDIM; ++c)
+            jac[c][a] = GPOLY ? num[c][ucode(a)] : (num[c][ucode(a)] - phi[c] * num[NDIM][ucode(a)]) * iW;
     }
     double det, adj[NDIM][NDIM];
     if constexpr (NDIM == 1) {
@@ -245,7 +250,7 @@ __device__ __forceinline__ void point_D(const double (&num)[NDIM + 1][27], const
                 const int cd = ucode(a) + ucode(b);
 #pragma unroll
                 for (int c = 0; c < NDIM; ++c) {
-                    const double v = (num[c][cd] - jac[c][a] * dW[b] - jac[c][b] * dW[a] - phi[c] * num[NDIM][cd]) * iW;
+                    const double v = GPOLY ? num[c][cd] : (num[c][cd] - jac[c][a] * dW[b] - jac[c][b] * dW[a] - phi[c] * num[NDIM][cd]) * iW;
                     hess[c][a][b] = v;
                     hess[c][b][a] = v;
                 }
@@ -367,7 +372,7 @@ struct GeomParams {
     double* D;               // [Gp2][U][Gp0][Dys]
 };
 
-template <int NDIM, int FORM, bool RAT>
+template <int NDIM, int FORM, bool RAT, bool GPOLY>
 __global__ void __launch_bounds__(256) geom_D_kernel(const GeomParams prm) {
     constexpr Tables TT = TermTables<NDIM, FORM, RAT>::T;
     constexpr int MS = TT.MS;
@@ -447,10 +452,11 @@ __global__ void __launch_bounds__(256) geom_D_kernel(const GeomParams prm) {
     const int wlo0 = x0 / g, wn0 = (x0 + X - 1) / g - x0 / g + 1 + p;
     int wlo1 = 0, wn1 = 1;
     if constexpr (NDIM >= 2) { wlo1 = y0 / g; wn1 = (y0 + Y - 1) / g - y0 / g + 1 + p; }
-    constexpr int C = NDIM + 1;
+    constexpr int C = GPOLY ? NDIM : NDIM + 1;  // field components evaluated (polynomial map: no weight)
+    constexpr int CS = NDIM + 1;                 // row stride of the homogeneous net
     const int hxs = gn1 * C * NCx<NDIM, NUG>::v;
     const int wxs = wn1 * NCx<NDIM, NU>::v;
-    field_plane_prep<NDIM, NUG, C>(prm.hom, pg, prm.mg, G0s, NBG, gs0, X, G2p, sz, glo0, gn0, glo1, gn1, Hz, Hx, hxs);
+    field_plane_prep<NDIM, NUG, C, CS>(prm.hom, pg, prm.mg, G0s, NBG, gs0, X, G2p, sz, glo0, gn0, glo1, gn1, Hz, Hx, hxs);
     if constexpr (RAT)
         field_plane_prep<NDIM, NU, 1>(prm.sol_w, p, prm.m, B0s, NB, ws0, X, B2p, szw, wlo0, wn0, wlo1, wn1, Wz, Wx, wxs);
     __syncthreads();
@@ -459,11 +465,12 @@ __global__ void __launch_bounds__(256) geom_D_kernel(const GeomParams prm) {
         const int y = it % Y, x = it / Y;  // a warp shares x: Hx reads broadcast, y tables per lane
         double num[NDIM + 1][27];
         double wf[1][27];
+        auto& numc = *reinterpret_cast<double(*)[C][27]>(&num);
         if constexpr (NDIM == 1) {
-            field_point<1, NUG, C>(prm.hom, pg, G0s + x * NBG, gs0[x], nullptr, 0, num);
+            field_point<1, NUG, C, -1, CS>(prm.hom, pg, G0s + x * NBG, gs0[x], nullptr, 0, numc);
             if constexpr (RAT) field_point<1, NU, 1>(prm.sol_w, p, B0s + x * NB, ws0[x], nullptr, 0, wf);
         } else {
-            field_point<NDIM, NUG, C>(prm.hom, pg, G1s + y * NBGp, gs1[y], Hx + x * hxs, glo1, num);
+            field_point<NDIM, NUG, C, -1, CS>(prm.hom, pg, G1s + y * NBGp, gs1[y], Hx + x * hxs, glo1, numc);
             if constexpr (RAT) field_point<NDIM, NU, 1>(prm.sol_w, p, B1s + y * NBp, ws1[y], Wx + x * wxs, wlo1, wf);
         }
         if constexpr (!RAT) wf[0][0] = 1.0;
@@ -472,7 +479,7 @@ __global__ void __launch_bounds__(256) geom_D_kernel(const GeomParams prm) {
         if constexpr (NDIM >= 2) wq = qwy[y] * wq;
         if constexpr (NDIM == 3) wq = wz * wq;
         double Dp[U];
-        point_D<NDIM, FORM, RAT>(num, wf, wq, prm.coef, Dp);
+        point_D<NDIM, FORM, RAT, GPOLY>(num, wf, wq, prm.coef, Dp);
         const long long plane = (long long)z * U;
 #pragma unroll
         for (int u = 0; u < U; ++u)

@@ -31,10 +31,11 @@ static void* mma_ptr() {
 #define SG_CAT(a, b) SG_CAT2(a, b)
 #define SG_NAME SG_CAT(SG_CAT(SG_CAT(kernel_ptr_, SG_INST_NDIM), SG_CAT(_, SG_INST_FORM)), SG_CAT(_, SG_INST_RAT))
 
-// which: 0 = SIMT tile kernel, 1 = DMMA tile kernel, 2 = geometry (K3)
+// which: 0 = SIMT tile kernel, 1 = DMMA tile kernel, 2 = geometry (K3), 3 = geometry of a polynomial map
 void* SG_NAME(int which, int p, int* kmax) {
     if (kmax) *kmax = which == 1 ? 32 * mma_warps(SG_INST_NDIM, p, SG_INST_FORM, kRat) : kmax_for(SG_INST_NDIM);
-    if (which == 2) return (void*)&geom_D_kernel<SG_INST_NDIM, SG_INST_FORM, kRat>;
+    if (which == 2) return (void*)&geom_D_kernel<SG_INST_NDIM, SG_INST_FORM, kRat, false>;
+    if (which == 3) return (void*)&geom_D_kernel<SG_INST_NDIM, SG_INST_FORM, kRat, true>;
     switch (p) {
         case 1: return which ? mma_ptr<1>() : simt_ptr<1>();
         case 2: return which ? mma_ptr<2>() : simt_ptr<2>();

@@ -85,6 +85,7 @@ struct DevProblem {
     int m[3], S[3], mg[3];
     int64_t N = 0, Ng = 0;
     bool rational = false;
+    bool geo_poly = false;     // geometry weights all exactly 1: K3 skips the quotient rule
     int canon[3] = {0, 0, 0};  // solution tables of direction d canonicalised on interior elements (K2)
     double* B[3];
     int* bspan[3];
