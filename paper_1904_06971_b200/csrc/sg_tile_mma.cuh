@@ -727,14 +727,20 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
     // streamed during phase 2); SG_NO_TMA=1 selects plain loads (debug)
     constexpr bool kTma = NDIM >= 2;
     const bool use_tma = kTma && prm.tma;
+    // warp-specialised 3D pipeline: plane j + 2 is issued into plane j's buffer as soon as the last
+    // phase-1 warp has finished plane j (a shared counter), ~half an interval before the next barrier;
+    // only the phase-1 warps wait for the D windows
+    const bool early = use_tma && NDIM == 3 && mma_spec_nb(NDIM, FORM) > 0 && !(prm.dbg & 16);
     if (use_tma) {
         if (tid == 0) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0) : "memory");
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0 + 8u) : "memory");
             asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+            reinterpret_cast<int*>(smem + M.o_bar + 3)[0] = 0;  // phase-1 warps done (early issue)
         }
         __syncthreads();
         if (tid == 0) issue_plane(0);
+        if (tid == 0 && early && nplanes > 1) issue_plane(1);
     }
     // 2D: the D window of the run's k-th tile (TMA box at the tile's window origin; barrier k & 1)
     auto issue_tile = [&](int k, int t) {
@@ -753,7 +759,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
     auto get_plane = [&](int j) {
         double* Ds = Dbuf(j & 1);
         if (use_tma) {
-            if (tid == 0 && j + 1 < nplanes) issue_plane(j + 1);  // prefetch the next plane
+            if (!early && tid == 0 && j + 1 < nplanes) issue_plane(j + 1);  // prefetch the next plane
             const uint32_t bar = bar0 + 8u * (uint32_t)(j & 1);
             const uint32_t par = (uint32_t)((j >> 1) & 1);
             uint32_t done = 0;
@@ -1351,11 +1357,29 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
 #define SG_PF(k, stmt) { stmt; }
 #endif
             if (warp < NAW) {
+                // warps with phase-1 items (compile-time schedule) and their count
+                constexpr int NP1W = [] {
+                    int c = 0;
+                    for (int w = 0; w < NW; ++w) c += TAB::S.v[TAB::S.o_off1 + w + 1] > TAB::S.v[TAB::S.o_off1 + w] ? 1 : 0;
+                    return c;
+                }();
+                const bool has_p1 = tab[TAB::S.o_off1 + warp + 1] > tab[TAB::S.o_off1 + warp];
+                int* p1cnt = reinterpret_cast<int*>(smem + M.o_bar + 3);
                 SG_PF(5,
                 for (int j = 0; j <= nplanes; ++j) {
                     const double* Ds = nullptr;
-                    SG_PF(0, Ds = j < nplanes ? get_plane(j) : nullptr);
-                    SG_PF(1, if (j < nplanes) phase1(Ds, T1s + (j & 1) * T1SZ));
+                    if (early) {
+                        if (j < nplanes && has_p1) {
+                            SG_PF(0, Ds = get_plane(j));
+                            SG_PF(1, phase1(Ds, T1s + (j & 1) * T1SZ));
+                            __syncwarp();
+                            // the last phase-1 warp of plane j refills its buffer with plane j + 2
+                            if (lane == 0 && atomicAdd(p1cnt, 1) == NP1W * (j + 1) - 1 && j + 2 < nplanes) issue_plane(j + 2);
+                        }
+                    } else {
+                        SG_PF(0, Ds = j < nplanes ? get_plane(j) : nullptr);
+                        SG_PF(1, if (j < nplanes) phase1(Ds, T1s + (j & 1) * T1SZ));
+                    }
                     SG_PF(2, if (j >= 1) phase2(T1s + ((j - 1) & 1) * T1SZ, T2s + (long)((j - 1) % NS) * M.T2PS));
                     // before the next interval's phase 2 writes plane j over plane j - NS: the last row
                     // plane reading that plane's layer must be done
