@@ -45,6 +45,7 @@ struct SurrParams {
     int64_t slab_lo, slab_hi;
     int64_t qlo, qhi;  // rows whose quadrature values this call needs (the slab and its p-plane halo)
     int tile0;         // first interpolation tile of the launch (row slabs launch their z range only)
+    int dbg;           // timing experiments only (SG_K7_DBG): 1 no value stores, 2 no index stores, 4 no passes
 };
 
 __device__ __forceinline__ bool row_interp(const SurrParams& s, int j0, int j1, int j2) {
@@ -1089,6 +1090,454 @@ __global__ void __launch_bounds__(256, 2) interp_rows3_kernel(SurrParams s) {
         if (n_rows) atomicAdd(&s.counters[3], n_rows);
     }
 }
+// ---------------------------------------------------------------------------------------------
+// K7 3D row-staged path, second form (the default): the tile, chunks and fp64 tensor-core passes of
+// interp_rows3_kernel, rebuilt around what bound it (ncu, profiles/r02_interp_rows3_ncu.txt: the
+// L1/shared data pipe at 73% of its wavefront peak, half of the shared stores bank-conflict replays;
+// compute and CSR writes of a CTA strictly alternating, both CTAs of an SM in step):
+//   * no CTA barrier in the loop.  The offsets of the whole tile are dealt to the 8 warps round robin
+//     (42 or 43 each).  The stage is a ring of three half-chunks (a chunk = K consecutive CSR slots of
+//     every row, written in halves of (K+1)/2 and K/2 slots); a warp that has finished its offsets of
+//     half-chunk u announces it on an mbarrier, writes ITS 16 rows of half-chunk u - 1 (values from
+//     the stage, column indices from registers) and goes on with half-chunk u + 1 once the ring slot
+//     has been released: CSR stores and tensor-core passes of one CTA overlap all the time;
+//   * a pass runs its second k-step (taps 4..7) only when the tile straddles two interpolant
+//     intervals in that direction at the offset's evaluation shift; otherwise tap 4 has zero weight
+//     for every tile point and the step would add exact zeros;
+//   * the (t1, t2) columns of the x pass are ordered t1 = lane quad index, t2 = (n-tile, half) and the
+//     z-pass operand rows are rotated by one column on odd t2: the x, y and z stores and the y and z
+//     fragment loads are bank-conflict free (odd stage row pitch, stage rows ordered so that the 32
+//     rows of a z-pass store cover every bank pair twice); the t1 = 4 columns form a fourth n-tile;
+//   * SKP row sums and the exact-zero count are accumulated from the z-pass accumulators (no stage
+//     reads); the per-offset window address, shifts and flags come from one table built at tile start;
+//     rows' CSR starts are 32-bit offsets from the tile's first row, broadcast by shuffles.
+// Every value is the same ascending FMA chain over its nonzero taps as before (skipped taps only
+// drop +-0 products), and a value depends on (row, offset) alone, so slabs, tiles and mirrored
+// entries agree bit for bit.  Tried and dropped (config 5, one B200): bulk async copies
+// (cp.async.bulk shared -> global) of 384 B / 192 B row segments sustain one copy per ~35-40 cycles
+// per SM whatever their size (3.7 ms); a dedicated writer warp per CTA cannot issue the stores fast
+// enough (4.9-5.8 ms); two writer warps cost the compute warps their registers (3.7 ms).
+// ---------------------------------------------------------------------------------------------
+namespace rows3v2 {
+constexpr int TB0 = 4, TB1 = 4, TB2 = 8, NR = TB0 * TB1 * TB2, CW = 5, MAXSH = 9;
+constexpr int NCW = 8, NWARP = NCW, NBUF = 3;  // every warp computes and writes; the stage is a ring of three half-chunks
+constexpr int SX = 20;                 // Ax[t1 (8)][SX]: column 4 t2 + b0
+constexpr int SZ = 20;                 // Bz[t2 (8)][SZ]: column (4 b1 + b0 + (t2 & 1)) mod 16
+constexpr int AXN = 8 * SX + 8, BZN = 8 * SZ, SCR = AXN + BZN;
+// stage row of tile point (b0, b1, b2)
+__host__ __device__ constexpr int srow(int b0, int b1, int b2) {
+    return ((b2 >> 1) << 1) + (b0 >> 1) + 8 * ((b2 & 1) + 2 * (b1 & 1) + 4 * (b1 >> 1) + 8 * (b0 & 1));
+}
+}  // namespace rows3v2
+
+// mbarriers addressed by their 32-bit shared address
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(unsigned bar, unsigned parity) {
+    unsigned ok;
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(ok)
+                 : "r"(bar), "r"(parity)
+                 : "memory");
+    return ok != 0;
+}
+__device__ __noinline__ void mbar_wait_slow(unsigned bar, unsigned parity) {
+    unsigned long long spins = 0;
+    while (!mbar_try(bar, parity))
+        if (++spins > (1ull << 26)) __trap();  // a lost hand-over must fail loudly, not hang the device
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+    if (!mbar_try(bar, parity)) mbar_wait_slow(bar, parity);
+}
+
+template <int NS>
+__global__ void __launch_bounds__(32 * rows3v2::NWARP, 2) interp_rows3v2_kernel(SurrParams s) {
+    using namespace rows3v2;
+    extern __shared__ double sm[];
+    constexpr int p = (NS - 1) / 2, K = NS * NS, PT = K * NS;
+    // a chunk (K consecutive CSR slots of every row) leaves in two halves of LA and LB slots
+    constexpr int LA = (K + 1) / 2, LB = K / 2, HP = LA, NU = 2 * NS;  // odd row pitch: conflict-free z-pass stores
+    static_assert((LA & 1) == 1 && LA <= 64, "odd first half");
+    const int P = s.P;  // == PT
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int lr = lane >> 2, lk = lane & 3;
+    // smem: W5 [3][MAXSH][CW][8] | scratch [NCW][SCR] | stage [NBUF][NR][HP] | dgv [NR] | rbS [NR] (int64) |
+    //       bars [6] | otab [P] (int2) | rowid [NR] | LO [3][MAXSH] | ST [3][MAXSH] | rfast [NR] | masks
+    double* W5 = sm;
+    double* scr = W5 + 3 * MAXSH * 8 * CW;
+    double* stage = scr + NCW * SCR;
+    double* dgv = stage + (size_t)NBUF * NR * HP;
+    int64_t* rbS = reinterpret_cast<int64_t*>(dgv + NR);
+    uint64_t* barp = reinterpret_cast<uint64_t*>(rbS + NR);  // full[NBUF], empty[NBUF]
+    const unsigned bars = (unsigned)__cvta_generic_to_shared(barp);
+    int2* otab = reinterpret_cast<int2*>(barp + 2 * NBUF);  // per offset: window element offset | shifts (+p) + straddle flags
+    int* rowid = reinterpret_cast<int*>(otab + PT);
+    int* LO = rowid + NR;
+    int* ST = LO + 3 * MAXSH;
+    uint8_t* rfast = reinterpret_cast<uint8_t*>(ST + 3 * MAXSH);
+    uint8_t* mk0 = rfast + NR;
+    constexpr int L0 = TB0 + 2 * p, L1 = TB1 + 2 * p, L2 = TB2 + 2 * p;
+    uint8_t* mk1 = mk0 + L0;
+    uint8_t* mk2 = mk1 + L1;
+    const int t = blockIdx.x + s.tile0;
+    const int tc0 = t % s.tg[0], tc1 = (t / s.tg[0]) % s.tg[1], tc2 = t / (s.tg[0] * s.tg[1]);
+    const int org0 = tc0 * TB0, org1 = tc1 * TB1, org2 = tc2 * TB2;
+    const int nl0 = s.nl[0], nl01 = s.nl[0] * s.nl[1], nl012 = nl01 * s.nl[2];
+    const int64_t tile_row0 = (int64_t)(s.blo[0] + org0) + (int64_t)s.m[0] * ((int64_t)(s.blo[1] + org1) + (int64_t)s.m[1] * (s.blo[2] + org2));
+    // ---- round 1 of the set-up (independent global loads): window origins and straddle flags, tap
+    //      weights, neighbour masks, row starts
+    for (int it = threadIdx.x; it < 3 * NS; it += blockDim.x) {
+        const int d = it / NS, sh = it % NS - p;
+        const int og = d == 0 ? org0 : (d == 1 ? org1 : org2), tb = d == 2 ? TB2 : TB0;
+        const int lo_ = s.esp[d][min(max(og + sh, 0), s.bn[d] - 1)] - 3;
+        const int lo = s.nl[d] >= CW ? min(lo_, s.nl[d] - CW) : lo_;
+        int st = 0;
+        for (int b = 0; b < tb; ++b) {
+            const int x = min(max(og + b + sh, 0), s.bn[d] - 1);
+            st |= (s.esp[d][x] - 3 - lo) != 0;
+        }
+        LO[d * MAXSH + sh + p] = lo;
+        ST[d * MAXSH + sh + p] = st;
+    }
+    for (int it = threadIdx.x; it < 3 * NS * 8; it += blockDim.x) {
+        const int d = it / (NS * 8), sh = (it / 8) % NS - p, b = it % 8;
+        const int og = d == 0 ? org0 : (d == 1 ? org1 : org2), tb = d == 2 ? TB2 : TB0;
+        double* w = W5 + (d * MAXSH + sh + p) * CW * 8 + b;
+        if (b >= tb) {
+#pragma unroll
+            for (int r = 0; r < CW; ++r) w[r * 8] = 0.0;
+            continue;
+        }
+        const int x = min(max(og + b + sh, 0), s.bn[d] - 1);
+        const int lo_ = s.esp[d][min(max(og + sh, 0), s.bn[d] - 1)] - 3;
+        const int lo = s.nl[d] >= CW ? min(lo_, s.nl[d] - CW) : lo_;
+        const int rel = s.esp[d][x] - 3 - lo;  // 0 or 1 (host checked the 5-wide window)
+        double e4[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) e4[q] = s.etab[d][x * 4 + q];
+#pragma unroll
+        for (int r = 0; r < CW; ++r) {
+            const int tap = r - rel;
+            w[r * 8] = tap == 0 ? e4[0] : (tap == 1 ? e4[1] : (tap == 2 ? e4[2] : (tap == 3 ? e4[3] : 0.0)));
+        }
+    }
+    for (int it = threadIdx.x; it < L0 + L1 + L2; it += blockDim.x) {
+        int d = 0, li = it;
+        if (li >= L0) { li -= L0; d = 1; if (li >= L1) { li -= L1; d = 2; } }
+        const int base = (d == 0 ? org0 : (d == 1 ? org1 : org2)) - p;
+        const int j = s.blo[d] + base + li;
+        uint8_t mk = 0;
+        if (j >= 0 && j < s.m[d]) mk = (uint8_t)(s.inb[d][j] | (s.smp[d][j] << 1));
+        (d == 0 ? mk0 : (d == 1 ? mk1 : mk2))[li] = mk;
+    }
+    // tile rows (stage order): CSR start (-1: not an interpolated row of this slab) and flat index
+    for (int r = threadIdx.x; r < NR; r += blockDim.x) {
+        const int b0 = ((r >> 6) & 1) | ((r & 1) << 1), b1 = ((r >> 4) & 1) | (((r >> 5) & 1) << 1);
+        const int b2 = ((r >> 3) & 1) | (((r >> 1) & 3) << 1);
+        bool ok = org0 + b0 < s.bn[0] && org1 + b1 < s.bn[1] && org2 + b2 < s.bn[2];
+        const int i0 = s.blo[0] + org0 + b0, i1 = s.blo[1] + org1 + b1, i2 = s.blo[2] + org2 + b2;
+        ok = ok && row_interp(s, i0, i1, i2);
+        const int64_t row = (int64_t)i0 + (int64_t)s.m[0] * ((int64_t)i1 + (int64_t)s.m[1] * i2);
+        ok = ok && row >= s.slab_lo && row < s.slab_hi;
+        rbS[r] = ok ? s.rowstart[row] : -1;
+        rowid[r] = (int)row;
+    }
+    for (int it = lane; it < SCR; it += 32) scr[warp * SCR + it] = 0.0;
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < 2 * NBUF; ++q) mbar_init(bars + 8 * q, NCW);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    // ---- round 2: per-offset table, fast-row flags
+    for (int o = threadIdx.x; o < P; o += blockDim.x) {
+        // mirrored offsets of the symmetric modes evaluate offset P-1-o at the shifted point
+        const bool mir = s.mode != SG_GENERAL && o < s.center;
+        const int a0 = mir ? o % NS : p, a1 = mir ? (o / NS) % NS : p, a2 = mir ? o / K : p;
+        const int op = mir ? P - 1 - o : o;
+        otab[o] = make_int2(op * nl012 + LO[2 * MAXSH + a2] * nl01 + LO[MAXSH + a1] * nl0 + LO[a0],
+                            a0 | (a1 << 4) | (a2 << 8) | (ST[a0] << 12) | (ST[MAXSH + a1] << 13) | (ST[2 * MAXSH + a2] << 14));
+    }
+    // whether every neighbour within +-p is an interpolated row (then every entry is the evaluated value)
+    for (int r = threadIdx.x; r < NR; r += blockDim.x) {
+        const int b0 = ((r >> 6) & 1) | ((r & 1) << 1), b1 = ((r >> 4) & 1) | (((r >> 5) & 1) << 1);
+        const int b2 = ((r >> 3) & 1) | (((r >> 1) & 3) << 1);
+        uint8_t all0 = 1, all1 = 1, all2 = 1, any0 = 0, any1 = 0, any2 = 0;
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+            const uint8_t a0 = mk0[b0 + q], a1 = mk1[b1 + q], a2 = mk2[b2 + q];
+            all0 &= a0;
+            all1 &= a1;
+            all2 &= a2;
+            any0 |= a0 >> 1;
+            any1 |= a1 >> 1;
+            any2 |= a2 >> 1;
+        }
+        rfast[r] = (all0 & all1 & all2 & 1) && !(any0 & any1 & any2 & 1);
+    }
+    __syncthreads();
+    double rs[4] = {0.0, 0.0, 0.0, 0.0};
+    int sb[4] = {0, 0, 0, 0};
+    unsigned n_zero = 0;
+    {
+        // ================= every warp: offsets g = warp, warp + NCW, ... of the whole tile; after its offsets of
+        // half-chunk u (= 2 c + h, stage buffer u mod NBUF) it writes its 16 rows of half-chunk u - 1
+        double* Ax = scr + (size_t)warp * SCR;
+        double* Bz = Ax + AXN;
+        // the lane's four stage rows (z-pass accumulators acc[j][h]): b2 = lr, b1 = 2j + (lk >> 1), b0 = 2 (lk & 1) + h
+        unsigned vmask = 0;  // valid rows
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int j = i >> 1, h = i & 1;
+            const int r = srow(2 * (lk & 1) + h, 2 * j + (lk >> 1), lr);
+            const int64_t rb = rbS[r];
+            sb[i] = r * HP;  // stage offset of the row
+            vmask |= (rb >= 0 ? 1u : 0u) << i;
+        }
+        // B-fragment element offsets of the x pass inside a coefficient window: n-tiles 0..2 hold
+        // (t1 = lr >> 1, t2 = 2 j + (lr & 1)), n-tile 3 holds (t1 = 4, t2 = lr); k = t0 = 4 kt + lk (clamped
+        // into the window: the weight is zero beyond tap 4, and columns past t2 = 4 are never stored)
+        int xoff[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int t1 = j < 3 ? (lr >> 1) : 4, t2 = j < 3 ? min(2 * j + (lr & 1), 4) : min(lr, 4);
+            xoff[j] = t2 * nl01 + t1 * nl0 + lk;
+        }
+        const int x1 = 4 - lk;  // k-step 1: t0 = 4 (lanes lk > 0 re-read tap 4 with zero weight)
+        auto fetch = [&](int g, double (&b)[2][4]) {
+            const int2 ot = otab[g];
+            const double* cf = s.coef + ot.x;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[0][j] = __ldg(cf + xoff[j]);
+            if (ot.y & (1 << 12)) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) b[1][j] = __ldg(cf + xoff[j] + x1);
+            }
+        };
+        // A fragment of direction d at evaluation shift sh: w[b = lr][t = 4 kt + lk]
+        auto wfrag = [&](int d, int sh, double (&a)[2]) {
+            a[0] = W5[((d * MAXSH + sh) * CW + lk) * 8 + lr];
+            a[1] = lk == 0 ? W5[((d * MAXSH + sh) * CW + 4) * 8 + lr] : 0.0;
+        };
+        // ---- write share: the rows [16 warp, 16 warp + 16) (stage order) of a finished half-chunk
+        constexpr int RW = NR / NCW, NKL = (LA + 31) / 32;
+        int colk[2][NKL];  // per-lane column constants of the slots k = h LA + lane + 32 qq
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int qq = 0; qq < NKL; ++qq) {
+                const int k = min(h * LA + lane + 32 * qq, K - 1);
+                colk[h][qq] = (k % NS - p) + s.m[0] * ((k / NS) % NS - p);
+            }
+        const int m01 = s.m[0] * s.m[1];
+        // CSR starts relative to the tile's first row (a tile spans 8 row planes: < 2^31 slots)
+        const int64_t trs = s.rowstart[tile_row0];
+        const int64_t rbl64 = rbS[RW * warp + (lane & (RW - 1))];
+        const int rbl = rbl64 >= 0 ? (int)(rbl64 - trs) : -1;
+        const int ridl = rowid[RW * warp + (lane & (RW - 1))];
+        auto write_share = [&](const int v) {
+            const int c = v >> 1, h = v & 1, G = c * K + h * LA, L = h ? LB : LA;
+            const double* sbuf = stage + (size_t)(v % NBUF) * NR * HP + (size_t)RW * warp * HP;
+            mbar_wait(bars + 8 * (v % NBUF), (v / NBUF) & 1);
+            // a row per step: its L values (stage -> CSR) and column indices, a lane per slot; the row's CSR
+            // start and id are broadcast from the lanes' registers (no shared loads in the address chain)
+#pragma unroll
+            for (int qq = 0; qq < NKL; ++qq) {
+                const int k = lane + 32 * qq;
+                const bool act = k < L;
+                const bool wv = act && !(s.dbg & 1), wi = act && !(s.dbg & 2);
+                const int cs = (c - p) * m01 + colk[h][qq];
+                double* db = s.data + trs + G + k;
+                int* ib = s.indices + trs + G + k;
+                const double* sk = sbuf + (act ? k : 0);
+#pragma unroll
+                for (int j = 0; j < RW; ++j) {
+                    const int rb = __shfl_sync(0xffffffffu, rbl, j);
+                    const int rid = __shfl_sync(0xffffffffu, ridl, j);
+                    const double val = sk[j * HP];
+                    if (rb >= 0 && wv) db[rb] = val;
+                    if (rb >= 0 && wi) ib[rb] = rid + cs;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bars + 8 * (NBUF + v % NBUF));
+        };
+        double wx[2], wy[2], wz[2];
+        int cur0 = -1, cur1 = -1, cur2 = -1;
+        int u = 0, gend = LA;   // current half-chunk and the end of its offsets
+        double* sp[4];          // sp[i][g]: stage slot of offset g in the lane's row i
+#pragma unroll
+        for (int i = 0; i < 4; ++i) sp[i] = stage + sb[i];
+        // one offset: passes x, y, z on the tensor cores; bx holds its x-pass B fragments, bn receives
+        // the next offset's
+        auto step = [&](const int g, double (&bx)[2][4], double (&bn)[2][4]) {
+            while (g >= gend) {
+                // this warp's offsets of half-chunk u are done: announce it, write the warp's rows of half-chunk
+                // u - 1, move to the next buffer (last used by half-chunk u + 1 - NBUF)
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bars + 8 * (u % NBUF));
+                if (u >= 1) write_share(u - 1);
+                ++u;
+                const int c = u >> 1, h = u & 1, G = c * K + h * LA;
+                gend = G + (h ? LB : LA);
+                if (u >= NBUF) mbar_wait(bars + 8 * (NBUF + u % NBUF), (u / NBUF - 1) & 1);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) sp[i] = stage + (size_t)(u % NBUF) * NR * HP + sb[i] - G;
+            }
+            const int fl = otab[g].y;
+            const int sh0 = fl & 15, sh1 = (fl >> 4) & 15, sh2 = (fl >> 8) & 15;  // shift + p
+            if (g + NCW < PT) fetch(g + NCW, bn);
+            if (sh0 != cur0) {
+                wfrag(0, sh0, wx);
+                cur0 = sh0;
+            }
+            if (sh1 != cur1) {
+                wfrag(1, sh1, wy);
+                cur1 = sh1;
+            }
+            if (sh2 != cur2) {
+                wfrag(2, sh2, wz);
+                cur2 = sh2;
+            }
+            // x pass -> Ax[t1][4 t2 + b0]
+            {
+                double acc[4][2];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    acc[j][0] = acc[j][1] = 0.0;
+                    dmma(acc[j][0], acc[j][1], wx[0], bx[0][j]);
+                }
+                if (fl & (1 << 12)) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) dmma(acc[j][0], acc[j][1], wx[1], bx[1][j]);
+                }
+                if (lr < TB0) {
+#pragma unroll
+                    for (int j = 0; j < 3; ++j)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+                            if (2 * j + h < CW) Ax[lk * SX + 4 * (2 * j + h) + lr] = acc[j][h];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        if (2 * lk + h < CW) Ax[4 * SX + 4 * (2 * lk + h) + lr] = acc[3][h];
+                }
+            }
+            __syncwarp();
+            // y pass -> Bz[t2][(4 b1 + b0 + (t2 & 1)) mod 16]
+            {
+                double acc[3][2];
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    acc[j][0] = acc[j][1] = 0.0;
+                    dmma(acc[j][0], acc[j][1], wy[0], Ax[lk * SX + 8 * j + lr]);
+                }
+                if (fl & (1 << 13)) {
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) dmma(acc[j][0], acc[j][1], wy[1], Ax[(4 + lk) * SX + 8 * j + lr]);
+                }
+                if (lr < TB1) {
+#pragma unroll
+                    for (int j = 0; j < 3; ++j)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int t2 = 2 * j + (lk >> 1), b0 = 2 * (lk & 1) + h;
+                            if (t2 < CW) Bz[t2 * SZ + ((4 * lr + b0 + (t2 & 1)) & 15)] = acc[j][h];
+                        }
+                }
+            }
+            __syncwarp();
+            // z pass -> stage
+            {
+                double acc[2][2];
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    acc[j][0] = acc[j][1] = 0.0;
+                    dmma(acc[j][0], acc[j][1], wz[0], Bz[lk * SZ + ((8 * j + lr + (lk & 1)) & 15)]);
+                }
+                if (fl & (1 << 14)) {
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) dmma(acc[j][0], acc[j][1], wz[1], Bz[(4 + lk) * SZ + ((8 * j + lr + (lk & 1)) & 15)]);
+                }
+                bool anyz = false;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const double v = acc[i >> 1][i & 1];
+                    sp[i][g] = v;
+                    rs[i] += v;
+                    anyz = anyz || v == 0.0;
+                }
+                if (anyz) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) n_zero += (acc[i >> 1][i & 1] == 0.0) & ((vmask >> i) & 1);
+                }
+                if (g == (PT - 1) / 2) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) dgv[sb[i] / HP] = acc[i >> 1][i & 1];
+                }
+            }
+            __syncwarp();
+        };
+        if (!(s.dbg & 4)) {
+            double bA[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}}, bB[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+            fetch(warp, bA);
+            int g = warp;
+            for (; g + NCW < PT; g += 2 * NCW) {
+                step(g, bA, bB);
+                step(g + NCW, bB, bA);
+            }
+            if (g < PT) step(g, bA, bB);
+        }
+        // the remaining half-chunks (the warp's offsets end before the last ones), then the last two writes
+        for (;;) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bars + 8 * (u % NBUF));
+            if (u >= 1) write_share(u - 1);
+            if (++u >= NU) break;
+            if (u >= NBUF) mbar_wait(bars + 8 * (NBUF + u % NBUF), (u / NBUF - 1) & 1);
+        }
+        write_share(NU - 1);
+    }
+    __syncthreads();
+    // ---- SKP row sums: the compute warps' partial sums joined in warp order (aliases the stage; the
+    //      last half-chunk has been written)
+    double* part = stage;  // [NCW][NR]
+#pragma unroll
+    for (int i = 0; i < 4; ++i) part[warp * NR + sb[i] / HP] = rs[i];
+    __syncthreads();
+    unsigned n_reset = 0, n_rows = 0;
+    if (threadIdx.x < NR) {
+        const int r = threadIdx.x;
+        if (rbS[r] >= 0) {
+            double rsum = 0.0;
+#pragma unroll
+            for (int w = 0; w < NCW; ++w) rsum += part[w * NR + r];
+            n_rows = 1;
+            if (s.mode == SG_SYMMETRIC_KERNEL_PRESERVING) s.newdiag[rowid[r]] = dgv[r] - rsum;
+            if (!rfast[r]) {
+                s.slow[atomicAdd(&s.counters[6], 1ull)] = rowid[r];  // finished by slow_rows_kernel
+            } else if (s.mode == SG_SYMMETRIC_KERNEL_PRESERVING) {
+                // every neighbour is interpolated: the row has interpolated off-diagonal entries
+                s.reset[rowid[r]] = 1;
+                n_reset = 1;
+            }
+        }
+    }
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) {
+        n_zero += __shfl_xor_sync(0xffffffffu, n_zero, m);
+        n_reset += __shfl_xor_sync(0xffffffffu, n_reset, m);
+        n_rows += __shfl_xor_sync(0xffffffffu, n_rows, m);
+    }
+    if (lane == 0) {
+        if (n_rows) atomicAdd(&s.counters[0], (unsigned long long)n_rows * P);  // provisional for slow rows
+        if (n_zero) atomicAdd(&s.counters[1], n_zero);
+        if (n_reset) atomicAdd(&s.counters[2], n_reset);
+        if (n_rows) atomicAdd(&s.counters[3], n_rows);
+    }
+}
 // Rows of the row-staged path with a non-interpolated neighbour (box boundary band, neighbours of
 // fully sampled rows).  interp_rows3_kernel wrote the interpolant into every slot of these rows,
 // counted every slot as interpolated and stored the provisional SKP diagonal (centre - row sum);
@@ -1167,6 +1616,12 @@ static size_t interp_rows3_smem(int p) {
            sizeof(int) * (2 * NR + 2 * P + 3 * MAXSH) + 2 * NR + 3 * (8 + 2 * p) + 16;
 }
 
+static size_t interp_rows3v2_smem(int p) {
+    using namespace rows3v2;
+    const int NS = 2 * p + 1, K = NS * NS, P = K * NS, HP = (K + 1) / 2;
+    return sizeof(double) * (3 * MAXSH * 8 * CW + NCW * SCR + (size_t)NBUF * NR * HP + NR) + sizeof(int64_t) * (NR + 2 * NBUF) +
+           sizeof(int) * (2 * P + NR + 6 * MAXSH) + NR + 3 * (8 + 2 * p) + 16;
+}
 static size_t interp_fix_smem(int n, int p) {
     const int Q = 3, CW = 5, NR = 64, MAXSH = 9, nw = 16;
     const int TB0 = n == 2 ? 8 : 4, TB1 = n == 2 ? 8 : 4, TB2 = n == 3 ? 4 : 1;
@@ -1609,15 +2064,22 @@ static int surr_finish(sg_surrogate_state& S, const sg_surrogate_params* sp, sg_
         s.slow = (int*)c.alloc(sizeof(int) * N, true);
         if (!s.slow) return fail(-4, "device allocation failed");
         for (int d = 0; d < n; ++d) s.cmax[d] = 5;
-        // tensor-core passes by default; SG_INTERP_SIMT=1 selects the SIMT passes (same values bitwise)
-        if (getenv("SG_INTERP_SIMT"))
+        // second form by default; SG_INTERP_V1=1 selects the first tensor-core form, SG_INTERP_SIMT=1 its
+        // SIMT passes (same values up to the sign of zero)
+        // (the second form keeps 32-bit CSR offsets relative to the tile's first row: 8 row planes of slots)
+        const bool v2 = !getenv("SG_INTERP_SIMT") && !getenv("SG_INTERP_V1") &&
+                        (int64_t)rows3v2::TB2 * dp.m[0] * dp.m[1] * P < (int64_t)INT32_MAX;
+        if (v2)
+            kfn = p == 1 ? (void*)interp_rows3v2_kernel<3>
+                         : (p == 2 ? (void*)interp_rows3v2_kernel<5> : (p == 3 ? (void*)interp_rows3v2_kernel<7> : (void*)interp_rows3v2_kernel<9>));
+        else if (getenv("SG_INTERP_SIMT"))
             kfn = p == 1 ? (void*)interp_rows3_kernel<3, false>
                          : (p == 2 ? (void*)interp_rows3_kernel<5, false> : (p == 3 ? (void*)interp_rows3_kernel<7, false> : (void*)interp_rows3_kernel<9, false>));
         else
             kfn = p == 1 ? (void*)interp_rows3_kernel<3, true>
                          : (p == 2 ? (void*)interp_rows3_kernel<5, true> : (p == 3 ? (void*)interp_rows3_kernel<7, true> : (void*)interp_rows3_kernel<9, true>));
-        smem = interp_rows3_smem(p);
-        nthr = rows3::NWARP * 32;
+        smem = v2 ? interp_rows3v2_smem(p) : interp_rows3_smem(p);
+        nthr = v2 ? rows3v2::NWARP * 32 : rows3::NWARP * 32;
     } else if (fixq && n >= 2 && p <= 4) {
         for (int d = 0; d < n; ++d) s.cmax[d] = 5;
         kfn = n == 2 ? (void*)interp_fix_kernel<2> : (void*)interp_fix_kernel<3>;
@@ -1651,6 +2113,7 @@ static int surr_finish(sg_surrogate_state& S, const sg_surrogate_params* sp, sg_
     }
     if (smem > 227 * 1024) return fail(-2, "surrogate tile does not fit shared memory (%zu B)", smem);
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptinMax);
+    s.dbg = getenv("SG_K7_DBG") ? atoi(getenv("SG_K7_DBG")) : 0;
     void* args[] = {&s};
     c.kbegin(rows3 ? "interp_rows3" : "interp_tiles");
     cudaError_t e = ntiles > 0 ? cudaLaunchKernel(kfn, dim3(ntiles), dim3(nthr), args, smem, c.stream) : cudaSuccess;
