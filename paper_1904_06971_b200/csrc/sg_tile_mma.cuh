@@ -318,13 +318,10 @@ __host__ __device__ constexpr TileChoice mma_tile(int ndim, int P, int form, boo
         // 2D bi-Laplacian, p = 3: a deeper y extent (2 x 5 instead of 3 x 3) halves the x-contraction
         // work per row (config 4: 7.04 -> 6.12 ms)
         if (form == 2 && P == 3 && mma_geom(2, P, form, rat, 2, 5).total <= cap) return {2, 5};
-        // 3 x 3 tiles with an odd Gauss count (p = 2, 4) raise an illegal-instruction fault under TMA
-        // (found by the full 2D matrix, tools/tma2d_matrix.py: p=2 rational bi-Laplacian and p=4
-        // Poisson fault, every other degree / form / map and the same boxes on other tiles pass; plain
-        // loads of the same tiles are correct); those instantiations take the next smaller tile
+        // (3 x 3 tiles with an odd Gauss count start their TMA windows at odd y points: see tma_ysh)
         const int cand[] = {12, 10, 8, 6, 4, 3, 2, 1};
         for (int t : cand)
-            if (!(t == 3 && (P % 2) == 0) && mma_geom(2, P, form, rat, t, t).total <= cap) return {t, t};
+            if (mma_geom(2, P, form, rat, t, t).total <= cap) return {t, t};
         return {1, 1};
     }
 #if defined(SG_FORCE_FORM) && defined(SG_FORCE_T0) && defined(SG_FORCE_T1)
@@ -707,6 +704,15 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
     constexpr int GZ = NDIM == 3 ? G : 1;
     const int nplanes = (ehi2 - elo2 + 1) * GZ;
     const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&bars[0]);
+    // A TMA box must start at a 16-byte aligned global address: with an odd Gauss count and an odd tile
+    // extent in y the window's first y point (y fastest, 8 B each) can be odd (3 x 3 tiles at p = 2, 4:
+    // the "illegal instruction" of profiles/r02_tma2d_matrix.txt).  Such a window is fetched from the
+    // point before it and read one column further in (DY >= YW + 1 there: YW is odd).
+    auto tma_ysh = [&](int e1) -> int {
+        if constexpr (G % 2 == 0 || NDIM < 2) return 0;
+        else return (prm.tma && NDIM >= 2) ? ((e1 * G) & 1) : 0;
+    };
+    static_assert(NDIM < 2 || G % 2 == 0 || T1 % 2 == 0 || DY >= YW + 1, "room for the shifted window");
     // D window of plane `pi` (TMA: one 4D box per plane; out-of-mesh coordinates are zero filled)
     auto issue_plane = [&](int pi) {
         const int z = elo2 * G + pi;
@@ -720,7 +726,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(DBYTES) : "memory");
         asm volatile(
             "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(dst),
-            "l"(reinterpret_cast<uint64_t>(&prm.dmap)), "r"(ew1 * G), "r"(ew0 * G), "r"(0), "r"(z), "r"(bar)
+            "l"(reinterpret_cast<uint64_t>(&prm.dmap)), "r"(ew1 * G - tma_ysh(ew1)), "r"(ew0 * G), "r"(0), "r"(z), "r"(bar)
             : "memory");
     };
     // TMA D windows: 3D (double-buffered pencil of planes), 2D (one window per tile, the next tile's
@@ -752,7 +758,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(DBYTES) : "memory");
         asm volatile(
             "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(dst),
-            "l"(reinterpret_cast<uint64_t>(&prm.dmap)), "r"(y0 * G), "r"(x0 * G), "r"(0), "r"(0), "r"(bar)
+            "l"(reinterpret_cast<uint64_t>(&prm.dmap)), "r"(y0 * G - tma_ysh(y0)), "r"(x0 * G), "r"(0), "r"(0), "r"(bar)
             : "memory");
     };
     // make the D window of plane j resident in Dbuf[j & 1] (plain path: all threads load, then a barrier)
@@ -770,6 +776,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
                     : "r"(bar), "r"(par)
                     : "memory");
             }
+            Ds += tma_ysh(ew1);
         } else {
             const long long gx0 = (long long)ew0 * G, gy0 = (long long)ew1 * G;
             const long long z = (long long)elo2 * G + j;
@@ -1107,7 +1114,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
                         : "r"(bar), "r"(par)
                         : "memory");
                 }
-                Ds = Dbuf(0);
+                Ds = Dbuf(0) + tma_ysh(ew1);
             } else {
                 Ds = get_plane(0);
             }
