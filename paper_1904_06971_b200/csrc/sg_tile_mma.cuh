@@ -113,9 +113,13 @@ __host__ __device__ constexpr int kind_of_slot2(const Tables& T, int slot) {
 }
 __host__ __device__ constexpr long align16(long o) { return (o + 15) & ~15L; }
 
-__host__ __device__ constexpr int pad_dy(int v) {  // w >= v, w % 16 in {4, 8, 12}: conflict-free B-fragment rows
+// D window row length: w >= v with w % 16 in {4, 12}.  Phase 1's B fragment takes four consecutive x rows
+// (lane bits 0-1) and eight consecutive y per row: the rows must start in distinct quarter-bank groups
+// (w = 8 mod 16 left rows 0/2 and 1/3 on the same banks: 2-way, 13% of the 3D Poisson kernel's shared
+// wavefronts, profiles/r02_assemble_mma_poisson128_ncu.txt)
+__host__ __device__ constexpr int pad_dy(int v) {
     int w = v;
-    while (w % 16 == 0 || w % 4 != 0) ++w;
+    while (w % 8 != 4) ++w;
     return w;
 }
 __host__ __device__ constexpr int pad8_4(int v) {  // smallest w >= v with w % 8 == 4 (conflict-free fragment rows)
@@ -246,6 +250,8 @@ __host__ __device__ constexpr MmaGeom mma_geom(int ndim, int P, int form, bool r
     m.NC1 = 1;
 #endif
     m.DY = pad_dy(m.NTY * 8);
+    // (3D p = 4 mass keeps its 2 x 4 tile: the conflict-free row would push it past the shared-memory cap)
+    if (ndim == 3 && form == 1 && P == 4 && T0 == 2 && m.T1 == 4) m.DY = m.NTY * 8;
     m.TY = pad8_4(m.NTY * 8 > m.YW + 4 ? m.NTY * 8 : m.YW + 4);
     // T1SW: T1 rows r placed at t1_row(r) = (r / 4) (4 TY + 8) + (r % 4) TY + 4 ((r >> 1) & 1) with
     // TY = 8 (mod 16): rows 0..3 of a half-warp start in distinct quarter-bank groups (phase 2's
