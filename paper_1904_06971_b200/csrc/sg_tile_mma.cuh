@@ -183,21 +183,35 @@ __host__ __device__ constexpr int mma_minb(int ndim, int P, int form, bool rat) 
     return ndim == 3 && form == 1 ? SG_MASS_MINB : 1;
 }
 
-// ---- warp specialisation of the 3D pipeline (Poisson / Stokes velocity): warps [0, NW - NB) run
+// ---- warp specialisation of the 3D pipeline (Poisson / Stokes velocity, mass): warps [0, NW - NB) run
 // phases 1-2 plane by plane (group A), warps [NW - NB, NW) run phase 3 layer by layer (group B); the
 // groups hand T2 planes over through mbarriers instead of one CTA barrier per plane, so the phase-3
 // burst of every G-th plane no longer stalls phases 1-2 (and B's barrier waits overlap A's work)
+// (6 of 24 warps: after the phase-1/2 work of group A shrank (static unit tables, conflict-free layouts)
+// the 4-warp phase-3 group had become the busier one: 88% of the loop, clock64 breakdown of the SG_K4_PROF
+// build; config 5 Poisson 25.0 -> 24.1 ms, 5 / 7 warps: 24.4 / 24.3)
 #ifndef SG_SPEC_NB
-#define SG_SPEC_NB 4
+#define SG_SPEC_NB 6
 #endif
 __host__ __device__ constexpr bool mma_spec(int ndim, int form) {
 #ifdef SG_NO_SPEC
     return false;
 #else
+    // mass too (two CTAs of 10 + 6 warps per SM; config 5 mass full 5.99 -> 4.71 ms, quadrature rows
+    // 1.92 -> 1.62; SG_NO_SPEC_MASS keeps one barrier interval per plane)
+#ifdef SG_NO_SPEC_MASS
     return ndim == 3 && form == 0;
+#else
+    return ndim == 3 && (form == 0 || form == 1);
+#endif
 #endif
 }
-__host__ __device__ constexpr int mma_spec_nb(int ndim, int form) { return mma_spec(ndim, form) ? SG_SPEC_NB : 0; }
+#ifndef SG_SPEC_NB_MASS
+#define SG_SPEC_NB_MASS 6
+#endif
+__host__ __device__ constexpr int mma_spec_nb(int ndim, int form) {
+    return mma_spec(ndim, form) ? (form == 1 ? SG_SPEC_NB_MASS : SG_SPEC_NB) : 0;
+}
 // T2 ring: G + 1 planes (phase 3 of a layer while phase 2 writes the next plane); + 1 under
 // specialisation (group A may run two planes ahead of the layer group B is consuming)
 // phase 3 contracts a row plane i2 over the whole z support of its rows (layers i2-P .. i2, (P+1) G
