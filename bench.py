@@ -305,7 +305,18 @@ def run_ours(args):
                          "algorithmic_frac": flops_alg / (avg / 1e3) / 1e12 / FP64_PEAK_TFLOPS,
                          "ms": avg, "issued_flops": issued, "algorithmic_flops": flops_alg, "share": sum(ts)})
         elif name == "geom_D":
-            rows.append({"kernel": f"geom_D[{f},{path}]", "bound": None, "ms": avg, "share": sum(ts)})
+            # K3 writes U = |Mset|(|Mset|+1)/2 doubles per Gauss point: its HBM roofline; the
+            # mass tensor (U = 1) is bound by the fp64 map / Jacobian evaluation instead (~300 flop / point)
+            U = {"poisson": n * (n + 1) // 2, "mass": 1}.get(f)
+            els = (E if path == "full" else plan.active_elements) / world
+            if U:
+                b = 8.0 * U * els * g ** n
+                ach = b / (avg / 1e3) / 1e9
+                rows.append({"kernel": f"geom_D[{f},{path}]", "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                             "frac": ach / hbm, "ms": avg, "bytes": b, "share": sum(ts),
+                             "fp64_frac_at_300_flop_per_point": 300.0 * els * g ** n / (avg / 1e3) / 1e12 / FP64_PEAK_TFLOPS})
+            else:
+                rows.append({"kernel": f"geom_D[{f},{path}]", "bound": None, "ms": avg, "share": sum(ts)})
         elif name in ("interp_tiles", "interp_rows3"):
             # the kernel's own output: value + column of every slot of the interpolated rows
             b = 12 * n_irows * (2 * cfg.p + 1) ** n

@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <cmath>
 #include <string>
 #include <thread>
 #include <vector>
@@ -1033,6 +1034,40 @@ int run_assembly(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>
             mp.ntiles = (int)col.size();
             mp.tiles = (const int*)c.upload(col.data(), sizeof(int) * col.size());
             nb = ((int64_t)col.size() + mp.run - 1) / mp.run;
+        } else if (dp.n == 3 && !getenv("SG_NO_RASTER")) {
+            // 3D launch order: the CTAs resident together (one wave) cover a compact patch of tiles in (x, y)
+            // and sweep z in step, so a D plane fetched for one tile's window is still in L2 for the
+            // neighbours whose windows overlap it.  (Plain x-fastest order made a wave a 131 x 1 strip: the
+            // y halo was re-read from HBM by the next wave, 25 GB of DRAM reads for the 6.4 GB D of config 5.)
+            const TileChoice tc = mma_tile(3, dp.p, dp.pr.form, dp.rational);
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.dev);
+            const int resident = sms * mma_minb(3, dp.p, dp.pr.form, dp.rational);
+            // patch of PX x PY tiles, PX PY ~ resident, as square as possible in rows (PX T0 ~ PY T1)
+            int PY = std::max(1, (int)std::lround(std::sqrt((double)resident * tc.T0 / tc.T1)));
+            int PX = std::max(1, resident / PY);
+            if (const char* e = getenv("SG_RASTER_PX")) PX = std::max(1, atoi(e));
+            if (const char* e = getenv("SG_RASTER_PY")) PY = std::max(1, atoi(e));
+            const int tg0 = pl.tgrid[0], tg1 = pl.tgrid[1];
+            std::vector<int> ord;
+            if (tiles) ord = *tiles;
+            else {
+                ord.resize(pl.ntiles);
+                for (int64_t q = 0; q < pl.ntiles; ++q) ord[q] = (int)q;
+            }
+            const int npx = (tg0 + PX - 1) / PX;
+            auto key = [&](int q) -> int64_t {
+                const int c0 = q % tg0, c1 = (q / tg0) % tg1, c2 = q / (tg0 * tg1);
+                const int64_t patch = (int64_t)(c1 / PY) * npx + c0 / PX;
+                return (((int64_t)c2 * ((int64_t)npx * ((tg1 + PY - 1) / PY)) + patch) * PY + c1 % PY) * PX + c0 % PX;
+            };
+            std::vector<std::pair<int64_t, int>> ks(ord.size());
+            for (size_t q = 0; q < ord.size(); ++q) ks[q] = {key(ord[q]), ord[q]};
+            std::sort(ks.begin(), ks.end());
+            for (size_t q = 0; q < ord.size(); ++q) ord[q] = ks[q].second;
+            mp.tiles = (const int*)c.upload(ord.data(), sizeof(int) * ord.size());
+            nb = (int64_t)ord.size();
+            mp.ntiles = (int)nb;
         } else if (tiles) {
             mp.tiles = (const int*)c.upload(tiles->data(), sizeof(int) * tiles->size());
             nb = (int64_t)tiles->size();
