@@ -1310,11 +1310,14 @@ __global__ void __launch_bounds__(32 * rows3v2::NWARP, 2) interp_rows3v2_kernel(
         auto fetch = [&](int g, double (&b)[2][4]) {
             const int2 ot = otab[g];
             const double* cf = s.coef + ot.x;
+            const bool s1 = ot.y & (1 << 13);  // the t1 = 4 columns are only read when the tile straddles in y
 #pragma unroll
-            for (int j = 0; j < 4; ++j) b[0][j] = __ldg(cf + xoff[j]);
+            for (int j = 0; j < 3; ++j) b[0][j] = __ldg(cf + xoff[j]);
+            if (s1) b[0][3] = __ldg(cf + xoff[3]);
             if (ot.y & (1 << 12)) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) b[1][j] = __ldg(cf + xoff[j] + x1);
+                for (int j = 0; j < 3; ++j) b[1][j] = __ldg(cf + xoff[j] + x1);
+                if (s1) b[1][3] = __ldg(cf + xoff[3] + x1);
             }
         };
         // A fragment of direction d at evaluation shift sh: w[b = lr][t = 4 kt + lk]
@@ -1405,14 +1408,18 @@ __global__ void __launch_bounds__(32 * rows3v2::NWARP, 2) interp_rows3v2_kernel(
             // x pass -> Ax[t1][4 t2 + b0]
             {
                 double acc[4][2];
+                const bool s1 = fl & (1 << 13);
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
+                for (int j = 0; j < 3; ++j) {
                     acc[j][0] = acc[j][1] = 0.0;
                     dmma(acc[j][0], acc[j][1], wx[0], bx[0][j]);
                 }
+                acc[3][0] = acc[3][1] = 0.0;
+                if (s1) dmma(acc[3][0], acc[3][1], wx[0], bx[0][3]);
                 if (fl & (1 << 12)) {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) dmma(acc[j][0], acc[j][1], wx[1], bx[1][j]);
+                    for (int j = 0; j < 3; ++j) dmma(acc[j][0], acc[j][1], wx[1], bx[1][j]);
+                    if (s1) dmma(acc[3][0], acc[3][1], wx[1], bx[1][3]);
                 }
                 if (lr < TB0) {
 #pragma unroll
@@ -1420,9 +1427,11 @@ __global__ void __launch_bounds__(32 * rows3v2::NWARP, 2) interp_rows3v2_kernel(
 #pragma unroll
                         for (int h = 0; h < 2; ++h)
                             if (2 * j + h < CW) Ax[lk * SX + 4 * (2 * j + h) + lr] = acc[j][h];
+                    if (s1) {
 #pragma unroll
-                    for (int h = 0; h < 2; ++h)
-                        if (2 * lk + h < CW) Ax[4 * SX + 4 * (2 * lk + h) + lr] = acc[3][h];
+                        for (int h = 0; h < 2; ++h)
+                            if (2 * lk + h < CW) Ax[4 * SX + 4 * (2 * lk + h) + lr] = acc[3][h];
+                    }
                 }
             }
             __syncwarp();
