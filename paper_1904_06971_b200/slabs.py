@@ -11,14 +11,15 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["plane_slabs", "weighted_plane_slabs", "surrogate_plane_cost", "job_slabs", "csr_checksum", "stitch",
+__all__ = ["plane_slabs", "weighted_plane_slabs", "halo_balanced_plane_slabs", "surrogate_plane_cost", "job_slabs",
+           "csr_checksum", "stitch",
            "allreduce_checksum", "lattice_owners", "exchange_samples"]
 
 # Relative device cost per row of the surrogate's parts (measured on one B200 at config 5, p=3,
 # DESIGN.md §8): quadrature row (K4 on the quadrature tiles), interpolated row (K7), any row (K3
 # geometry of the needed planes, row pointers).  Only the ratios matter.
-SURROGATE_ROW_COST = {"poisson": (24.7, 2.8, 0.84), "stokes_velocity": (24.7, 2.8, 0.84),
-                      "mass": (6.2, 2.8, 0.77), "biharmonic": (24.7, 2.8, 0.84)}
+SURROGATE_ROW_COST = {"poisson": (15.2, 2.25, 0.5), "stokes_velocity": (15.2, 2.25, 0.5),
+                      "mass": (3.1, 2.25, 0.4), "biharmonic": (15.2, 2.25, 0.5)}
 
 
 def plane_slabs(ms, world: int):
@@ -47,7 +48,39 @@ def weighted_plane_slabs(plane_cost, per: int, world: int):
     return [(cuts[r] * per, cuts[r + 1] * per) for r in range(world)]
 
 
-def surrogate_plane_cost(ms, p, lattice_indices, form: str) -> np.ndarray:
+def halo_balanced_plane_slabs(plane_cost, halo_cost, p: int, per: int, world: int):
+    """Slabs minimising the dearest slab when a slab also pays for its p-plane halo on either side
+    (the surrogate recomputes the halo's quadrature rows: next to the box's all-quadrature boundary
+    planes that halo costs as much as a dozen interior planes, which per-plane balancing ignores).
+    cost[a, b) = sum plane_cost[a:b] + sum halo_cost[a-p:a] + sum halo_cost[b:b+p]; exact by dynamic
+    programming over the cut positions (planes x planes x world steps)."""
+    c = np.r_[0.0, np.cumsum(np.asarray(plane_cost, dtype=float))]
+    h = np.r_[0.0, np.cumsum(np.asarray(halo_cost, dtype=float))]
+    n = len(c) - 1
+    if world < 1 or world > n:
+        raise ValueError(f"cannot cut {n} planes into {world} slabs")
+
+    lo_h = h - h[np.maximum(np.arange(n + 1) - p, 0)]           # halo below a cut at plane a
+    hi_h = h[np.minimum(np.arange(n + 1) + p, n)] - h             # halo above a cut at plane b
+    inf = float("inf")
+    best = np.full((world + 1, n + 1), inf)
+    arg = np.zeros((world + 1, n + 1), dtype=np.int64)
+    best[0, 0] = 0.0
+    for r in range(1, world + 1):
+        for b in range(r, n - (world - r) + 1):
+            a = np.arange(r - 1, b)
+            v = np.maximum(best[r - 1, a], c[b] - c[a] + lo_h[a] + hi_h[b])
+            k = int(np.argmin(v))
+            best[r, b] = v[k]
+            arg[r, b] = a[k]
+    cuts = [n]
+    for r in range(world, 0, -1):
+        cuts.append(int(arg[r, cuts[-1]]))
+    cuts = cuts[::-1]
+    return [(cuts[r] * per, cuts[r + 1] * per) for r in range(world)]
+
+
+def surrogate_plane_cost(ms, p, lattice_indices, form: str, parts: bool = False):
     """Estimated surrogate cost of every slowest-direction plane (quadrature rows are ~9x dearer
     than interpolated rows for Poisson): the boundary layers of the box make the first and last
     slabs heavy, so equal plane counts do not balance the surrogate."""
@@ -67,7 +100,9 @@ def surrogate_plane_cost(ms, p, lattice_indices, form: str) -> np.ndarray:
     interp = np.where(~box[-1], 0, np.where(smp[-1], inner_box - inner_smp, inner_box)).astype(float)
     quad = per - interp
     cq, ci, c0 = SURROGATE_ROW_COST.get(form, SURROGATE_ROW_COST["poisson"])
-    return cq * quad + ci * interp + c0 * per
+    total = cq * quad + ci * interp + c0 * per
+    # parts: also the cost of a plane as a halo plane (its quadrature rows and their geometry)
+    return (total, (cq + c0) * quad) if parts else total
 
 
 def job_slabs(ms, p, world: int, path: str, form: str, lattice_indices=None):
@@ -77,8 +112,8 @@ def job_slabs(ms, p, world: int, path: str, form: str, lattice_indices=None):
         return [None]
     if path == "full" or lattice_indices is None:
         return plane_slabs(ms, world)
-    cost = surrogate_plane_cost(ms, p, lattice_indices, form)
-    return weighted_plane_slabs(cost, int(np.prod(ms[:-1])), world)
+    cost, halo = surrogate_plane_cost(ms, p, lattice_indices, form, parts=True)
+    return halo_balanced_plane_slabs(cost, halo, p, int(np.prod(ms[:-1])), world)
 
 
 def csr_checksum(indptr, data) -> np.ndarray:

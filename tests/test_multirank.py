@@ -107,3 +107,47 @@ def test_surrogate_plane_cost_rows_and_balance():
         return max(c) / np.mean(c)
     assert imbalance(weighted_plane_slabs(cost, per, 8)) < 1.08 < 1.3 < imbalance(plane_slabs(ms, 8))
     assert imbalance(weighted_plane_slabs(cost, per, 4)) < 1.05
+
+
+def test_halo_balanced_slabs_beat_per_plane_balancing_under_the_halo_cost():
+    """Slabs that pay for their p-plane halo (the surrogate recomputes its quadrature rows): the dynamic
+    program is never worse than per-plane balancing under that cost, covers every plane once and is
+    exact on a case small enough to enumerate."""
+    import itertools
+
+    import paper_1904_06971_b200 as pkg
+    from paper_1904_06971_b200.configs import CONFIGS
+    from paper_1904_06971_b200.slabs import halo_balanced_plane_slabs, job_slabs, surrogate_plane_cost
+    from paper_1904_06971_b200.surrogate import build_sampling_lattice
+
+    def slab_cost(cost, halo, p, per, sl):
+        out = []
+        for lo, hi in sl:
+            a, b = lo // per, hi // per
+            out.append(cost[a:b].sum() + halo[max(a - p, 0):a].sum() + halo[b:b + p].sum())
+        return max(out)
+
+    cfg = CONFIGS[5]
+    disc = pkg.make_discretization(cfg.geom(), cfg.p, cfg.spans)
+    ms = tuple(kv.m for kv in disc.space.kvs)
+    lat = build_sampling_lattice(disc.space.kvs, cfg.M)
+    per = int(np.prod(ms[:-1]))
+    for form in ("poisson", "mass"):
+        cost, halo = surrogate_plane_cost(ms, cfg.p, lat.indices, form, parts=True)
+        for world in (2, 4, 8):
+            new = halo_balanced_plane_slabs(cost, halo, cfg.p, per, world)
+            assert new[0][0] == 0 and new[-1][1] == per * ms[-1]
+            assert all(new[r][1] == new[r + 1][0] and new[r][1] > new[r][0] for r in range(world - 1))
+            old = weighted_plane_slabs(cost, per, world)
+            assert slab_cost(cost, halo, cfg.p, per, new) <= slab_cost(cost, halo, cfg.p, per, old) * (1 + 1e-12)
+            assert job_slabs(ms, cfg.p, world, "surrogate", form, lat.indices) == new
+    # the all-quadrature boundary planes of config 5 make the halo matter at 8 slabs
+    cost, halo = surrogate_plane_cost(ms, cfg.p, lat.indices, "poisson", parts=True)
+    assert slab_cost(cost, halo, cfg.p, per, halo_balanced_plane_slabs(cost, halo, cfg.p, per, 8)) < \
+        0.9 * slab_cost(cost, halo, cfg.p, per, weighted_plane_slabs(cost, per, 8))
+    # exactness: brute force over every cut set of a small case
+    rng = np.random.default_rng(5)
+    c, h = rng.random(11) + 0.1, 3 * rng.random(11)
+    best = min(slab_cost(c, h, 2, 1, [(a, b) for a, b in zip((0,) + cuts, cuts + (11,))])
+               for cuts in itertools.combinations(range(1, 11), 3))
+    assert abs(slab_cost(c, h, 2, 1, halo_balanced_plane_slabs(c, h, 2, 1, 4)) - best) < 1e-12
