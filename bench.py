@@ -695,10 +695,25 @@ def run_reference(args):
     value = statistics.median(vals)
     cpu = dict(last)
     cpu["value"] = value
-    line = {"metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
+    # the same workload keys as our arm's line (sizes from the closed-form pattern, no assembly)
+    import numpy as np
+    import paper_1904_06971_b200 as pkg
+    disc = pkg.make_discretization(cfg.geom(), cfg.p, cfg.spans)
+    ms = [int(kv.m) for kv in disc.space.kvs]
+    nnz1 = 1.0
+    for m in ms:  # rows of the basis-overlap pattern per direction: sum_i |{j : |i - j| <= p}|
+        i = np.arange(m)
+        nnz1 *= float((np.minimum(i + cfg.p, m - 1) - np.maximum(i - cfg.p, 0) + 1).sum())
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    line = {"metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * len(forms) * len(paths) * nnz1 / value,
+            "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (deterministic geometry)", "impl": "reference",
-            "config": {"workload": f"config{cfg.idx}:{cfg.name}", "forms": forms, "paths": paths},
+            "config": {"workload": f"config{cfg.idx}:{cfg.name}", "forms": forms, "paths": paths, "p": cfg.p,
+                       "spans": list(cfg.spans), "M": cfg.M, "q": cfg.q, "N": int(np.prod(ms)), "nnz_per_matrix": nnz1,
+                       "parallelism": f"row-slab x{world} (surrogate: lattice-sample all-gather)" if world > 1
+                       else "single GPU",
+                       "l2": "outputs (8.9 GB/matrix at config 5) exceed L2; no flush needed"},
             "cpu_baseline": cpu, "e2e": {"value": value, "unit": "nnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
