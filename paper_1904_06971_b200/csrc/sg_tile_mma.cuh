@@ -151,8 +151,12 @@ __host__ __device__ constexpr int pad8_4(int v) {  // smallest w >= v with w % 8
 #ifndef SG_P3_EPI
 #define SG_P3_EPI 3
 #endif
+// 3D Poisson: 20 warps = 16 (phases 1-2) + 4 (phase 3).  Sweep at config 5 (ms): 16+4: 23.1 | 15+5: 23.9 |
+// 15+4: 23.9 | 18+6: 24.1 | 14+6: 24.9 | 20+4: 25.0 | 12+4: 25.1 | 17+4: 25.7 | 16+5: 26.0 | 16+6: 26.1 |
+// 21+7: 25.3 | 24+8: 27.0.  Warp w runs on sub-partition w mod 4: group sizes that are multiples of 4 give
+// every sub-partition the same mix (one phase-3 warp each), and 640 threads leave 96 registers per thread.
 #ifndef SG_3D_NW
-#define SG_3D_NW 24
+#define SG_3D_NW 20
 #endif
 #ifndef SG_MASS_NW
 #define SG_MASS_NW 16
@@ -187,11 +191,8 @@ __host__ __device__ constexpr int mma_minb(int ndim, int P, int form, bool rat) 
 // phases 1-2 plane by plane (group A), warps [NW - NB, NW) run phase 3 layer by layer (group B); the
 // groups hand T2 planes over through mbarriers instead of one CTA barrier per plane, so the phase-3
 // burst of every G-th plane no longer stalls phases 1-2 (and B's barrier waits overlap A's work)
-// (6 of 24 warps: after the phase-1/2 work of group A shrank (static unit tables, conflict-free layouts)
-// the 4-warp phase-3 group had become the busier one: 88% of the loop, clock64 breakdown of the SG_K4_PROF
-// build; config 5 Poisson 25.0 -> 24.1 ms, 5 / 7 warps: 24.4 / 24.3)
 #ifndef SG_SPEC_NB
-#define SG_SPEC_NB 6
+#define SG_SPEC_NB 4
 #endif
 __host__ __device__ constexpr bool mma_spec(int ndim, int form) {
 #ifdef SG_NO_SPEC
