@@ -179,7 +179,7 @@ __host__ __device__ constexpr int mma_warps(int ndim, int P, int form, bool rat)
     // pipelined intervals better than 16 (cfg5 Poisson 52.4 -> 48.2 ms); more spills registers.
     // 3D mass: two CTAs of SG_MASS_NW warps per SM on half-size tiles (the barrier waits of one CTA
     // overlap the other's work)
-    return ndim == 3 ? (form == 1 ? SG_MASS_NW : SG_3D_NW) : 16;
+    return ndim == 3 ? (form == 1 ? SG_MASS_NW : (P == 3 ? SG_3D_NW : 24)) : 16;
 #endif
 }
 // CTAs per SM the kernel is compiled for (register budget of __launch_bounds__)
@@ -210,8 +210,9 @@ __host__ __device__ constexpr bool mma_spec(int ndim, int form) {
 #ifndef SG_SPEC_NB_MASS
 #define SG_SPEC_NB_MASS 6
 #endif
-__host__ __device__ constexpr int mma_spec_nb(int ndim, int form) {
-    return mma_spec(ndim, form) ? (form == 1 ? SG_SPEC_NB_MASS : SG_SPEC_NB) : 0;
+__host__ __device__ constexpr int mma_spec_nb(int ndim, int form, int P) {
+    // (p = 3 Poisson: 16 + 4 of 20 warps; other degrees keep 18 + 6 of 24: config 3, p = 2, 1.68 vs 1.74 ms)
+    return mma_spec(ndim, form) ? (form == 1 ? SG_SPEC_NB_MASS : (P == 3 ? SG_SPEC_NB : 6)) : 0;
 }
 // T2 ring: G + 1 planes (phase 3 of a layer while phase 2 writes the next plane); + 1 under
 // specialisation (group A may run two planes ahead of the layer group B is consuming)
@@ -401,7 +402,7 @@ __host__ __device__ constexpr MmaTab mma_tab(int ndim, int P, int form, bool rat
     int kind[1024] = {}, idx[1024] = {};
     bool done[1024] = {};
     int n = 0;
-    const int NBs = mma_spec_nb(ndim, form);
+    const int NBs = mma_spec_nb(ndim, form, P);
     int wlo = 0, whi = NW;  // warps the next lpt() pass may use
     auto lpt = [&]() {
         for (int it = 0; it < n; ++it) {
@@ -757,7 +758,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
     // warp-specialised 3D pipeline: plane j + 2 is issued into plane j's buffer as soon as the last
     // phase-1 warp has finished plane j (a shared counter), ~half an interval before the next barrier;
     // only the phase-1 warps wait for the D windows
-    const bool early = use_tma && NDIM == 3 && mma_spec_nb(NDIM, FORM) > 0 && !(prm.dbg & 16);
+    const bool early = use_tma && NDIM == 3 && mma_spec_nb(NDIM, FORM, P) > 0 && !(prm.dbg & 16);
     if (use_tma) {
         if (tid == 0) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0) : "memory");
@@ -803,7 +804,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
             const long long z = (long long)elo2 * G + j;
             const long long G1 = NDIM >= 2 ? prm.Gp[1] : 1;
             // (under warp specialisation only group A loads planes)
-            const int nld = mma_spec_nb(NDIM, FORM) > 0 ? (NW - mma_spec_nb(NDIM, FORM)) * 32 : (int)blockDim.x;
+            const int nld = mma_spec_nb(NDIM, FORM, P) > 0 ? (NW - mma_spec_nb(NDIM, FORM, P)) * 32 : (int)blockDim.x;
             for (int it = tid; it < M.U * XWp * DY; it += nld) {
                 const int y = it % DY, r = it / DY;
                 const int u = r / XWp, x = r % XWp;
@@ -813,8 +814,8 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
                     v = prm.D[((z * M.U + u) * G0 + gx) * (long long)prm.Dys + gy];
                 Ds[r * DY + y] = v;
             }
-            if constexpr (mma_spec_nb(NDIM, FORM) > 0) {
-                asm volatile("bar.sync 1, %0;\n" ::"r"((NW - mma_spec_nb(NDIM, FORM)) * 32) : "memory");
+            if constexpr (mma_spec_nb(NDIM, FORM, P) > 0) {
+                asm volatile("bar.sync 1, %0;\n" ::"r"((NW - mma_spec_nb(NDIM, FORM, P)) * 32) : "memory");
             } else {
                 __syncthreads();
             }
@@ -1357,7 +1358,7 @@ __global__ void __launch_bounds__(32 * mma_warps(NDIM, P, FORM, RAT), mma_minb(N
                 }
             }
         };
-        constexpr int NBW = mma_spec_nb(NDIM, FORM);
+        constexpr int NBW = mma_spec_nb(NDIM, FORM, P);
         if constexpr (NBW > 0) {
             // ---- warp-specialised pipeline: group A (phases 1-2, planes) / group B (phase 3, row planes),
             // handing over through two monotonic counters: ready = layers whose planes are in T2,
