@@ -753,20 +753,14 @@ int compute_D(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* t
     gp.U = U;
     gp.Dys = n >= 2 ? ((gp.Gp[1] + 1) & ~1) : 1;
     dp.Dys = gp.Dys;
-    // 32 x 32 points per block (16 x 16 for the sparse restricted plans measured slower: the per-block
-    // table set-up dominates; SG_GEOM_BXY_RESTR for experiments)
-    const int bxy = (n == 3 && tiles) ? env_int("SG_GEOM_BXY_RESTR", 32) : 32;
-    gp.BX = n == 1 ? 256 : bxy;
-    gp.BY = n >= 2 ? bxy : 1;
-    gp.nbx = (gp.Gp[0] + gp.BX - 1) / gp.BX;
-    gp.nby = (gp.Gp[1] + gp.BY - 1) / gp.BY;
-    const int64_t nblk_all = (int64_t)gp.nbx * gp.nby * gp.Gp[2];
-    // 3D: several z-planes per block (the x/y tables and spans are loaded once), enough blocks for
-    // every SM several times over
-    gp.ZB = 1;
-    if (n == 3)
-        while (gp.ZB < 8 && (int64_t)gp.nbx * gp.nby * ((gp.Gp[2] + 2 * gp.ZB - 1) / (2 * gp.ZB)) >= 8 * 148) gp.ZB *= 2;
-    // function-range bounds per block
+    // Points per block: 32 x 32 for restricted plans (16 x 16 measured slower: the per-block table set-up
+    // dominates; larger blocks compute more unneeded points); whole-mesh plans take 32 x 256 where it fits
+    // (a warp shares x and walks y: the per-plane Hz / Hx preparation and its barriers are amortised over
+    // 8x the points; config 5: Poisson 2.10 -> 1.67 ms, mass 1.69 -> 1.18 ms; 32 x 128: 1.72 / 1.25,
+    // 32 x 512: 1.78 / 1.22, 64 x 256: 1.79 / 1.23, 16 x 256: 1.69 / 1.20)
+    const int C = n + 1;
+    const int NCg = n == 3 ? (NUG + 1) * (NUG + 2) / 2 : NUG + 1;
+    const int NCw = n == 3 ? (NU + 1) * (NU + 2) / 2 : NU + 1;
     auto gbound = [&](int d, int B) {
         int mx = 1;
         if (d >= n) return 1;
@@ -776,36 +770,59 @@ int compute_D(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* t
         }
         return mx;
     };
-    gp.GN0 = gbound(0, gp.BX);
-    gp.GN1 = gbound(1, gp.BY);
-    gp.WN0 = (gp.BX + g - 1) / g + 1 + P;
-    gp.WN1 = n >= 2 ? (gp.BY + g - 1) / g + 1 + P : 1;
-    const int C = n + 1;
-    const int NCg = n == 3 ? (NUG + 1) * (NUG + 2) / 2 : NUG + 1;
-    const int NCw = n == 3 ? (NU + 1) * (NU + 2) / 2 : NU + 1;
-    size_t sz[13];
-    sz[0] = (size_t)gp.BX * NBG;
-    sz[1] = n >= 2 ? (size_t)gp.BY * (NBG | 1) : 0;
-    sz[2] = gp.BX / 2 + 1;
-    sz[3] = gp.BY / 2 + 1;
-    sz[4] = dp.rational ? (size_t)gp.BX * NB : 0;
-    sz[5] = (dp.rational && n >= 2) ? (size_t)gp.BY * (NB | 1) : 0;
-    sz[6] = gp.BX / 2 + 1;
-    sz[7] = gp.BY / 2 + 1;
-    sz[8] = n == 3 ? (size_t)gp.GN0 * gp.GN1 * C * (NUG + 1) : 0;
-    sz[9] = n >= 2 ? (size_t)gp.BX * gp.GN1 * C * NCg : 0;
-    sz[10] = (n == 3 && dp.rational) ? (size_t)gp.WN0 * gp.WN1 * (NU + 1) : 0;
-    sz[11] = (n >= 2 && dp.rational) ? (size_t)gp.BX * gp.WN1 * NCw : 0;
-    sz[12] = 64 + gp.BX + gp.BY + 8;
-    int* offs[13] = {&gp.off_G0, &gp.off_G1, &gp.off_gs0, &gp.off_gs1, &gp.off_B0, &gp.off_B1, &gp.off_ws0,
-                     &gp.off_ws1, &gp.off_Hz, &gp.off_Hy, &gp.off_Wz, &gp.off_Wy, &gp.off_misc};
-    size_t o = 0;
-    for (int k = 0; k < 13; ++k) {
-        *offs[k] = (int)o;
-        o += sz[k];
-        o = (o + 1) & ~size_t(1);
+    auto set_layout = [&](int BX, int BY) -> size_t {
+        gp.BX = BX;
+        gp.BY = BY;
+        gp.nbx = (gp.Gp[0] + gp.BX - 1) / gp.BX;
+        gp.nby = (gp.Gp[1] + gp.BY - 1) / gp.BY;
+        // 3D: several z-planes per block (the x/y tables and spans are loaded once), enough blocks for
+        // every SM several times over
+        gp.ZB = 1;
+        if (n == 3)
+            while (gp.ZB < 8 && (int64_t)gp.nbx * gp.nby * ((gp.Gp[2] + 2 * gp.ZB - 1) / (2 * gp.ZB)) >= 8 * 148) gp.ZB *= 2;
+        // function-range bounds per block
+        gp.GN0 = gbound(0, gp.BX);
+        gp.GN1 = gbound(1, gp.BY);
+        gp.WN0 = (gp.BX + g - 1) / g + 1 + P;
+        gp.WN1 = n >= 2 ? (gp.BY + g - 1) / g + 1 + P : 1;
+        size_t sz[13];
+        sz[0] = (size_t)gp.BX * NBG;
+        sz[1] = n >= 2 ? (size_t)gp.BY * (NBG | 1) : 0;
+        sz[2] = gp.BX / 2 + 1;
+        sz[3] = gp.BY / 2 + 1;
+        sz[4] = dp.rational ? (size_t)gp.BX * NB : 0;
+        sz[5] = (dp.rational && n >= 2) ? (size_t)gp.BY * (NB | 1) : 0;
+        sz[6] = gp.BX / 2 + 1;
+        sz[7] = gp.BY / 2 + 1;
+        sz[8] = n == 3 ? (size_t)gp.GN0 * gp.GN1 * C * (NUG + 1) : 0;
+        sz[9] = n >= 2 ? (size_t)gp.BX * gp.GN1 * C * NCg : 0;
+        sz[10] = (n == 3 && dp.rational) ? (size_t)gp.WN0 * gp.WN1 * (NU + 1) : 0;
+        sz[11] = (n >= 2 && dp.rational) ? (size_t)gp.BX * gp.WN1 * NCw : 0;
+        sz[12] = 64 + gp.BX + gp.BY + 8;
+        int* offs[13] = {&gp.off_G0, &gp.off_G1, &gp.off_gs0, &gp.off_gs1, &gp.off_B0, &gp.off_B1, &gp.off_ws0,
+                         &gp.off_ws1, &gp.off_Hz, &gp.off_Hy, &gp.off_Wz, &gp.off_Wy, &gp.off_misc};
+        size_t o = 0;
+        for (int k = 0; k < 13; ++k) {
+            *offs[k] = (int)o;
+            o += sz[k];
+            o = (o + 1) & ~size_t(1);
+        }
+        return o * sizeof(double);
+    };
+    size_t smem = 0;
+    if (n >= 2 && !tiles && !getenv("SG_GEOM_BY") && !getenv("SG_GEOM_BX")) {
+        for (int by : {256, 128, 64}) {
+            if (by >= 2 * gp.Gp[1]) continue;  // a block taller than the mesh buys nothing
+            smem = set_layout(32, by);
+            if (smem <= 72 * 1024) break;  // three blocks per SM
+            smem = 0;
+        }
     }
-    const size_t smem = o * sizeof(double);
+    if (!smem) {
+        const int bxy = (n == 3 && tiles) ? env_int("SG_GEOM_BXY_RESTR", 32) : 32;
+        smem = set_layout(n == 1 ? 256 : env_int("SG_GEOM_BX", bxy), n >= 2 ? env_int("SG_GEOM_BY", bxy) : 1);
+    }
+    const int64_t nblk_all = (int64_t)gp.nbx * gp.nby * gp.Gp[2];
     if (smem > kSmemCap) return fail(-2, "geometry block does not fit shared memory (%zu B)", smem);
     const size_t npts = (size_t)gp.Gp[0] * gp.Dys * gp.Gp[2];
     c.hmark("compute_D:layout");
