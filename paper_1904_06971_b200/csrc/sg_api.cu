@@ -779,7 +779,7 @@ int compute_D(Call& c, DevProblem& dp, const Plan& pl, const std::vector<int>* t
         // every SM several times over
         gp.ZB = 1;
         if (n == 3)
-            while (gp.ZB < 8 && (int64_t)gp.nbx * gp.nby * ((gp.Gp[2] + 2 * gp.ZB - 1) / (2 * gp.ZB)) >= 8 * 148) gp.ZB *= 2;
+            while (gp.ZB < env_int("SG_GEOM_ZB", 8) && (int64_t)gp.nbx * gp.nby * ((gp.Gp[2] + 2 * gp.ZB - 1) / (2 * gp.ZB)) >= 8 * 148) gp.ZB *= 2;
         // function-range bounds per block
         gp.GN0 = gbound(0, gp.BX);
         gp.GN1 = gbound(1, gp.BY);
