@@ -161,6 +161,10 @@ __host__ __device__ constexpr int pad8_4(int v) {  // smallest w >= v with w % 8
 #ifndef SG_MASS_NW
 #define SG_MASS_NW 16
 #endif
+// 2D: 20 warps (16: config 2 Poisson 0.407 / mass 0.145 / config 4 3.23 ms; 20: 0.384 / 0.134 / 3.23; 12: 0.403 / 0.173 / 3.16)
+#ifndef SG_2D_NW
+#define SG_2D_NW 20
+#endif
 #ifndef SG_MASS_MINB
 #define SG_MASS_MINB 2
 #endif
@@ -179,7 +183,7 @@ __host__ __device__ constexpr int mma_warps(int ndim, int P, int form, bool rat)
     // pipelined intervals better than 16 (cfg5 Poisson 52.4 -> 48.2 ms); more spills registers.
     // 3D mass: two CTAs of SG_MASS_NW warps per SM on half-size tiles (the barrier waits of one CTA
     // overlap the other's work)
-    return ndim == 3 ? (form == 1 ? SG_MASS_NW : (P == 3 ? SG_3D_NW : 24)) : 16;
+    return ndim == 3 ? (form == 1 ? SG_MASS_NW : (P == 3 ? SG_3D_NW : 24)) : SG_2D_NW;
 #endif
 }
 // CTAs per SM the kernel is compiled for (register budget of __launch_bounds__)
