@@ -179,8 +179,8 @@ __host__ __device__ constexpr int mma_warps(int ndim, int P, int form, bool rat)
 #ifdef SG_MMA_NW
     return SG_MMA_NW;
 #else
-    // 3D: 24 warps (6 per sub-partition) hide the smem -> DMMA -> smem latency chains of the
-    // pipelined intervals better than 16 (cfg5 Poisson 52.4 -> 48.2 ms); more spills registers.
+    // 3D Poisson: 20 warps (16 + 4) at p = 3, 24 (18 + 6) otherwise: see SG_3D_NW above (round 1's
+    // unspecialised kernel wanted 24: 52.4 -> 48.2 ms against 16).
     // 3D mass: two CTAs of SG_MASS_NW warps per SM on half-size tiles (the barrier waits of one CTA
     // overlap the other's work)
     return ndim == 3 ? (form == 1 ? SG_MASS_NW : (P == 3 ? SG_3D_NW : 24)) : SG_2D_NW;
