@@ -228,8 +228,11 @@ __host__ __device__ constexpr int mma_ns(int ndim, int P, int form) {
 }
 
 // ---- compile-time tile geometry (shared by host planning and the kernel)
+// (136: the 131 row planes of config 5 in ONE z tile instead of two of 66: no second start-up and no
+// re-streamed halo layers, Poisson 23.05 -> 22.27 ms; the row-start table grows by 1.5-4 KB, every 3D tile
+// choice stays the same and the p = 3 mass kernel still fits two CTAs per SM at 112 KB)
 #ifndef SG_MMA_T2
-#define SG_MMA_T2 72
+#define SG_MMA_T2 136
 #endif
 constexpr int kMmaT2 = SG_MMA_T2;  // max rows per CTA in z (3D); the plan picks the depth T2 <= kMmaT2 per call
 
