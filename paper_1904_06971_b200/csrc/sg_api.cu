@@ -941,7 +941,10 @@ static bool plan_mma(DevProblem& dp, Plan& pl, int t2, int z0) {
 }
 
 int plan_assembly(DevProblem& dp, Plan& pl, bool restricted, int t2, int z0) {
-    if (t2 <= 0 && restricted) t2 = env_int("SG_T2_RESTR", kT2Restricted);
+    // restricted plans: 24 row planes per tile; 3D p = 3 Poisson-type forms on deep meshes take 48 (config 5
+    // surrogate call 13.09 -> 12.68 ms, 66: 12.74, 96: 12.85; mass and p = 2 are faster at 24: 6.65 vs 6.83, 1.85 vs 1.91)
+    if (t2 <= 0 && restricted)
+        t2 = env_int("SG_T2_RESTR", (dp.n == 3 && dp.pr.form == 0 && dp.p == 3 && dp.m[2] >= 96) ? 48 : kT2Restricted);
     pl.mma = false;
     pl.z0 = 0;
     if (plan_mma(dp, pl, t2, z0)) return 0;

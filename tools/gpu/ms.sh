@@ -1,4 +1,4 @@
-for d in . expbuild/t136; do timeout 300 python - $d <<'PY'
+for d in . expbuild/nc3; do timeout 300 python - $d <<'PY'
 import sys
 sys.path.insert(0, sys.argv[1])
 import numpy as np
