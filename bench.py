@@ -92,7 +92,42 @@ class Clocks:
         self.proc = None
         self.lines = []
 
+    def _nvml_loop(self):
+        # in-process NVML sampling (no second process polling the driver during the timed region)
+        nv = self.nv
+        R = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
+        while not self.stop_flag.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                self.samples.append((float(sm), float(mx), [k for k, b in R.items() if rs & b]))
+            except Exception:
+                pass
+            self.stop_flag.wait(0.05)
+
     def start(self):
+        self.nv = None
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            # NVML enumerates physical devices: honour CUDA_VISIBLE_DEVICES (indices or UUIDs)
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            ids = [x.strip() for x in vis.split(",") if x.strip()]
+            if ids and self.dev < len(ids):
+                tok = ids[self.dev]
+                self.h = nv.nvmlDeviceGetHandleByIndex(int(tok)) if tok.isdigit() else nv.nvmlDeviceGetHandleByUUID(tok)
+            else:
+                self.h = nv.nvmlDeviceGetHandleByIndex(self.dev)
+            nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+            self.nv = nv
+            self.samples = []
+            self.stop_flag = threading.Event()
+            self.t = threading.Thread(target=self._nvml_loop, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nv = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
@@ -107,6 +142,15 @@ class Clocks:
             self.lines.append(ln.strip())
 
     def stop(self):
+        if getattr(self, "nv", None) is not None:
+            time.sleep(0.1)
+            self.stop_flag.set()
+            self.t.join(timeout=1)
+            sm = [s[0] for s in self.samples]
+            mx = [s[1] for s in self.samples]
+            reasons = sorted({r for s in self.samples for r in s[2]})
+            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                    "reasons": reasons, "samples": len(sm), "source": "nvml"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         time.sleep(0.25)
